@@ -1,0 +1,118 @@
+"""Seeded parity cases shared by the CPU (oracle vs golden) and GPU (kernel vs
+oracle) tests.  Each case mirrors one generator in ``tests/golden/make_golden.py``
+but is built from this repo's own host-init layer, so it runs on the GPU box
+where the reference tree does not exist.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+from paper_2605_08528_b200 import config as C
+from paper_2605_08528_b200.friction import SURFACE_ORDER, assign_friction
+from paper_2605_08528_b200.params import ObsConfig, SimConfig
+from paper_2605_08528_b200.policies import LaneFollower
+from paper_2605_08528_b200.scenes import build_world_batch, prepare_scene, straight_scene
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def cfg_of(W, M, seed=42, mode="dynamic", assignment="random_fill", invincible=False,
+           episode_len=1500):
+    cfg = C.RootConfig()
+    cfg.env.num_envs = W
+    cfg.env.num_agents_per_env = M
+    cfg.env.dynamics_mode = mode
+    cfg.env.episode_len = episode_len
+    cfg.eval.invincible = invincible
+    cfg.seed = seed
+    cfg.scene_factory.assignment_mode = assignment
+    return cfg
+
+
+def philox_actions(seed, T, W, M):
+    g = np.random.Generator(np.random.Philox(seed))
+    return g.uniform(-1.0, 1.0, (T, W, M, 3)).astype(np.float32)
+
+
+def event_actions(T, W, M):
+    steer = np.array([0.0, 0.08, -0.08, 0.3, -0.3, 0.02, -0.5, 0.15, 0.0, -0.15, 1.0,
+                      -0.02, 0.6, 0.0, -1.0, 0.04])[:M]
+    acts = np.zeros((T, W, M, 3), dtype=np.float32)
+    acts[..., 0] = 1.0
+    acts[..., 1] = steer[None, None, :] * (1.0 - 0.25 * (np.arange(W)[None, :, None] % 2))
+    rows = (np.arange(M) % 5 == 0)
+    acts[100:160, :, rows, 2] = 1.0
+    acts[100:160, :, rows, 0] = -1.0
+    return acts
+
+
+def wet_frictions(W):
+    films = (0.0, 0.3, 0.5, 0.8, 1.0, 2.0)
+    return [assign_friction(SURFACE_ORDER[(w // len(films)) % 3], films[w % len(films)])
+            for w in range(W)]
+
+
+@dataclass
+class Case:
+    name: str
+    inputs: C.EngineInputs
+    actions: np.ndarray | None = None     # (T, W, M, 3) float32, None = LaneFollower
+    steps: int = 0
+    full_obs_steps: tuple = field(default_factory=tuple)
+
+
+def case_inputs(name: str) -> Case:
+    if name == "traj_c1":
+        scene = prepare_scene(straight_scene(agent_count=1, goal_dist=50.0))
+        inp = C.build_inputs(cfg_of(1, 1, invincible=True, episode_len=2000), scenes=[scene])
+        return Case(name, inp, philox_actions(3, 1000, 1, 1), 1000, tuple(range(1, 1001)))
+    if name == "traj_pool":
+        return Case(name, C.build_inputs(cfg_of(4, 16)), None, 60, (1, 24, 25, 60))
+    if name == "traj_wet":
+        W, M = 12, 16
+        cfg = cfg_of(W, M, seed=5)
+        inp = C.build_inputs(cfg)
+        pool = inp.scenes
+        worlds, assignment = build_world_batch(pool, W, mode="random_fill", seed=5)
+        inp.worlds, inp.assignment, inp.frictions = worlds, assignment, wet_frictions(W)
+        inp.sim = SimConfig(num_envs=W, num_agents=M, seed=5)
+        acts = philox_actions(9, 80, W, M)
+        acts[..., 0] = np.abs(acts[..., 0])
+        return Case(name, inp, acts, 80, (1, 40, 80))
+    if name == "traj_bicycle":
+        inp = C.build_inputs(cfg_of(2, 3, mode="bicycle", assignment="fixed", seed=11))
+        return Case(name, inp, philox_actions(4, 50, 2, 3), 50, (1, 50))
+    if name == "traj_custom_obs":
+        cfg = cfg_of(2, 5, assignment="fixed", seed=19)
+        cfg.obs = ObsConfig(include_weather=False, k_road=20, k_vehicles=3, road_radius=12.5)
+        return Case(name, C.build_inputs(cfg), philox_actions(6, 40, 2, 5), 40, tuple(range(1, 41)))
+    if name in ("traj_events", "traj_events_inv"):
+        inp = C.build_inputs(cfg_of(4, 16, seed=31, invincible=name.endswith("_inv")))
+        return Case(name, inp, event_actions(420, 4, 16), 420, (1, 150, 420))
+    raise KeyError(name)
+
+
+TRAJ_CASES = ("traj_c1", "traj_pool", "traj_wet", "traj_bicycle", "traj_custom_obs",
+              "traj_events", "traj_events_inv")
+
+
+def run_case(engine, case: Case, on_step):
+    """Drive ``engine`` (oracle or GPU) through the case; ``on_step(t, out,
+    actions)`` sees every step (t is 1-based)."""
+    if case.actions is None:
+        pol = LaneFollower(obs_config=engine.obs_config)
+        obs = np.asarray(engine.observe())
+        for t in range(case.steps):
+            a = pol(obs)
+            out = engine.step(a)
+            on_step(t + 1, out, a)
+            obs = np.asarray(out.obs)
+    else:
+        for t in range(case.steps):
+            a = case.actions[t].astype(np.float64)
+            out = engine.step(a)
+            on_step(t + 1, out, a)

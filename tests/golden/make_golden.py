@@ -1,0 +1,267 @@
+"""Generate the golden fixtures from the reference package (run in the dev container).
+
+The reference (``/root/reference/pkg``) is pure Python + numpy; it is imported
+read-only from its source tree and never travels to the GPU box.  This script
+records what the reference computes for a set of seeded cases; the CPU tests
+pin the oracle restatement (``oracle/``) and the host-init layer of the product
+against these files.
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Cases (each an .npz under tests/golden/):
+  init_default      256x16 default pool: world tables, spawn table, mu, weather
+  friction          mu_effective / assign_friction over surfaces x film depths
+  traj_c1           1x1 straight road, invincible, 1000 fp32 Philox(3) actions
+  traj_pool         4x16 default pool (random_fill, seed 42), LaneFollower, 60 steps
+  traj_wet          12x16 default pool, per-world friction sweep, fp32 random actions
+  traj_bicycle      2x3 bicycle backend, random actions
+  traj_custom_obs   2x5, reduced ObsConfig (no weather, k_road 20, k_vehicles 3)
+  traj_reset        2x4: steps, EnvHandle.reset quirk, overlapping teleport starts
+  traj_events       4x16, scripted throttle/steer/brake: goal, edge, crash, collision
+  traj_events_inv   same actions, invincible mode (latched events, no termination)
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path(os.environ.get("DRIVEGRID_REF", "/root/reference/pkg"))
+sys.dont_write_bytecode = True
+sys.path[:0] = [str(REF / "src"), str(REF / "bindings" / "src")]
+
+from drivegrid import vehicle as vh  # noqa: E402
+from drivegrid.config import RootConfig, build_engine, prepare_scene  # noqa: E402
+from drivegrid.friction import SURFACE_ORDER, assign_friction, mu_effective  # noqa: E402
+from drivegrid.observation import ObsConfig  # noqa: E402
+from drivegrid.policies import LaneFollower  # noqa: E402
+from drivegrid.synth import default_scene_pool, straight_scene  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+EVENTS = ("goal", "collision", "crash", "lane_forbidden")
+TERMS = ("progress", "lane", "offroad", "idle", "ttc_vehicle", "ttc_edge", "total")
+
+
+def cfg_of(W, M, seed=42, mode="dynamic", assignment="random_fill", invincible=False,
+           episode_len=1500):
+    cfg = RootConfig()
+    cfg.env.num_envs = W
+    cfg.env.num_agents_per_env = M
+    cfg.env.dynamics_mode = mode
+    cfg.env.episode_len = episode_len
+    cfg.eval.invincible = invincible
+    cfg.seed = seed
+    cfg.scene_factory.assignment_mode = assignment
+    return cfg
+
+
+def philox_actions(seed, T, W, M):
+    g = np.random.Generator(np.random.Philox(seed))
+    return g.uniform(-1.0, 1.0, (T, W, M, 3)).astype(np.float32)
+
+
+class Recorder:
+    """Per-step outputs; full obs only at the listed steps (1-based)."""
+
+    def __init__(self, full_obs_steps=()):
+        self.full_steps = set(full_obs_steps)
+        self.rows = {}
+        self.obs_full = {}
+
+    def add(self, t, eng, out, actions):
+        row = {
+            "actions": np.asarray(actions, dtype=np.float64),
+            "rewards": out.rewards, "dones": out.dones,
+            "reason": out.info["reason"], "alive": out.info["alive"],
+            "alive_pre": out.info["alive_pre"], "ttc_min": out.info["ttc_min"],
+            "obs_sum": out.obs.astype(np.float64).sum(axis=-1),
+            "obs_abs": np.abs(out.obs.astype(np.float64)).sum(axis=-1),
+            "obs_nnz": (out.obs != 0).sum(axis=-1),
+            "obs_ego": out.obs[..., :16].copy(),
+        }
+        for k in EVENTS:
+            row["ev_" + k] = out.events[k]
+        for k in TERMS:
+            row["term_" + k] = out.info["reward_terms"][k]
+        for k in vh.STATE_FIELDS:
+            row["snap_" + k] = out.info["state"][k]
+            row["state_" + k] = eng.state[k]
+        for k, v in row.items():
+            self.rows.setdefault(k, []).append(np.asarray(v))
+        if t in self.full_steps:
+            self.obs_full[t] = out.obs.copy()
+
+    def save(self, name, **extra):
+        arrays = {k: np.stack(v) for k, v in self.rows.items()}
+        for t, o in self.obs_full.items():
+            arrays[f"obs_full_{t}"] = o
+        arrays.update(extra)
+        np.savez_compressed(OUT / f"{name}.npz", **arrays)
+        print(name, sum(a.nbytes for a in arrays.values()) // 1024, "KiB raw")
+
+
+def run_actions(eng, actions, rec):
+    for t in range(actions.shape[0]):
+        out = eng.step(actions[t].astype(np.float64))
+        rec.add(t + 1, eng, out, actions[t])
+
+
+def init_default():
+    eng = build_engine(cfg_of(256, 16))
+    w = eng.worlds
+    np.savez_compressed(
+        OUT / "init_default.npz",
+        midpoints=w.midpoints, directions=w.directions, type_codes=w.type_codes,
+        half_lengths=w.half_lengths, half_widths=w.half_widths, mask=w.mask,
+        grid_offsets=w.grid_offsets, mu_eff=eng.mu_eff, weather=eng.weather,
+        valid=eng.valid, start_xy=eng.start_xy, goal_xy=eng.goal_xy, length=eng.length,
+        width=eng.width, r_hull=eng.r_hull, d_hull=eng.d_hull,
+        lane_mid=eng.lane["mid"], edge_mid=eng.edge["mid"],
+        **{"state_" + k: eng.state[k] for k in vh.STATE_FIELDS},
+        obs0=eng.observe())
+    print("init_default")
+
+
+def friction():
+    films = np.array([0.0, 0.1, 0.3, 0.5, 0.8, 0.86, 1.0, 2.0])
+    mu_s = np.array([[mu_effective(s, h) for h in films] for s in SURFACE_ORDER])
+    mu_d = np.array([[mu_effective(s, h, slip=0.8) for h in films] for s in SURFACE_ORDER])
+    asg = np.array([[assign_friction(s, h).mu_static for h in films] for s in SURFACE_ORDER])
+    np.savez_compressed(OUT / "friction.npz", films=films, mu_static=mu_s, mu_dynamic=mu_d,
+                        assigned=asg)
+    print("friction")
+
+
+def traj_c1():
+    scene = prepare_scene(straight_scene(agent_count=1, goal_dist=50.0))
+    eng = build_engine(cfg_of(1, 1, invincible=True, episode_len=2000), scenes=[scene])
+    rec = Recorder(full_obs_steps=range(1, 1001))
+    run_actions(eng, philox_actions(3, 1000, 1, 1), rec)
+    rec.save("traj_c1")
+
+
+def traj_pool():
+    eng = build_engine(cfg_of(4, 16))
+    pol = LaneFollower(obs_config=eng.obs_config)
+    rec = Recorder(full_obs_steps=(1, 24, 25, 60))
+    obs = eng.observe()
+    obs0 = obs.copy()
+    for t in range(60):
+        a = pol(obs)
+        out = eng.step(a)
+        rec.add(t + 1, eng, out, a)
+        obs = out.obs
+    rec.save("traj_pool", obs0=obs0)
+
+
+def wet_frictions(W):
+    films = (0.0, 0.3, 0.5, 0.8, 1.0, 2.0)
+    out = []
+    for w in range(W):
+        s = SURFACE_ORDER[(w // len(films)) % 3]
+        out.append(assign_friction(s, films[w % len(films)]))
+    return out
+
+
+def traj_wet():
+    from drivegrid.config import load_scene_pool
+    from drivegrid.engine import Engine, SimConfig
+    from drivegrid.world import build_world_batch
+
+    W, M = 12, 16
+    cfg = cfg_of(W, M, seed=5)
+    pool = load_scene_pool(cfg.scene_factory)
+    worlds, assignment = build_world_batch(pool, W, mode="random_fill", seed=5)
+    fr = wet_frictions(W)
+    eng = Engine(worlds, pool, assignment, fr, SimConfig(num_envs=W, num_agents=M, seed=5))
+    rec = Recorder(full_obs_steps=(1, 40, 80))
+    acts = philox_actions(9, 80, W, M)
+    acts[..., 0] = np.abs(acts[..., 0])  # keep agents moving so crash/edge events occur
+    run_actions(eng, acts, rec)
+    rec.save("traj_wet", mu_eff=eng.mu_eff, weather=eng.weather,
+             films=np.array([f.water_film_mm for f in fr]),
+             surfaces=np.array([SURFACE_ORDER.index(f.surface.name) for f in fr]))
+
+
+def traj_bicycle():
+    eng = build_engine(cfg_of(2, 3, mode="bicycle", assignment="fixed", seed=11))
+    rec = Recorder(full_obs_steps=(1, 50))
+    run_actions(eng, philox_actions(4, 50, 2, 3), rec)
+    rec.save("traj_bicycle")
+
+
+def traj_custom_obs():
+    cfg = cfg_of(2, 5, assignment="fixed", seed=19)
+    cfg.obs = ObsConfig(include_weather=False, k_road=20, k_vehicles=3, road_radius=12.5)
+    eng = build_engine(cfg)
+    rec = Recorder(full_obs_steps=range(1, 41))
+    run_actions(eng, philox_actions(6, 40, 2, 5), rec)
+    rec.save("traj_custom_obs")
+
+
+def traj_reset():
+    from drivegrid_bindings import EnvHandle
+    eng = build_engine(cfg_of(2, 4, assignment="fixed", seed=23))
+    env = EnvHandle(eng)
+    acts = philox_actions(8, 30, 2, 4)
+    rec = Recorder(full_obs_steps=(1, 30, 31, 60, 90))
+    for t in range(30):
+        env.step(acts[t].astype(np.float64))
+    # snapshot of the engine output is taken through the recorder below
+    obs_reset = env.reset()
+    spawn_after_reset = eng.spawn_step.copy()
+    step_after_reset = eng.step_count
+    # overlapping starts through teleport_reset (new_starts) -> collision warmup
+    starts = eng.start_xy.copy()
+    starts[0, 1] = starts[0, 0] + np.array([1.0, 0.0])
+    mask = np.zeros((2, 4), dtype=bool)
+    mask[0] = True  # world 1 keeps the reset quirk (spawn_step = 30, age = -30)
+    eng.teleport_reset(mask, new_starts=starts)
+    zeros = np.zeros((60, 2, 4, 3), dtype=np.float32)
+    zeros[:, 1] = acts[:30].repeat(2, axis=0)[:, 1]
+    for t in range(60):
+        out = eng.step(zeros[t].astype(np.float64))
+        rec.add(t + 31, eng, out, zeros[t])
+    rec.save("traj_reset", actions_pre=acts, obs_reset=obs_reset,
+             spawn_after_reset=spawn_after_reset, step_after_reset=np.array(step_after_reset),
+             starts=starts, mask=mask)
+
+
+def event_actions(T, W, M):
+    """Full throttle with a fixed per-agent steer; some agents brake hard
+    mid-run.  Drives agents into goals, road edges and out past the 100 m
+    drift limit so every event type fires."""
+    steer = np.array([0.0, 0.08, -0.08, 0.3, -0.3, 0.02, -0.5, 0.15, 0.0, -0.15, 1.0,
+                      -0.02, 0.6, 0.0, -1.0, 0.04])[:M]
+    acts = np.zeros((T, W, M, 3), dtype=np.float32)
+    acts[..., 0] = 1.0
+    acts[..., 1] = steer[None, None, :] * (1.0 - 0.25 * (np.arange(W)[None, :, None] % 2))
+    brake_rows = (np.arange(M) % 5 == 0)
+    acts[100:160, :, brake_rows, 2] = 1.0
+    acts[100:160, :, brake_rows, 0] = -1.0
+    return acts
+
+
+def traj_events():
+    eng = build_engine(cfg_of(4, 16, seed=31))
+    rec = Recorder(full_obs_steps=(1, 150, 420))
+    run_actions(eng, event_actions(420, 4, 16), rec)
+    rec.save("traj_events")
+
+
+def traj_events_inv():
+    eng = build_engine(cfg_of(4, 16, seed=31, invincible=True))
+    rec = Recorder(full_obs_steps=(1, 150, 420))
+    run_actions(eng, event_actions(420, 4, 16), rec)
+    rec.save("traj_events_inv")
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
+                             "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
+                             "traj_events_inv"]
+    for name in which:
+        globals()[name]()
