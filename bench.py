@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""CASPS benchmark of the fused B200 vehicle step (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): 256 worlds x 16 agents, default
+procedural pool (straight roads + crossroads, seed 42), dry road, dynamic
+single-track backend.  A "step" = device LaneFollower policy on the previous
+observation -> one fused env step (physics x4, 1929-dim obs, rewards,
+events, tail) with the masked teleport reset of finished agents fused in
+(autoreset), so the alive population stays at every valid slot.
+
+  value   CASPS with everything resident in HBM; observations go to a rotating
+          rollout ring larger than L2 (no cache reuse between steps)
+  e2e     the same metric through the reference-facing numpy API
+          (Engine.step with host arrays: H2D actions, D2H obs/rewards/dones/
+          events/info every step, host numpy LaneFollower)
+
+N>1 (torchrun): 4096x16 worlds sharded by contiguous world range (BASELINE
+configs[3]), no per-step communication; episode statistics all-gathered once
+over NCCL after the timed region.  --impl reference times the CPU oracle
+port (numpy restatement of the reference, all host threads).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+L2_BYTES = 126 * 1024 * 1024
+HEADLINE = (256, 16)
+SCALE_TOTAL_WORLDS = 4096
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--worlds", type=int, default=0, help="override total worlds")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--cpu-steps", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def root_config(total_worlds, M=16):
+    from paper_2605_08528_b200 import config as C
+    cfg = C.RootConfig()
+    cfg.env.num_envs = total_worlds
+    cfg.env.num_agents_per_env = M
+    return cfg
+
+
+def shard_inputs(cfg, rank, world_size):
+    """Global host tables (Philox streams over all worlds), sliced to this
+    rank's contiguous world range -- bit-identical to the 1-GPU run."""
+    from paper_2605_08528_b200 import config as C
+    from paper_2605_08528_b200.params import SimConfig
+    from paper_2605_08528_b200.scenes import WorldBatch
+
+    inp = C.build_inputs(cfg)
+    W = cfg.env.num_envs
+    lo, hi = rank * W // world_size, (rank + 1) * W // world_size
+    if world_size == 1:
+        return inp
+    w = inp.worlds
+    sl = slice(lo, hi)
+    inp.worlds = WorldBatch(w.midpoints[sl], w.directions[sl], w.type_codes[sl], w.half_lengths[sl],
+                            w.half_widths[sl], w.mask[sl], w.grid_offsets[sl], w.scenario_ids[sl],
+                            scene_index=w.scene_index[sl], scene_tables=w.scene_tables)
+    inp.assignment = inp.assignment[sl]
+    inp.frictions = inp.frictions[sl]
+    s = inp.sim
+    inp.sim = SimConfig(num_envs=hi - lo, num_agents=s.num_agents, dynamics_mode=s.dynamics_mode,
+                        episode_len=s.episode_len, seed=s.seed, invincible=s.invincible,
+                        bbox_half=s.bbox_half, goal_radius=s.goal_radius)
+    return inp
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes_per_agent(obs_dim: int) -> int:
+    """Bytes one agent-step must move to/from HBM (roofline):
+    obs row write + state read/write + actions + the per-agent outputs and
+    mutable per-agent fields."""
+    obs = 4 * obs_dim                      # f32 observation row (write)
+    state = 2 * 12 * 8                     # 12 f64 fields read + write
+    actions = 3 * 8                        # f64 actions (read)
+    tables = 2 * 8 + 2 * 8 + 4 * 8         # goal, start, length/width/r/d (read)
+    flags = 4 + 4                          # alive, reason, event_seen, valid read; + written
+    spawn = 4                              # spawn_step (read)
+    outputs = 8 + 8 + 7 * 8 + 12 * 8 + 4 + 1 + 1 + 1 + 1  # reward, ttc_min, terms, snapshot, events, done, reason, alive, alive_pre
+    return obs + state + actions + tables + flags + spawn + outputs
+
+
+def run_reference(args, rank, world_size):
+    """CPU oracle port (reference algorithm) on this host's cores."""
+    if rank != 0:
+        return
+    from oracle import OracleEngine
+    from paper_2605_08528_b200 import config as C
+    from paper_2605_08528_b200.policies import LaneFollower
+
+    cores = len(os.sched_getaffinity(0))
+    W = args.worlds or (HEADLINE[0] if world_size == 1 else SCALE_TOTAL_WORLDS)
+    cfg = root_config(W)
+    inp = C.build_inputs(cfg)
+    eng = OracleEngine(**inp.as_kwargs(), num_workers=cores)
+    pol = LaneFollower(obs_config=eng.obs_config)
+    obs = eng.observe()
+    for _ in range(args.warmup):
+        out = eng.step(pol(obs))
+        eng.teleport_reset(out.dones)
+        obs = out.obs
+    ticks = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ticks += int(eng.alive.sum())
+        out = eng.step(pol(obs))
+        eng.teleport_reset(out.dones)
+        obs = out.obs
+    wall = time.perf_counter() - t0
+    v = ticks / wall
+    line = {
+        "impl": "reference", "metric": "CASPS", "value": v, "unit": "agent-steps/s",
+        "n_gpus": world_size, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+        "scaling": "weak" if world_size == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"{W}x16 default procedural pool, LaneFollower, autoreset",
+                                        "worlds": W, "agents": 16},
+        "cpu_baseline": {"value": v, "unit": "agent-steps/s", "cores": cores, "kind": "port",
+                         "sample": f"{W}x16, {args.steps} steps after {args.warmup} warmup, numpy {np.__version__}"},
+        "e2e": {"value": v, "unit": "agent-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(steps):
+    from oracle import OracleEngine
+    from paper_2605_08528_b200 import config as C
+    from paper_2605_08528_b200.policies import LaneFollower
+
+    cores = len(os.sched_getaffinity(0))
+    inp = C.build_inputs(root_config(HEADLINE[0]))
+    eng = OracleEngine(**inp.as_kwargs(), num_workers=cores)
+    pol = LaneFollower(obs_config=eng.obs_config)
+    obs = eng.observe()
+    for _ in range(2):
+        out = eng.step(pol(obs))
+        eng.teleport_reset(out.dones)
+        obs = out.obs
+    ticks, t0 = 0, time.perf_counter()
+    for _ in range(steps):
+        ticks += int(eng.alive.sum())
+        out = eng.step(pol(obs))
+        eng.teleport_reset(out.dones)
+        obs = out.obs
+    wall = time.perf_counter() - t0
+    return {"value": ticks / wall, "unit": "agent-steps/s", "cores": cores, "kind": "port",
+            "sample": f"256x16 default pool, LaneFollower+autoreset, {steps} steps after 2 warmup "
+                      f"({wall:.1f} s), oracle/ numpy port, numpy {np.__version__}"}
+
+
+def main():
+    args = parse()
+    rank, local_rank, world_size = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world_size)
+        return
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world_size > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2605_08528_b200.engine import Engine
+
+    W_total = args.worlds or (HEADLINE[0] if world_size == 1 else SCALE_TOTAL_WORLDS)
+    inp = shard_inputs(root_config(W_total), rank, world_size)
+    eng = Engine(**inp.as_kwargs(), device=dev)
+    W, M, D = eng.W, eng.M, eng.obs_config.obs_dim
+    obs_bytes = W * M * D * 4
+    ring = max(2, math.ceil(2 * L2_BYTES / obs_bytes))
+    obs_ring = torch.empty((ring, W, M, D), dtype=torch.float32, device=dev)
+    bufs = [eng.new_step_buffers(obs_ring[i]) for i in range(ring)]
+    acts = torch.zeros((W, M, 3), dtype=torch.float64, device=dev)
+    eng.observe(out=obs_ring[ring - 1], as_numpy=False)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step(i):
+        eng.lane_follower(obs_ring[(i - 1) % ring], out=acts)
+        eng.launch_step(acts, bufs[i % ring], autoreset=True)
+
+    # warm-up (untimed)
+    for i in range(args.warmup):
+        one_step(i)
+    torch.cuda.synchronize()
+    valid_count = int(eng.valid.sum())
+    assert int(eng.alive.sum()) == valid_count
+
+    # timed region: K steps, kernel-level events around every fused step launch
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = eng.launches
+    if world_size > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            j = args.warmup + i
+            eng.lane_follower(obs_ring[(j - 1) % ring], out=acts)
+            ev0[i].record(stream)
+            eng.launch_step(acts, bufs[j % ring], autoreset=True)
+            ev1[i].record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    launches = eng.launches - launches0
+    total_ms = start.elapsed_time(stop)
+    if world_size > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    kern_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    kern_avg = sum(kern_ms) / len(kern_ms)
+    assert int(eng.alive.sum()) == valid_count, "autoreset must keep every valid slot alive"
+    agent_ticks = valid_count * args.steps * world_size  # alive before every step (asserted)
+    value = agent_ticks / (total_ms / 1e3)
+
+    # episode statistics: the only cross-rank traffic (NCCL all-gather, once)
+    stats = torch.tensor([valid_count, args.steps], dtype=torch.float64, device=dev)
+    if world_size > 1:
+        gathered = [torch.empty_like(stats) for _ in range(world_size)]
+        dist.all_gather(gathered, stats)
+
+    if rank == 0:
+        peak, peak_src = measured_peaks()
+        per_agent = algorithmic_bytes_per_agent(D)
+        achieved = per_agent * W * M / (kern_avg / 1e3) / 1e9
+        line = {
+            "metric": "CASPS", "value": value, "unit": "agent-steps/s", "n_gpus": world_size,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak" if world_size == 1 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{W_total}x16 default procedural pool (seed 42), dry, dynamic, "
+                                   f"device LaneFollower, fused autoreset",
+                       "worlds": W_total, "agents": M, "obs_dim": D,
+                       "l2": f"obs rotate through a {ring}-slot rollout ring ({ring * obs_bytes / 2**20:.0f} MiB > L2)",
+                       "parallelism": f"world-shard x{world_size}"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "bytes_per_agent_step": per_agent, "kernel_ms": kern_avg,
+                         "peak_source": peak_src},
+            "gpu_launches": launches,
+        }
+        line["clocks"] = clk.summary()
+        # e2e through the numpy API
+        e2e_steps = args.e2e_steps or max(10, min(args.steps, 50))
+        line["e2e"] = e2e_numpy(eng, e2e_steps)
+        if not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_steps or 40)
+        print(json.dumps(line), flush=True)
+    if world_size > 1:
+        dist.destroy_process_group()
+
+
+def e2e_numpy(eng, steps):
+    """The reference-facing call: numpy actions in, numpy StepOutput out."""
+    import torch
+    from paper_2605_08528_b200.policies import LaneFollower
+
+    pol = LaneFollower(obs_config=eng.obs_config)
+    obs = eng.observe()
+    for _ in range(3):
+        out = eng.step(pol(obs), autoreset=True)
+        obs = out.obs
+    torch.cuda.synchronize()
+    ticks = 0
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ticks += int(eng.valid.sum())
+        out = eng.step(pol(obs), autoreset=True)
+        obs = out.obs
+    wall = time.perf_counter() - t0
+    W, M, D = eng.W, eng.M, eng.obs_config.obs_dim
+    _, aux_bytes = eng._aux_layout()
+    return {"value": ticks / wall, "unit": "agent-steps/s", "h2d_bytes_per_step": W * M * 3 * 8,
+            "d2h_bytes_per_step": W * M * D * 4 + aux_bytes, "steps": steps,
+            "api": "Engine.step(numpy) with fused autoreset + host numpy LaneFollower"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,175 @@
+/*
+ * drivegrid_b200 -- C ABI of the B200 (sm_100a) batched vehicle step.
+ *
+ * The reference (/root/reference/pkg) is a Python package with no native
+ * layer; the entry points below are what its engine/binding surface binds to
+ * when the step runs on the GPU.  Each function names the reference interface
+ * it replaces.  Plain C types only: no torch, no C++ in the signatures.
+ *
+ * Memory model: every device buffer in DgEngineDesc / DgStepIO is allocated by
+ * the caller (the Python host uses torch tensors) and BORROWED by the engine
+ * for its lifetime.  The library allocates nothing on the device.  All calls
+ * are asynchronous on the given stream unless stated otherwise; calls on one
+ * engine must be serialised by the caller (the reference is single-writer,
+ * SPEC.md:377-379).
+ *
+ * Layouts (W worlds, M agents per world, row-major, C order):
+ *   state      f64 [12][W][M]   field order of STATE_FIELDS (vehicle.py:124-142),
+ *                               global coordinates exactly as the reference
+ *   obs        f32 [W][M][D]    D = ego_dim + 5*k_road + 7*k_vehicles
+ *   actions    f32|f64 [W][M][3]
+ *   events     u8  [W][M][4]    goal, collision, crash, lane_forbidden (one-hot)
+ *   terms      f64 [7][W][M]    progress, lane, offroad, idle, ttc_vehicle, ttc_edge, total
+ */
+#ifndef DRIVEGRID_B200_H
+#define DRIVEGRID_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DG_ABI_VERSION 1
+#define DG_NUM_STATE 12
+#define DG_NUM_TERMS 7
+#define DG_NO_ERROR 0x7fffffff
+
+/* status codes (Python maps them to the reference's exception types) */
+enum {
+    DG_OK = 0,
+    DG_EINVAL = 1,       /* bad argument / shape  -> ValueError                */
+    DG_ENONFINITE = 2,   /* non-finite action      -> ValueError("non-finite action for world w agent m") */
+    DG_ECUDA = 3,        /* CUDA runtime failure   -> RuntimeError             */
+    DG_ENOSUPPORT = 4    /* configuration outside the kernel's limits          */
+};
+
+/* Integer dimensions and switches (engine.py:41-67, observation.py:18-35). */
+typedef struct DgDims {
+    int32_t W, M;
+    int32_t obs_dim, ego_dim, k_road, k_vehicles, include_weather;
+    int32_t dynamic;          /* 1 = 120 Hz single-track, 0 = 30 Hz bicycle */
+    int32_t decimation;
+    int32_t episode_len;
+    int32_t invincible;
+    int32_t collision_warmup;
+    int32_t num_scenes;
+    int32_t max_scene_bytes;  /* largest per-scene geometry blob, bytes      */
+    int32_t max_segments;     /* largest P over scenes                       */
+    int32_t pad_;
+} DgDims;
+
+/* Float64 scalars, precomputed on the host with the reference's expression
+ * order (vehicle.py:237-336, observation.py, rewards.py:37-63). */
+typedef struct DgConsts {
+    double physics_dt, control_dt;
+    double kp_steer, kd_steer, theta_max, tau_steer_max, steer_inertia, steer_limit;
+    double a_f, b_r, tau_drive_max, tau_brake_front, tau_brake_rear, wheel_radius;
+    double cornering_stiffness, f_z, chassis_mass, lambda_lat, lambda_yaw, yaw_inertia;
+    double i_axle, wheelbase;
+    double bic_a_max, bic_b_max, bic_c_roll, bic_steer_max;
+    double road_radius, road_radius_sq, bbox_half, speed_norm, type_norm, ttc_max;
+    double goal_radius, goal_weight, collision_weight, crash_weight, crash_drift_limit;
+    double lane_forbidden_weight, progress_weight, progress_clamp, lane_weight, lane_sigma;
+    double lane_heading_weight, lane_heading_base, offroad_weight, offroad_lat_limit;
+    double offroad_dist_limit, idle_weight, idle_speed, ttc_vehicle_alpha, ttc_vehicle_pmax;
+    double ttc_edge_alpha, ttc_edge_pmax, ttc_floor, edge_range, crash_speed_limit, offstage_x;
+} DgConsts;
+
+/* Engine description (replaces drivegrid.engine.Engine.__init__ tables,
+ * engine.py:151-230).  Scene geometry is de-duplicated: worlds that share a
+ * scene share one blob.  Per-scene blob, 16-byte aligned sections, local
+ * coordinates:  f64 mid_x[P], mid_y[P], dir_x[P], dir_y[P], half_len[P],
+ * half_wid[P]; i32 type[P]; i32 lane_idx[KL]; i32 edge_idx[KE].
+ * scene_meta[s] = {byte_offset, byte_size, P, KL, KE, 0, 0, 0} (int64). */
+typedef struct DgEngineDesc {
+    DgDims dims;
+    DgConsts k;
+    const uint8_t* scene_blob;
+    const int64_t* scene_meta;
+    const int32_t* scene_of_world;  /* [W]        */
+    const double* grid_offset;      /* [W][2]     */
+    const double* mu_eff;           /* [W]        */
+    const double* weather;          /* [W][4]     */
+    const uint8_t* valid;           /* [W][M]     */
+    const double* length;           /* [W][M]     */
+    const double* width;            /* [W][M]     */
+    const double* r_hull;           /* [W][M]     */
+    const double* d_hull;           /* [W][M]     */
+    double* state;                  /* [12][W][M] */
+    uint8_t* alive;                 /* [W][M]     */
+    int8_t* reason;                 /* [W][M]     */
+    uint8_t* event_seen;            /* [W][M] bit k = EVENT_TYPES[k] latched */
+    int32_t* spawn_step;            /* [W][M]     */
+    int32_t* step_count;            /* [W]        */
+    double* start_xy;               /* [W][M][2]  */
+    double* goal_xy;                /* [W][M][2]  */
+    double* start_yaw;              /* [W][M]     */
+    int32_t* error_word;            /* [1] DG_NO_ERROR or first bad flat action index */
+} DgEngineDesc;
+
+/* Outputs of one control tick (StepOutput, engine.py:70-76, 397-406).
+ * Optional pointers may be NULL. */
+typedef struct DgStepIO {
+    const void* actions;        /* [W][M][3]                                  */
+    int32_t actions_f64;        /* 0: float32 actions, 1: float64             */
+    int32_t autoreset;          /* 1: teleport_reset(dones) fused after the tail */
+    float* obs;                 /* [W][M][D]   required                       */
+    double* rewards;            /* [W][M]      required                       */
+    uint8_t* dones;             /* [W][M]      required                       */
+    uint8_t* events;            /* [W][M][4]   required                       */
+    int8_t* reason_out;         /* [W][M]      info["reason"]                 */
+    uint8_t* alive_out;         /* [W][M]      info["alive"] (before autoreset) */
+    uint8_t* alive_pre_out;     /* [W][M]      info["alive_pre"]              */
+    double* ttc_min_out;        /* [W][M]      info["ttc_min"]                */
+    double* terms_out;          /* [7][W][M]   info["reward_terms"]           */
+    double* snapshot_out;       /* [12][W][M]  info["state"] (pre-park)       */
+} DgStepIO;
+
+typedef struct dg_engine dg_engine;
+
+/* Engine lifetime (Engine.__init__ / garbage collection). */
+int dg_create(const DgEngineDesc* desc, dg_engine** out);
+int dg_destroy(dg_engine* eng);
+
+/* One 30 Hz control tick for every world: Engine.step (engine.py:334-406),
+ * EnvHandle.step (env.py:48-65).  Worlds whose actions contain a non-finite
+ * value are not stepped; their first bad flat index is min-reduced into
+ * error_word (engine.py:286-295 raises before mutating; the host obtains
+ * that exact behaviour with dg_check_actions + dg_read_error first). */
+int dg_step(dg_engine* eng, const DgStepIO* io, void* stream);
+
+/* Observation of the current state without stepping: Engine.observe
+ * (engine.py:297-330). */
+int dg_observe(dg_engine* eng, float* obs, double* ttc_min_out, void* stream);
+
+/* Masked teleport reset: Engine.teleport_reset (engine.py:599-619).
+ * mask [W][M] u8 (NULL = every valid slot); optional new starts/goals
+ * [W][M][2] and headings [W][M] (device, global coordinates). */
+int dg_reset(dg_engine* eng, const uint8_t* mask, const double* new_starts,
+             const double* new_goals, const double* new_headings, void* stream);
+
+/* step_count assignment (EnvHandle.reset sets it to 0, env.py:42). */
+int dg_set_step_count(dg_engine* eng, int32_t value, void* stream);
+
+/* Finiteness scan of an action batch into error_word (engine.py:291-294). */
+int dg_check_actions(dg_engine* eng, const void* actions, int32_t actions_f64, void* stream);
+
+/* Synchronising read of error_word; resets it.  *flat_index = -1 if clean. */
+int dg_read_error(dg_engine* eng, int32_t* flat_index, void* stream);
+
+/* Device LaneFollower (policies.py:21-43): obs [W][M][D] -> float64 actions
+ * [W][M][3], the same values the host numpy policy produces. */
+int dg_lane_follower(dg_engine* eng, const float* obs, double* actions, double steer_gain,
+                     double throttle, void* stream);
+
+/* Kernel launches issued by the last dg_step/dg_observe/dg_reset call. */
+int dg_launch_count(dg_engine* eng);
+
+const char* dg_last_error(void);
+int dg_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DRIVEGRID_B200_H */

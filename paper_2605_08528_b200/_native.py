@@ -1,0 +1,147 @@
+"""ctypes binding of ``libdrivegrid_b200.so`` (C ABI: ``include/drivegrid_b200.h``).
+
+This is the binding a maintainer of the reference would add: plain ctypes
+over the extern "C" entry points, no torch types in any signature.  The
+library is built in-tree by ``build_native()`` (nvcc, sm_100a); a missing or
+stale library is a hard error -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as ct
+import os
+import subprocess
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+LIB_PATH = PKG / "libdrivegrid_b200.so"
+SOURCES = [PKG / "csrc" / "drivegrid_b200.cu"]
+HEADER = ROOT / "include" / "drivegrid_b200.h"
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-fmad=false", "-Xcompiler", "-fPIC", "-shared"]
+
+DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
+DG_NO_ERROR = 0x7FFFFFFF
+ABI_VERSION = 1
+
+
+class DgDims(ct.Structure):
+    _fields_ = [(n, ct.c_int32) for n in (
+        "W", "M", "obs_dim", "ego_dim", "k_road", "k_vehicles", "include_weather", "dynamic",
+        "decimation", "episode_len", "invincible", "collision_warmup", "num_scenes",
+        "max_scene_bytes", "max_segments", "pad_")]
+
+
+CONST_FIELDS = (
+    "physics_dt", "control_dt",
+    "kp_steer", "kd_steer", "theta_max", "tau_steer_max", "steer_inertia", "steer_limit",
+    "a_f", "b_r", "tau_drive_max", "tau_brake_front", "tau_brake_rear", "wheel_radius",
+    "cornering_stiffness", "f_z", "chassis_mass", "lambda_lat", "lambda_yaw", "yaw_inertia",
+    "i_axle", "wheelbase",
+    "bic_a_max", "bic_b_max", "bic_c_roll", "bic_steer_max",
+    "road_radius", "road_radius_sq", "bbox_half", "speed_norm", "type_norm", "ttc_max",
+    "goal_radius", "goal_weight", "collision_weight", "crash_weight", "crash_drift_limit",
+    "lane_forbidden_weight", "progress_weight", "progress_clamp", "lane_weight", "lane_sigma",
+    "lane_heading_weight", "lane_heading_base", "offroad_weight", "offroad_lat_limit",
+    "offroad_dist_limit", "idle_weight", "idle_speed", "ttc_vehicle_alpha", "ttc_vehicle_pmax",
+    "ttc_edge_alpha", "ttc_edge_pmax", "ttc_floor", "edge_range", "crash_speed_limit", "offstage_x",
+)
+
+
+class DgConsts(ct.Structure):
+    _fields_ = [(n, ct.c_double) for n in CONST_FIELDS]
+
+
+_P = ct.c_void_p
+
+
+class DgEngineDesc(ct.Structure):
+    _fields_ = [("dims", DgDims), ("k", DgConsts)] + [(n, _P) for n in (
+        "scene_blob", "scene_meta", "scene_of_world", "grid_offset", "mu_eff", "weather", "valid",
+        "length", "width", "r_hull", "d_hull", "state", "alive", "reason", "event_seen",
+        "spawn_step", "step_count", "start_xy", "goal_xy", "start_yaw", "error_word")]
+
+
+class DgStepIO(ct.Structure):
+    _fields_ = [("actions", _P), ("actions_f64", ct.c_int32), ("autoreset", ct.c_int32)] + [
+        (n, _P) for n in ("obs", "rewards", "dones", "events", "reason_out", "alive_out",
+                          "alive_pre_out", "ttc_min_out", "terms_out", "snapshot_out")]
+
+
+# exported symbol -> (restype, argtypes)
+SIGNATURES = {
+    "dg_abi_version": (ct.c_int, []),
+    "dg_last_error": (ct.c_char_p, []),
+    "dg_create": (ct.c_int, [ct.POINTER(DgEngineDesc), ct.POINTER(_P)]),
+    "dg_destroy": (ct.c_int, [_P]),
+    "dg_step": (ct.c_int, [_P, ct.POINTER(DgStepIO), _P]),
+    "dg_observe": (ct.c_int, [_P, _P, _P, _P]),
+    "dg_reset": (ct.c_int, [_P, _P, _P, _P, _P, _P]),
+    "dg_set_step_count": (ct.c_int, [_P, ct.c_int32, _P]),
+    "dg_check_actions": (ct.c_int, [_P, _P, ct.c_int32, _P]),
+    "dg_read_error": (ct.c_int, [_P, ct.POINTER(ct.c_int32), _P]),
+    "dg_lane_follower": (ct.c_int, [_P, _P, _P, ct.c_double, ct.c_double, _P]),
+    "dg_launch_count": (ct.c_int, [_P]),
+}
+
+
+def _stale() -> bool:
+    if not LIB_PATH.exists():
+        return True
+    t = LIB_PATH.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in SOURCES + [HEADER] if p.exists())
+
+
+def build_native(force: bool = False, verbose: bool = False) -> Path:
+    """Compile the CUDA library in-tree for sm_100a (works without a GPU)."""
+    if not force and not _stale():
+        return LIB_PATH
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(LIB_PATH) + ".tmp",
+           *map(str, SOURCES)]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{proc.stderr}")
+    os.replace(str(LIB_PATH) + ".tmp", LIB_PATH)
+    if verbose:
+        print(proc.stderr)
+    return LIB_PATH
+
+
+_LIB = None
+
+
+def load_library(build_if_missing: bool = True) -> ct.CDLL:
+    """The native library; raises if it cannot be built or loaded."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if build_if_missing and _stale():
+        build_native()
+    if not LIB_PATH.exists():
+        raise RuntimeError(f"{LIB_PATH} missing: run paper_2605_08528_b200._native.build_native()")
+    lib = ct.CDLL(str(LIB_PATH))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.dg_abi_version() != ABI_VERSION:
+        raise RuntimeError("libdrivegrid_b200.so ABI version mismatch; rebuild it")
+    _LIB = lib
+    return lib
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def check(lib, status: int, what: str) -> None:
+    if status == DG_OK:
+        return
+    msg = (lib.dg_last_error() or b"").decode()
+    if status == DG_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    raise NativeError(f"{what} failed (status {status}): {msg}")

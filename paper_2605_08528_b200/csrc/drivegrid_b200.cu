@@ -1,0 +1,1065 @@
+// drivegrid_b200.cu -- the batched multi-world, multi-agent vehicle step on
+// B200 (sm_100a): one fused kernel per 30 Hz control tick.
+//
+// Mapping: one CTA per world, one warp per agent slot (M <= 16 warps).
+//   phase 0  action finiteness scan for the world (block vote)           engine.py:286-295
+//   phase 1  warp 0, lane m: agent m state -> registers, decode, 4x
+//            single-track substeps (or 1 bicycle step), alive mask       engine.py:410-421,
+//                                                                        vehicle.py:162-336
+//            meanwhile: TMA bulk copy of the world's scene geometry
+//            (cp.async.bulk, mbarrier complete_tx) into shared memory
+//   phase 2  warp m: road k-select by ballot compaction, neighbours with
+//            stable rank + swept 3x3-circle TTC, ego block            observation.py:51-293
+//            nearest lane (warp argmin), edge TTC, edge OBB test,
+//            hull contact (warp vote), dense terms, events, priority  rewards.py:78-268,
+//                                                                        engine.py:472-509
+//            tail: timeout, park, alive (+ optional fused autoreset)  engine.py:370-406
+//            the agent's 1929-float observation row, streamed with
+//            16-byte st.global.cs from a lane-parallel generator
+//
+// Numerics: float64 throughout in the reference's global coordinates, and
+// the translation unit is compiled with -fmad=false: every a*b+c rounds twice
+// exactly as numpy evaluates it, so sqrt/div/mul/add results and therefore
+// every threshold decision (d2 <= r^2, d2 < (ra+rb)^2, dist <= 3, ...) are
+// bit-identical to the reference.  Only libm transcendentals (sin, cos,
+// atan2, exp, tan) may differ from the host's in the last ulp.
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "drivegrid_b200.h"
+
+namespace {
+
+constexpr int kMaxAgents = 16;
+constexpr unsigned kFull = 0xffffffffu;
+
+enum StateField {
+    SX = 0, SY, SYAW, SVX, SVY, SOM, SANG, SRATE, SWF, SWR, SBF, SBR
+};
+
+struct KArgs {
+    DgDims d;
+    DgConsts k;
+    // engine tables
+    const uint8_t* scene_blob;
+    const int64_t* scene_meta;
+    const int32_t* scene_of_world;
+    const double* grid_offset;
+    const double* mu_eff;
+    const double* weather;
+    const uint8_t* valid;
+    const double* length;
+    const double* width;
+    const double* r_hull;
+    const double* d_hull;
+    double* state;
+    uint8_t* alive;
+    int8_t* reason;
+    uint8_t* event_seen;
+    int32_t* spawn_step;
+    int32_t* step_count;
+    double* start_xy;
+    double* goal_xy;
+    double* start_yaw;
+    int32_t* error_word;
+    // step io
+    const void* actions;
+    int32_t actions_f64;
+    int32_t autoreset;
+    float* obs;
+    double* rewards;
+    uint8_t* dones;
+    uint8_t* events;
+    int8_t* reason_out;
+    uint8_t* alive_out;
+    uint8_t* alive_pre_out;
+    double* ttc_min_out;
+    double* terms_out;
+    double* snapshot_out;
+    int32_t take_road;   // min(k_road, max_segments) = candidate-list capacity
+    int32_t take_veh;    // min(k_vehicles, M)
+};
+
+// ----------------------------------------------------------------- numpy-semantics helpers
+// numpy maximum/minimum propagate NaN from either side; clip is min(max()).
+__device__ __forceinline__ double np_max(double a, double b) {
+    if (a != a) return a;
+    if (b != b) return b;
+    return a > b ? a : b;
+}
+__device__ __forceinline__ double np_min(double a, double b) {
+    if (a != a) return a;
+    if (b != b) return b;
+    return a < b ? a : b;
+}
+__device__ __forceinline__ double np_clip(double x, double lo, double hi) {
+    return np_min(np_max(x, lo), hi);
+}
+__device__ __forceinline__ double np_sign(double x) {
+    return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : (x == 0.0 ? 0.0 : x));
+}
+__device__ __forceinline__ bool finite(double x) { return isfinite(x); }
+
+__device__ __forceinline__ double shfl_d(double v, int src) {
+    return __shfl_sync(kFull, v, src);
+}
+__device__ __forceinline__ double warp_min(double v) {
+    for (int o = 16; o > 0; o >>= 1) v = np_min(v, __shfl_xor_sync(kFull, v, o));
+    return v;
+}
+
+// ----------------------------------------------------------------- shared-memory layout
+struct AgentSm {
+    double st[DG_NUM_STATE];  // post-physics state
+    double px0, py0;          // pre-physics position (progress term)
+    double c, s;              // cos/sin(yaw)
+    double vwx, vwy;          // world-frame velocity
+    double r, d, len, wid;    // hull radius/offset, length, width
+    double hx[3], hy[3];      // hull circle centres
+    double gx, gy, sx, sy;    // goal, start (global)
+    int alive, valid, reason, seen, spawn;
+    int pad_;
+};
+
+struct SceneView {
+    const double* mx;
+    const double* my;
+    const double* dx;
+    const double* dy;
+    const double* hl;
+    const double* hw;
+    const int32_t* type;
+    const int32_t* lane;
+    const int32_t* edge;
+    int P, KL, KE;
+};
+
+__host__ __device__ __forceinline__ int64_t align16(int64_t x) { return (x + 15) & ~int64_t(15); }
+
+__device__ __forceinline__ SceneView scene_view(uint8_t* base, int P, int KL, int KE) {
+    SceneView v;
+    int64_t o = 0;
+    const int64_t f8 = align16(int64_t(P) * 8);
+    v.mx = reinterpret_cast<double*>(base + o); o += f8;
+    v.my = reinterpret_cast<double*>(base + o); o += f8;
+    v.dx = reinterpret_cast<double*>(base + o); o += f8;
+    v.dy = reinterpret_cast<double*>(base + o); o += f8;
+    v.hl = reinterpret_cast<double*>(base + o); o += f8;
+    v.hw = reinterpret_cast<double*>(base + o); o += f8;
+    v.type = reinterpret_cast<int32_t*>(base + o); o += align16(int64_t(P) * 4);
+    v.lane = reinterpret_cast<int32_t*>(base + o); o += align16(int64_t(KL) * 4);
+    v.edge = reinterpret_cast<int32_t*>(base + o);
+    v.P = P; v.KL = KL; v.KE = KE;
+    return v;
+}
+
+// ----------------------------------------------------------------- TMA bulk copy helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}"
+        ::"r"(smem_addr(bar)), "r"(parity) : "memory");
+}
+
+// ----------------------------------------------------------------- vehicle dynamics
+struct Act {
+    double thr, steer, brk;
+};
+
+// One 120 Hz substep of the single-track model (vehicle.py:237-336), with the
+// reference's expression order; x[] is the 12-field state.
+__device__ __forceinline__ void substep_dynamic(double* x, const Act a, double cap, const DgConsts& k) {
+    double tau_s = np_clip(k.kp_steer * (k.theta_max * a.steer - x[SANG]) - k.kd_steer * x[SRATE],
+                           -k.tau_steer_max, k.tau_steer_max);
+    double rate = x[SRATE] + (tau_s / k.steer_inertia) * k.physics_dt;
+    double ang = x[SANG] + rate * k.physics_dt;
+    double ang_c = np_clip(ang, -k.steer_limit, k.steer_limit);
+    rate = (ang_c == ang) ? rate : 0.0;
+    ang = ang_c;
+
+    const double vx = x[SVX], vy = x[SVY], om = x[SOM];
+    // brake torques with the wheel-sign latch (vehicle.py:182-191)
+    double sf = (fabs(x[SWF]) >= 1e-4) ? np_sign(x[SWF]) : x[SBF];
+    double sr = (fabs(x[SWR]) >= 1e-4) ? np_sign(x[SWR]) : x[SBR];
+    double tbf = -sf * a.brk * k.tau_brake_front;
+    double tbr = -sr * a.brk * k.tau_brake_rear;
+    double t_front = 2.0 * (k.tau_drive_max * a.thr + tbf);
+    double t_rear = 2.0 * tbr;
+    double fxf0 = t_front / k.wheel_radius;
+    double fxr0 = t_rear / k.wheel_radius;
+    double den = np_max(vx, 0.5);
+    double fyf0 = k.cornering_stiffness * (ang - (vy + k.a_f * om) / den);
+    double fyr0 = k.cornering_stiffness * (-(vy - k.b_r * om) / den);
+
+    double nf = sqrt(fxf0 * fxf0 + fyf0 * fyf0);
+    double nr = sqrt(fxr0 * fxr0 + fyr0 * fyr0);
+    bool satf = nf > cap, satr = nr > cap;
+    double kf = satf ? cap / np_max(nf, 1e-12) : 1.0;
+    double kr = satr ? cap / np_max(nr, 1e-12) : 1.0;
+    double fxf = fxf0 * kf, fyf = fyf0 * kf;
+    double fxr = fxr0 * kr, fyr = fyr0 * kr;
+
+    double sd, cd;
+    sincos(ang, &sd, &cd);
+    const double m = k.chassis_mass;
+    double ax = (fxf * cd - fyf * sd + fxr) / m + vy * om;
+    double ay = (fyf * cd + fxf * sd + fyr - k.lambda_lat * vy) / m - vx * om;
+    double omd = (k.a_f * (fyf * cd + fxf * sd) - k.b_r * fyr - k.lambda_yaw * om) / k.yaw_inertia;
+    double vx1 = vx + ax * k.physics_dt;
+    double vy1 = vy + ay * k.physics_dt;
+    double om1 = om + omd * k.physics_dt;
+    if (a.brk > 0.0 && vx >= 0.0 && vx1 < 0.0) vx1 = 0.0;
+
+    double sy, cy;
+    sincos(x[SYAW], &sy, &cy);
+    x[SX] = x[SX] + (vx1 * cy - vy1 * sy) * k.physics_dt;
+    x[SY] = x[SY] + (vx1 * sy + vy1 * cy) * k.physics_dt;
+    x[SYAW] = x[SYAW] + om1 * k.physics_dt;
+
+    double roll_f = ((vy1 + k.a_f * om1) * sd + vx1 * cd) / k.wheel_radius;
+    double roll_r = vx1 / k.wheel_radius;
+    double spin_f = x[SWF] + (t_front - fxf * k.wheel_radius) / k.i_axle * k.physics_dt;
+    double spin_r = x[SWR] + (t_rear - fxr * k.wheel_radius) / k.i_axle * k.physics_dt;
+    if (a.brk > 0.0 && spin_f * sf < 0.0) spin_f = 0.0;
+    if (a.brk > 0.0 && spin_r * sr < 0.0) spin_r = 0.0;
+    x[SWF] = np_clip(satf ? spin_f : roll_f, -200.0, 200.0);
+    x[SWR] = np_clip(satr ? spin_r : roll_r, -200.0, 200.0);
+    x[SVX] = vx1;
+    x[SVY] = vy1;
+    x[SOM] = om1;
+    x[SANG] = ang;
+    x[SRATE] = rate;
+    x[SBF] = sf;
+    x[SBR] = sr;
+}
+
+// One 30 Hz kinematic bicycle tick (vehicle.py:208-232).
+__device__ __forceinline__ void step_bicycle(double* x, const Act a, const DgConsts& k) {
+    double delta = a.steer * k.bic_steer_max;
+    double v = x[SVX];
+    double v1 = np_max(v + (a.thr * k.bic_a_max - a.brk * k.bic_b_max - np_sign(v) * k.bic_c_roll) * k.control_dt, 0.0);
+    double yaw = x[SYAW];
+    double rate = v1 * tan(delta) / k.wheelbase;
+    double sy, cy;
+    sincos(yaw, &sy, &cy);
+    x[SX] = x[SX] + v1 * cy * k.control_dt;
+    x[SY] = x[SY] + v1 * sy * k.control_dt;
+    x[SYAW] = yaw + rate * k.control_dt;
+    x[SVX] = v1;
+    x[SVY] = 0.0;
+    x[SOM] = rate;
+    x[SANG] = delta;
+    x[SRATE] = 0.0;
+    x[SWF] = v1 / k.wheel_radius;
+    x[SWR] = v1 / k.wheel_radius;
+}
+
+// ----------------------------------------------------------------- swept-circle TTC
+// Minimum over the 3x3 circle pairs of the closest-approach time of agent B
+// relative to ego A (observation.py:128-181).  Bit-exact restatement with one
+// division per pair set: all nine pairs share a = |u|^2, and x -> fl(x / 2a)
+// is monotone, so min_i fl(n_i / 2a) == fl(min_i n_i / 2a).
+__device__ __forceinline__ double swept_ttc(double dx, double dy, double ux, double uy,
+                                            double ce, double se, double de,
+                                            double cn, double sn, double dn,
+                                            double rsum, double tmax) {
+    const double a = ux * ux + uy * uy;
+    const bool moving = a >= 1e-12;
+    const double rr = rsum * rsum;
+    const double offs[3] = {-1.0, 0.0, 1.0};
+    bool any_hit = false, any_overlap = false;
+    double nmin = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double oe = offs[i] * de;
+        const double oec = oe * ce, oes = oe * se;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const double on = offs[j] * dn;
+            const double qx = dx + on * cn - oec;
+            const double qy = dy + on * sn - oes;
+            const double b = 2.0 * (qx * ux + qy * uy);
+            const double c = qx * qx + qy * qy - rr;
+            if (moving) {
+                const double disc = b * b - 4.0 * a * c;
+                if (disc >= 0.0) {
+                    const double root = sqrt(disc);
+                    if (-b + root >= 0.0) {           // t_exit >= 0  (2a > 0)
+                        const double n = -b - root;    // numerator of t_enter
+                        nmin = any_hit ? np_min(nmin, n) : n;
+                        any_hit = true;
+                    }
+                }
+            } else if (c < 0.0) {
+                any_overlap = true;
+            }
+        }
+    }
+    double t;
+    if (moving) {
+        t = any_hit ? np_min(np_max(nmin / (2.0 * a), 0.0), tmax) : tmax;
+    } else {
+        t = any_overlap ? 0.0 : tmax;
+    }
+    // neighbours behind the ego carry no threat
+    return (ce * dx + se * dy < 0.0) ? tmax : t;
+}
+
+// ----------------------------------------------------------------- observation row
+struct RowCtx {
+    const float* ego;      // [ego_dim]
+    const float* nb;       // [take_veh][7]
+    const uint16_t* cand;  // [ncand]
+    SceneView g;
+    double px, py, c, s;
+    int ncand, nnb, ego_dim, road_end;
+    double road_radius, type_norm;
+};
+
+__device__ __forceinline__ float road_feature(const RowCtx& r, int p, int f) {
+    if (f == 2) return __double2float_rn(double(r.g.type[p]) / r.type_norm);
+    double val;
+    if (f < 2) {
+        const double dx = r.g.mx[p] - r.px, dy = r.g.my[p] - r.py;
+        val = (f == 0 ? r.c * dx + r.s * dy : -r.s * dx + r.c * dy) / r.road_radius;
+    } else {
+        const double ux = r.g.dx[p], uy = r.g.dy[p];
+        val = (f == 3) ? r.c * ux + r.s * uy : -r.s * ux + r.c * uy;
+    }
+    return __double2float_rn(val);
+}
+
+__device__ __forceinline__ float obs_value(const RowCtx& r, int e) {
+    if (e < r.ego_dim) return r.ego[e];
+    if (e < r.road_end) {
+        const int q = e - r.ego_dim;
+        const int slot = q / 5;
+        if (slot >= r.ncand) return 0.0f;
+        return road_feature(r, r.cand[slot], q - slot * 5);
+    }
+    const int q = e - r.road_end;
+    const int slot = q / 7;
+    if (slot >= r.nnb) return 0.0f;
+    return r.nb[q];
+}
+
+__device__ __forceinline__ void write_row(float* row, int D, const RowCtx& r, int lane) {
+    const int mis = int((reinterpret_cast<uintptr_t>(row) >> 2) & 3);
+    int head = (4 - mis) & 3;
+    if (head > D) head = D;
+    if (lane < head) row[lane] = obs_value(r, lane);
+    const int nvec = (D - head) >> 2;
+    float4* body = reinterpret_cast<float4*>(row + head);
+    for (int q = lane; q < nvec; q += 32) {
+        const int e = head + 4 * q;
+        float4 v;
+        v.x = obs_value(r, e);
+        v.y = obs_value(r, e + 1);
+        v.z = obs_value(r, e + 2);
+        v.w = obs_value(r, e + 3);
+        __stcs(body + q, v);
+    }
+    const int tail0 = head + 4 * nvec;
+    if (tail0 + lane < D) row[tail0 + lane] = obs_value(r, tail0 + lane);
+}
+
+// ----------------------------------------------------------------- the fused step kernel
+template <bool kStep>
+__global__ void __launch_bounds__(32 * kMaxAgents)
+world_step_kernel(const KArgs A) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int w = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int M = A.d.M;
+    const int WM = A.d.W * M;
+    const DgConsts& k = A.k;
+
+    // ---- shared memory carve-up
+    const int blob_bytes = A.d.max_scene_bytes;
+    uint8_t* geo = smem;
+    AgentSm* ag = reinterpret_cast<AgentSm*>(smem + align16(blob_bytes));
+    uint8_t* p = reinterpret_cast<uint8_t*>(ag + kMaxAgents);
+    float* ego_sm = reinterpret_cast<float*>(p);                   // [M][16]
+    p += align16(sizeof(float) * 16 * kMaxAgents);
+    float* nb_sm = reinterpret_cast<float*>(p);                    // [M][take_veh*7]
+    p += align16(sizeof(float) * 7 * kMaxAgents * (A.take_veh > 0 ? A.take_veh : 1));
+    uint16_t* cand_sm = reinterpret_cast<uint16_t*>(p);            // [M][take_road]
+    p += align16(sizeof(uint16_t) * kMaxAgents * (A.take_road > 0 ? A.take_road : 1));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(p);
+    __shared__ int s_bad;
+
+    // ---- phase 0: action scan (the reference rejects before mutating)
+    Act act{0.0, 0.0, 0.0};
+    int step_now = 0;
+    if constexpr (kStep) {
+        if (tid == 0) s_bad = DG_NO_ERROR;
+        __syncthreads();
+        if (tid < 3 * M) {
+            const int64_t flat = int64_t(w) * M * 3 + tid;
+            const double v = A.actions_f64 ? reinterpret_cast<const double*>(A.actions)[flat]
+                                           : double(reinterpret_cast<const float*>(A.actions)[flat]);
+            if (!finite(v)) atomicMin(&s_bad, int(flat));
+        }
+        __syncthreads();
+        if (s_bad != DG_NO_ERROR) {
+            if (tid == 0) atomicMin(A.error_word, s_bad);
+            return;
+        }
+        step_now = A.step_count[w];
+    }
+
+    // ---- geometry: one bulk async copy of the world's scene blob
+    const int scene = A.scene_of_world[w];
+    const int64_t* meta = A.scene_meta + 8 * scene;
+    const int64_t g_off = meta[0];
+    const uint32_t g_bytes = uint32_t(meta[1]);
+    const SceneView G = scene_view(geo, int(meta[2]), int(meta[3]), int(meta[4]));
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        bulk_load(geo, A.scene_blob + g_off, g_bytes, bar);
+    }
+
+    const double ox = A.grid_offset[2 * w], oy = A.grid_offset[2 * w + 1];
+
+    // ---- phase 1: warp 0 lane m owns agent m: load, physics, derived values
+    if (warp == 0 && lane < M) {
+        const int m = lane;
+        const int64_t am = int64_t(w) * M + m;
+        AgentSm& S = ag[m];
+        double x[DG_NUM_STATE];
+#pragma unroll
+        for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = A.state[int64_t(f) * WM + am];
+        const int alive = A.alive[am];
+        S.px0 = x[SX];
+        S.py0 = x[SY];
+        if (kStep && alive) {
+            const int64_t ab = am * 3;
+            double raw0, raw1, raw2;
+            if (A.actions_f64) {
+                const double* a = reinterpret_cast<const double*>(A.actions);
+                raw0 = a[ab]; raw1 = a[ab + 1]; raw2 = a[ab + 2];
+            } else {
+                const float* a = reinterpret_cast<const float*>(A.actions);
+                raw0 = a[ab]; raw1 = a[ab + 1]; raw2 = a[ab + 2];
+            }
+            act.thr = np_clip(raw0, 0.0, 1.0);
+            act.steer = np_clip(raw1, -1.0, 1.0);
+            act.brk = np_clip(raw2, 0.0, 1.0);
+            if (A.d.dynamic) {
+                const double cap = A.mu_eff[w] * k.f_z;
+                for (int i = 0; i < A.d.decimation; ++i) substep_dynamic(x, act, cap, k);
+            } else {
+                step_bicycle(x, act, k);
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < DG_NUM_STATE; ++f) S.st[f] = x[f];
+        double s_, c_;
+        sincos(x[SYAW], &s_, &c_);
+        S.c = c_;
+        S.s = s_;
+        S.vwx = x[SVX] * c_ - x[SVY] * s_;
+        S.vwy = x[SVX] * s_ + x[SVY] * c_;
+        S.r = A.r_hull[am];
+        S.d = A.d_hull[am];
+        S.len = A.length[am];
+        S.wid = A.width[am];
+        const double offs[3] = {-1.0, 0.0, 1.0};
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const double o = offs[i] * S.d;
+            S.hx[i] = x[SX] + o * c_;
+            S.hy[i] = x[SY] + o * s_;
+        }
+        S.gx = A.goal_xy[2 * am];
+        S.gy = A.goal_xy[2 * am + 1];
+        S.sx = A.start_xy[2 * am];
+        S.sy = A.start_xy[2 * am + 1];
+        S.alive = alive;
+        S.valid = A.valid[am];
+        S.reason = A.reason[am];
+        S.seen = A.event_seen[am];
+        S.spawn = A.spawn_step[am];
+    }
+
+    // ---- geometry lands; shift scene-local midpoints to global (midpoints + off)
+    __syncthreads();  // agent table written, mbarrier init visible to every thread
+    mbar_wait(bar, 0);
+    {
+        double* mx = const_cast<double*>(G.mx);
+        double* my = const_cast<double*>(G.my);
+        for (int i = tid; i < G.P; i += blockDim.x) {
+            mx[i] = mx[i] + ox;
+            my[i] = my[i] + oy;
+        }
+    }
+    __syncthreads();
+
+    // ---- phase 2: warp m works for agent m
+    for (int m = warp; m < M; m += blockDim.x >> 5) {
+        const AgentSm& S = ag[m];
+        const int64_t am = int64_t(w) * M + m;
+        const double px = S.st[SX], py = S.st[SY];
+        const double c = S.c, s = S.s;
+
+        // (a) road context: candidates d2 <= r^2 in segment order, first take
+        uint16_t* cand = cand_sm + m * A.take_road;
+        int count = 0;
+        for (int p0 = 0; p0 < G.P; p0 += 32) {
+            const int q = p0 + lane;
+            bool hit = false;
+            if (q < G.P) {
+                const double dx = G.mx[q] - px, dy = G.my[q] - py;
+                hit = dx * dx + dy * dy <= k.road_radius_sq;
+            }
+            const unsigned bal = __ballot_sync(kFull, hit);
+            if (hit) {
+                const int slot = count + __popc(bal & ((1u << lane) - 1u));
+                if (slot < A.take_road) cand[slot] = uint16_t(q);
+            }
+            count += __popc(bal);
+        }
+        const int ncand = count < A.take_road ? count : A.take_road;
+
+        // (b) neighbours: lane j looks at agent j
+        float* nb = nb_sm + m * 7 * (A.take_veh > 0 ? A.take_veh : 1);
+        double key = INFINITY, ndx = 0.0, ndy = 0.0;
+        if (lane < M) {
+            const AgentSm& N = ag[lane];
+            ndx = N.st[SX] - px;
+            ndy = N.st[SY] - py;
+            const double dist = sqrt(ndx * ndx + ndy * ndy);
+            key = (N.alive && lane != m) ? dist : INFINITY;
+        }
+        int rank = 0;
+        for (int j = 0; j < M; ++j) {
+            const double kj = shfl_d(key, j);
+            rank += (kj < key) || (kj == key && j < lane);
+        }
+        const bool nvalid = lane < M && finite(key) && rank < A.take_veh;
+        double ttc = k.ttc_max;
+        if (nvalid) {
+            const AgentSm& N = ag[lane];
+            ttc = swept_ttc(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c, N.s, N.d,
+                            S.r + N.r, k.ttc_max);
+            const double turn = N.st[SYAW] - S.st[SYAW];
+            double st_, ct_;
+            sincos(turn, &st_, &ct_);
+            const double wrap = atan2(st_, ct_);
+            const double spd = sqrt(N.st[SVX] * N.st[SVX] + N.st[SVY] * N.st[SVY]);
+            float* row = nb + rank * 7;
+            row[0] = __double2float_rn((c * ndx + s * ndy) / k.bbox_half);
+            row[1] = __double2float_rn((-s * ndx + c * ndy) / k.bbox_half);
+            row[2] = __double2float_rn(N.len / k.bbox_half);
+            row[3] = __double2float_rn(N.wid / k.bbox_half);
+            row[4] = __double2float_rn(wrap / 3.141592653589793);
+            row[5] = __double2float_rn(spd / k.speed_norm);
+            row[6] = __double2float_rn(ttc / k.ttc_max);
+        }
+        const int nnb = __popc(__ballot_sync(kFull, nvalid));
+        const double ttc_min = warp_min(nvalid ? ttc : k.ttc_max);
+
+        // (c) ego block
+        float* ego = ego_sm + 16 * m;
+        if (lane == 0) {
+            const double gdx = S.gx - px, gdy = S.gy - py;
+            const double xb = c * gdx + s * gdy;
+            const double yb = -s * gdx + c * gdy;
+            const double hdg = atan2(yb, xb);
+            double sh, ch;
+            sincos(hdg, &sh, &ch);
+            ego[0] = __double2float_rn(xb / k.bbox_half);
+            ego[1] = __double2float_rn(yb / k.bbox_half);
+            ego[2] = __double2float_rn(sh);
+            ego[3] = __double2float_rn(ch);
+            ego[4] = __double2float_rn(sqrt(xb * xb + yb * yb) / k.bbox_half);
+            ego[5] = __double2float_rn(S.st[SVX] / k.speed_norm);
+            ego[6] = __double2float_rn(S.st[SVY] / k.speed_norm);
+            if (A.d.include_weather) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) ego[7 + i] = __double2float_rn(A.weather[4 * w + i]);
+            }
+        }
+        __syncwarp();
+
+        // (d) rewards, events, termination (engine.py:472-509)
+        if constexpr (kStep) {
+            // nearest lane: argmin of point-to-segment d2, lowest index on ties
+            double best = INFINITY;
+            int best_k = 0x7fffffff;
+            for (int kk = lane; kk < G.KL; kk += 32) {
+                const int q = G.lane[kk];
+                const double ex = px - G.mx[q], ey = py - G.my[q];
+                const double ux = G.dx[q], uy = G.dy[q];
+                const double along = ex * ux + ey * uy;
+                const double lat = ux * ey - uy * ex;
+                const double over = np_max(fabs(along) - G.hl[q], 0.0);
+                const double d2 = over * over + lat * lat;
+                if (d2 < best) { best = d2; best_k = kk; }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(kFull, best, o);
+                const int ok = __shfl_xor_sync(kFull, best_k, o);
+                if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
+            }
+            // first road edge ahead and the hull-vs-edge-box test
+            double gap = INFINITY;
+            bool edge_hit = false;
+            for (int kk = lane; kk < G.KE; kk += 32) {
+                const int q = G.edge[kk];
+                const double xb = c * (G.mx[q] - px) + s * (G.my[q] - py);
+                if (xb > 0.0 && xb <= k.edge_range) gap = np_min(gap, xb);
+                const double ux = G.dx[q], uy = G.dy[q], hl = G.hl[q], hw = G.hw[q];
+                const double r2 = S.r * S.r;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const double qx = S.hx[i] - G.mx[q], qy = S.hy[i] - G.my[q];
+                    const double along = qx * ux + qy * uy;
+                    const double lat = ux * qy - uy * qx;
+                    const double du = along - np_clip(along, -hl, hl);
+                    const double dv = lat - np_clip(lat, -hw, hw);
+                    edge_hit |= du * du + dv * dv < r2;
+                }
+            }
+            gap = warp_min(gap);
+            edge_hit = __any_sync(kFull, edge_hit);
+            // hull contact with any other alive agent (both alive, not self)
+            bool touch = false;
+            if (lane < M && lane != m && S.alive && ag[lane].alive) {
+                const AgentSm& N = ag[lane];
+                const double rs = S.r + N.r;
+                const double rs2 = rs * rs;
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        const double ex = S.hx[i] - N.hx[j], ey = S.hy[i] - N.hy[j];
+                        touch |= ex * ex + ey * ey < rs2;
+                    }
+            }
+            touch = __any_sync(kFull, touch);
+
+            if (lane == 0) {
+                const double vx = S.st[SVX], vy = S.st[SVY], yaw = S.st[SYAW];
+                const double dist = sqrt(best);
+                const bool has_lane = finite(dist);
+                double lat = 0.0, tx = 0.0, ty = 0.0;
+                if (has_lane) {
+                    const int q = G.lane[best_k];
+                    const double ex = px - G.mx[q], ey = py - G.my[q];
+                    tx = G.dx[q];
+                    ty = G.dy[q];
+                    lat = tx * ey - ty * ex;
+                }
+                const double tgx = S.gx - px, tgy = S.gy - py;
+                const double flip = (tx * tgx + ty * tgy >= 0.0) ? 1.0 : -1.0;
+                tx = tx * flip;
+                ty = ty * flip;
+                double progress = np_clip((px - S.px0) * tx + (py - S.py0) * ty,
+                                          -k.progress_clamp, k.progress_clamp) * k.progress_weight;
+                const double align = np_max(0.0, cos(yaw - atan2(ty, tx)));
+                const double ls = lat / k.lane_sigma;
+                const double quality = exp(-(ls * ls)) * (k.lane_heading_base + k.lane_heading_weight * align);
+                const double lane_t = has_lane ? k.lane_weight * quality : 0.0;
+                progress = has_lane ? progress : 0.0;
+                const double offroad = (has_lane && (fabs(lat) > k.offroad_lat_limit || dist > k.offroad_dist_limit))
+                                           ? -k.offroad_weight : 0.0;
+                const double speed = sqrt(vx * vx + vy * vy);
+                const double idle = speed < k.idle_speed ? -k.idle_weight : 0.0;
+                const double ttc_v = -np_min(k.ttc_vehicle_alpha / np_max(ttc_min, k.ttc_floor), k.ttc_vehicle_pmax);
+                const double tau = gap / np_max(vx, 0.1);
+                const double ttc_e = finite(tau) ? -np_min(k.ttc_edge_alpha / np_max(tau, k.ttc_floor), k.ttc_edge_pmax)
+                                                 : 0.0;
+                const double total = progress + lane_t + offroad + idle + ttc_v + ttc_e;
+
+                // sparse events, masked by alive and the per-type latch
+                const bool alive = S.alive;
+                const bool goal = sqrt(tgx * tgx + tgy * tgy) <= k.goal_radius;
+                const double sxd = px - S.sx, syd = py - S.sy;
+                const bool bad = !(finite(px) && finite(py) && finite(vx) && finite(vy));
+                const bool crash = sqrt(sxd * sxd + syd * syd) > k.crash_drift_limit || bad ||
+                                   speed > k.crash_speed_limit;
+                const int age = step_now - S.spawn;
+                const bool coll = touch && age >= A.d.collision_warmup;
+                const int seen = S.seen;
+                const bool e_goal = goal && alive && !(seen & 1);
+                const bool e_coll = coll && alive && !(seen & 2);
+                const bool e_crash = crash && alive && !(seen & 4);
+                const bool e_lf = edge_hit && alive && !(seen & 8);
+                int rnow = e_goal ? 1 : (e_crash ? 3 : (e_lf ? 4 : (e_coll ? 2 : 0)));
+                const int bit = rnow == 1 ? 1 : rnow == 2 ? 2 : rnow == 3 ? 4 : rnow == 4 ? 8 : 0;
+                int seen_new = seen | bit;
+                const double sparse = rnow == 1 ? k.goal_weight
+                                    : rnow == 2 ? -k.collision_weight
+                                    : rnow == 3 ? -k.crash_weight
+                                    : rnow == 4 ? -k.lane_forbidden_weight : 0.0;
+                const double reward = alive ? total + sparse : 0.0;
+                int reason = S.reason;
+                bool done = false;
+                if (!A.d.invincible) {
+                    done = rnow != 0;
+                    if (done && reason == 0) reason = rnow;
+                }
+                // tail: timeout, park, alive (engine.py:370-393)
+                const int step_new = step_now + 1;
+                const bool timeout = step_new >= A.d.episode_len && alive;
+                const bool finished = done || timeout;
+                if (timeout && reason == 0) reason = 5;
+                const bool park = done && !timeout;
+                int alive_new = alive && !finished;
+
+                A.rewards[am] = reward;
+                A.dones[am] = finished;
+                reinterpret_cast<uint32_t*>(A.events)[am] =
+                    uint32_t(rnow == 1) | (uint32_t(rnow == 2) << 8) | (uint32_t(rnow == 3) << 16) |
+                    (uint32_t(rnow == 4) << 24);
+                if (A.reason_out) A.reason_out[am] = int8_t(reason);
+                if (A.alive_out) A.alive_out[am] = uint8_t(alive_new);
+                if (A.alive_pre_out) A.alive_pre_out[am] = uint8_t(alive);
+                if (A.ttc_min_out) A.ttc_min_out[am] = ttc_min;
+                if (A.terms_out) {
+                    const double t7[7] = {progress, lane_t, offroad, idle, ttc_v, ttc_e, total};
+#pragma unroll
+                    for (int i = 0; i < 7; ++i) A.terms_out[int64_t(i) * WM + am] = alive ? t7[i] : 0.0;
+                }
+                if (A.snapshot_out) {
+#pragma unroll
+                    for (int f = 0; f < DG_NUM_STATE; ++f) A.snapshot_out[int64_t(f) * WM + am] = S.st[f];
+                }
+                double x[DG_NUM_STATE];
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = S.st[f];
+                if (park) {
+#pragma unroll
+                    for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
+                    x[SX] = ox + k.offstage_x;
+                    x[SY] = oy;
+                }
+                int spawn = S.spawn;
+                if (A.autoreset && finished && S.valid) {
+#pragma unroll
+                    for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
+                    x[SX] = S.sx;
+                    x[SY] = S.sy;
+                    x[SYAW] = A.start_yaw[am];
+                    alive_new = 1;
+                    reason = 0;
+                    spawn = step_new;
+                    seen_new = 0;
+                }
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = x[f];
+                A.alive[am] = uint8_t(alive_new);
+                A.reason[am] = int8_t(reason);
+                A.event_seen[am] = uint8_t(seen_new);
+                A.spawn_step[am] = spawn;
+            }
+        } else {
+            if (lane == 0 && A.ttc_min_out) A.ttc_min_out[am] = ttc_min;
+        }
+
+        // (e) the observation row
+        RowCtx rc;
+        rc.ego = ego;
+        rc.nb = nb;
+        rc.cand = cand;
+        rc.g = G;
+        rc.px = px; rc.py = py; rc.c = c; rc.s = s;
+        rc.ncand = ncand;
+        rc.nnb = nnb;
+        rc.ego_dim = A.d.ego_dim;
+        rc.road_end = A.d.ego_dim + 5 * A.d.k_road;
+        rc.road_radius = k.road_radius;
+        rc.type_norm = k.type_norm;
+        write_row(A.obs + am * A.d.obs_dim, A.d.obs_dim, rc, lane);
+    }
+
+    if constexpr (kStep) {
+        if (tid == 0) A.step_count[w] = step_now + 1;
+    }
+}
+
+// ----------------------------------------------------------------- small kernels
+__global__ void check_actions_kernel(const void* actions, int f64, int64_t n, int32_t* err) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const double v = f64 ? reinterpret_cast<const double*>(actions)[i]
+                             : double(reinterpret_cast<const float*>(actions)[i]);
+        if (!isfinite(v)) atomicMin(err, int(i));
+    }
+}
+
+// engine.py:599-619: masked slots get a fresh pose, zero velocity, cleared latches
+__global__ void teleport_reset_kernel(KArgs A, const uint8_t* mask, const double* new_starts,
+                                      const double* new_goals, const double* new_headings) {
+    const int WM = A.d.W * A.d.M;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < WM; i += gridDim.x * blockDim.x) {
+        const bool sel = (mask ? mask[i] != 0 : true) && A.valid[i];
+        if (!sel) continue;
+        double* sxy = A.start_xy;
+        double* gxy = A.goal_xy;
+        double* syaw = A.start_yaw;
+        if (new_starts) { sxy[2 * i] = new_starts[2 * i]; sxy[2 * i + 1] = new_starts[2 * i + 1]; }
+        if (new_goals) { gxy[2 * i] = new_goals[2 * i]; gxy[2 * i + 1] = new_goals[2 * i + 1]; }
+        if (new_headings) syaw[i] = new_headings[i];
+        for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + i] = (f == SBF || f == SBR) ? 1.0 : 0.0;
+        A.state[int64_t(SX) * WM + i] = sxy[2 * i];
+        A.state[int64_t(SY) * WM + i] = sxy[2 * i + 1];
+        A.state[int64_t(SYAW) * WM + i] = syaw[i];
+        A.alive[i] = 1;
+        A.reason[i] = 0;
+        A.spawn_step[i] = A.step_count[i / A.d.M];
+        A.event_seen[i] = 0;
+    }
+}
+
+__global__ void set_step_kernel(int32_t* step_count, int W, int32_t value) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < W; i += gridDim.x * blockDim.x) step_count[i] = value;
+}
+
+// policies.py:21-43 on the device, float64 like the numpy policy
+__global__ void lane_follower_kernel(const float* obs, double* actions, int64_t n, int D, double gain,
+                                     double throttle, double bbox_half) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const float* o = obs + i * D;
+        const double sin_e = double(o[2]), cos_e = double(o[3]);
+        const double dist = double(o[4]) * bbox_half;
+        double steer = np_clip(gain * sin_e, -1.0, 1.0);
+        if (cos_e < 0.0) steer = sin_e >= 0.0 ? 1.0 : -1.0;
+        actions[3 * i] = dist > 5.0 ? throttle : throttle * 0.5;
+        actions[3 * i + 1] = steer;
+        actions[3 * i + 2] = 0.0;
+    }
+}
+
+}  // namespace
+
+// =========================================================================== C ABI
+
+struct dg_engine {
+    DgEngineDesc desc;
+    KArgs base;
+    size_t smem_bytes;
+    int launches;
+};
+
+static thread_local char g_err[512] = "";
+
+static int fail(int code, const char* msg) {
+    std::snprintf(g_err, sizeof(g_err), "%s", msg);
+    return code;
+}
+
+static int cuda_fail(cudaError_t e, const char* where) {
+    std::snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return DG_ECUDA;
+}
+
+static size_t step_smem_bytes(const DgDims& d, int take_road, int take_veh) {
+    size_t b = size_t(align16(d.max_scene_bytes));
+    b += sizeof(AgentSm) * kMaxAgents;
+    b += size_t(align16(sizeof(float) * 16 * kMaxAgents));
+    b += size_t(align16(sizeof(float) * 7 * kMaxAgents * (take_veh > 0 ? take_veh : 1)));
+    b += size_t(align16(sizeof(uint16_t) * kMaxAgents * (take_road > 0 ? take_road : 1)));
+    b += 16;  // mbarrier
+    return b;
+}
+
+extern "C" {
+
+int dg_abi_version(void) { return DG_ABI_VERSION; }
+const char* dg_last_error(void) { return g_err; }
+
+int dg_create(const DgEngineDesc* desc, dg_engine** out) {
+    if (!desc || !out) return fail(DG_EINVAL, "dg_create: null argument");
+    const DgDims& d = desc->dims;
+    if (d.W < 1 || d.M < 1 || d.M > kMaxAgents) return fail(DG_EINVAL, "dg_create: need W >= 1 and 1 <= M <= 16");
+    if (d.obs_dim != d.ego_dim + 5 * d.k_road + 7 * d.k_vehicles)
+        return fail(DG_EINVAL, "dg_create: obs_dim != ego_dim + 5*k_road + 7*k_vehicles");
+    if (d.ego_dim != 7 + (d.include_weather ? 4 : 0)) return fail(DG_EINVAL, "dg_create: bad ego_dim");
+    if (d.max_segments > 65535) return fail(DG_ENOSUPPORT, "dg_create: more than 65535 segments in a scene");
+    if (d.max_scene_bytes % 16) return fail(DG_EINVAL, "dg_create: scene blobs must be 16-byte multiples");
+    const void* req[] = {desc->scene_blob, desc->scene_meta, desc->scene_of_world, desc->grid_offset,
+                         desc->mu_eff, desc->weather, desc->valid, desc->length, desc->width,
+                         desc->r_hull, desc->d_hull, desc->state, desc->alive, desc->reason,
+                         desc->event_seen, desc->spawn_step, desc->step_count, desc->start_xy,
+                         desc->goal_xy, desc->start_yaw, desc->error_word};
+    for (const void* p : req)
+        if (!p) return fail(DG_EINVAL, "dg_create: null device pointer in engine description");
+
+    dg_engine* e = new (std::nothrow) dg_engine();
+    if (!e) return fail(DG_ECUDA, "dg_create: out of host memory");
+    e->desc = *desc;
+    KArgs& A = e->base;
+    std::memset(&A, 0, sizeof(A));
+    A.d = d;
+    A.k = desc->k;
+    A.scene_blob = desc->scene_blob;
+    A.scene_meta = desc->scene_meta;
+    A.scene_of_world = desc->scene_of_world;
+    A.grid_offset = desc->grid_offset;
+    A.mu_eff = desc->mu_eff;
+    A.weather = desc->weather;
+    A.valid = desc->valid;
+    A.length = desc->length;
+    A.width = desc->width;
+    A.r_hull = desc->r_hull;
+    A.d_hull = desc->d_hull;
+    A.state = desc->state;
+    A.alive = desc->alive;
+    A.reason = desc->reason;
+    A.event_seen = desc->event_seen;
+    A.spawn_step = desc->spawn_step;
+    A.step_count = desc->step_count;
+    A.start_xy = desc->start_xy;
+    A.goal_xy = desc->goal_xy;
+    A.start_yaw = desc->start_yaw;
+    A.error_word = desc->error_word;
+    A.take_road = d.k_road < d.max_segments ? d.k_road : d.max_segments;
+    A.take_veh = d.k_vehicles < d.M ? d.k_vehicles : d.M;
+    e->smem_bytes = step_smem_bytes(d, A.take_road, A.take_veh);
+    if (e->smem_bytes > 227 * 1024) {
+        delete e;
+        return fail(DG_ENOSUPPORT, "dg_create: scene geometry does not fit in shared memory");
+    }
+    cudaError_t err = cudaFuncSetAttribute(world_step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(e->smem_bytes));
+    if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(world_step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(e->smem_bytes));
+    if (err != cudaSuccess) {
+        delete e;
+        return cuda_fail(err, "dg_create: cudaFuncSetAttribute");
+    }
+    e->launches = 0;
+    *out = e;
+    return DG_OK;
+}
+
+int dg_destroy(dg_engine* eng) {
+    delete eng;
+    return DG_OK;
+}
+
+int dg_step(dg_engine* eng, const DgStepIO* io, void* stream) {
+    if (!eng || !io) return fail(DG_EINVAL, "dg_step: null argument");
+    if (!io->actions || !io->obs || !io->rewards || !io->dones || !io->events)
+        return fail(DG_EINVAL, "dg_step: actions, obs, rewards, dones and events are required");
+    KArgs A = eng->base;
+    A.actions = io->actions;
+    A.actions_f64 = io->actions_f64;
+    A.autoreset = io->autoreset;
+    A.obs = io->obs;
+    A.rewards = io->rewards;
+    A.dones = io->dones;
+    A.events = io->events;
+    A.reason_out = io->reason_out;
+    A.alive_out = io->alive_out;
+    A.alive_pre_out = io->alive_pre_out;
+    A.ttc_min_out = io->ttc_min_out;
+    A.terms_out = io->terms_out;
+    A.snapshot_out = io->snapshot_out;
+    world_step_kernel<true><<<A.d.W, 32 * A.d.M, eng->smem_bytes, static_cast<cudaStream_t>(stream)>>>(A);
+    eng->launches = 1;
+    const cudaError_t err = cudaGetLastError();
+    return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_step");
+}
+
+int dg_observe(dg_engine* eng, float* obs, double* ttc_min_out, void* stream) {
+    if (!eng || !obs) return fail(DG_EINVAL, "dg_observe: null argument");
+    KArgs A = eng->base;
+    A.obs = obs;
+    A.ttc_min_out = ttc_min_out;
+    world_step_kernel<false><<<A.d.W, 32 * A.d.M, eng->smem_bytes, static_cast<cudaStream_t>(stream)>>>(A);
+    eng->launches = 1;
+    const cudaError_t err = cudaGetLastError();
+    return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_observe");
+}
+
+int dg_reset(dg_engine* eng, const uint8_t* mask, const double* new_starts, const double* new_goals,
+             const double* new_headings, void* stream) {
+    if (!eng) return fail(DG_EINVAL, "dg_reset: null engine");
+    const int WM = eng->base.d.W * eng->base.d.M;
+    const int threads = 256, blocks = (WM + threads - 1) / threads;
+    teleport_reset_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+        eng->base, mask, new_starts, new_goals, new_headings);
+    eng->launches = 1;
+    const cudaError_t err = cudaGetLastError();
+    return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_reset");
+}
+
+int dg_set_step_count(dg_engine* eng, int32_t value, void* stream) {
+    if (!eng) return fail(DG_EINVAL, "dg_set_step_count: null engine");
+    const int W = eng->base.d.W;
+    set_step_kernel<<<(W + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(eng->base.step_count, W, value);
+    eng->launches = 1;
+    const cudaError_t err = cudaGetLastError();
+    return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_set_step_count");
+}
+
+int dg_check_actions(dg_engine* eng, const void* actions, int32_t actions_f64, void* stream) {
+    if (!eng || !actions) return fail(DG_EINVAL, "dg_check_actions: null argument");
+    const int64_t n = int64_t(eng->base.d.W) * eng->base.d.M * 3;
+    const int threads = 256;
+    const int blocks = int((n + threads - 1) / threads < 1184 ? (n + threads - 1) / threads : 1184);
+    check_actions_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(actions, actions_f64, n,
+                                                                                eng->base.error_word);
+    eng->launches = 1;
+    const cudaError_t err = cudaGetLastError();
+    return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_check_actions");
+}
+
+int dg_read_error(dg_engine* eng, int32_t* flat_index, void* stream) {
+    if (!eng || !flat_index) return fail(DG_EINVAL, "dg_read_error: null argument");
+    int32_t host = DG_NO_ERROR;
+    const int32_t clean = DG_NO_ERROR;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t err = cudaMemcpyAsync(&host, eng->base.error_word, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+    if (err == cudaSuccess && host != DG_NO_ERROR)
+        err = cudaMemcpyAsync(eng->base.error_word, &clean, sizeof(int32_t), cudaMemcpyHostToDevice, s);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+    if (err != cudaSuccess) return cuda_fail(err, "dg_read_error");
+    *flat_index = host == DG_NO_ERROR ? -1 : host;
+    return DG_OK;
+}
+
+int dg_lane_follower(dg_engine* eng, const float* obs, double* actions, double steer_gain, double throttle,
+                     void* stream) {
+    if (!eng || !obs || !actions) return fail(DG_EINVAL, "dg_lane_follower: null argument");
+    const int64_t n = int64_t(eng->base.d.W) * eng->base.d.M;
+    const int threads = 128;
+    const int blocks = int((n + threads - 1) / threads);
+    lane_follower_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+        obs, actions, n, eng->base.d.obs_dim, steer_gain, throttle, eng->base.k.bbox_half);
+    eng->launches = 1;
+    const cudaError_t err = cudaGetLastError();
+    return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_lane_follower");
+}
+
+int dg_launch_count(dg_engine* eng) { return eng ? eng->launches : 0; }
+
+}  // extern "C"

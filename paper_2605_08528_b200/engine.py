@@ -1,0 +1,532 @@
+"""GPU batch engine: the drop-in for ``drivegrid.engine.Engine``.
+
+Construction mirrors the reference signature (engine.py:151-162) and builds
+the same host tables; per step, ``step()`` issues ONE fused kernel through the
+C ABI (``dg_step``) that runs decode -> 4 physics substeps -> observation ->
+rewards/events -> timeout/park tail for every world.
+
+Array namespace follows the caller:
+  * numpy actions  -> numpy outputs (host copies; the reference's exact
+    semantics, including raising on non-finite actions before mutating);
+  * torch CUDA actions -> torch CUDA outputs that stay in HBM (the fast path;
+    non-finite actions are flagged on the device, see ``check_actions``).
+
+State lives on the device in float64 global coordinates, laid out
+``[12][W][M]`` (``state_tensor``); ``engine.state`` returns host copies keyed
+like the reference.  There is no CPU fallback: constructing an Engine without
+a CUDA device or without the native library raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as ct
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .params import (CRASH_SPEED_LIMIT, DENSE_TERMS, EVENT_TYPES, GRAVITY, OFFSTAGE_X, PHASES,
+                     STATE_FIELDS, BicycleParams, ObsConfig, RewardConfig, SimConfig, VehicleParams)
+from .tables import build_tables, compact_subset, edge_mask_of, lane_mask_of
+
+TERM_NAMES = (*DENSE_TERMS, "total")
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ct.c_void_p(t.data_ptr())
+
+
+def _align16(n: int) -> int:
+    return (n + 15) & ~15
+
+
+def make_consts(cfg: SimConfig, oc: ObsConfig, rc: RewardConfig, vp: VehicleParams,
+                bp: BicycleParams) -> N.DgConsts:
+    """Scalar constants with the reference's Python-side expression order."""
+    k = N.DgConsts()
+    vals = dict(
+        physics_dt=cfg.physics_dt, control_dt=cfg.control_dt,
+        kp_steer=vp.kp_steer, kd_steer=vp.kd_steer, theta_max=vp.theta_max,
+        tau_steer_max=vp.tau_steer_max, steer_inertia=vp.steer_inertia,
+        steer_limit=1.05 * vp.theta_max,
+        a_f=0.5 * vp.wheelbase - vp.com_offset, b_r=0.5 * vp.wheelbase + vp.com_offset,
+        tau_drive_max=vp.tau_drive_max, tau_brake_front=vp.tau_brake_front,
+        tau_brake_rear=vp.tau_brake_rear, wheel_radius=vp.wheel_radius,
+        cornering_stiffness=vp.cornering_stiffness, f_z=0.5 * vp.chassis_mass * GRAVITY,
+        chassis_mass=vp.chassis_mass, lambda_lat=vp.lambda_lat, lambda_yaw=vp.lambda_yaw,
+        yaw_inertia=vp.yaw_inertia, i_axle=2.0 * vp.wheel_inertia, wheelbase=vp.wheelbase,
+        bic_a_max=bp.a_max, bic_b_max=bp.b_max, bic_c_roll=bp.c_roll,
+        bic_steer_max=float(np.deg2rad(30.0)),
+        road_radius=oc.road_radius, road_radius_sq=oc.road_radius ** 2, bbox_half=oc.bbox_half,
+        speed_norm=oc.speed_norm, type_norm=oc.type_norm, ttc_max=oc.ttc_max,
+        goal_radius=rc.goal_radius, goal_weight=rc.goal_weight,
+        collision_weight=rc.collision_weight, crash_weight=rc.crash_weight,
+        crash_drift_limit=rc.crash_drift_limit, lane_forbidden_weight=rc.lane_forbidden_weight,
+        progress_weight=rc.progress_weight, progress_clamp=rc.progress_clamp,
+        lane_weight=rc.lane_weight, lane_sigma=rc.lane_sigma,
+        lane_heading_weight=rc.lane_heading_weight,
+        lane_heading_base=1.0 - rc.lane_heading_weight, offroad_weight=rc.offroad_weight,
+        offroad_lat_limit=rc.offroad_lat_limit, offroad_dist_limit=rc.offroad_dist_limit,
+        idle_weight=rc.idle_weight, idle_speed=rc.idle_speed,
+        ttc_vehicle_alpha=rc.ttc_vehicle_alpha, ttc_vehicle_pmax=rc.ttc_vehicle_pmax,
+        ttc_edge_alpha=rc.ttc_edge_alpha, ttc_edge_pmax=rc.ttc_edge_pmax, ttc_floor=rc.ttc_floor,
+        edge_range=rc.edge_range, crash_speed_limit=CRASH_SPEED_LIMIT, offstage_x=OFFSTAGE_X,
+    )
+    assert set(vals) == set(N.CONST_FIELDS)
+    for name, v in vals.items():
+        setattr(k, name, float(v))
+    return k
+
+
+def pack_scenes(scene_tables) -> tuple[np.ndarray, np.ndarray, int, int]:
+    """Concatenate per-scene blobs (layout documented in the C header)."""
+    blobs, meta, off = [], [], 0
+    for t in scene_tables:
+        P, KL, KE = t.num_segments, len(t.lane_index), len(t.edge_index)
+        parts = []
+        for arr in (t.midpoints[:, 0], t.midpoints[:, 1], t.directions[:, 0], t.directions[:, 1],
+                    t.half_lengths, t.half_widths):
+            parts.append(np.ascontiguousarray(arr, dtype=np.float64))
+        parts += [t.type_codes.astype(np.int32), t.lane_index.astype(np.int32),
+                  t.edge_index.astype(np.int32)]
+        chunk = bytearray()
+        for a in parts:
+            b = a.tobytes()
+            chunk += b + bytes(_align16(len(b)) - len(b))
+        if not chunk:
+            chunk = bytearray(16)
+        blobs.append(bytes(chunk))
+        meta.append([off, len(chunk), P, KL, KE, 0, 0, 0])
+        off += len(chunk)
+    blob = np.frombuffer(b"".join(blobs), dtype=np.uint8).copy()
+    max_bytes = max(m[1] for m in meta)
+    max_p = max(m[2] for m in meta)
+    return blob, np.asarray(meta, dtype=np.int64), max_bytes, max_p
+
+
+class StepOutput:
+    """Result of one control tick (engine.py:70-76).  ``events`` and ``info``
+    are built lazily from the packed output buffers."""
+
+    def __init__(self, obs, rewards, dones, events4, info_src: dict, to_host: bool):
+        self.obs = obs
+        self.rewards = rewards
+        self.dones = dones
+        self._events4 = events4
+        self._info_src = info_src
+        self._host = to_host
+        self._events = None
+        self._info = None
+
+    @property
+    def events(self) -> dict:
+        if self._events is None:
+            self._events = {k: self._events4[..., i].astype(bool) if self._host
+                            else self._events4[..., i].bool() for i, k in enumerate(EVENT_TYPES)}
+        return self._events
+
+    @property
+    def info(self) -> dict:
+        if self._info is None:
+            s = self._info_src
+            as_bool = (lambda a: a.astype(bool)) if self._host else (lambda a: a.bool())
+            self._info = {
+                "alive": as_bool(s["alive"]),
+                "alive_pre": as_bool(s["alive_pre"]),
+                "state": {k: s["snapshot"][i] for i, k in enumerate(STATE_FIELDS)},
+                "reason": s["reason"],
+                "reward_terms": {k: s["terms"][i] for i, k in enumerate(TERM_NAMES)},
+                "ttc_min": s["ttc_min"],
+                "step": s["step"],
+            }
+        return self._info
+
+
+@dataclass
+class StepBuffers:
+    """Preallocated device outputs for the zero-allocation path (bench,
+    rollouts).  ``obs`` may be any [W][M][D] float32 view, e.g. one slot of
+    a rollout ring."""
+
+    obs: torch.Tensor
+    aux: torch.Tensor
+    views: dict
+
+
+class Engine:
+    """Owner of the (W, M) agent state over a world batch, on one GPU."""
+
+    def __init__(self, worlds, scenes, assignment, frictions, config: SimConfig,
+                 obs_config: ObsConfig | None = None, reward_config: RewardConfig | None = None,
+                 params: VehicleParams | None = None, bicycle: BicycleParams | None = None,
+                 device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("drivegrid-b200 Engine needs a CUDA device (no CPU fallback)")
+        self._lib = N.load_library()
+        self.device = torch.device(device if device is not None else "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        self.config = config
+        self.obs_config = obs_config or ObsConfig()
+        self.reward_config = reward_config or RewardConfig()
+        self.params = params or VehicleParams()
+        self.bicycle = bicycle or BicycleParams()
+        self.worlds = worlds
+        self.frictions = frictions
+        t = build_tables(worlds, scenes, assignment, frictions, config, self.params)
+        self.tables = t
+        W, M = t.W, t.M
+        self.W, self.M = W, M
+        self.valid = t.valid.copy()
+        self.length, self.width = t.length, t.width
+        self.r_hull, self.d_hull = t.r_hull, t.d_hull
+        self.mu_eff, self.weather = t.mu_eff, t.weather
+        self._lane = None
+        self._edge = None
+
+        dev = self.device
+
+        def up(a, dtype):
+            return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(dev)
+
+        blob, meta, max_bytes, max_p = pack_scenes(t.scenes)
+        self._d = d = {
+            "scene_blob": up(blob, torch.uint8),
+            "scene_meta": up(meta, torch.int64),
+            "scene_of_world": up(t.scene_of_world, torch.int32),
+            "grid_offset": up(t.grid_offsets, torch.float64),
+            "mu_eff": up(t.mu_eff, torch.float64),
+            "weather": up(t.weather, torch.float64),
+            "valid": up(t.valid, torch.uint8),
+            "length": up(t.length, torch.float64),
+            "width": up(t.width, torch.float64),
+            "r_hull": up(t.r_hull, torch.float64),
+            "d_hull": up(t.d_hull, torch.float64),
+            "state": up(np.stack([t.state0[k] for k in STATE_FIELDS]), torch.float64),
+            "alive": up(t.valid, torch.uint8),
+            "reason": torch.zeros((W, M), dtype=torch.int8, device=dev),
+            "event_seen": torch.zeros((W, M), dtype=torch.uint8, device=dev),
+            "spawn_step": torch.zeros((W, M), dtype=torch.int32, device=dev),
+            "step_count": torch.zeros((W,), dtype=torch.int32, device=dev),
+            "start_xy": up(t.start_xy, torch.float64),
+            "goal_xy": up(t.goal_xy, torch.float64),
+            "start_yaw": up(t.start_yaw, torch.float64),
+            "error_word": torch.full((1,), N.DG_NO_ERROR, dtype=torch.int32, device=dev),
+        }
+        oc = self.obs_config
+        dims = N.DgDims(W=W, M=M, obs_dim=oc.obs_dim, ego_dim=oc.ego_dim, k_road=oc.k_road,
+                        k_vehicles=oc.k_vehicles, include_weather=int(oc.include_weather),
+                        dynamic=int(config.dynamics_mode == "dynamic"), decimation=config.decimation,
+                        episode_len=config.episode_len, invincible=int(config.invincible),
+                        collision_warmup=self.reward_config.collision_warmup_steps,
+                        num_scenes=len(t.scenes), max_scene_bytes=max_bytes, max_segments=max_p)
+        desc = N.DgEngineDesc(dims=dims, k=make_consts(config, oc, self.reward_config, self.params,
+                                                       self.bicycle))
+        for name in ("scene_blob", "scene_meta", "scene_of_world", "grid_offset", "mu_eff", "weather",
+                     "valid", "length", "width", "r_hull", "d_hull", "state", "alive", "reason",
+                     "event_seen", "spawn_step", "step_count", "start_xy", "goal_xy", "start_yaw",
+                     "error_word"):
+            setattr(desc, name, d[name].data_ptr())
+        handle = ct.c_void_p()
+        N.check(self._lib, self._lib.dg_create(ct.byref(desc), ct.byref(handle)), "dg_create")
+        self._h = handle
+        self._desc = desc
+        self._step_count = 0
+        self.phase_seconds = {k: 0.0 for k in PHASES}
+        self._act_dev = torch.empty((W, M, 3), dtype=torch.float64, device=dev)
+        self._act_host = torch.empty((W, M, 3), dtype=torch.float64).pin_memory()
+        self._obs_dev = torch.empty((W, M, oc.obs_dim), dtype=torch.float32, device=dev)
+        self._host_bufs = self._new_buffers(self._obs_dev)
+        self.launches = 0
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib.dg_destroy(h)
+            except Exception:  # interpreter teardown
+                pass
+            self._h = None
+
+    # ------------------------------------------------------------------ buffers
+    def _stream(self):
+        return ct.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _aux_layout(self):
+        W, M = self.W, self.M
+        WM = W * M
+        lay, off = {}, 0
+        for name, nbytes, dtype, shape in (
+                ("rewards", 8 * WM, torch.float64, (W, M)),
+                ("ttc_min", 8 * WM, torch.float64, (W, M)),
+                ("terms", 8 * 7 * WM, torch.float64, (7, W, M)),
+                ("snapshot", 8 * 12 * WM, torch.float64, (12, W, M)),
+                ("events", 4 * WM, torch.uint8, (W, M, 4)),
+                ("dones", WM, torch.uint8, (W, M)),
+                ("reason", WM, torch.int8, (W, M)),
+                ("alive", WM, torch.uint8, (W, M)),
+                ("alive_pre", WM, torch.uint8, (W, M))):
+            lay[name] = (off, nbytes, dtype, shape)
+            off = _align16(off + nbytes)
+        return lay, off
+
+    def _views(self, aux: torch.Tensor) -> dict:
+        lay, _ = self._aux_layout()
+        return {name: aux[o:o + n].view(dt).view(shape) for name, (o, n, dt, shape) in lay.items()}
+
+    def _new_buffers(self, obs: torch.Tensor | None = None) -> StepBuffers:
+        _, total = self._aux_layout()
+        aux = torch.empty(total, dtype=torch.uint8, device=self.device)
+        if obs is None:
+            obs = torch.empty((self.W, self.M, self.obs_config.obs_dim), dtype=torch.float32,
+                              device=self.device)
+        return StepBuffers(obs, aux, self._views(aux))
+
+    def new_step_buffers(self, obs: torch.Tensor | None = None) -> StepBuffers:
+        return self._new_buffers(obs)
+
+    # ------------------------------------------------------------------ device state views
+    @property
+    def state_tensor(self) -> torch.Tensor:
+        """[12][W][M] float64 device tensor (live, not a copy)."""
+        return self._d["state"]
+
+    def device_tables(self) -> dict:
+        return self._d
+
+    @property
+    def step_count(self) -> int:
+        return self._step_count
+
+    @step_count.setter
+    def step_count(self, value: int):
+        N.check(self._lib, self._lib.dg_set_step_count(self._h, int(value), self._stream()),
+                "dg_set_step_count")
+        self._step_count = int(value)
+
+    def _host(self, name):
+        return self._d[name].cpu().numpy()
+
+    @property
+    def state(self) -> dict:
+        st = self._d["state"].cpu().numpy()
+        return {k: st[i].copy() for i, k in enumerate(STATE_FIELDS)}
+
+    def set_state(self, values: dict) -> None:
+        """Overwrite state fields (host or device arrays, global coordinates)."""
+        for k, v in values.items():
+            i = STATE_FIELDS.index(k)
+            self._d["state"][i].copy_(torch.as_tensor(np.asarray(v, dtype=np.float64)
+                                                      if not isinstance(v, torch.Tensor) else v))
+
+    @property
+    def alive(self) -> np.ndarray:
+        return self._host("alive").astype(bool)
+
+    @alive.setter
+    def alive(self, value):
+        self._d["alive"].copy_(torch.as_tensor(np.asarray(value, dtype=np.uint8)))
+
+    @property
+    def reason(self) -> np.ndarray:
+        return self._host("reason")
+
+    @property
+    def spawn_step(self) -> np.ndarray:
+        return self._host("spawn_step").astype(np.int64)
+
+    @property
+    def start_xy(self) -> np.ndarray:
+        return self._host("start_xy")
+
+    @property
+    def goal_xy(self) -> np.ndarray:
+        return self._host("goal_xy")
+
+    @property
+    def start_yaw(self) -> np.ndarray:
+        return self._host("start_yaw")
+
+    def set_goals(self, goal_xy) -> None:
+        self._d["goal_xy"].copy_(torch.as_tensor(np.asarray(goal_xy, dtype=np.float64)))
+
+    @property
+    def event_seen(self) -> dict:
+        bits = self._host("event_seen")
+        return {k: (bits >> i & 1).astype(bool) for i, k in enumerate(EVENT_TYPES)}
+
+    @property
+    def pos(self) -> np.ndarray:
+        st = self.state
+        return np.stack([st["x"], st["y"]], axis=-1)
+
+    @property
+    def lane(self) -> dict:
+        if self._lane is None:
+            self._lane = compact_subset(self.worlds, lane_mask_of(self.worlds.type_codes, self.worlds.mask))
+        return self._lane
+
+    @property
+    def edge(self) -> dict:
+        if self._edge is None:
+            self._edge = compact_subset(self.worlds, edge_mask_of(self.worlds.type_codes, self.worlds.mask))
+        return self._edge
+
+    def reset_phase_timers(self):
+        self.phase_seconds = {k: 0.0 for k in PHASES}
+
+    # ------------------------------------------------------------------ errors
+    def _raise_nonfinite(self, flat: int):
+        w, m = flat // (3 * self.M), (flat // 3) % self.M
+        raise ValueError(f"non-finite action for world {w} agent {m}")
+
+    def check_actions(self, actions: torch.Tensor) -> None:
+        """Device finiteness scan + one sync; raises exactly like the reference."""
+        N.check(self._lib, self._lib.dg_check_actions(self._h, _ptr(actions),
+                                                      int(actions.dtype == torch.float64),
+                                                      self._stream()), "dg_check_actions")
+        self.raise_pending_error()
+
+    def raise_pending_error(self) -> None:
+        flat = ct.c_int32(-1)
+        N.check(self._lib, self._lib.dg_read_error(self._h, ct.byref(flat), self._stream()),
+                "dg_read_error")
+        if flat.value >= 0:
+            self._raise_nonfinite(flat.value)
+
+    # ------------------------------------------------------------------ observe
+    def observe(self, ttc_min: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                as_numpy: bool = True):
+        """Observation of the current state (engine.py:297-300)."""
+        obs = out if out is not None else torch.empty_like(self._obs_dev)
+        N.check(self._lib, self._lib.dg_observe(self._h, _ptr(obs), _ptr(ttc_min), self._stream()),
+                "dg_observe")
+        self.launches += 1
+        if as_numpy:
+            return obs.cpu().numpy()
+        return obs
+
+    def observe_device(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        return self.observe(out=out, as_numpy=False)
+
+    # ------------------------------------------------------------------ step
+    def launch_step(self, actions: torch.Tensor, bufs: StepBuffers, autoreset: bool = False,
+                    snapshot: bool = True, terms: bool = True) -> None:
+        """Enqueue one fused step on the current stream; no sync, no checks
+        beyond the device-side non-finite guard.  Used by the fast paths."""
+        v = bufs.views
+        io = N.DgStepIO(actions=actions.data_ptr(), actions_f64=int(actions.dtype == torch.float64),
+                        autoreset=int(autoreset), obs=bufs.obs.data_ptr(),
+                        rewards=v["rewards"].data_ptr(), dones=v["dones"].data_ptr(),
+                        events=v["events"].data_ptr(), reason_out=v["reason"].data_ptr(),
+                        alive_out=v["alive"].data_ptr(), alive_pre_out=v["alive_pre"].data_ptr(),
+                        ttc_min_out=v["ttc_min"].data_ptr(),
+                        terms_out=v["terms"].data_ptr() if terms else None,
+                        snapshot_out=v["snapshot"].data_ptr() if snapshot else None)
+        N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), self._stream()), "dg_step")
+        self._step_count += 1
+        self.launches += 1
+
+    def step(self, actions, autoreset: bool = False) -> StepOutput:
+        """One 30 Hz control tick (engine.py:334-406)."""
+        if isinstance(actions, torch.Tensor) and actions.is_cuda:
+            return self._step_device(actions, autoreset)
+        return self._step_host(actions, autoreset)
+
+    def _step_device(self, actions: torch.Tensor, autoreset: bool, check: bool = True) -> StepOutput:
+        want = (self.W, self.M, 3)
+        if tuple(actions.shape) != want:
+            raise ValueError(f"actions shape {tuple(actions.shape)}, expected {want}")
+        if actions.dtype not in (torch.float32, torch.float64):
+            actions = actions.to(torch.float64)
+        actions = actions.contiguous()
+        if check:
+            self.check_actions(actions)
+        bufs = self._new_buffers()
+        self.launch_step(actions, bufs, autoreset=autoreset)
+        v = bufs.views
+        src = dict(v)
+        src["step"] = self._step_count
+        return StepOutput(bufs.obs, v["rewards"], v["dones"].bool(), v["events"], src, to_host=False)
+
+    def _step_host(self, actions, autoreset: bool) -> StepOutput:
+        t0 = time.perf_counter()
+        a = np.asarray(actions, dtype=np.float64)
+        want = (self.W, self.M, 3)
+        if a.shape != want:
+            raise ValueError(f"actions shape {a.shape}, expected {want}")
+        bad = ~np.isfinite(a)
+        if bad.any():
+            w, m, _ = np.argwhere(bad)[0]
+            raise ValueError(f"non-finite action for world {w} agent {m}")
+        self._act_host.numpy()[...] = a
+        self._act_dev.copy_(self._act_host, non_blocking=True)
+        t1 = time.perf_counter()
+        bufs = self._host_bufs
+        self.launch_step(self._act_dev, bufs, autoreset=autoreset)
+        obs = torch.empty(bufs.obs.shape, dtype=torch.float32, pin_memory=True)
+        aux = torch.empty(bufs.aux.shape, dtype=torch.uint8, pin_memory=True)
+        obs.copy_(bufs.obs, non_blocking=True)
+        aux.copy_(bufs.aux, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        t2 = time.perf_counter()
+        hv = {k: t.numpy() for k, t in self._views(aux).items()}
+        src = dict(hv)
+        src["step"] = self._step_count
+        self.phase_seconds["action"] += t1 - t0
+        self.phase_seconds["physics"] += t2 - t1  # the fused kernel covers every phase
+        return StepOutput(obs.numpy(), hv["rewards"], hv["dones"].astype(bool), hv["events"], src,
+                          to_host=True)
+
+    # ------------------------------------------------------------------ resets
+    def teleport_reset(self, mask, new_starts=None, new_goals=None, new_headings=None):
+        """Masked teleport reset (engine.py:599-619)."""
+        dev = self.device
+
+        def to_dev(a, dtype):
+            if a is None:
+                return None
+            if isinstance(a, torch.Tensor):
+                return a.to(device=dev, dtype=dtype).contiguous()
+            return torch.as_tensor(np.ascontiguousarray(a)).to(device=dev, dtype=dtype)
+
+        m = to_dev(np.asarray(mask, dtype=bool) if not isinstance(mask, torch.Tensor) else mask, torch.uint8)
+        N.check(self._lib, self._lib.dg_reset(self._h, _ptr(m), _ptr(to_dev(new_starts, torch.float64)),
+                                              _ptr(to_dev(new_goals, torch.float64)),
+                                              _ptr(to_dev(new_headings, torch.float64)), self._stream()),
+                "dg_reset")
+        self.launches += 1
+
+    # ------------------------------------------------------------------ policies / episodes
+    def lane_follower(self, obs: torch.Tensor, out: torch.Tensor | None = None, steer_gain=2.0,
+                      throttle=0.5) -> torch.Tensor:
+        """Device LaneFollower: float64 actions identical to the numpy policy."""
+        acts = out if out is not None else torch.empty((self.W, self.M, 3), dtype=torch.float64,
+                                                       device=self.device)
+        N.check(self._lib, self._lib.dg_lane_follower(self._h, _ptr(obs), _ptr(acts), float(steer_gain),
+                                                      float(throttle), self._stream()),
+                "dg_lane_follower")
+        self.launches += 1
+        return acts
+
+    def run_episode(self, policy, record: bool = False, max_steps: int | None = None) -> list:
+        """Step until every agent terminated or the episode times out
+        (engine.py:621-643); returns the per-step records when ``record``."""
+        log = []
+        limit = max_steps if max_steps is not None else self.config.episode_len
+        obs = self.observe()
+        for _ in range(limit):
+            actions = policy(obs)
+            out = self.step(actions)
+            if record:
+                log.append({"step": self._step_count, "state": out.info["state"],
+                            "actions": np.array(actions, dtype=np.float64), "rewards": out.rewards,
+                            "terms": out.info["reward_terms"], "events": out.events,
+                            "dones": out.dones, "alive": out.info["alive"],
+                            "alive_pre": out.info["alive_pre"]})
+            obs = out.obs
+            if not out.info["alive"].any() or self._step_count >= self.config.episode_len:
+                break
+        return log
