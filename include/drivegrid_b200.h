@@ -166,6 +166,10 @@ int dg_lane_follower(dg_engine* eng, const float* obs, double* actions, double s
 /* Kernel launches issued by the last dg_step/dg_observe/dg_reset call. */
 int dg_launch_count(dg_engine* eng);
 
+/* Launch shape: warps per world CTA (1..16, default M); agents are strided
+ * over the warps.  A performance knob only -- results do not depend on it. */
+int dg_tune(dg_engine* eng, int32_t warps_per_world);
+
 const char* dg_last_error(void);
 int dg_abi_version(void);
 

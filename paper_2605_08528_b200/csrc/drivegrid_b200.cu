@@ -328,92 +328,57 @@ __device__ __forceinline__ double swept_ttc(double dx, double dy, double ux, dou
 }
 
 // ----------------------------------------------------------------- observation row
-struct RowCtx {
-    const float* ego;      // [ego_dim]
-    const float* nb;       // [take_veh][7]
-    const uint16_t* cand;  // [ncand]
-    SceneView g;
-    double px, py, c, s;
-    int ncand, nnb, ego_dim, road_end;
-    double road_radius, type_norm;
-};
-
-__device__ __forceinline__ float road_feature(const RowCtx& r, int p, int f) {
-    if (f == 2) return __double2float_rn(double(r.g.type[p]) / r.type_norm);
-    double val;
-    if (f < 2) {
-        const double dx = r.g.mx[p] - r.px, dy = r.g.my[p] - r.py;
-        val = (f == 0 ? r.c * dx + r.s * dy : -r.s * dx + r.c * dy) / r.road_radius;
-    } else {
-        const double ux = r.g.dx[p], uy = r.g.dy[p];
-        val = (f == 3) ? r.c * ux + r.s * uy : -r.s * ux + r.c * uy;
-    }
-    return __double2float_rn(val);
-}
-
-__device__ __forceinline__ float obs_value(const RowCtx& r, int e) {
-    if (e < r.ego_dim) return r.ego[e];
-    if (e < r.road_end) {
-        const int q = e - r.ego_dim;
-        const int slot = q / 5;
-        if (slot >= r.ncand) return 0.0f;
-        return road_feature(r, r.cand[slot], q - slot * 5);
-    }
-    const int q = e - r.road_end;
-    const int slot = q / 7;
-    if (slot >= r.nnb) return 0.0f;
-    return r.nb[q];
-}
-
-__device__ __forceinline__ void write_row(float* row, int D, const RowCtx& r, int lane) {
+// The row is mostly zeros (~190 of 1929 values are non-zero): the owning warp
+// streams zeros with 16-byte st.global.cs, then -- ordered by a barrier --
+// the non-zero features are scattered by the lanes that computed them.
+__device__ __forceinline__ void zero_row(float* row, int D, int lane) {
     const int mis = int((reinterpret_cast<uintptr_t>(row) >> 2) & 3);
     int head = (4 - mis) & 3;
     if (head > D) head = D;
-    if (lane < head) row[lane] = obs_value(r, lane);
+    if (lane < head) row[lane] = 0.0f;
     const int nvec = (D - head) >> 2;
     float4* body = reinterpret_cast<float4*>(row + head);
-    for (int q = lane; q < nvec; q += 32) {
-        const int e = head + 4 * q;
-        float4 v;
-        v.x = obs_value(r, e);
-        v.y = obs_value(r, e + 1);
-        v.z = obs_value(r, e + 2);
-        v.w = obs_value(r, e + 3);
-        __stcs(body + q, v);
-    }
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+    for (int q = lane; q < nvec; q += 32) __stcs(body + q, z);
     const int tail0 = head + 4 * nvec;
-    if (tail0 + lane < D) row[tail0 + lane] = obs_value(r, tail0 + lane);
+    if (tail0 + lane < D) row[tail0 + lane] = 0.0f;
 }
 
+// Per-agent results of the warp scans, consumed by the finalize warp.
+struct ScanSm {
+    double ttc_min;
+    double lane_d2;
+    double gap;
+    int lane_k;
+    int edge_hit;
+    int touch;
+    int pad_;
+};
+
 // ----------------------------------------------------------------- the fused step kernel
-template <bool kStep>
-__global__ void __launch_bounds__(32 * kMaxAgents)
+template <bool kStep, int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
 world_step_kernel(const KArgs A) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int w = blockIdx.x;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
+    const int nwarps = blockDim.x >> 5;
     const int M = A.d.M;
     const int WM = A.d.W * M;
+    const int D = A.d.obs_dim;
     const DgConsts& k = A.k;
 
     // ---- shared memory carve-up
-    const int blob_bytes = A.d.max_scene_bytes;
     uint8_t* geo = smem;
-    AgentSm* ag = reinterpret_cast<AgentSm*>(smem + align16(blob_bytes));
-    uint8_t* p = reinterpret_cast<uint8_t*>(ag + kMaxAgents);
-    float* ego_sm = reinterpret_cast<float*>(p);                   // [M][16]
-    p += align16(sizeof(float) * 16 * kMaxAgents);
-    float* nb_sm = reinterpret_cast<float*>(p);                    // [M][take_veh*7]
-    p += align16(sizeof(float) * 7 * kMaxAgents * (A.take_veh > 0 ? A.take_veh : 1));
-    uint16_t* cand_sm = reinterpret_cast<uint16_t*>(p);            // [M][take_road]
-    p += align16(sizeof(uint16_t) * kMaxAgents * (A.take_road > 0 ? A.take_road : 1));
-    uint64_t* bar = reinterpret_cast<uint64_t*>(p);
+    AgentSm* ag = reinterpret_cast<AgentSm*>(smem + align16(A.d.max_scene_bytes));
+    ScanSm* sc = reinterpret_cast<ScanSm*>(ag + kMaxAgents);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sc + kMaxAgents);
     __shared__ int s_bad;
 
     // ---- phase 0: action scan (the reference rejects before mutating)
-    Act act{0.0, 0.0, 0.0};
     int step_now = 0;
     if constexpr (kStep) {
         if (tid == 0) s_bad = DG_NO_ERROR;
@@ -432,20 +397,19 @@ world_step_kernel(const KArgs A) {
         step_now = A.step_count[w];
     }
 
-    // ---- geometry: one bulk async copy of the world's scene blob
+    // ---- geometry: one bulk async copy of the world's scene blob (TMA engine)
     const int scene = A.scene_of_world[w];
     const int64_t* meta = A.scene_meta + 8 * scene;
-    const int64_t g_off = meta[0];
-    const uint32_t g_bytes = uint32_t(meta[1]);
     const SceneView G = scene_view(geo, int(meta[2]), int(meta[3]), int(meta[4]));
     if (tid == 0) {
         mbar_init(bar, 1);
-        bulk_load(geo, A.scene_blob + g_off, g_bytes, bar);
+        bulk_load(geo, A.scene_blob + meta[0], uint32_t(meta[1]), bar);
     }
-
     const double ox = A.grid_offset[2 * w], oy = A.grid_offset[2 * w + 1];
+    float* obs_w = A.obs + int64_t(w) * M * D;
 
-    // ---- phase 1: warp 0 lane m owns agent m: load, physics, derived values
+    // ---- phase 1: warp 0, lane m: agent m load + physics (SIMT across agents);
+    //      every warp streams the zero background of its agents' obs rows
     if (warp == 0 && lane < M) {
         const int m = lane;
         const int64_t am = int64_t(w) * M + m;
@@ -466,6 +430,7 @@ world_step_kernel(const KArgs A) {
                 const float* a = reinterpret_cast<const float*>(A.actions);
                 raw0 = a[ab]; raw1 = a[ab + 1]; raw2 = a[ab + 2];
             }
+            Act act;
             act.thr = np_clip(raw0, 0.0, 1.0);
             act.steer = np_clip(raw1, -1.0, 1.0);
             act.brk = np_clip(raw2, 0.0, 1.0);
@@ -505,11 +470,11 @@ world_step_kernel(const KArgs A) {
         S.seen = A.event_seen[am];
         S.spawn = A.spawn_step[am];
     }
+    for (int m = warp; m < M; m += nwarps) zero_row(obs_w + int64_t(m) * D, D, lane);
 
-    // ---- geometry lands; shift scene-local midpoints to global (midpoints + off)
-    __syncthreads();  // agent table written, mbarrier init visible to every thread
+    __syncthreads();  // agent table + zero rows done, mbarrier init visible
     mbar_wait(bar, 0);
-    {
+    {   // scene-local midpoints -> global, exactly midpoints + grid offset
         double* mx = const_cast<double*>(G.mx);
         double* my = const_cast<double*>(G.my);
         for (int i = tid; i < G.P; i += blockDim.x) {
@@ -519,34 +484,43 @@ world_step_kernel(const KArgs A) {
     }
     __syncthreads();
 
-    // ---- phase 2: warp m works for agent m
-    for (int m = warp; m < M; m += blockDim.x >> 5) {
+    // ---- phase 2: warp m scans for agent m and scatters its road/neighbour rows
+    const int road0 = A.d.ego_dim;
+    const int veh0 = A.d.ego_dim + 5 * A.d.k_road;
+    for (int m = warp; m < M; m += nwarps) {
         const AgentSm& S = ag[m];
-        const int64_t am = int64_t(w) * M + m;
+        float* row = obs_w + int64_t(m) * D;
         const double px = S.st[SX], py = S.st[SY];
         const double c = S.c, s = S.s;
 
-        // (a) road context: candidates d2 <= r^2 in segment order, first take
-        uint16_t* cand = cand_sm + m * A.take_road;
+        // (a) road context: candidates d2 <= r^2, ordered by segment index, first take
         int count = 0;
         for (int p0 = 0; p0 < G.P; p0 += 32) {
             const int q = p0 + lane;
             bool hit = false;
+            double dx = 0.0, dy = 0.0;
             if (q < G.P) {
-                const double dx = G.mx[q] - px, dy = G.my[q] - py;
+                dx = G.mx[q] - px;
+                dy = G.my[q] - py;
                 hit = dx * dx + dy * dy <= k.road_radius_sq;
             }
             const unsigned bal = __ballot_sync(kFull, hit);
             if (hit) {
                 const int slot = count + __popc(bal & ((1u << lane) - 1u));
-                if (slot < A.take_road) cand[slot] = uint16_t(q);
+                if (slot < A.take_road) {
+                    float* o = row + road0 + 5 * slot;
+                    const double ux = G.dx[q], uy = G.dy[q];
+                    o[0] = __double2float_rn((c * dx + s * dy) / k.road_radius);
+                    o[1] = __double2float_rn((-s * dx + c * dy) / k.road_radius);
+                    o[2] = __double2float_rn(double(G.type[q]) / k.type_norm);
+                    o[3] = __double2float_rn(c * ux + s * uy);
+                    o[4] = __double2float_rn(-s * ux + c * uy);
+                }
             }
             count += __popc(bal);
         }
-        const int ncand = count < A.take_road ? count : A.take_road;
 
-        // (b) neighbours: lane j looks at agent j
-        float* nb = nb_sm + m * 7 * (A.take_veh > 0 ? A.take_veh : 1);
+        // (b) neighbours: lane j <-> agent j; stable rank by distance
         double key = INFINITY, ndx = 0.0, ndy = 0.0;
         if (lane < M) {
             const AgentSm& N = ag[lane];
@@ -566,49 +540,23 @@ world_step_kernel(const KArgs A) {
             const AgentSm& N = ag[lane];
             ttc = swept_ttc(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c, N.s, N.d,
                             S.r + N.r, k.ttc_max);
-            const double turn = N.st[SYAW] - S.st[SYAW];
             double st_, ct_;
-            sincos(turn, &st_, &ct_);
+            sincos(N.st[SYAW] - S.st[SYAW], &st_, &ct_);
             const double wrap = atan2(st_, ct_);
             const double spd = sqrt(N.st[SVX] * N.st[SVX] + N.st[SVY] * N.st[SVY]);
-            float* row = nb + rank * 7;
-            row[0] = __double2float_rn((c * ndx + s * ndy) / k.bbox_half);
-            row[1] = __double2float_rn((-s * ndx + c * ndy) / k.bbox_half);
-            row[2] = __double2float_rn(N.len / k.bbox_half);
-            row[3] = __double2float_rn(N.wid / k.bbox_half);
-            row[4] = __double2float_rn(wrap / 3.141592653589793);
-            row[5] = __double2float_rn(spd / k.speed_norm);
-            row[6] = __double2float_rn(ttc / k.ttc_max);
+            float* o = row + veh0 + 7 * rank;
+            o[0] = __double2float_rn((c * ndx + s * ndy) / k.bbox_half);
+            o[1] = __double2float_rn((-s * ndx + c * ndy) / k.bbox_half);
+            o[2] = __double2float_rn(N.len / k.bbox_half);
+            o[3] = __double2float_rn(N.wid / k.bbox_half);
+            o[4] = __double2float_rn(wrap / 3.141592653589793);
+            o[5] = __double2float_rn(spd / k.speed_norm);
+            o[6] = __double2float_rn(ttc / k.ttc_max);
         }
-        const int nnb = __popc(__ballot_sync(kFull, nvalid));
         const double ttc_min = warp_min(nvalid ? ttc : k.ttc_max);
 
-        // (c) ego block
-        float* ego = ego_sm + 16 * m;
-        if (lane == 0) {
-            const double gdx = S.gx - px, gdy = S.gy - py;
-            const double xb = c * gdx + s * gdy;
-            const double yb = -s * gdx + c * gdy;
-            const double hdg = atan2(yb, xb);
-            double sh, ch;
-            sincos(hdg, &sh, &ch);
-            ego[0] = __double2float_rn(xb / k.bbox_half);
-            ego[1] = __double2float_rn(yb / k.bbox_half);
-            ego[2] = __double2float_rn(sh);
-            ego[3] = __double2float_rn(ch);
-            ego[4] = __double2float_rn(sqrt(xb * xb + yb * yb) / k.bbox_half);
-            ego[5] = __double2float_rn(S.st[SVX] / k.speed_norm);
-            ego[6] = __double2float_rn(S.st[SVY] / k.speed_norm);
-            if (A.d.include_weather) {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) ego[7 + i] = __double2float_rn(A.weather[4 * w + i]);
-            }
-        }
-        __syncwarp();
-
-        // (d) rewards, events, termination (engine.py:472-509)
         if constexpr (kStep) {
-            // nearest lane: argmin of point-to-segment d2, lowest index on ties
+            // (c) nearest lane: argmin of point-to-segment d2, lowest index on ties
             double best = INFINITY;
             int best_k = 0x7fffffff;
             for (int kk = lane; kk < G.KL; kk += 32) {
@@ -617,7 +565,7 @@ world_step_kernel(const KArgs A) {
                 const double ux = G.dx[q], uy = G.dy[q];
                 const double along = ex * ux + ey * uy;
                 const double lat = ux * ey - uy * ex;
-                const double over = np_max(fabs(along) - G.hl[q], 0.0);
+                const double over = fmax(fabs(along) - G.hl[q], 0.0);
                 const double d2 = over * over + lat * lat;
                 if (d2 < best) { best = d2; best_k = kk; }
             }
@@ -626,28 +574,34 @@ world_step_kernel(const KArgs A) {
                 const int ok = __shfl_xor_sync(kFull, best_k, o);
                 if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
             }
-            // first road edge ahead and the hull-vs-edge-box test
+            // (d) first road edge ahead, and the hull-vs-edge-box test behind a
+            //     conservative distance filter (skips boxes farther than
+            //     r + d + half_len + half_wid, + 1 micron of rounding slack)
             double gap = INFINITY;
             bool edge_hit = false;
+            const double r2 = S.r * S.r;
             for (int kk = lane; kk < G.KE; kk += 32) {
                 const int q = G.edge[kk];
-                const double xb = c * (G.mx[q] - px) + s * (G.my[q] - py);
-                if (xb > 0.0 && xb <= k.edge_range) gap = np_min(gap, xb);
+                const double ex = G.mx[q] - px, ey = G.my[q] - py;
+                const double xb = c * ex + s * ey;
+                if (xb > 0.0 && xb <= k.edge_range) gap = fmin(gap, xb);
                 const double ux = G.dx[q], uy = G.dy[q], hl = G.hl[q], hw = G.hw[q];
-                const double r2 = S.r * S.r;
+                const double reach = S.r + S.d + hl + hw + 1e-6;
+                if (ex * ex + ey * ey <= reach * reach) {
 #pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    const double qx = S.hx[i] - G.mx[q], qy = S.hy[i] - G.my[q];
-                    const double along = qx * ux + qy * uy;
-                    const double lat = ux * qy - uy * qx;
-                    const double du = along - np_clip(along, -hl, hl);
-                    const double dv = lat - np_clip(lat, -hw, hw);
-                    edge_hit |= du * du + dv * dv < r2;
+                    for (int i = 0; i < 3; ++i) {
+                        const double qx = S.hx[i] - G.mx[q], qy = S.hy[i] - G.my[q];
+                        const double along = qx * ux + qy * uy;
+                        const double lat = ux * qy - uy * qx;
+                        const double du = along - fmin(fmax(along, -hl), hl);
+                        const double dv = lat - fmin(fmax(lat, -hw), hw);
+                        edge_hit |= du * du + dv * dv < r2;
+                    }
                 }
             }
-            gap = warp_min(gap);
+            for (int o = 16; o > 0; o >>= 1) gap = fmin(gap, __shfl_xor_sync(kFull, gap, o));
             edge_hit = __any_sync(kFull, edge_hit);
-            // hull contact with any other alive agent (both alive, not self)
+            // (e) hull contact with any other alive agent
             bool touch = false;
             if (lane < M && lane != m && S.alive && ag[lane].alive) {
                 const AgentSm& N = ag[lane];
@@ -662,143 +616,166 @@ world_step_kernel(const KArgs A) {
                     }
             }
             touch = __any_sync(kFull, touch);
-
             if (lane == 0) {
-                const double vx = S.st[SVX], vy = S.st[SVY], yaw = S.st[SYAW];
-                const double dist = sqrt(best);
-                const bool has_lane = finite(dist);
-                double lat = 0.0, tx = 0.0, ty = 0.0;
-                if (has_lane) {
-                    const int q = G.lane[best_k];
-                    const double ex = px - G.mx[q], ey = py - G.my[q];
-                    tx = G.dx[q];
-                    ty = G.dy[q];
-                    lat = tx * ey - ty * ex;
-                }
-                const double tgx = S.gx - px, tgy = S.gy - py;
-                const double flip = (tx * tgx + ty * tgy >= 0.0) ? 1.0 : -1.0;
-                tx = tx * flip;
-                ty = ty * flip;
-                double progress = np_clip((px - S.px0) * tx + (py - S.py0) * ty,
-                                          -k.progress_clamp, k.progress_clamp) * k.progress_weight;
-                const double align = np_max(0.0, cos(yaw - atan2(ty, tx)));
-                const double ls = lat / k.lane_sigma;
-                const double quality = exp(-(ls * ls)) * (k.lane_heading_base + k.lane_heading_weight * align);
-                const double lane_t = has_lane ? k.lane_weight * quality : 0.0;
-                progress = has_lane ? progress : 0.0;
-                const double offroad = (has_lane && (fabs(lat) > k.offroad_lat_limit || dist > k.offroad_dist_limit))
-                                           ? -k.offroad_weight : 0.0;
-                const double speed = sqrt(vx * vx + vy * vy);
-                const double idle = speed < k.idle_speed ? -k.idle_weight : 0.0;
-                const double ttc_v = -np_min(k.ttc_vehicle_alpha / np_max(ttc_min, k.ttc_floor), k.ttc_vehicle_pmax);
-                const double tau = gap / np_max(vx, 0.1);
-                const double ttc_e = finite(tau) ? -np_min(k.ttc_edge_alpha / np_max(tau, k.ttc_floor), k.ttc_edge_pmax)
-                                                 : 0.0;
-                const double total = progress + lane_t + offroad + idle + ttc_v + ttc_e;
-
-                // sparse events, masked by alive and the per-type latch
-                const bool alive = S.alive;
-                const bool goal = sqrt(tgx * tgx + tgy * tgy) <= k.goal_radius;
-                const double sxd = px - S.sx, syd = py - S.sy;
-                const bool bad = !(finite(px) && finite(py) && finite(vx) && finite(vy));
-                const bool crash = sqrt(sxd * sxd + syd * syd) > k.crash_drift_limit || bad ||
-                                   speed > k.crash_speed_limit;
-                const int age = step_now - S.spawn;
-                const bool coll = touch && age >= A.d.collision_warmup;
-                const int seen = S.seen;
-                const bool e_goal = goal && alive && !(seen & 1);
-                const bool e_coll = coll && alive && !(seen & 2);
-                const bool e_crash = crash && alive && !(seen & 4);
-                const bool e_lf = edge_hit && alive && !(seen & 8);
-                int rnow = e_goal ? 1 : (e_crash ? 3 : (e_lf ? 4 : (e_coll ? 2 : 0)));
-                const int bit = rnow == 1 ? 1 : rnow == 2 ? 2 : rnow == 3 ? 4 : rnow == 4 ? 8 : 0;
-                int seen_new = seen | bit;
-                const double sparse = rnow == 1 ? k.goal_weight
-                                    : rnow == 2 ? -k.collision_weight
-                                    : rnow == 3 ? -k.crash_weight
-                                    : rnow == 4 ? -k.lane_forbidden_weight : 0.0;
-                const double reward = alive ? total + sparse : 0.0;
-                int reason = S.reason;
-                bool done = false;
-                if (!A.d.invincible) {
-                    done = rnow != 0;
-                    if (done && reason == 0) reason = rnow;
-                }
-                // tail: timeout, park, alive (engine.py:370-393)
-                const int step_new = step_now + 1;
-                const bool timeout = step_new >= A.d.episode_len && alive;
-                const bool finished = done || timeout;
-                if (timeout && reason == 0) reason = 5;
-                const bool park = done && !timeout;
-                int alive_new = alive && !finished;
-
-                A.rewards[am] = reward;
-                A.dones[am] = finished;
-                reinterpret_cast<uint32_t*>(A.events)[am] =
-                    uint32_t(rnow == 1) | (uint32_t(rnow == 2) << 8) | (uint32_t(rnow == 3) << 16) |
-                    (uint32_t(rnow == 4) << 24);
-                if (A.reason_out) A.reason_out[am] = int8_t(reason);
-                if (A.alive_out) A.alive_out[am] = uint8_t(alive_new);
-                if (A.alive_pre_out) A.alive_pre_out[am] = uint8_t(alive);
-                if (A.ttc_min_out) A.ttc_min_out[am] = ttc_min;
-                if (A.terms_out) {
-                    const double t7[7] = {progress, lane_t, offroad, idle, ttc_v, ttc_e, total};
-#pragma unroll
-                    for (int i = 0; i < 7; ++i) A.terms_out[int64_t(i) * WM + am] = alive ? t7[i] : 0.0;
-                }
-                if (A.snapshot_out) {
-#pragma unroll
-                    for (int f = 0; f < DG_NUM_STATE; ++f) A.snapshot_out[int64_t(f) * WM + am] = S.st[f];
-                }
-                double x[DG_NUM_STATE];
-#pragma unroll
-                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = S.st[f];
-                if (park) {
-#pragma unroll
-                    for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
-                    x[SX] = ox + k.offstage_x;
-                    x[SY] = oy;
-                }
-                int spawn = S.spawn;
-                if (A.autoreset && finished && S.valid) {
-#pragma unroll
-                    for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
-                    x[SX] = S.sx;
-                    x[SY] = S.sy;
-                    x[SYAW] = A.start_yaw[am];
-                    alive_new = 1;
-                    reason = 0;
-                    spawn = step_new;
-                    seen_new = 0;
-                }
-#pragma unroll
-                for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = x[f];
-                A.alive[am] = uint8_t(alive_new);
-                A.reason[am] = int8_t(reason);
-                A.event_seen[am] = uint8_t(seen_new);
-                A.spawn_step[am] = spawn;
+                ScanSm& R = sc[m];
+                R.ttc_min = ttc_min;
+                R.lane_d2 = best;
+                R.lane_k = best_k;
+                R.gap = gap;
+                R.edge_hit = edge_hit;
+                R.touch = touch;
             }
         } else {
-            if (lane == 0 && A.ttc_min_out) A.ttc_min_out[am] = ttc_min;
+            if (lane == 0 && A.ttc_min_out) A.ttc_min_out[int64_t(w) * M + m] = ttc_min;
         }
-
-        // (e) the observation row
-        RowCtx rc;
-        rc.ego = ego;
-        rc.nb = nb;
-        rc.cand = cand;
-        rc.g = G;
-        rc.px = px; rc.py = py; rc.c = c; rc.s = s;
-        rc.ncand = ncand;
-        rc.nnb = nnb;
-        rc.ego_dim = A.d.ego_dim;
-        rc.road_end = A.d.ego_dim + 5 * A.d.k_road;
-        rc.road_radius = k.road_radius;
-        rc.type_norm = k.type_norm;
-        write_row(A.obs + am * A.d.obs_dim, A.d.obs_dim, rc, lane);
     }
+    __syncthreads();
 
+    // ---- phase 3: one lane per agent (SIMT across the world's agents):
+    //      warp 0 -> rewards, events, termination, state write-back;
+    //      warp 1 (or warp 0 afterwards) -> the ego block
+    const int ego_warp = nwarps > 1 ? 1 : 0;
+    if (warp == ego_warp && lane < M) {
+        const int m = lane;
+        const AgentSm& S = ag[m];
+        float* row = obs_w + int64_t(m) * D;
+        const double px = S.st[SX], py = S.st[SY], c = S.c, s = S.s;
+        const double gdx = S.gx - px, gdy = S.gy - py;
+        const double xb = c * gdx + s * gdy;
+        const double yb = -s * gdx + c * gdy;
+        double sh, ch;
+        sincos(atan2(yb, xb), &sh, &ch);
+        row[0] = __double2float_rn(xb / k.bbox_half);
+        row[1] = __double2float_rn(yb / k.bbox_half);
+        row[2] = __double2float_rn(sh);
+        row[3] = __double2float_rn(ch);
+        row[4] = __double2float_rn(sqrt(xb * xb + yb * yb) / k.bbox_half);
+        row[5] = __double2float_rn(S.st[SVX] / k.speed_norm);
+        row[6] = __double2float_rn(S.st[SVY] / k.speed_norm);
+        if (A.d.include_weather) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) row[7 + i] = __double2float_rn(A.weather[4 * w + i]);
+        }
+    }
     if constexpr (kStep) {
+        if (warp == 0 && lane < M) {
+            const int m = lane;
+            const int64_t am = int64_t(w) * M + m;
+            const AgentSm& S = ag[m];
+            const ScanSm& R = sc[m];
+            const double px = S.st[SX], py = S.st[SY];
+            const double vx = S.st[SVX], vy = S.st[SVY], yaw = S.st[SYAW];
+            const double dist = sqrt(R.lane_d2);
+            const bool has_lane = finite(dist);
+            double lat = 0.0, tx = 0.0, ty = 0.0;
+            if (has_lane) {
+                const int q = G.lane[R.lane_k];
+                const double ex = px - G.mx[q], ey = py - G.my[q];
+                tx = G.dx[q];
+                ty = G.dy[q];
+                lat = tx * ey - ty * ex;
+            }
+            const double tgx = S.gx - px, tgy = S.gy - py;
+            const double flip = (tx * tgx + ty * tgy >= 0.0) ? 1.0 : -1.0;
+            tx = tx * flip;
+            ty = ty * flip;
+            double progress = np_clip((px - S.px0) * tx + (py - S.py0) * ty,
+                                      -k.progress_clamp, k.progress_clamp) * k.progress_weight;
+            const double align = np_max(0.0, cos(yaw - atan2(ty, tx)));
+            const double ls = lat / k.lane_sigma;
+            const double quality = exp(-(ls * ls)) * (k.lane_heading_base + k.lane_heading_weight * align);
+            const double lane_t = has_lane ? k.lane_weight * quality : 0.0;
+            progress = has_lane ? progress : 0.0;
+            const double offroad = (has_lane && (fabs(lat) > k.offroad_lat_limit || dist > k.offroad_dist_limit))
+                                       ? -k.offroad_weight : 0.0;
+            const double speed = sqrt(vx * vx + vy * vy);
+            const double idle = speed < k.idle_speed ? -k.idle_weight : 0.0;
+            const double ttc_v = -np_min(k.ttc_vehicle_alpha / np_max(R.ttc_min, k.ttc_floor), k.ttc_vehicle_pmax);
+            const double tau = R.gap / np_max(vx, 0.1);
+            const double ttc_e = finite(tau) ? -np_min(k.ttc_edge_alpha / np_max(tau, k.ttc_floor), k.ttc_edge_pmax)
+                                             : 0.0;
+            const double total = progress + lane_t + offroad + idle + ttc_v + ttc_e;
+
+            // sparse events, masked by alive and the per-type latch
+            const bool alive = S.alive;
+            const bool goal = sqrt(tgx * tgx + tgy * tgy) <= k.goal_radius;
+            const double sxd = px - S.sx, syd = py - S.sy;
+            const bool bad = !(finite(px) && finite(py) && finite(vx) && finite(vy));
+            const bool crash = sqrt(sxd * sxd + syd * syd) > k.crash_drift_limit || bad ||
+                               speed > k.crash_speed_limit;
+            const bool coll = R.touch && step_now - S.spawn >= A.d.collision_warmup;
+            const int seen = S.seen;
+            const bool e_goal = goal && alive && !(seen & 1);
+            const bool e_coll = coll && alive && !(seen & 2);
+            const bool e_crash = crash && alive && !(seen & 4);
+            const bool e_lf = R.edge_hit && alive && !(seen & 8);
+            const int rnow = e_goal ? 1 : (e_crash ? 3 : (e_lf ? 4 : (e_coll ? 2 : 0)));
+            int seen_new = seen | (rnow == 0 ? 0 : 1 << (rnow == 1 ? 0 : rnow == 2 ? 1 : rnow == 3 ? 2 : 3));
+            const double sparse = rnow == 1 ? k.goal_weight
+                                : rnow == 2 ? -k.collision_weight
+                                : rnow == 3 ? -k.crash_weight
+                                : rnow == 4 ? -k.lane_forbidden_weight : 0.0;
+            const double reward = alive ? total + sparse : 0.0;
+            int reason = S.reason;
+            bool done = false;
+            if (!A.d.invincible) {
+                done = rnow != 0;
+                if (done && reason == 0) reason = rnow;
+            }
+            // tail: timeout, park, alive (engine.py:370-393)
+            const int step_new = step_now + 1;
+            const bool timeout = step_new >= A.d.episode_len && alive;
+            const bool finished = done || timeout;
+            if (timeout && reason == 0) reason = 5;
+            const bool park = done && !timeout;
+            int alive_new = alive && !finished;
+
+            A.rewards[am] = reward;
+            A.dones[am] = finished;
+            reinterpret_cast<uint32_t*>(A.events)[am] =
+                uint32_t(rnow == 1) | (uint32_t(rnow == 2) << 8) | (uint32_t(rnow == 3) << 16) |
+                (uint32_t(rnow == 4) << 24);
+            if (A.reason_out) A.reason_out[am] = int8_t(reason);
+            if (A.alive_out) A.alive_out[am] = uint8_t(alive_new);
+            if (A.alive_pre_out) A.alive_pre_out[am] = uint8_t(alive);
+            if (A.ttc_min_out) A.ttc_min_out[am] = R.ttc_min;
+            if (A.terms_out) {
+                const double t7[7] = {progress, lane_t, offroad, idle, ttc_v, ttc_e, total};
+#pragma unroll
+                for (int i = 0; i < 7; ++i) A.terms_out[int64_t(i) * WM + am] = alive ? t7[i] : 0.0;
+            }
+            if (A.snapshot_out) {
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) A.snapshot_out[int64_t(f) * WM + am] = S.st[f];
+            }
+            double x[DG_NUM_STATE];
+#pragma unroll
+            for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = S.st[f];
+            if (park) {
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
+                x[SX] = ox + k.offstage_x;
+                x[SY] = oy;
+            }
+            int spawn = S.spawn;
+            if (A.autoreset && finished && S.valid) {
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
+                x[SX] = S.sx;
+                x[SY] = S.sy;
+                x[SYAW] = A.start_yaw[am];
+                alive_new = 1;
+                reason = 0;
+                spawn = step_new;
+                seen_new = 0;
+            }
+#pragma unroll
+            for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = x[f];
+            A.alive[am] = uint8_t(alive_new);
+            A.reason[am] = int8_t(reason);
+            A.event_seen[am] = uint8_t(seen_new);
+            A.spawn_step[am] = spawn;
+        }
         if (tid == 0) A.step_count[w] = step_now + 1;
     }
 }
@@ -864,7 +841,36 @@ struct dg_engine {
     KArgs base;
     size_t smem_bytes;
     int launches;
+    int warps_per_world;   // CTA = warps_per_world warps, agents strided over warps
 };
+
+// Kernel variants: (threads per CTA, min resident CTAs per SM) bounds trade
+// registers for occupancy; dg_tune picks one.
+template <bool kStep>
+static cudaError_t launch_world_step(const dg_engine* e, const KArgs& A, cudaStream_t st) {
+    const int nw = e->warps_per_world;
+    const dim3 grid(A.d.W);
+    if (nw > 8)
+        world_step_kernel<kStep, 512, 1><<<grid, 32 * nw, e->smem_bytes, st>>>(A);
+    else if (nw > 4)
+        world_step_kernel<kStep, 256, 2><<<grid, 32 * nw, e->smem_bytes, st>>>(A);
+    else
+        world_step_kernel<kStep, 128, 4><<<grid, 32 * nw, e->smem_bytes, st>>>(A);
+    return cudaGetLastError();
+}
+
+template <bool kStep>
+static cudaError_t set_smem_attr(size_t bytes) {
+    cudaError_t e = cudaFuncSetAttribute(world_step_kernel<kStep, 512, 1>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(world_step_kernel<kStep, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(bytes));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(world_step_kernel<kStep, 128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(bytes));
+    return e;
+}
 
 static thread_local char g_err[512] = "";
 
@@ -878,12 +884,9 @@ static int cuda_fail(cudaError_t e, const char* where) {
     return DG_ECUDA;
 }
 
-static size_t step_smem_bytes(const DgDims& d, int take_road, int take_veh) {
+static size_t step_smem_bytes(const DgDims& d) {
     size_t b = size_t(align16(d.max_scene_bytes));
-    b += sizeof(AgentSm) * kMaxAgents;
-    b += size_t(align16(sizeof(float) * 16 * kMaxAgents));
-    b += size_t(align16(sizeof(float) * 7 * kMaxAgents * (take_veh > 0 ? take_veh : 1)));
-    b += size_t(align16(sizeof(uint16_t) * kMaxAgents * (take_road > 0 ? take_road : 1)));
+    b += sizeof(AgentSm) * kMaxAgents + sizeof(ScanSm) * kMaxAgents;
     b += 16;  // mbarrier
     return b;
 }
@@ -940,21 +943,19 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
     A.error_word = desc->error_word;
     A.take_road = d.k_road < d.max_segments ? d.k_road : d.max_segments;
     A.take_veh = d.k_vehicles < d.M ? d.k_vehicles : d.M;
-    e->smem_bytes = step_smem_bytes(d, A.take_road, A.take_veh);
+    e->smem_bytes = step_smem_bytes(d);
     if (e->smem_bytes > 227 * 1024) {
         delete e;
         return fail(DG_ENOSUPPORT, "dg_create: scene geometry does not fit in shared memory");
     }
-    cudaError_t err = cudaFuncSetAttribute(world_step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(e->smem_bytes));
-    if (err == cudaSuccess)
-        err = cudaFuncSetAttribute(world_step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(e->smem_bytes));
+    cudaError_t err = set_smem_attr<true>(e->smem_bytes);
+    if (err == cudaSuccess) err = set_smem_attr<false>(e->smem_bytes);
     if (err != cudaSuccess) {
         delete e;
         return cuda_fail(err, "dg_create: cudaFuncSetAttribute");
     }
     e->launches = 0;
+    e->warps_per_world = d.M;
     *out = e;
     return DG_OK;
 }
@@ -982,9 +983,8 @@ int dg_step(dg_engine* eng, const DgStepIO* io, void* stream) {
     A.ttc_min_out = io->ttc_min_out;
     A.terms_out = io->terms_out;
     A.snapshot_out = io->snapshot_out;
-    world_step_kernel<true><<<A.d.W, 32 * A.d.M, eng->smem_bytes, static_cast<cudaStream_t>(stream)>>>(A);
     eng->launches = 1;
-    const cudaError_t err = cudaGetLastError();
+    const cudaError_t err = launch_world_step<true>(eng, A, static_cast<cudaStream_t>(stream));
     return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_step");
 }
 
@@ -993,9 +993,8 @@ int dg_observe(dg_engine* eng, float* obs, double* ttc_min_out, void* stream) {
     KArgs A = eng->base;
     A.obs = obs;
     A.ttc_min_out = ttc_min_out;
-    world_step_kernel<false><<<A.d.W, 32 * A.d.M, eng->smem_bytes, static_cast<cudaStream_t>(stream)>>>(A);
     eng->launches = 1;
-    const cudaError_t err = cudaGetLastError();
+    const cudaError_t err = launch_world_step<false>(eng, A, static_cast<cudaStream_t>(stream));
     return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_observe");
 }
 
@@ -1061,5 +1060,13 @@ int dg_lane_follower(dg_engine* eng, const float* obs, double* actions, double s
 }
 
 int dg_launch_count(dg_engine* eng) { return eng ? eng->launches : 0; }
+
+int dg_tune(dg_engine* eng, int32_t warps_per_world) {
+    if (!eng) return fail(DG_EINVAL, "dg_tune: null engine");
+    if (warps_per_world < 1 || warps_per_world > kMaxAgents)
+        return fail(DG_EINVAL, "dg_tune: warps_per_world must lie in [1, 16]");
+    eng->warps_per_world = warps_per_world < eng->base.d.M ? warps_per_world : eng->base.d.M;
+    return DG_OK;
+}
 
 }  // extern "C"

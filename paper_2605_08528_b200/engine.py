@@ -287,6 +287,10 @@ class Engine:
     def new_step_buffers(self, obs: torch.Tensor | None = None) -> StepBuffers:
         return self._new_buffers(obs)
 
+    def tune(self, warps_per_world: int) -> None:
+        """Launch shape knob (warps per world CTA); results are unaffected."""
+        N.check(self._lib, self._lib.dg_tune(self._h, int(warps_per_world)), "dg_tune")
+
     # ------------------------------------------------------------------ device state views
     @property
     def state_tensor(self) -> torch.Tensor:
