@@ -80,7 +80,8 @@ typedef struct DgConsts {
  * engine.py:151-230).  Scene geometry is de-duplicated: worlds that share a
  * scene share one blob.  Per-scene blob, 16-byte aligned sections, local
  * coordinates:  f64 mid_x[P], mid_y[P], dir_x[P], dir_y[P], half_len[P],
- * half_wid[P]; i32 type[P]; i32 lane_idx[KL]; i32 edge_idx[KE].
+ * half_wid[P]; f32 type_feat[P] = float32(type / type_norm); i32 lane_idx[KL];
+ * i32 edge_idx[KE].
  * scene_meta[s] = {byte_offset, byte_size, P, KL, KE, 0, 0, 0} (int64). */
 typedef struct DgEngineDesc {
     DgDims dims;

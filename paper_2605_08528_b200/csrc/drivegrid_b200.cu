@@ -123,8 +123,8 @@ struct AgentSm {
     double r, d, len, wid;    // hull radius/offset, length, width
     double hx[3], hy[3];      // hull circle centres
     double gx, gy, sx, sy;    // goal, start (global)
+    float f_len, f_wid, f_spd; // neighbour-row features of this agent: L/100, W/100, speed/10
     int alive, valid, reason, seen, spawn;
-    int pad_;
 };
 
 struct SceneView {
@@ -134,11 +134,21 @@ struct SceneView {
     const double* dy;
     const double* hl;
     const double* hw;
-    const int32_t* type;
+    const float* type_feat;   // float32(type / type_norm), precomputed on the host
     const int32_t* lane;
     const int32_t* edge;
+    // spatial index (paper_2605_08528_b200/spatial.py); flags == 0 -> full scans
+    double gx0, gy0, cell, half;
+    int nx, ny, words, flags;
+    const uint32_t* seg_bits;   // [nx*ny][words]  bit q: midpoint q in the cell
+    const uint32_t* edge_bits;  // [words]         bit q: segment q is a road edge
+    const int32_t* lane_start;  // [nx*ny + 1]
+    const int32_t* lane_list;   // lane-list indices (into lane[]), ascending per cell
     int P, KL, KE;
 };
+
+constexpr int kFlagGrid = 1;
+constexpr int kFlagLanes = 2;
 
 __host__ __device__ __forceinline__ int64_t align16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
@@ -152,9 +162,22 @@ __device__ __forceinline__ SceneView scene_view(uint8_t* base, int P, int KL, in
     v.dy = reinterpret_cast<double*>(base + o); o += f8;
     v.hl = reinterpret_cast<double*>(base + o); o += f8;
     v.hw = reinterpret_cast<double*>(base + o); o += f8;
-    v.type = reinterpret_cast<int32_t*>(base + o); o += align16(int64_t(P) * 4);
+    v.type_feat = reinterpret_cast<float*>(base + o); o += align16(int64_t(P) * 4);
     v.lane = reinterpret_cast<int32_t*>(base + o); o += align16(int64_t(KL) * 4);
-    v.edge = reinterpret_cast<int32_t*>(base + o);
+    v.edge = reinterpret_cast<int32_t*>(base + o); o += align16(int64_t(KE) * 4);
+    const double* hd = reinterpret_cast<const double*>(base + o);
+    const int32_t* hi = reinterpret_cast<const int32_t*>(base + o + 32);
+    v.gx0 = hd[0]; v.gy0 = hd[1]; v.cell = hd[2]; v.half = hd[3];
+    v.nx = hi[0]; v.ny = hi[1]; v.words = hi[2]; v.flags = hi[3];
+    o += 48;
+    const int64_t ncell = int64_t(v.nx) * v.ny;
+    v.seg_bits = reinterpret_cast<const uint32_t*>(base + o);
+    if (v.flags) o += align16(ncell * v.words * 4);
+    v.edge_bits = reinterpret_cast<const uint32_t*>(base + o);
+    if (v.flags) o += align16(int64_t(v.words) * 4);
+    v.lane_start = reinterpret_cast<const int32_t*>(base + o);
+    if (v.flags) o += align16((ncell + 1) * 4);
+    v.lane_list = reinterpret_cast<const int32_t*>(base + o);
     v.P = P; v.KL = KL; v.KE = KE;
     return v;
 }
@@ -285,12 +308,15 @@ __device__ __forceinline__ double swept_ttc(double dx, double dy, double ux, dou
                                             double ce, double se, double de,
                                             double cn, double sn, double dn,
                                             double rsum, double tmax) {
+    // neighbours behind the ego carry no threat (decided first: it overrides)
+    if (ce * dx + se * dy < 0.0) return tmax;
     const double a = ux * ux + uy * uy;
     const bool moving = a >= 1e-12;
+    const double a4 = 4.0 * a;
     const double rr = rsum * rsum;
     const double offs[3] = {-1.0, 0.0, 1.0};
-    bool any_hit = false, any_overlap = false;
-    double nmin = 0.0;
+    bool any_overlap = false;
+    double nmin = INFINITY;  // min over pairs with t_exit >= 0 of the t_enter numerator
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         const double oe = offs[i] * de;
@@ -303,28 +329,18 @@ __device__ __forceinline__ double swept_ttc(double dx, double dy, double ux, dou
             const double b = 2.0 * (qx * ux + qy * uy);
             const double c = qx * qx + qy * qy - rr;
             if (moving) {
-                const double disc = b * b - 4.0 * a * c;
+                const double disc = b * b - a4 * c;
                 if (disc >= 0.0) {
                     const double root = sqrt(disc);
-                    if (-b + root >= 0.0) {           // t_exit >= 0  (2a > 0)
-                        const double n = -b - root;    // numerator of t_enter
-                        nmin = any_hit ? np_min(nmin, n) : n;
-                        any_hit = true;
-                    }
+                    if (-b + root >= 0.0) nmin = fmin(nmin, -b - root);  // t_exit >= 0 (2a > 0)
                 }
             } else if (c < 0.0) {
                 any_overlap = true;
             }
         }
     }
-    double t;
-    if (moving) {
-        t = any_hit ? np_min(np_max(nmin / (2.0 * a), 0.0), tmax) : tmax;
-    } else {
-        t = any_overlap ? 0.0 : tmax;
-    }
-    // neighbours behind the ego carry no threat
-    return (ce * dx + se * dy < 0.0) ? tmax : t;
+    if (moving) return nmin < INFINITY ? fmin(fmax(nmin / (2.0 * a), 0.0), tmax) : tmax;
+    return any_overlap ? 0.0 : tmax;
 }
 
 // ----------------------------------------------------------------- observation row
@@ -376,6 +392,7 @@ world_step_kernel(const KArgs A) {
     AgentSm* ag = reinterpret_cast<AgentSm*>(smem + align16(A.d.max_scene_bytes));
     ScanSm* sc = reinterpret_cast<ScanSm*>(ag + kMaxAgents);
     uint64_t* bar = reinterpret_cast<uint64_t*>(sc + kMaxAgents);
+    uint16_t* cand_sm = reinterpret_cast<uint16_t*>(bar + 2);   // [M][take_road]
     __shared__ int s_bad;
 
     // ---- phase 0: action scan (the reference rejects before mutating)
@@ -400,7 +417,6 @@ world_step_kernel(const KArgs A) {
     // ---- geometry: one bulk async copy of the world's scene blob (TMA engine)
     const int scene = A.scene_of_world[w];
     const int64_t* meta = A.scene_meta + 8 * scene;
-    const SceneView G = scene_view(geo, int(meta[2]), int(meta[3]), int(meta[4]));
     if (tid == 0) {
         mbar_init(bar, 1);
         bulk_load(geo, A.scene_blob + meta[0], uint32_t(meta[1]), bar);
@@ -453,6 +469,9 @@ world_step_kernel(const KArgs A) {
         S.d = A.d_hull[am];
         S.len = A.length[am];
         S.wid = A.width[am];
+        S.f_len = __double2float_rn(S.len / k.bbox_half);
+        S.f_wid = __double2float_rn(S.wid / k.bbox_half);
+        S.f_spd = __double2float_rn(sqrt(x[SVX] * x[SVX] + x[SVY] * x[SVY]) / k.speed_norm);
         const double offs[3] = {-1.0, 0.0, 1.0};
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
@@ -474,6 +493,8 @@ world_step_kernel(const KArgs A) {
 
     __syncthreads();  // agent table + zero rows done, mbarrier init visible
     mbar_wait(bar, 0);
+    // the view reads the index header from the copied blob: only after the wait
+    const SceneView G = scene_view(geo, int(meta[2]), int(meta[3]), int(meta[4]));
     {   // scene-local midpoints -> global, exactly midpoints + grid offset
         double* mx = const_cast<double*>(G.mx);
         double* my = const_cast<double*>(G.my);
@@ -484,107 +505,183 @@ world_step_kernel(const KArgs A) {
     }
     __syncthreads();
 
-    // ---- phase 2: warp m scans for agent m and scatters its road/neighbour rows
+    // ---- phase 2a: agent pairs, 16 lanes per ego agent (lane j <-> other agent j):
+    //      stable distance rank, swept-circle TTC, neighbour rows, hull contact
     const int road0 = A.d.ego_dim;
     const int veh0 = A.d.ego_dim + 5 * A.d.k_road;
+    {
+        const int half_id = lane >> 4;          // two ego agents per warp
+        const int j = lane & 15;
+        const unsigned gmask = half_id ? 0xffff0000u : 0x0000ffffu;
+        for (int i = 2 * warp + half_id; i - half_id < M; i += 2 * nwarps) {
+            const bool ego_ok = i < M;
+            const int ii = ego_ok ? i : 0;
+            const AgentSm& S = ag[ii];
+            const double px = S.st[SX], py = S.st[SY], c = S.c, s = S.s;
+            double key = INFINITY, ndx = 0.0, ndy = 0.0;
+            if (ego_ok && j < M) {
+                const AgentSm& N = ag[j];
+                ndx = N.st[SX] - px;
+                ndy = N.st[SY] - py;
+                const double dist = sqrt(ndx * ndx + ndy * ndy);
+                key = (N.alive && j != ii) ? dist : INFINITY;
+            }
+            int rank = 0;
+            for (int t = 0; t < M; ++t) {
+                const double kt = __shfl_sync(kFull, key, t, 16);
+                rank += (kt < key) || (kt == key && t < j);
+            }
+            const bool nvalid = ego_ok && j < M && finite(key) && rank < A.take_veh;
+            double ttc = k.ttc_max;
+            if (nvalid) {
+                const AgentSm& N = ag[j];
+                ttc = swept_ttc(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c, N.s, N.d,
+                                S.r + N.r, k.ttc_max);
+                double st_, ct_;
+                sincos(N.st[SYAW] - S.st[SYAW], &st_, &ct_);
+                const double wrap = atan2(st_, ct_);
+                float* o = obs_w + int64_t(ii) * D + veh0 + 7 * rank;
+                o[0] = __double2float_rn((c * ndx + s * ndy) / k.bbox_half);
+                o[1] = __double2float_rn((-s * ndx + c * ndy) / k.bbox_half);
+                o[2] = N.f_len;
+                o[3] = N.f_wid;
+                o[4] = __double2float_rn(wrap / 3.141592653589793);
+                o[5] = N.f_spd;
+                o[6] = __double2float_rn(ttc / k.ttc_max);
+            }
+            for (int o = 8; o > 0; o >>= 1) ttc = fmin(ttc, __shfl_xor_sync(kFull, ttc, o, 16));
+            bool touch = false;
+            if (kStep && ego_ok && j < M && j != ii && S.alive && ag[j].alive) {
+                const AgentSm& N = ag[j];
+                const double rs = S.r + N.r;
+                const double rs2 = rs * rs;
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b) {
+                        const double ex = S.hx[a] - N.hx[b], ey = S.hy[a] - N.hy[b];
+                        touch |= ex * ex + ey * ey < rs2;
+                    }
+            }
+            touch = (__ballot_sync(kFull, touch) & gmask) != 0;
+            if (ego_ok && j == 0) {
+                sc[ii].ttc_min = ttc;
+                sc[ii].touch = touch;
+                if (!kStep && A.ttc_min_out) A.ttc_min_out[int64_t(w) * M + ii] = ttc;
+            }
+        }
+    }
+
+    // ---- phase 2b: warp m scans the scene for agent m
     for (int m = warp; m < M; m += nwarps) {
         const AgentSm& S = ag[m];
         float* row = obs_w + int64_t(m) * D;
         const double px = S.st[SX], py = S.st[SY];
         const double c = S.c, s = S.s;
+        const bool rewards_needed = kStep && S.alive;   // dead agents: rewards/events masked
+        const double r2 = S.r * S.r;
+        bool edge_hit = false;
 
-        // (a) road context: candidates d2 <= r^2, ordered by segment index, first take
+        // (a) road context: exact d2 <= r^2 over the candidate superset, ordered
+        //     compaction into shared memory; edge boxes tested on the same pass
+        uint16_t* cand = cand_sm + m * A.take_road;
         int count = 0;
-        for (int p0 = 0; p0 < G.P; p0 += 32) {
-            const int q = p0 + lane;
+        auto visit = [&](int q, bool in, bool edge_q) {
             bool hit = false;
-            double dx = 0.0, dy = 0.0;
-            if (q < G.P) {
-                dx = G.mx[q] - px;
-                dy = G.my[q] - py;
-                hit = dx * dx + dy * dy <= k.road_radius_sq;
+            if (in) {
+                const double dx = G.mx[q] - px, dy = G.my[q] - py;
+                const double d2 = dx * dx + dy * dy;
+                hit = d2 <= k.road_radius_sq;
+                if (rewards_needed && edge_q) {
+                    const double hl = G.hl[q], hw = G.hw[q];
+                    const double reach = S.r + S.d + hl + hw + 1e-6;
+                    if (d2 <= reach * reach) {
+                        const double ux = G.dx[q], uy = G.dy[q];
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) {
+                            const double qx = S.hx[i] - G.mx[q], qy = S.hy[i] - G.my[q];
+                            const double along = qx * ux + qy * uy;
+                            const double lat = ux * qy - uy * qx;
+                            const double du = along - fmin(fmax(along, -hl), hl);
+                            const double dv = lat - fmin(fmax(lat, -hw), hw);
+                            edge_hit |= du * du + dv * dv < r2;
+                        }
+                    }
+                }
             }
             const unsigned bal = __ballot_sync(kFull, hit);
             if (hit) {
                 const int slot = count + __popc(bal & ((1u << lane) - 1u));
-                if (slot < A.take_road) {
-                    float* o = row + road0 + 5 * slot;
-                    const double ux = G.dx[q], uy = G.dy[q];
-                    o[0] = __double2float_rn((c * dx + s * dy) / k.road_radius);
-                    o[1] = __double2float_rn((-s * dx + c * dy) / k.road_radius);
-                    o[2] = __double2float_rn(double(G.type[q]) / k.type_norm);
-                    o[3] = __double2float_rn(c * ux + s * uy);
-                    o[4] = __double2float_rn(-s * ux + c * uy);
-                }
+                if (slot < A.take_road) cand[slot] = uint16_t(q);
             }
             count += __popc(bal);
+        };
+        const bool use_grid = (G.flags & kFlagGrid) != 0;
+        if (use_grid) {
+            const double plx = px - ox, ply = py - oy;
+            const double inv = 1.0 / G.cell;
+            int cx0 = int(floor((plx - G.half - G.gx0) * inv)), cx1 = int(floor((plx + G.half - G.gx0) * inv));
+            int cy0 = int(floor((ply - G.half - G.gy0) * inv)), cy1 = int(floor((ply + G.half - G.gy0) * inv));
+            const bool finite_pos = finite(plx) && finite(ply);
+            cx0 = cx0 < 0 ? 0 : cx0;
+            cy0 = cy0 < 0 ? 0 : cy0;
+            cx1 = cx1 >= G.nx ? G.nx - 1 : cx1;
+            cy1 = cy1 >= G.ny ? G.ny - 1 : cy1;
+            const bool any_cell = finite_pos && cx0 <= cx1 && cy0 <= cy1 &&
+                                  plx + G.half >= G.gx0 && ply + G.half >= G.gy0;
+            for (int wb = 0; wb < G.words; wb += 32) {
+                const int wi = wb + lane;
+                uint32_t bits = 0;
+                if (any_cell && wi < G.words) {
+                    for (int cy = cy0; cy <= cy1; ++cy)
+                        for (int cx = cx0; cx <= cx1; ++cx) bits |= G.seg_bits[(cy * G.nx + cx) * G.words + wi];
+                }
+                unsigned nz = __ballot_sync(kFull, bits != 0);
+                while (nz) {
+                    const int l = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    const uint32_t wbits = __shfl_sync(kFull, bits, l);
+                    const uint32_t ebits = G.edge_bits[wb + l];
+                    const int q = (wb + l) * 32 + lane;
+                    visit(q, (wbits >> lane) & 1u, (ebits >> lane) & 1u);
+                }
+            }
+        } else {
+            for (int p0 = 0; p0 < G.P; p0 += 32) visit(p0 + lane, p0 + lane < G.P, false);
+        }
+        const int ncand = count < A.take_road ? count : A.take_road;
+        __syncwarp();
+        for (int slot = lane; slot < ncand; slot += 32) {
+            const int q = cand[slot];
+            const double dx = G.mx[q] - px, dy = G.my[q] - py;
+            const double ux = G.dx[q], uy = G.dy[q];
+            float* o = row + road0 + 5 * slot;
+            o[0] = __double2float_rn((c * dx + s * dy) / k.road_radius);
+            o[1] = __double2float_rn((-s * dx + c * dy) / k.road_radius);
+            o[2] = G.type_feat[q];
+            o[3] = __double2float_rn(c * ux + s * uy);
+            o[4] = __double2float_rn(-s * ux + c * uy);
         }
 
-        // (b) neighbours: lane j <-> agent j; stable rank by distance
-        double key = INFINITY, ndx = 0.0, ndy = 0.0;
-        if (lane < M) {
-            const AgentSm& N = ag[lane];
-            ndx = N.st[SX] - px;
-            ndy = N.st[SY] - py;
-            const double dist = sqrt(ndx * ndx + ndy * ndy);
-            key = (N.alive && lane != m) ? dist : INFINITY;
-        }
-        int rank = 0;
-        for (int j = 0; j < M; ++j) {
-            const double kj = shfl_d(key, j);
-            rank += (kj < key) || (kj == key && j < lane);
-        }
-        const bool nvalid = lane < M && finite(key) && rank < A.take_veh;
-        double ttc = k.ttc_max;
-        if (nvalid) {
-            const AgentSm& N = ag[lane];
-            ttc = swept_ttc(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c, N.s, N.d,
-                            S.r + N.r, k.ttc_max);
-            double st_, ct_;
-            sincos(N.st[SYAW] - S.st[SYAW], &st_, &ct_);
-            const double wrap = atan2(st_, ct_);
-            const double spd = sqrt(N.st[SVX] * N.st[SVX] + N.st[SVY] * N.st[SVY]);
-            float* o = row + veh0 + 7 * rank;
-            o[0] = __double2float_rn((c * ndx + s * ndy) / k.bbox_half);
-            o[1] = __double2float_rn((-s * ndx + c * ndy) / k.bbox_half);
-            o[2] = __double2float_rn(N.len / k.bbox_half);
-            o[3] = __double2float_rn(N.wid / k.bbox_half);
-            o[4] = __double2float_rn(wrap / 3.141592653589793);
-            o[5] = __double2float_rn(spd / k.speed_norm);
-            o[6] = __double2float_rn(ttc / k.ttc_max);
-        }
-        const double ttc_min = warp_min(nvalid ? ttc : k.ttc_max);
-
-        if constexpr (kStep) {
-            // (c) nearest lane: argmin of point-to-segment d2, lowest index on ties
-            double best = INFINITY;
-            int best_k = 0x7fffffff;
-            for (int kk = lane; kk < G.KL; kk += 32) {
-                const int q = G.lane[kk];
-                const double ex = px - G.mx[q], ey = py - G.my[q];
-                const double ux = G.dx[q], uy = G.dy[q];
-                const double along = ex * ux + ey * uy;
-                const double lat = ux * ey - uy * ex;
-                const double over = fmax(fabs(along) - G.hl[q], 0.0);
-                const double d2 = over * over + lat * lat;
-                if (d2 < best) { best = d2; best_k = kk; }
+        if (!rewards_needed) {
+            if (kStep && lane == 0) {
+                ScanSm& R = sc[m];
+                R.lane_d2 = INFINITY;
+                R.lane_k = 0;
+                R.gap = INFINITY;
+                R.edge_hit = 0;
             }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ob = __shfl_xor_sync(kFull, best, o);
-                const int ok = __shfl_xor_sync(kFull, best_k, o);
-                if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
-            }
-            // (d) first road edge ahead, and the hull-vs-edge-box test behind a
-            //     conservative distance filter (skips boxes farther than
-            //     r + d + half_len + half_wid, + 1 micron of rounding slack)
-            double gap = INFINITY;
-            bool edge_hit = false;
-            const double r2 = S.r * S.r;
-            for (int kk = lane; kk < G.KE; kk += 32) {
-                const int q = G.edge[kk];
-                const double ex = G.mx[q] - px, ey = G.my[q] - py;
-                const double xb = c * ex + s * ey;
-                if (xb > 0.0 && xb <= k.edge_range) gap = fmin(gap, xb);
+            continue;
+        }
+        // (b) first road edge ahead over every edge (xb in (0, edge_range]); the
+        //     edge boxes when the grid could not take them
+        double gap = INFINITY;
+        for (int kk = lane; kk < G.KE; kk += 32) {
+            const int q = G.edge[kk];
+            const double ex = G.mx[q] - px, ey = G.my[q] - py;
+            const double xb = c * ex + s * ey;
+            if (xb > 0.0 && xb <= k.edge_range) gap = fmin(gap, xb);
+            if (!use_grid) {
                 const double ux = G.dx[q], uy = G.dy[q], hl = G.hl[q], hw = G.hw[q];
                 const double reach = S.r + S.d + hl + hw + 1e-6;
                 if (ex * ex + ey * ey <= reach * reach) {
@@ -599,34 +696,47 @@ world_step_kernel(const KArgs A) {
                     }
                 }
             }
-            for (int o = 16; o > 0; o >>= 1) gap = fmin(gap, __shfl_xor_sync(kFull, gap, o));
-            edge_hit = __any_sync(kFull, edge_hit);
-            // (e) hull contact with any other alive agent
-            bool touch = false;
-            if (lane < M && lane != m && S.alive && ag[lane].alive) {
-                const AgentSm& N = ag[lane];
-                const double rs = S.r + N.r;
-                const double rs2 = rs * rs;
-#pragma unroll
-                for (int i = 0; i < 3; ++i)
-#pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        const double ex = S.hx[i] - N.hx[j], ey = S.hy[i] - N.hy[j];
-                        touch |= ex * ex + ey * ey < rs2;
-                    }
-            }
-            touch = __any_sync(kFull, touch);
-            if (lane == 0) {
-                ScanSm& R = sc[m];
-                R.ttc_min = ttc_min;
-                R.lane_d2 = best;
-                R.lane_k = best_k;
-                R.gap = gap;
-                R.edge_hit = edge_hit;
-                R.touch = touch;
-            }
+        }
+        for (int o = 16; o > 0; o >>= 1) gap = fmin(gap, __shfl_xor_sync(kFull, gap, o));
+        edge_hit = __any_sync(kFull, edge_hit);
+
+        // (c) nearest lane: argmin of point-to-segment d2, lowest index on ties,
+        //     over the cell's candidate list when the agent is inside the grid
+        double best = INFINITY;
+        int best_k = 0x7fffffff;
+        auto lane_test = [&](int kk) {
+            const int q = G.lane[kk];
+            const double ex = px - G.mx[q], ey = py - G.my[q];
+            const double ux = G.dx[q], uy = G.dy[q];
+            const double along = ex * ux + ey * uy;
+            const double lat = ux * ey - uy * ex;
+            const double over = fmax(fabs(along) - G.hl[q], 0.0);
+            const double d2 = over * over + lat * lat;
+            if (d2 < best || (d2 == best && kk < best_k)) { best = d2; best_k = kk; }
+        };
+        int lcell = -1;
+        if (G.flags & kFlagLanes) {
+            const double plx = px - ox, ply = py - oy;
+            const double fx = floor((plx - G.gx0) / G.cell), fy = floor((ply - G.gy0) / G.cell);
+            if (fx >= 0.0 && fy >= 0.0 && fx < double(G.nx) && fy < double(G.ny)) lcell = int(fy) * G.nx + int(fx);
+        }
+        if (lcell >= 0) {
+            const int b0 = G.lane_start[lcell], b1 = G.lane_start[lcell + 1];
+            for (int i = b0 + lane; i < b1; i += 32) lane_test(G.lane_list[i]);
         } else {
-            if (lane == 0 && A.ttc_min_out) A.ttc_min_out[int64_t(w) * M + m] = ttc_min;
+            for (int kk = lane; kk < G.KL; kk += 32) lane_test(kk);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(kFull, best, o);
+            const int ok = __shfl_xor_sync(kFull, best_k, o);
+            if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
+        }
+        if (lane == 0) {
+            ScanSm& R = sc[m];
+            R.lane_d2 = best;
+            R.lane_k = best_k;
+            R.gap = gap;
+            R.edge_hit = edge_hit;
         }
     }
     __syncthreads();
@@ -884,10 +994,11 @@ static int cuda_fail(cudaError_t e, const char* where) {
     return DG_ECUDA;
 }
 
-static size_t step_smem_bytes(const DgDims& d) {
+static size_t step_smem_bytes(const DgDims& d, int take_road) {
     size_t b = size_t(align16(d.max_scene_bytes));
     b += sizeof(AgentSm) * kMaxAgents + sizeof(ScanSm) * kMaxAgents;
     b += 16;  // mbarrier
+    b += sizeof(uint16_t) * kMaxAgents * size_t(take_road > 0 ? take_road : 1);
     return b;
 }
 
@@ -943,7 +1054,7 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
     A.error_word = desc->error_word;
     A.take_road = d.k_road < d.max_segments ? d.k_road : d.max_segments;
     A.take_veh = d.k_vehicles < d.M ? d.k_vehicles : d.M;
-    e->smem_bytes = step_smem_bytes(d);
+    e->smem_bytes = step_smem_bytes(d, A.take_road);
     if (e->smem_bytes > 227 * 1024) {
         delete e;
         return fail(DG_ENOSUPPORT, "dg_create: scene geometry does not fit in shared memory");

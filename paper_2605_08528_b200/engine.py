@@ -29,6 +29,7 @@ import torch
 from . import _native as N
 from .params import (CRASH_SPEED_LIMIT, DENSE_TERMS, EVENT_TYPES, GRAVITY, OFFSTAGE_X, PHASES,
                      STATE_FIELDS, BicycleParams, ObsConfig, RewardConfig, SimConfig, VehicleParams)
+from .spatial import build_scene_index
 from .tables import build_tables, compact_subset, edge_mask_of, lane_mask_of
 
 TERM_NAMES = (*DENSE_TERMS, "total")
@@ -80,8 +81,11 @@ def make_consts(cfg: SimConfig, oc: ObsConfig, rc: RewardConfig, vp: VehiclePara
     return k
 
 
-def pack_scenes(scene_tables) -> tuple[np.ndarray, np.ndarray, int, int]:
-    """Concatenate per-scene blobs (layout documented in the C header)."""
+def pack_scenes(scene_tables, type_norm: float, road_radius: float = 10.0,
+                 agent_reach: float = 0.0, spatial_index: bool = True):
+    """Concatenate per-scene blobs (layout documented in the C header).  The
+    type feature is float32(type / type_norm), the reference's own cast; the
+    spatial index (spatial.py) follows the segment arrays."""
     blobs, meta, off = [], [], 0
     for t in scene_tables:
         P, KL, KE = t.num_segments, len(t.lane_index), len(t.edge_index)
@@ -89,14 +93,21 @@ def pack_scenes(scene_tables) -> tuple[np.ndarray, np.ndarray, int, int]:
         for arr in (t.midpoints[:, 0], t.midpoints[:, 1], t.directions[:, 0], t.directions[:, 1],
                     t.half_lengths, t.half_widths):
             parts.append(np.ascontiguousarray(arr, dtype=np.float64))
-        parts += [t.type_codes.astype(np.int32), t.lane_index.astype(np.int32),
+        parts += [(t.type_codes.astype(np.float64) / type_norm).astype(np.float32),
+                  t.lane_index.astype(np.int32),
                   t.edge_index.astype(np.int32)]
         chunk = bytearray()
         for a in parts:
             b = a.tobytes()
             chunk += b + bytes(_align16(len(b)) - len(b))
-        if not chunk:
-            chunk = bytearray(16)
+        edge_ext = float((t.half_lengths[t.edge_index] + t.half_widths[t.edge_index]).max()) \
+            if len(t.edge_index) else 0.0
+        idx = build_scene_index(t.midpoints, t.directions, t.half_lengths, t.half_widths,
+                                t.lane_index, t.edge_index, road_radius,
+                                agent_reach + edge_ext + 1e-6)
+        if not spatial_index:
+            idx = idx[:32] + bytes(16)
+        chunk += idx + bytes(_align16(len(idx)) - len(idx))
         blobs.append(bytes(chunk))
         meta.append([off, len(chunk), P, KL, KE, 0, 0, 0])
         off += len(chunk)
@@ -161,7 +172,7 @@ class Engine:
     def __init__(self, worlds, scenes, assignment, frictions, config: SimConfig,
                  obs_config: ObsConfig | None = None, reward_config: RewardConfig | None = None,
                  params: VehicleParams | None = None, bicycle: BicycleParams | None = None,
-                 device=None):
+                 device=None, spatial_index: bool = True, warps_per_world: int | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("drivegrid-b200 Engine needs a CUDA device (no CPU fallback)")
         self._lib = N.load_library()
@@ -191,7 +202,10 @@ class Engine:
         def up(a, dtype):
             return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(dev)
 
-        blob, meta, max_bytes, max_p = pack_scenes(t.scenes)
+        reach = float((t.r_hull + t.d_hull).max())
+        blob, meta, max_bytes, max_p = pack_scenes(t.scenes, self.obs_config.type_norm,
+                                                   self.obs_config.road_radius, reach,
+                                                   spatial_index=spatial_index)
         self._d = d = {
             "scene_blob": up(blob, torch.uint8),
             "scene_meta": up(meta, torch.int64),
@@ -233,6 +247,7 @@ class Engine:
         N.check(self._lib, self._lib.dg_create(ct.byref(desc), ct.byref(handle)), "dg_create")
         self._h = handle
         self._desc = desc
+        self.tune(warps_per_world or min(M, 8))
         self._step_count = 0
         self.phase_seconds = {k: 0.0 for k in PHASES}
         self._act_dev = torch.empty((W, M, 3), dtype=torch.float64, device=dev)

@@ -73,10 +73,19 @@ def compare(dev: Dev, t, g, o, oc):
     dev.f("obs", g.obs, o.obs, rtol=OBS_RTOL, atol=OBS_ATOL)
 
 
-@pytest.mark.parametrize("name", TRAJ_CASES)
-def test_trajectory_parity(name, device):
+VARIANTS = [(n, True, None) for n in TRAJ_CASES] + [
+    ("traj_events", False, 3), ("traj_wet", True, 16), ("traj_pool", False, 1),
+    ("traj_events_inv", True, 5)]
+
+
+@pytest.mark.parametrize("name,spatial,warps", VARIANTS,
+                         ids=[f"{n}-{'idx' if s else 'scan'}-w{w}" for n, s, w in VARIANTS])
+def test_trajectory_parity(name, spatial, warps, device):
+    """Launch shape and the spatial index are performance knobs: every
+    variant must reproduce the oracle."""
     case = case_inputs(name)
-    gpu = Engine(**case.inputs.as_kwargs(), device=device)
+    gpu = Engine(**case.inputs.as_kwargs(), device=device, spatial_index=spatial,
+                 warps_per_world=warps)
     ora = OracleEngine(**case.inputs.as_kwargs())
     dev = Dev()
     dev.f("obs0", gpu.observe(), ora.observe(), rtol=OBS_RTOL, atol=OBS_ATOL)

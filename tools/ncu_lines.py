@@ -40,5 +40,6 @@ for r in rows:
 tot_i = sum(v[0] for v in agg.values()) or 1
 tot_s = sum(v[1] for v in agg.values()) or 1
 print(f"total warp-instructions {tot_i}, stall samples {tot_s}")
-for line, (ins, samp, src) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+key = 0 if (len(sys.argv) > 3 and sys.argv[3] == "inst") else 1
+for line, (ins, samp, src) in sorted(agg.items(), key=lambda kv: -kv[1][key])[:top]:
     print(f"{line:5d} inst {100*ins/tot_i:5.1f}%  samples {100*samp/tot_s:5.1f}%  {src}")
