@@ -79,9 +79,10 @@ typedef struct DgConsts {
 /* Engine description (replaces drivegrid.engine.Engine.__init__ tables,
  * engine.py:151-230).  Scene geometry is de-duplicated: worlds that share a
  * scene share one blob.  Per-scene blob, 16-byte aligned sections, local
- * coordinates:  f64 mid_x[P], mid_y[P], dir_x[P], dir_y[P], half_len[P],
- * half_wid[P]; f32 type_feat[P] = float32(type / type_norm); i32 lane_idx[KL];
- * i32 edge_idx[KE].
+ * coordinates:  f64x2 mid[P]; f64x2 dir[P]; f64 half_len[P]; f64 half_wid[P];
+ * f32 type_feat[P] = float32(type / type_norm); lane subset f64x4
+ * {mid, dir}[KL], f64 half_len[KL]; edge subset f64x2 mid[KE], i32 index[KE];
+ * then the spatial index of paper_2605_08528_b200/spatial.py.
  * scene_meta[s] = {byte_offset, byte_size, P, KL, KE, 0, 0, 0} (int64). */
 typedef struct DgEngineDesc {
     DgDims dims;

@@ -17,6 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB_PATH = PKG / "libdrivegrid_b200.so"
 SOURCES = [PKG / "csrc" / "drivegrid_b200.cu"]
+DEPS = [PKG / "csrc" / "dg_fastmath.cuh"]
 HEADER = ROOT / "include" / "drivegrid_b200.h"
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-fmad=false", "-Xcompiler", "-fPIC", "-shared"]
@@ -91,7 +92,7 @@ def _stale() -> bool:
     if not LIB_PATH.exists():
         return True
     t = LIB_PATH.stat().st_mtime
-    return any(p.stat().st_mtime > t for p in SOURCES + [HEADER] if p.exists())
+    return any(p.stat().st_mtime > t for p in SOURCES + DEPS + [HEADER] if p.exists())
 
 
 def build_native(force: bool = False, verbose: bool = False) -> Path:

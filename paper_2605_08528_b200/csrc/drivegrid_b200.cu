@@ -32,6 +32,7 @@
 #include <cstring>
 #include <new>
 
+#include "dg_fastmath.cuh"
 #include "drivegrid_b200.h"
 
 namespace {
@@ -88,15 +89,13 @@ struct KArgs {
 
 // ----------------------------------------------------------------- numpy-semantics helpers
 // numpy maximum/minimum propagate NaN from either side; clip is min(max()).
-__device__ __forceinline__ double np_max(double a, double b) {
-    if (a != a) return a;
-    if (b != b) return b;
-    return a > b ? a : b;
-}
-__device__ __forceinline__ double np_min(double a, double b) {
-    if (a != a) return a;
-    if (b != b) return b;
-    return a < b ? a : b;
+// (one compare + NaN test + select; fmin/fmax on f64 expand to ~8 SASS ops)
+__device__ __forceinline__ double np_max(double a, double b) { return (a != a || a > b) ? a : b; }
+__device__ __forceinline__ double np_min(double a, double b) { return (a != a || a < b) ? a : b; }
+// plain selects for values that cannot be NaN (or whose NaN is irrelevant)
+__device__ __forceinline__ double sel_min(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double sel_clip(double x, double lo, double hi) {
+    return x < lo ? lo : (x > hi ? hi : x);
 }
 __device__ __forceinline__ double np_clip(double x, double lo, double hi) {
     return np_min(np_max(x, lo), hi);
@@ -106,11 +105,8 @@ __device__ __forceinline__ double np_sign(double x) {
 }
 __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
 
-__device__ __forceinline__ double shfl_d(double v, int src) {
-    return __shfl_sync(kFull, v, src);
-}
-__device__ __forceinline__ double warp_min(double v) {
-    for (int o = 16; o > 0; o >>= 1) v = np_min(v, __shfl_xor_sync(kFull, v, o));
+__device__ __forceinline__ double warp_min(double v, int width = 32) {
+    for (int o = width >> 1; o > 0; o >>= 1) v = sel_min(v, __shfl_xor_sync(kFull, v, o, width));
     return v;
 }
 
@@ -128,15 +124,15 @@ struct AgentSm {
 };
 
 struct SceneView {
-    const double* mx;
-    const double* my;
-    const double* dx;
-    const double* dy;
-    const double* hl;
-    const double* hw;
-    const float* type_feat;   // float32(type / type_norm), precomputed on the host
-    const int32_t* lane;
-    const int32_t* edge;
+    double2* mid;             // [P]  segment midpoints (global after the fix-up pass)
+    const double2* dir;       // [P]  unit directions
+    const double* hl;         // [P]  half lengths
+    const double* hw;         // [P]  half widths
+    const float* type_feat;   // [P]  float32(type / type_norm), precomputed on the host
+    double4* lane_seg;        // [KL] lane subset {mid x, mid y, dir x, dir y}
+    const double* lane_hl;    // [KL]
+    double2* edge_mid;        // [KE] edge subset midpoints
+    const int32_t* edge;      // [KE] edge subset -> segment index
     // spatial index (paper_2605_08528_b200/spatial.py); flags == 0 -> full scans
     double gx0, gy0, cell, half;
     int nx, ny, words, flags;
@@ -155,16 +151,15 @@ __host__ __device__ __forceinline__ int64_t align16(int64_t x) { return (x + 15)
 __device__ __forceinline__ SceneView scene_view(uint8_t* base, int P, int KL, int KE) {
     SceneView v;
     int64_t o = 0;
-    const int64_t f8 = align16(int64_t(P) * 8);
-    v.mx = reinterpret_cast<double*>(base + o); o += f8;
-    v.my = reinterpret_cast<double*>(base + o); o += f8;
-    v.dx = reinterpret_cast<double*>(base + o); o += f8;
-    v.dy = reinterpret_cast<double*>(base + o); o += f8;
-    v.hl = reinterpret_cast<double*>(base + o); o += f8;
-    v.hw = reinterpret_cast<double*>(base + o); o += f8;
-    v.type_feat = reinterpret_cast<float*>(base + o); o += align16(int64_t(P) * 4);
-    v.lane = reinterpret_cast<int32_t*>(base + o); o += align16(int64_t(KL) * 4);
-    v.edge = reinterpret_cast<int32_t*>(base + o); o += align16(int64_t(KE) * 4);
+    v.mid = reinterpret_cast<double2*>(base + o); o += int64_t(P) * 16;
+    v.dir = reinterpret_cast<const double2*>(base + o); o += int64_t(P) * 16;
+    v.hl = reinterpret_cast<const double*>(base + o); o += align16(int64_t(P) * 8);
+    v.hw = reinterpret_cast<const double*>(base + o); o += align16(int64_t(P) * 8);
+    v.type_feat = reinterpret_cast<const float*>(base + o); o += align16(int64_t(P) * 4);
+    v.lane_seg = reinterpret_cast<double4*>(base + o); o += int64_t(KL) * 32;
+    v.lane_hl = reinterpret_cast<const double*>(base + o); o += align16(int64_t(KL) * 8);
+    v.edge_mid = reinterpret_cast<double2*>(base + o); o += int64_t(KE) * 16;
+    v.edge = reinterpret_cast<const int32_t*>(base + o); o += align16(int64_t(KE) * 4);
     const double* hd = reinterpret_cast<const double*>(base + o);
     const int32_t* hi = reinterpret_cast<const int32_t*>(base + o + 32);
     v.gx0 = hd[0]; v.gy0 = hd[1]; v.cell = hd[2]; v.half = hd[3];
@@ -216,7 +211,7 @@ struct Act {
 __device__ __forceinline__ void substep_dynamic(double* x, const Act a, double cap, const DgConsts& k) {
     double tau_s = np_clip(k.kp_steer * (k.theta_max * a.steer - x[SANG]) - k.kd_steer * x[SRATE],
                            -k.tau_steer_max, k.tau_steer_max);
-    double rate = x[SRATE] + (tau_s / k.steer_inertia) * k.physics_dt;
+    double rate = x[SRATE] + dg::ddiv(tau_s, k.steer_inertia) * k.physics_dt;
     double ang = x[SANG] + rate * k.physics_dt;
     double ang_c = np_clip(ang, -k.steer_limit, k.steer_limit);
     rate = (ang_c == ang) ? rate : 0.0;
@@ -230,26 +225,26 @@ __device__ __forceinline__ void substep_dynamic(double* x, const Act a, double c
     double tbr = -sr * a.brk * k.tau_brake_rear;
     double t_front = 2.0 * (k.tau_drive_max * a.thr + tbf);
     double t_rear = 2.0 * tbr;
-    double fxf0 = t_front / k.wheel_radius;
-    double fxr0 = t_rear / k.wheel_radius;
+    double fxf0 = dg::ddiv(t_front, k.wheel_radius);
+    double fxr0 = dg::ddiv(t_rear, k.wheel_radius);
     double den = np_max(vx, 0.5);
-    double fyf0 = k.cornering_stiffness * (ang - (vy + k.a_f * om) / den);
-    double fyr0 = k.cornering_stiffness * (-(vy - k.b_r * om) / den);
+    double fyf0 = k.cornering_stiffness * (ang - dg::ddiv(vy + k.a_f * om, den));
+    double fyr0 = k.cornering_stiffness * dg::ddiv(-(vy - k.b_r * om), den);
 
-    double nf = sqrt(fxf0 * fxf0 + fyf0 * fyf0);
-    double nr = sqrt(fxr0 * fxr0 + fyr0 * fyr0);
+    double nf = dg::dsqrt(fxf0 * fxf0 + fyf0 * fyf0);
+    double nr = dg::dsqrt(fxr0 * fxr0 + fyr0 * fyr0);
     bool satf = nf > cap, satr = nr > cap;
-    double kf = satf ? cap / np_max(nf, 1e-12) : 1.0;
-    double kr = satr ? cap / np_max(nr, 1e-12) : 1.0;
+    double kf = satf ? dg::ddiv(cap, np_max(nf, 1e-12)) : 1.0;
+    double kr = satr ? dg::ddiv(cap, np_max(nr, 1e-12)) : 1.0;
     double fxf = fxf0 * kf, fyf = fyf0 * kf;
     double fxr = fxr0 * kr, fyr = fyr0 * kr;
 
     double sd, cd;
     sincos(ang, &sd, &cd);
     const double m = k.chassis_mass;
-    double ax = (fxf * cd - fyf * sd + fxr) / m + vy * om;
-    double ay = (fyf * cd + fxf * sd + fyr - k.lambda_lat * vy) / m - vx * om;
-    double omd = (k.a_f * (fyf * cd + fxf * sd) - k.b_r * fyr - k.lambda_yaw * om) / k.yaw_inertia;
+    double ax = dg::ddiv(fxf * cd - fyf * sd + fxr, m) + vy * om;
+    double ay = dg::ddiv(fyf * cd + fxf * sd + fyr - k.lambda_lat * vy, m) - vx * om;
+    double omd = dg::ddiv(k.a_f * (fyf * cd + fxf * sd) - k.b_r * fyr - k.lambda_yaw * om, k.yaw_inertia);
     double vx1 = vx + ax * k.physics_dt;
     double vy1 = vy + ay * k.physics_dt;
     double om1 = om + omd * k.physics_dt;
@@ -261,10 +256,10 @@ __device__ __forceinline__ void substep_dynamic(double* x, const Act a, double c
     x[SY] = x[SY] + (vx1 * sy + vy1 * cy) * k.physics_dt;
     x[SYAW] = x[SYAW] + om1 * k.physics_dt;
 
-    double roll_f = ((vy1 + k.a_f * om1) * sd + vx1 * cd) / k.wheel_radius;
-    double roll_r = vx1 / k.wheel_radius;
-    double spin_f = x[SWF] + (t_front - fxf * k.wheel_radius) / k.i_axle * k.physics_dt;
-    double spin_r = x[SWR] + (t_rear - fxr * k.wheel_radius) / k.i_axle * k.physics_dt;
+    double roll_f = dg::ddiv((vy1 + k.a_f * om1) * sd + vx1 * cd, k.wheel_radius);
+    double roll_r = dg::ddiv(vx1, k.wheel_radius);
+    double spin_f = x[SWF] + dg::ddiv(t_front - fxf * k.wheel_radius, k.i_axle) * k.physics_dt;
+    double spin_r = x[SWR] + dg::ddiv(t_rear - fxr * k.wheel_radius, k.i_axle) * k.physics_dt;
     if (a.brk > 0.0 && spin_f * sf < 0.0) spin_f = 0.0;
     if (a.brk > 0.0 && spin_r * sr < 0.0) spin_r = 0.0;
     x[SWF] = np_clip(satf ? spin_f : roll_f, -200.0, 200.0);
@@ -284,7 +279,7 @@ __device__ __forceinline__ void step_bicycle(double* x, const Act a, const DgCon
     double v = x[SVX];
     double v1 = np_max(v + (a.thr * k.bic_a_max - a.brk * k.bic_b_max - np_sign(v) * k.bic_c_roll) * k.control_dt, 0.0);
     double yaw = x[SYAW];
-    double rate = v1 * tan(delta) / k.wheelbase;
+    double rate = dg::ddiv(v1 * tan(delta), k.wheelbase);
     double sy, cy;
     sincos(yaw, &sy, &cy);
     x[SX] = x[SX] + v1 * cy * k.control_dt;
@@ -295,8 +290,8 @@ __device__ __forceinline__ void step_bicycle(double* x, const Act a, const DgCon
     x[SOM] = rate;
     x[SANG] = delta;
     x[SRATE] = 0.0;
-    x[SWF] = v1 / k.wheel_radius;
-    x[SWR] = v1 / k.wheel_radius;
+    x[SWF] = dg::ddiv(v1, k.wheel_radius);
+    x[SWR] = dg::ddiv(v1, k.wheel_radius);
 }
 
 // ----------------------------------------------------------------- swept-circle TTC
@@ -331,15 +326,15 @@ __device__ __forceinline__ double swept_ttc(double dx, double dy, double ux, dou
             if (moving) {
                 const double disc = b * b - a4 * c;
                 if (disc >= 0.0) {
-                    const double root = sqrt(disc);
-                    if (-b + root >= 0.0) nmin = fmin(nmin, -b - root);  // t_exit >= 0 (2a > 0)
+                    const double root = dg::dsqrt(disc);
+                    if (-b + root >= 0.0) nmin = sel_min(nmin, -b - root);  // t_exit >= 0 (2a > 0)
                 }
             } else if (c < 0.0) {
                 any_overlap = true;
             }
         }
     }
-    if (moving) return nmin < INFINITY ? fmin(fmax(nmin / (2.0 * a), 0.0), tmax) : tmax;
+    if (moving) return nmin < INFINITY ? sel_clip(dg::ddiv(nmin, 2.0 * a), 0.0, tmax) : tmax;
     return any_overlap ? 0.0 : tmax;
 }
 
@@ -372,6 +367,20 @@ struct ScanSm {
     int pad_;
 };
 
+// ----------------------------------------------------------------- optional phase timers
+// Built with -DDG_PHASE_TIMERS: every CTA records clock64() at its phase
+// boundaries (slot 0 start .. 7 end) plus the per-warp end of phase 2.
+#ifdef DG_PHASE_TIMERS
+__device__ long long g_phase_clock[65536][24];
+#define PHASE_MARK(i) do { if (threadIdx.x == 0 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][i] = clock64(); } while (0)
+#define WARP_MARK(i) do { if ((threadIdx.x & 31) == 0 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][8 + (threadIdx.x >> 5)] = clock64(); } while (0)
+#define LANE0_MARK(i) do { if (threadIdx.x == 0 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][i] = clock64(); } while (0)
+#else
+#define LANE0_MARK(i) do { } while (0)
+#define PHASE_MARK(i) do { } while (0)
+#define WARP_MARK(i) do { } while (0)
+#endif
+
 // ----------------------------------------------------------------- the fused step kernel
 template <bool kStep, int kThreads, int kMinBlocks>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
@@ -396,6 +405,7 @@ world_step_kernel(const KArgs A) {
     __shared__ int s_bad;
 
     // ---- phase 0: action scan (the reference rejects before mutating)
+    PHASE_MARK(0);
     int step_now = 0;
     if constexpr (kStep) {
         if (tid == 0) s_bad = DG_NO_ERROR;
@@ -424,6 +434,7 @@ world_step_kernel(const KArgs A) {
     const double ox = A.grid_offset[2 * w], oy = A.grid_offset[2 * w + 1];
     float* obs_w = A.obs + int64_t(w) * M * D;
 
+    PHASE_MARK(1);
     // ---- phase 1: warp 0, lane m: agent m load + physics (SIMT across agents);
     //      every warp streams the zero background of its agents' obs rows
     if (warp == 0 && lane < M) {
@@ -436,6 +447,7 @@ world_step_kernel(const KArgs A) {
         const int alive = A.alive[am];
         S.px0 = x[SX];
         S.py0 = x[SY];
+        if (alive && x[SX] != -12345.678) LANE0_MARK(17);  // after the state loads landed
         if (kStep && alive) {
             const int64_t ab = am * 3;
             double raw0, raw1, raw2;
@@ -452,11 +464,17 @@ world_step_kernel(const KArgs A) {
             act.brk = np_clip(raw2, 0.0, 1.0);
             if (A.d.dynamic) {
                 const double cap = A.mu_eff[w] * k.f_z;
-                for (int i = 0; i < A.d.decimation; ++i) substep_dynamic(x, act, cap, k);
+                for (int i = 0; i < A.d.decimation; ++i) {
+                    substep_dynamic(x, act, cap, k);
+#ifdef DG_PHASE_TIMERS
+                    if (i < 4 && x[SX] != -12345.678) LANE0_MARK(20 + i);
+#endif
+                }
             } else {
                 step_bicycle(x, act, k);
             }
         }
+        if (x[SX] != -12345.678) LANE0_MARK(18);          // after the substeps
 #pragma unroll
         for (int f = 0; f < DG_NUM_STATE; ++f) S.st[f] = x[f];
         double s_, c_;
@@ -469,9 +487,9 @@ world_step_kernel(const KArgs A) {
         S.d = A.d_hull[am];
         S.len = A.length[am];
         S.wid = A.width[am];
-        S.f_len = __double2float_rn(S.len / k.bbox_half);
-        S.f_wid = __double2float_rn(S.wid / k.bbox_half);
-        S.f_spd = __double2float_rn(sqrt(x[SVX] * x[SVX] + x[SVY] * x[SVY]) / k.speed_norm);
+        S.f_len = __double2float_rn(dg::ddiv(S.len, k.bbox_half));
+        S.f_wid = __double2float_rn(dg::ddiv(S.wid, k.bbox_half));
+        S.f_spd = __double2float_rn(dg::ddiv(dg::dsqrt(x[SVX] * x[SVX] + x[SVY] * x[SVY]), k.speed_norm));
         const double offs[3] = {-1.0, 0.0, 1.0};
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
@@ -488,23 +506,39 @@ world_step_kernel(const KArgs A) {
         S.reason = A.reason[am];
         S.seen = A.event_seen[am];
         S.spawn = A.spawn_step[am];
+        LANE0_MARK(19);
     }
     for (int m = warp; m < M; m += nwarps) zero_row(obs_w + int64_t(m) * D, D, lane);
 
+    if (warp == 0) PHASE_MARK(2);
     __syncthreads();  // agent table + zero rows done, mbarrier init visible
+    PHASE_MARK(3);
     mbar_wait(bar, 0);
     // the view reads the index header from the copied blob: only after the wait
     const SceneView G = scene_view(geo, int(meta[2]), int(meta[3]), int(meta[4]));
     {   // scene-local midpoints -> global, exactly midpoints + grid offset
-        double* mx = const_cast<double*>(G.mx);
-        double* my = const_cast<double*>(G.my);
         for (int i = tid; i < G.P; i += blockDim.x) {
-            mx[i] = mx[i] + ox;
-            my[i] = my[i] + oy;
+            double2 m2 = G.mid[i];
+            m2.x = m2.x + ox;
+            m2.y = m2.y + oy;
+            G.mid[i] = m2;
+        }
+        for (int i = tid; i < G.KL; i += blockDim.x) {
+            double4 l4 = G.lane_seg[i];
+            l4.x = l4.x + ox;
+            l4.y = l4.y + oy;
+            G.lane_seg[i] = l4;
+        }
+        for (int i = tid; i < G.KE; i += blockDim.x) {
+            double2 e2 = G.edge_mid[i];
+            e2.x = e2.x + ox;
+            e2.y = e2.y + oy;
+            G.edge_mid[i] = e2;
         }
     }
     __syncthreads();
 
+    PHASE_MARK(4);
     // ---- phase 2a: agent pairs, 16 lanes per ego agent (lane j <-> other agent j):
     //      stable distance rank, swept-circle TTC, neighbour rows, hull contact
     const int road0 = A.d.ego_dim;
@@ -523,7 +557,7 @@ world_step_kernel(const KArgs A) {
                 const AgentSm& N = ag[j];
                 ndx = N.st[SX] - px;
                 ndy = N.st[SY] - py;
-                const double dist = sqrt(ndx * ndx + ndy * ndy);
+                const double dist = dg::dsqrt(ndx * ndx + ndy * ndy);
                 key = (N.alive && j != ii) ? dist : INFINITY;
             }
             int rank = 0;
@@ -541,15 +575,15 @@ world_step_kernel(const KArgs A) {
                 sincos(N.st[SYAW] - S.st[SYAW], &st_, &ct_);
                 const double wrap = atan2(st_, ct_);
                 float* o = obs_w + int64_t(ii) * D + veh0 + 7 * rank;
-                o[0] = __double2float_rn((c * ndx + s * ndy) / k.bbox_half);
-                o[1] = __double2float_rn((-s * ndx + c * ndy) / k.bbox_half);
+                o[0] = __double2float_rn(dg::ddiv(c * ndx + s * ndy, k.bbox_half));
+                o[1] = __double2float_rn(dg::ddiv(-s * ndx + c * ndy, k.bbox_half));
                 o[2] = N.f_len;
                 o[3] = N.f_wid;
-                o[4] = __double2float_rn(wrap / 3.141592653589793);
+                o[4] = __double2float_rn(dg::ddiv(wrap, 3.141592653589793));
                 o[5] = N.f_spd;
-                o[6] = __double2float_rn(ttc / k.ttc_max);
+                o[6] = __double2float_rn(dg::ddiv(ttc, k.ttc_max));
             }
-            for (int o = 8; o > 0; o >>= 1) ttc = fmin(ttc, __shfl_xor_sync(kFull, ttc, o, 16));
+            ttc = warp_min(ttc, 16);
             bool touch = false;
             if (kStep && ego_ok && j < M && j != ii && S.alive && ag[j].alive) {
                 const AgentSm& N = ag[j];
@@ -589,21 +623,22 @@ world_step_kernel(const KArgs A) {
         auto visit = [&](int q, bool in, bool edge_q) {
             bool hit = false;
             if (in) {
-                const double dx = G.mx[q] - px, dy = G.my[q] - py;
+                const double2 m2 = G.mid[q];
+                const double dx = m2.x - px, dy = m2.y - py;
                 const double d2 = dx * dx + dy * dy;
                 hit = d2 <= k.road_radius_sq;
                 if (rewards_needed && edge_q) {
                     const double hl = G.hl[q], hw = G.hw[q];
                     const double reach = S.r + S.d + hl + hw + 1e-6;
                     if (d2 <= reach * reach) {
-                        const double ux = G.dx[q], uy = G.dy[q];
+                        const double2 u2 = G.dir[q];
 #pragma unroll
                         for (int i = 0; i < 3; ++i) {
-                            const double qx = S.hx[i] - G.mx[q], qy = S.hy[i] - G.my[q];
-                            const double along = qx * ux + qy * uy;
-                            const double lat = ux * qy - uy * qx;
-                            const double du = along - fmin(fmax(along, -hl), hl);
-                            const double dv = lat - fmin(fmax(lat, -hw), hw);
+                            const double qx = S.hx[i] - m2.x, qy = S.hy[i] - m2.y;
+                            const double along = qx * u2.x + qy * u2.y;
+                            const double lat = u2.x * qy - u2.y * qx;
+                            const double du = along - sel_clip(along, -hl, hl);
+                            const double dv = lat - sel_clip(lat, -hw, hw);
                             edge_hit |= du * du + dv * dv < r2;
                         }
                     }
@@ -653,11 +688,12 @@ world_step_kernel(const KArgs A) {
         __syncwarp();
         for (int slot = lane; slot < ncand; slot += 32) {
             const int q = cand[slot];
-            const double dx = G.mx[q] - px, dy = G.my[q] - py;
-            const double ux = G.dx[q], uy = G.dy[q];
+            const double2 m2 = G.mid[q], u2 = G.dir[q];
+            const double dx = m2.x - px, dy = m2.y - py;
+            const double ux = u2.x, uy = u2.y;
             float* o = row + road0 + 5 * slot;
-            o[0] = __double2float_rn((c * dx + s * dy) / k.road_radius);
-            o[1] = __double2float_rn((-s * dx + c * dy) / k.road_radius);
+            o[0] = __double2float_rn(dg::ddiv(c * dx + s * dy, k.road_radius));
+            o[1] = __double2float_rn(dg::ddiv(-s * dx + c * dy, k.road_radius));
             o[2] = G.type_feat[q];
             o[3] = __double2float_rn(c * ux + s * uy);
             o[4] = __double2float_rn(-s * ux + c * uy);
@@ -676,28 +712,31 @@ world_step_kernel(const KArgs A) {
         // (b) first road edge ahead over every edge (xb in (0, edge_range]); the
         //     edge boxes when the grid could not take them
         double gap = INFINITY;
+#pragma unroll 2
         for (int kk = lane; kk < G.KE; kk += 32) {
-            const int q = G.edge[kk];
-            const double ex = G.mx[q] - px, ey = G.my[q] - py;
+            const double2 m2 = G.edge_mid[kk];
+            const double ex = m2.x - px, ey = m2.y - py;
             const double xb = c * ex + s * ey;
-            if (xb > 0.0 && xb <= k.edge_range) gap = fmin(gap, xb);
+            if (xb > 0.0 && xb <= k.edge_range && xb < gap) gap = xb;
             if (!use_grid) {
-                const double ux = G.dx[q], uy = G.dy[q], hl = G.hl[q], hw = G.hw[q];
+                const int q = G.edge[kk];
+                const double2 u2 = G.dir[q];
+                const double hl = G.hl[q], hw = G.hw[q];
                 const double reach = S.r + S.d + hl + hw + 1e-6;
                 if (ex * ex + ey * ey <= reach * reach) {
 #pragma unroll
                     for (int i = 0; i < 3; ++i) {
-                        const double qx = S.hx[i] - G.mx[q], qy = S.hy[i] - G.my[q];
-                        const double along = qx * ux + qy * uy;
-                        const double lat = ux * qy - uy * qx;
-                        const double du = along - fmin(fmax(along, -hl), hl);
-                        const double dv = lat - fmin(fmax(lat, -hw), hw);
+                        const double qx = S.hx[i] - m2.x, qy = S.hy[i] - m2.y;
+                        const double along = qx * u2.x + qy * u2.y;
+                        const double lat = u2.x * qy - u2.y * qx;
+                        const double du = along - sel_clip(along, -hl, hl);
+                        const double dv = lat - sel_clip(lat, -hw, hw);
                         edge_hit |= du * du + dv * dv < r2;
                     }
                 }
             }
         }
-        for (int o = 16; o > 0; o >>= 1) gap = fmin(gap, __shfl_xor_sync(kFull, gap, o));
+        gap = warp_min(gap);
         edge_hit = __any_sync(kFull, edge_hit);
 
         // (c) nearest lane: argmin of point-to-segment d2, lowest index on ties,
@@ -705,19 +744,20 @@ world_step_kernel(const KArgs A) {
         double best = INFINITY;
         int best_k = 0x7fffffff;
         auto lane_test = [&](int kk) {
-            const int q = G.lane[kk];
-            const double ex = px - G.mx[q], ey = py - G.my[q];
-            const double ux = G.dx[q], uy = G.dy[q];
-            const double along = ex * ux + ey * uy;
-            const double lat = ux * ey - uy * ex;
-            const double over = fmax(fabs(along) - G.hl[q], 0.0);
+            const double4 l4 = G.lane_seg[kk];
+            const double ex = px - l4.x, ey = py - l4.y;
+            const double along = ex * l4.z + ey * l4.w;
+            const double lat = l4.z * ey - l4.w * ex;
+            const double t = fabs(along) - G.lane_hl[kk];
+            const double over = t > 0.0 ? t : 0.0;   // NaN along -> NaN lat, d2 NaN either way
             const double d2 = over * over + lat * lat;
-            if (d2 < best || (d2 == best && kk < best_k)) { best = d2; best_k = kk; }
+            if (d2 < best) { best = d2; best_k = kk; }
         };
         int lcell = -1;
         if (G.flags & kFlagLanes) {
             const double plx = px - ox, ply = py - oy;
-            const double fx = floor((plx - G.gx0) / G.cell), fy = floor((ply - G.gy0) / G.cell);
+            const double inv = 1.0 / G.cell;
+            const double fx = floor((plx - G.gx0) * inv), fy = floor((ply - G.gy0) * inv);
             if (fx >= 0.0 && fy >= 0.0 && fx < double(G.nx) && fy < double(G.ny)) lcell = int(fy) * G.nx + int(fx);
         }
         if (lcell >= 0) {
@@ -739,7 +779,9 @@ world_step_kernel(const KArgs A) {
             R.edge_hit = edge_hit;
         }
     }
+    WARP_MARK(0);
     __syncthreads();
+    PHASE_MARK(5);
 
     // ---- phase 3: one lane per agent (SIMT across the world's agents):
     //      warp 0 -> rewards, events, termination, state write-back;
@@ -755,13 +797,13 @@ world_step_kernel(const KArgs A) {
         const double yb = -s * gdx + c * gdy;
         double sh, ch;
         sincos(atan2(yb, xb), &sh, &ch);
-        row[0] = __double2float_rn(xb / k.bbox_half);
-        row[1] = __double2float_rn(yb / k.bbox_half);
+        row[0] = __double2float_rn(dg::ddiv(xb, k.bbox_half));
+        row[1] = __double2float_rn(dg::ddiv(yb, k.bbox_half));
         row[2] = __double2float_rn(sh);
         row[3] = __double2float_rn(ch);
-        row[4] = __double2float_rn(sqrt(xb * xb + yb * yb) / k.bbox_half);
-        row[5] = __double2float_rn(S.st[SVX] / k.speed_norm);
-        row[6] = __double2float_rn(S.st[SVY] / k.speed_norm);
+        row[4] = __double2float_rn(dg::ddiv(dg::dsqrt(xb * xb + yb * yb), k.bbox_half));
+        row[5] = __double2float_rn(dg::ddiv(S.st[SVX], k.speed_norm));
+        row[6] = __double2float_rn(dg::ddiv(S.st[SVY], k.speed_norm));
         if (A.d.include_weather) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) row[7 + i] = __double2float_rn(A.weather[4 * w + i]);
@@ -775,14 +817,14 @@ world_step_kernel(const KArgs A) {
             const ScanSm& R = sc[m];
             const double px = S.st[SX], py = S.st[SY];
             const double vx = S.st[SVX], vy = S.st[SVY], yaw = S.st[SYAW];
-            const double dist = sqrt(R.lane_d2);
+            const double dist = dg::dsqrt(R.lane_d2);
             const bool has_lane = finite(dist);
             double lat = 0.0, tx = 0.0, ty = 0.0;
             if (has_lane) {
-                const int q = G.lane[R.lane_k];
-                const double ex = px - G.mx[q], ey = py - G.my[q];
-                tx = G.dx[q];
-                ty = G.dy[q];
+                const double4 l4 = G.lane_seg[R.lane_k];
+                const double ex = px - l4.x, ey = py - l4.y;
+                tx = l4.z;
+                ty = l4.w;
                 lat = tx * ey - ty * ex;
             }
             const double tgx = S.gx - px, tgy = S.gy - py;
@@ -792,26 +834,26 @@ world_step_kernel(const KArgs A) {
             double progress = np_clip((px - S.px0) * tx + (py - S.py0) * ty,
                                       -k.progress_clamp, k.progress_clamp) * k.progress_weight;
             const double align = np_max(0.0, cos(yaw - atan2(ty, tx)));
-            const double ls = lat / k.lane_sigma;
+            const double ls = dg::ddiv(lat, k.lane_sigma);
             const double quality = exp(-(ls * ls)) * (k.lane_heading_base + k.lane_heading_weight * align);
             const double lane_t = has_lane ? k.lane_weight * quality : 0.0;
             progress = has_lane ? progress : 0.0;
             const double offroad = (has_lane && (fabs(lat) > k.offroad_lat_limit || dist > k.offroad_dist_limit))
                                        ? -k.offroad_weight : 0.0;
-            const double speed = sqrt(vx * vx + vy * vy);
+            const double speed = dg::dsqrt(vx * vx + vy * vy);
             const double idle = speed < k.idle_speed ? -k.idle_weight : 0.0;
-            const double ttc_v = -np_min(k.ttc_vehicle_alpha / np_max(R.ttc_min, k.ttc_floor), k.ttc_vehicle_pmax);
-            const double tau = R.gap / np_max(vx, 0.1);
-            const double ttc_e = finite(tau) ? -np_min(k.ttc_edge_alpha / np_max(tau, k.ttc_floor), k.ttc_edge_pmax)
+            const double ttc_v = -np_min(dg::ddiv(k.ttc_vehicle_alpha, np_max(R.ttc_min, k.ttc_floor)), k.ttc_vehicle_pmax);
+            const double tau = R.gap < INFINITY ? dg::ddiv(R.gap, np_max(vx, 0.1)) : R.gap / np_max(vx, 0.1);
+            const double ttc_e = finite(tau) ? -np_min(dg::ddiv(k.ttc_edge_alpha, np_max(tau, k.ttc_floor)), k.ttc_edge_pmax)
                                              : 0.0;
             const double total = progress + lane_t + offroad + idle + ttc_v + ttc_e;
 
             // sparse events, masked by alive and the per-type latch
             const bool alive = S.alive;
-            const bool goal = sqrt(tgx * tgx + tgy * tgy) <= k.goal_radius;
+            const bool goal = dg::dsqrt(tgx * tgx + tgy * tgy) <= k.goal_radius;
             const double sxd = px - S.sx, syd = py - S.sy;
             const bool bad = !(finite(px) && finite(py) && finite(vx) && finite(vy));
-            const bool crash = sqrt(sxd * sxd + syd * syd) > k.crash_drift_limit || bad ||
+            const bool crash = dg::dsqrt(sxd * sxd + syd * syd) > k.crash_drift_limit || bad ||
                                speed > k.crash_speed_limit;
             const bool coll = R.touch && step_now - S.spawn >= A.d.collision_warmup;
             const int seen = S.seen;
@@ -887,6 +929,7 @@ world_step_kernel(const KArgs A) {
             A.spawn_step[am] = spawn;
         }
         if (tid == 0) A.step_count[w] = step_now + 1;
+        PHASE_MARK(6);
     }
 }
 
@@ -1171,6 +1214,14 @@ int dg_lane_follower(dg_engine* eng, const float* obs, double* actions, double s
 }
 
 int dg_launch_count(dg_engine* eng) { return eng ? eng->launches : 0; }
+
+#ifdef DG_PHASE_TIMERS
+int dg_debug_phase_clocks(long long* host_out, int n_blocks) {
+    const int n = n_blocks < 65536 ? n_blocks : 65536;
+    const cudaError_t e = cudaMemcpyFromSymbol(host_out, g_phase_clock, sizeof(long long) * 24 * n);
+    return e == cudaSuccess ? DG_OK : cuda_fail(e, "dg_debug_phase_clocks");
+}
+#endif
 
 int dg_tune(dg_engine* eng, int32_t warps_per_world) {
     if (!eng) return fail(DG_EINVAL, "dg_tune: null engine");

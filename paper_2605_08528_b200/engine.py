@@ -89,13 +89,16 @@ def pack_scenes(scene_tables, type_norm: float, road_radius: float = 10.0,
     blobs, meta, off = [], [], 0
     for t in scene_tables:
         P, KL, KE = t.num_segments, len(t.lane_index), len(t.edge_index)
-        parts = []
-        for arr in (t.midpoints[:, 0], t.midpoints[:, 1], t.directions[:, 0], t.directions[:, 1],
-                    t.half_lengths, t.half_widths):
-            parts.append(np.ascontiguousarray(arr, dtype=np.float64))
-        parts += [(t.type_codes.astype(np.float64) / type_norm).astype(np.float32),
-                  t.lane_index.astype(np.int32),
-                  t.edge_index.astype(np.int32)]
+        L, E = t.lane_index, t.edge_index
+        parts = [np.ascontiguousarray(t.midpoints, dtype=np.float64),        # f64x2 mid[P]
+                 np.ascontiguousarray(t.directions, dtype=np.float64),       # f64x2 dir[P]
+                 np.ascontiguousarray(t.half_lengths, dtype=np.float64),
+                 np.ascontiguousarray(t.half_widths, dtype=np.float64),
+                 (t.type_codes.astype(np.float64) / type_norm).astype(np.float32),
+                 np.ascontiguousarray(np.concatenate([t.midpoints[L], t.directions[L]], axis=1)),
+                 np.ascontiguousarray(t.half_lengths[L], dtype=np.float64),
+                 np.ascontiguousarray(t.midpoints[E], dtype=np.float64),
+                 E.astype(np.int32)]
         chunk = bytearray()
         for a in parts:
             b = a.tobytes()
