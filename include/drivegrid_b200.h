@@ -82,8 +82,11 @@ typedef struct DgConsts {
  * coordinates:  f64x2 mid[P]; f64x2 dir[P]; f64 half_len[P]; f64 half_wid[P];
  * f32 type_feat[P] = float32(type / type_norm); lane subset f64x4
  * {mid, dir}[KL], f64 half_len[KL]; edge subset f64x2 mid[KE], i32 index[KE];
- * then the spatial index of paper_2605_08528_b200/spatial.py.
- * scene_meta[s] = {byte_offset, byte_size, P, KL, KE, 0, 0, 0} (int64). */
+ * then the 64-byte spatial-index header of paper_2605_08528_b200/spatial.py;
+ * that prefix is what the kernel copies to shared memory.  The index's
+ * candidate lists follow in global memory.
+ * scene_meta[s] = {byte_offset, smem_bytes, P, KL, KE, aux_offset, aux_bytes, 0}
+ * (int64, byte offsets from scene_blob). */
 typedef struct DgEngineDesc {
     DgDims dims;
     DgConsts k;
@@ -168,9 +171,11 @@ int dg_lane_follower(dg_engine* eng, const float* obs, double* actions, double s
 /* Kernel launches issued by the last dg_step/dg_observe/dg_reset call. */
 int dg_launch_count(dg_engine* eng);
 
-/* Launch shape: warps per world CTA (1..16, default M); agents are strided
- * over the warps.  A performance knob only -- results do not depend on it. */
-int dg_tune(dg_engine* eng, int32_t warps_per_world);
+/* Launch shape: warps per world CTA (1..16, default M; agents are strided
+ * over the warps) and the kernel variant's register budget, expressed as
+ * resident CTAs per SM (0 = default).  A performance knob only -- results
+ * do not depend on it. */
+int dg_tune(dg_engine* eng, int32_t warps_per_world, int32_t ctas_per_sm);
 
 const char* dg_last_error(void);
 int dg_abi_version(void);

@@ -84,7 +84,7 @@ SIGNATURES = {
     "dg_read_error": (ct.c_int, [_P, ct.POINTER(ct.c_int32), _P]),
     "dg_lane_follower": (ct.c_int, [_P, _P, _P, ct.c_double, ct.c_double, _P]),
     "dg_launch_count": (ct.c_int, [_P]),
-    "dg_tune": (ct.c_int, [_P, ct.c_int32]),
+    "dg_tune": (ct.c_int, [_P, ct.c_int32, ct.c_int32]),
 }
 
 

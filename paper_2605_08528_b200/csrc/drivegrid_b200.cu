@@ -133,13 +133,15 @@ struct SceneView {
     const double* lane_hl;    // [KL]
     double2* edge_mid;        // [KE] edge subset midpoints
     const int32_t* edge;      // [KE] edge subset -> segment index
-    // spatial index (paper_2605_08528_b200/spatial.py); flags == 0 -> full scans
+    // spatial index (paper_2605_08528_b200/spatial.py); flags == 0 -> full scans.
+    // Header in shared memory, candidate lists in global memory (L1-cached).
     double gx0, gy0, cell, half;
     int nx, ny, words, flags;
-    const uint32_t* seg_bits;   // [nx*ny][words]  bit q: midpoint q in the cell
-    const uint32_t* edge_bits;  // [words]         bit q: segment q is a road edge
+    const int32_t* road_start;  // [nx*ny + 1]
+    const uint16_t* road_list;  // segments with midpoint within `half` of the cell, ascending
     const int32_t* lane_start;  // [nx*ny + 1]
-    const int32_t* lane_list;   // lane-list indices (into lane[]), ascending per cell
+    const uint16_t* lane_list;  // lane-subset indices that can be the nearest lane, ascending
+    const uint32_t* edge_bits;  // [words] bit q: segment q is a road edge
     int P, KL, KE;
 };
 
@@ -148,7 +150,7 @@ constexpr int kFlagLanes = 2;
 
 __host__ __device__ __forceinline__ int64_t align16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
-__device__ __forceinline__ SceneView scene_view(uint8_t* base, int P, int KL, int KE) {
+__device__ __forceinline__ SceneView scene_view(uint8_t* base, const uint8_t* aux, int P, int KL, int KE) {
     SceneView v;
     int64_t o = 0;
     v.mid = reinterpret_cast<double2*>(base + o); o += int64_t(P) * 16;
@@ -164,15 +166,11 @@ __device__ __forceinline__ SceneView scene_view(uint8_t* base, int P, int KL, in
     const int32_t* hi = reinterpret_cast<const int32_t*>(base + o + 32);
     v.gx0 = hd[0]; v.gy0 = hd[1]; v.cell = hd[2]; v.half = hd[3];
     v.nx = hi[0]; v.ny = hi[1]; v.words = hi[2]; v.flags = hi[3];
-    o += 48;
-    const int64_t ncell = int64_t(v.nx) * v.ny;
-    v.seg_bits = reinterpret_cast<const uint32_t*>(base + o);
-    if (v.flags) o += align16(ncell * v.words * 4);
-    v.edge_bits = reinterpret_cast<const uint32_t*>(base + o);
-    if (v.flags) o += align16(int64_t(v.words) * 4);
-    v.lane_start = reinterpret_cast<const int32_t*>(base + o);
-    if (v.flags) o += align16((ncell + 1) * 4);
-    v.lane_list = reinterpret_cast<const int32_t*>(base + o);
+    v.road_start = reinterpret_cast<const int32_t*>(aux);
+    v.road_list = reinterpret_cast<const uint16_t*>(aux + hi[4]);
+    v.lane_start = reinterpret_cast<const int32_t*>(aux + hi[5]);
+    v.lane_list = reinterpret_cast<const uint16_t*>(aux + hi[6]);
+    v.edge_bits = reinterpret_cast<const uint32_t*>(aux + hi[7]);
     v.P = P; v.KL = KL; v.KE = KE;
     return v;
 }
@@ -375,7 +373,9 @@ __device__ long long g_phase_clock[65536][24];
 #define PHASE_MARK(i) do { if (threadIdx.x == 0 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][i] = clock64(); } while (0)
 #define WARP_MARK(i) do { if ((threadIdx.x & 31) == 0 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][8 + (threadIdx.x >> 5)] = clock64(); } while (0)
 #define LANE0_MARK(i) do { if (threadIdx.x == 0 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][i] = clock64(); } while (0)
+#define W1_MARK(i) do { if (threadIdx.x == 32 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][i] = clock64(); } while (0)
 #else
+#define W1_MARK(i) do { } while (0)
 #define LANE0_MARK(i) do { } while (0)
 #define PHASE_MARK(i) do { } while (0)
 #define WARP_MARK(i) do { } while (0)
@@ -515,7 +515,7 @@ world_step_kernel(const KArgs A) {
     PHASE_MARK(3);
     mbar_wait(bar, 0);
     // the view reads the index header from the copied blob: only after the wait
-    const SceneView G = scene_view(geo, int(meta[2]), int(meta[3]), int(meta[4]));
+    const SceneView G = scene_view(geo, A.scene_blob + meta[5], int(meta[2]), int(meta[3]), int(meta[4]));
     {   // scene-local midpoints -> global, exactly midpoints + grid offset
         for (int i = tid; i < G.P; i += blockDim.x) {
             double2 m2 = G.mid[i];
@@ -606,6 +606,7 @@ world_step_kernel(const KArgs A) {
         }
     }
 
+    W1_MARK(10);
     // ---- phase 2b: warp m scans the scene for agent m
     for (int m = warp; m < M; m += nwarps) {
         const AgentSm& S = ag[m];
@@ -652,39 +653,30 @@ world_step_kernel(const KArgs A) {
             count += __popc(bal);
         };
         const bool use_grid = (G.flags & kFlagGrid) != 0;
-        if (use_grid) {
-            const double plx = px - ox, ply = py - oy;
+        // the agent's grid cell (scene-local coordinates); -1 off the grid
+        int cell_id = -1;
+        if (G.flags) {
             const double inv = 1.0 / G.cell;
-            int cx0 = int(floor((plx - G.half - G.gx0) * inv)), cx1 = int(floor((plx + G.half - G.gx0) * inv));
-            int cy0 = int(floor((ply - G.half - G.gy0) * inv)), cy1 = int(floor((ply + G.half - G.gy0) * inv));
-            const bool finite_pos = finite(plx) && finite(ply);
-            cx0 = cx0 < 0 ? 0 : cx0;
-            cy0 = cy0 < 0 ? 0 : cy0;
-            cx1 = cx1 >= G.nx ? G.nx - 1 : cx1;
-            cy1 = cy1 >= G.ny ? G.ny - 1 : cy1;
-            const bool any_cell = finite_pos && cx0 <= cx1 && cy0 <= cy1 &&
-                                  plx + G.half >= G.gx0 && ply + G.half >= G.gy0;
-            for (int wb = 0; wb < G.words; wb += 32) {
-                const int wi = wb + lane;
-                uint32_t bits = 0;
-                if (any_cell && wi < G.words) {
-                    for (int cy = cy0; cy <= cy1; ++cy)
-                        for (int cx = cx0; cx <= cx1; ++cx) bits |= G.seg_bits[(cy * G.nx + cx) * G.words + wi];
-                }
-                unsigned nz = __ballot_sync(kFull, bits != 0);
-                while (nz) {
-                    const int l = __ffs(nz) - 1;
-                    nz &= nz - 1;
-                    const uint32_t wbits = __shfl_sync(kFull, bits, l);
-                    const uint32_t ebits = G.edge_bits[wb + l];
-                    const int q = (wb + l) * 32 + lane;
-                    visit(q, (wbits >> lane) & 1u, (ebits >> lane) & 1u);
+            const double fx = floor((px - ox - G.gx0) * inv), fy = floor((py - oy - G.gy0) * inv);
+            if (fx >= 0.0 && fy >= 0.0 && fx < double(G.nx) && fy < double(G.ny)) cell_id = int(fy) * G.nx + int(fx);
+        }
+        if (use_grid) {
+            // the cell's superset list (ascending) -> exact predicates, index order;
+            // off the grid nothing is within the road radius or an edge box
+            if (cell_id >= 0) {
+                const int lo = __ldg(G.road_start + cell_id), hi = __ldg(G.road_start + cell_id + 1);
+                for (int b0 = lo; b0 < hi; b0 += 32) {
+                    const int i = b0 + lane;
+                    const int q = i < hi ? int(__ldg(G.road_list + i)) : 0;
+                    const bool edge_q = (__ldg(G.edge_bits + (q >> 5)) >> (q & 31)) & 1u;
+                    visit(q, i < hi, edge_q);
                 }
             }
         } else {
             for (int p0 = 0; p0 < G.P; p0 += 32) visit(p0 + lane, p0 + lane < G.P, false);
         }
         const int ncand = count < A.take_road ? count : A.take_road;
+        if (m == 1) W1_MARK(11);
         __syncwarp();
         for (int slot = lane; slot < ncand; slot += 32) {
             const int q = cand[slot];
@@ -699,6 +691,7 @@ world_step_kernel(const KArgs A) {
             o[4] = __double2float_rn(-s * ux + c * uy);
         }
 
+        if (m == 1) W1_MARK(12);
         if (!rewards_needed) {
             if (kStep && lane == 0) {
                 ScanSm& R = sc[m];
@@ -738,6 +731,7 @@ world_step_kernel(const KArgs A) {
         }
         gap = warp_min(gap);
         edge_hit = __any_sync(kFull, edge_hit);
+        if (m == 1) W1_MARK(13);
 
         // (c) nearest lane: argmin of point-to-segment d2, lowest index on ties,
         //     over the cell's candidate list when the agent is inside the grid
@@ -753,16 +747,10 @@ world_step_kernel(const KArgs A) {
             const double d2 = over * over + lat * lat;
             if (d2 < best) { best = d2; best_k = kk; }
         };
-        int lcell = -1;
-        if (G.flags & kFlagLanes) {
-            const double plx = px - ox, ply = py - oy;
-            const double inv = 1.0 / G.cell;
-            const double fx = floor((plx - G.gx0) * inv), fy = floor((ply - G.gy0) * inv);
-            if (fx >= 0.0 && fy >= 0.0 && fx < double(G.nx) && fy < double(G.ny)) lcell = int(fy) * G.nx + int(fx);
-        }
+        const int lcell = (G.flags & kFlagLanes) ? cell_id : -1;
         if (lcell >= 0) {
-            const int b0 = G.lane_start[lcell], b1 = G.lane_start[lcell + 1];
-            for (int i = b0 + lane; i < b1; i += 32) lane_test(G.lane_list[i]);
+            const int b0 = __ldg(G.lane_start + lcell), b1 = __ldg(G.lane_start + lcell + 1);
+            for (int i = b0 + lane; i < b1; i += 32) lane_test(__ldg(G.lane_list + i));
         } else {
             for (int kk = lane; kk < G.KL; kk += 32) lane_test(kk);
         }
@@ -771,6 +759,7 @@ world_step_kernel(const KArgs A) {
             const int ok = __shfl_xor_sync(kFull, best_k, o);
             if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
         }
+        if (m == 1) W1_MARK(14);
         if (lane == 0) {
             ScanSm& R = sc[m];
             R.lane_d2 = best;
@@ -995,34 +984,46 @@ struct dg_engine {
     size_t smem_bytes;
     int launches;
     int warps_per_world;   // CTA = warps_per_world warps, agents strided over warps
+    int min_blocks;        // register budget: resident CTAs per SM the variant is built for
 };
+
+#define DG_VARIANTS(X)                                                                 \
+    X(512, 1) X(256, 2) X(256, 3) X(256, 4) X(128, 4) X(128, 6) X(128, 8)
 
 // Kernel variants: (threads per CTA, min resident CTAs per SM) bounds trade
 // registers for occupancy; dg_tune picks one.
 template <bool kStep>
 static cudaError_t launch_world_step(const dg_engine* e, const KArgs& A, cudaStream_t st) {
     const int nw = e->warps_per_world;
+    const int threads = nw > 8 ? 512 : (nw > 4 ? 256 : 128);
     const dim3 grid(A.d.W);
-    if (nw > 8)
-        world_step_kernel<kStep, 512, 1><<<grid, 32 * nw, e->smem_bytes, st>>>(A);
-    else if (nw > 4)
-        world_step_kernel<kStep, 256, 2><<<grid, 32 * nw, e->smem_bytes, st>>>(A);
-    else
-        world_step_kernel<kStep, 128, 4><<<grid, 32 * nw, e->smem_bytes, st>>>(A);
-    return cudaGetLastError();
+#define DG_LAUNCH(T, B)                                                                  \
+    if (threads == T && e->min_blocks == B) {                                            \
+        world_step_kernel<kStep, T, B><<<grid, 32 * nw, e->smem_bytes, st>>>(A);         \
+        return cudaGetLastError();                                                       \
+    }
+    DG_VARIANTS(DG_LAUNCH)
+#undef DG_LAUNCH
+    return cudaErrorInvalidConfiguration;
 }
 
 template <bool kStep>
 static cudaError_t set_smem_attr(size_t bytes) {
-    cudaError_t e = cudaFuncSetAttribute(world_step_kernel<kStep, 512, 1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(world_step_kernel<kStep, 256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(bytes));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(world_step_kernel<kStep, 128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(bytes));
+    cudaError_t e = cudaSuccess;
+#define DG_ATTR(T, B)                                                                    \
+    if (e == cudaSuccess)                                                                \
+        e = cudaFuncSetAttribute(world_step_kernel<kStep, T, B>,                         \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    DG_VARIANTS(DG_ATTR)
+#undef DG_ATTR
     return e;
+}
+
+static bool has_variant(int threads, int blocks) {
+#define DG_HAS(T, B) if (threads == T && blocks == B) return true;
+    DG_VARIANTS(DG_HAS)
+#undef DG_HAS
+    return false;
 }
 
 static thread_local char g_err[512] = "";
@@ -1110,6 +1111,7 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
     }
     e->launches = 0;
     e->warps_per_world = d.M;
+    e->min_blocks = 1;
     *out = e;
     return DG_OK;
 }
@@ -1223,11 +1225,16 @@ int dg_debug_phase_clocks(long long* host_out, int n_blocks) {
 }
 #endif
 
-int dg_tune(dg_engine* eng, int32_t warps_per_world) {
+int dg_tune(dg_engine* eng, int32_t warps_per_world, int32_t ctas_per_sm) {
     if (!eng) return fail(DG_EINVAL, "dg_tune: null engine");
     if (warps_per_world < 1 || warps_per_world > kMaxAgents)
         return fail(DG_EINVAL, "dg_tune: warps_per_world must lie in [1, 16]");
-    eng->warps_per_world = warps_per_world < eng->base.d.M ? warps_per_world : eng->base.d.M;
+    const int nw = warps_per_world < eng->base.d.M ? warps_per_world : eng->base.d.M;
+    const int threads = nw > 8 ? 512 : (nw > 4 ? 256 : 128);
+    int blocks = ctas_per_sm > 0 ? ctas_per_sm : (threads == 512 ? 1 : threads == 256 ? 2 : 4);
+    if (!has_variant(threads, blocks)) return fail(DG_EINVAL, "dg_tune: no kernel variant for this shape");
+    eng->warps_per_world = nw;
+    eng->min_blocks = blocks;
     return DG_OK;
 }
 

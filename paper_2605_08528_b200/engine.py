@@ -84,8 +84,9 @@ def make_consts(cfg: SimConfig, oc: ObsConfig, rc: RewardConfig, vp: VehiclePara
 def pack_scenes(scene_tables, type_norm: float, road_radius: float = 10.0,
                  agent_reach: float = 0.0, spatial_index: bool = True):
     """Concatenate per-scene blobs (layout documented in the C header).  The
-    type feature is float32(type / type_norm), the reference's own cast; the
-    spatial index (spatial.py) follows the segment arrays."""
+    type feature is float32(type / type_norm), the reference's own cast.  The
+    part the kernel copies to shared memory ends with the spatial-index header;
+    the index's candidate lists follow it and stay in global memory."""
     blobs, meta, off = [], [], 0
     for t in scene_tables:
         P, KL, KE = t.num_segments, len(t.lane_index), len(t.edge_index)
@@ -105,14 +106,16 @@ def pack_scenes(scene_tables, type_norm: float, road_radius: float = 10.0,
             chunk += b + bytes(_align16(len(b)) - len(b))
         edge_ext = float((t.half_lengths[t.edge_index] + t.half_widths[t.edge_index]).max()) \
             if len(t.edge_index) else 0.0
-        idx = build_scene_index(t.midpoints, t.directions, t.half_lengths, t.half_widths,
-                                t.lane_index, t.edge_index, road_radius,
-                                agent_reach + edge_ext + 1e-6)
+        head, aux = build_scene_index(t.midpoints, t.directions, t.half_lengths, t.half_widths,
+                                      t.lane_index, t.edge_index, road_radius,
+                                      agent_reach + edge_ext + 1e-6)
         if not spatial_index:
-            idx = idx[:32] + bytes(16)
-        chunk += idx + bytes(_align16(len(idx)) - len(idx))
+            head, aux = head[:32] + bytes(32), b""
+        chunk += head
+        smem_bytes = len(chunk)
+        chunk += aux + bytes(_align16(len(aux)) - len(aux))
         blobs.append(bytes(chunk))
-        meta.append([off, len(chunk), P, KL, KE, 0, 0, 0])
+        meta.append([off, smem_bytes, P, KL, KE, off + smem_bytes, len(aux), 0])
         off += len(chunk)
     blob = np.frombuffer(b"".join(blobs), dtype=np.uint8).copy()
     max_bytes = max(m[1] for m in meta)
@@ -305,9 +308,10 @@ class Engine:
     def new_step_buffers(self, obs: torch.Tensor | None = None) -> StepBuffers:
         return self._new_buffers(obs)
 
-    def tune(self, warps_per_world: int) -> None:
-        """Launch shape knob (warps per world CTA); results are unaffected."""
-        N.check(self._lib, self._lib.dg_tune(self._h, int(warps_per_world)), "dg_tune")
+    def tune(self, warps_per_world: int, ctas_per_sm: int = 0) -> None:
+        """Launch shape knob (warps per world CTA, register budget as resident
+        CTAs per SM); results are unaffected."""
+        N.check(self._lib, self._lib.dg_tune(self._h, int(warps_per_world), int(ctas_per_sm)), "dg_tune")
 
     # ------------------------------------------------------------------ device state views
     @property

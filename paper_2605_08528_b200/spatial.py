@@ -6,11 +6,10 @@ rewards.py:212-223).  The kernel keeps those exact float64 predicates and
 only shrinks the set it evaluates them on, with candidate sets that are
 provably supersets of every segment that can pass:
 
-  * road context / edge boxes: a uniform grid of cell size >= 2 * (road
-    radius + margin); a point's query square of half-width road_radius +
-    margin touches at most 2 x 2 cells, and a per-cell bitmask over segment
-    indices (bit q <=> midpoint q lies in the cell) OR-ed over those cells
-    is a superset of all segments with d2 <= r^2, already in index order.
+  * road context / edge boxes: a uniform grid (cell = half / 2, half =
+    road radius + margin); per cell, the ascending list of segments whose
+    midpoint lies within `half` of the cell rectangle.  For any point in the
+    cell it is a superset of the segments with d2 <= r^2, in index order.
     Every edge box that a hull circle can touch has its midpoint within
     r + d + half_len + half_wid <= road_radius of the agent (checked here;
     otherwise the edge test falls back to the full scan).
@@ -32,7 +31,7 @@ import numpy as np
 
 GRID_MARGIN = 4e-3      # m, query half-width = road_radius + GRID_MARGIN
 LANE_MARGIN = 1e-6      # m, slack on the nearest-lane bound
-HEADER_BYTES = 48       # f64 x0, y0, cell, half; i32 nx, ny, words, flags
+HEADER_BYTES = 64       # f64 x0, y0, cell, half; i32 nx, ny, words, flags, 4 aux offsets
 FLAG_GRID = 1
 FLAG_LANES = 2
 
@@ -81,18 +80,42 @@ def _seg_rect_dist(ax, ay, bx, by, x0, y0, x1, y1):
     return np.where(inside, 0.0, d)
 
 
+def _pt_rect_dist(px, py, x0, y0, x1, y1):
+    dx = np.maximum(np.maximum(x0 - px, 0.0), px - x1)
+    dy = np.maximum(np.maximum(y0 - py, 0.0), py - y1)
+    return np.sqrt(dx * dx + dy * dy)
+
+
+def _csr_u16(keep: np.ndarray):
+    starts = np.zeros(keep.shape[0] + 1, dtype=np.int32)
+    starts[1:] = np.cumsum(keep.sum(axis=1))
+    rows, cols = np.nonzero(keep)          # row-major: per cell ascending index
+    return starts, cols.astype(np.uint16)
+
+
+def _pad16(b: bytes) -> bytes:
+    return b + bytes((-len(b)) % 16)
+
+
 def build_scene_index(mid, dirs, hl, hw, lane_index, edge_index, road_radius: float,
-                      reach_max: float, max_cells: int = 4096, max_bytes: int = 96 * 1024):
-    """Serialized index for one scene (little-endian bytes, 16-byte padded),
-    or a header with flags = 0 when the scene does not qualify."""
+                      reach_max: float, cells_per_radius: int = 2, max_cells: int = 1 << 16):
+    """Index of one scene: (header, aux).
+
+    ``header`` (64 bytes) rides in the shared-memory scene blob:
+    f64 x0, y0, cell, half; i32 nx, ny, words, flags; i32 byte offsets in aux
+    of road_list, lane_start, lane_list, edge_bits.  ``aux`` stays in global
+    memory (read through L1): i32 road_start[ncell+1], u16 road_list[],
+    i32 lane_start[ncell+1], u16 lane_list[], u32 edge_bits[words].
+    Cell c = cy * nx + cx covers [x0 + cell*cx, +cell) x [y0 + cell*cy, +cell).
+    """
     P = int(mid.shape[0])
     words = max(1, (P + 31) // 32)
     half = road_radius + GRID_MARGIN
-    cell = 2.0 * half + 1e-3
+    cell = half / cells_per_radius
     head = np.zeros(4, dtype=np.float64)
-    ints = np.zeros(4, dtype=np.int32)
-    if P == 0:
-        return head.tobytes() + ints.tobytes()
+    ints = np.zeros(8, dtype=np.int32)
+    if P == 0 or P > 65535:
+        return head.tobytes() + ints.tobytes(), b""
     x0 = float(mid[:, 0].min()) - half
     y0 = float(mid[:, 1].min()) - half
     nx = int(math.floor((float(mid[:, 0].max()) + half - x0) / cell)) + 1
@@ -101,30 +124,26 @@ def build_scene_index(mid, dirs, hl, hw, lane_index, edge_index, road_radius: fl
     head[:] = (x0, y0, cell, half)
     ints[:3] = (nx, ny, words)
     if ncell > max_cells:
-        return head.tobytes() + ints.tobytes()
+        return head.tobytes() + ints.tobytes(), b""
+    cid = np.arange(ncell)
+    rx0 = x0 + cell * (cid % nx)
+    ry0 = y0 + cell * (cid // nx)
+    rx1, ry1 = rx0 + cell, ry0 + cell
 
-    cx = np.floor((mid[:, 0] - x0) / cell).astype(np.int64)
-    cy = np.floor((mid[:, 1] - y0) / cell).astype(np.int64)
-    bits = np.zeros((ncell, words), dtype=np.uint32)
-    for q in range(P):
-        bits[cy[q] * nx + cx[q], q >> 5] |= np.uint32(1 << (q & 31))
-    edge_bits = np.zeros(words, dtype=np.uint32)
-    for q in edge_index:
-        edge_bits[q >> 5] |= np.uint32(1 << (int(q) & 31))
+    # road / edge-box superset: segments whose midpoint is within `half` of the cell
+    near = _pt_rect_dist(mid[None, :, 0], mid[None, :, 1], rx0[:, None], ry0[:, None],
+                         rx1[:, None], ry1[:, None]) <= half
+    road_start, road_list = _csr_u16(near)
     flags = FLAG_GRID if reach_max <= road_radius else 0
 
-    # nearest-lane candidate lists (indices into lane_index, ascending)
-    starts = np.zeros(ncell + 1, dtype=np.int32)
-    lists = []
+    # nearest-lane candidates: lanes within ub(C) = min_s max_corner dist of the cell
+    lane_start = np.zeros(ncell + 1, dtype=np.int32)
+    lane_list = np.zeros(0, dtype=np.uint16)
     if len(lane_index):
         L = np.asarray(lane_index)
         lmx, lmy = mid[L, 0], mid[L, 1]
         lux, luy = dirs[L, 0], dirs[L, 1]
         lhl = hl[L]
-        cid = np.arange(ncell)
-        rx0 = x0 + cell * (cid % nx)          # cell c = cy * nx + cx
-        ry0 = y0 + cell * (cid // nx)
-        rx1, ry1 = rx0 + cell, ry0 + cell
         worst = np.zeros((ncell, len(L)))
         for qx, qy in ((rx0, ry0), (rx1, ry0), (rx0, ry1), (rx1, ry1)):
             worst = np.maximum(worst, _pt_seg_dist(qx[:, None], qy[:, None], lmx, lmy, lux, luy, lhl))
@@ -133,19 +152,17 @@ def build_scene_index(mid, dirs, hl, hw, lane_index, edge_index, road_radius: fl
         bx, by = lmx + lhl * lux, lmy + lhl * luy
         lb = _seg_rect_dist(ax[None, :], ay[None, :], bx[None, :], by[None, :],
                             rx0[:, None], ry0[:, None], rx1[:, None], ry1[:, None])
-        keep = lb <= (ub + LANE_MARGIN)[:, None]
-        for c in range(ncell):
-            ids = np.nonzero(keep[c])[0].astype(np.int32)
-            lists.append(ids)
-            starts[c + 1] = starts[c] + len(ids)
+        lane_start, lane_list = _csr_u16(lb <= (ub + LANE_MARGIN)[:, None])
         flags |= FLAG_LANES
-    lane_list = np.concatenate(lists).astype(np.int32) if lists else np.zeros(0, np.int32)
+    edge_bits = np.zeros(words, dtype=np.uint32)
+    for q in edge_index:
+        edge_bits[int(q) >> 5] |= np.uint32(1 << (int(q) & 31))
+
+    aux = b""
+    offs = []
+    for arr in (road_start, road_list, lane_start, lane_list, edge_bits):
+        offs.append(len(aux))
+        aux += _pad16(arr.tobytes())
     ints[3] = flags
-    out = head.tobytes() + ints.tobytes()
-    for arr in (bits.reshape(-1), edge_bits, starts, lane_list):
-        b = arr.tobytes()
-        out += b + bytes((-len(b)) % 16)
-    if len(out) > max_bytes:
-        ints[3] = 0
-        return head.tobytes() + ints.tobytes()
-    return out
+    ints[4:8] = offs[1:]
+    return head.tobytes() + ints.tobytes(), aux

@@ -16,42 +16,32 @@ from paper_2605_08528_b200.tables import SceneTable, _scene_table
 from paper_2605_08528_b200.scenes import scene_segments
 
 
-def parse(blob: bytes, P: int):
-    hd = np.frombuffer(blob[:32], np.float64)
-    nx, ny, words, flags = np.frombuffer(blob[32:48], np.int32)
-    o = 48
+def parse(head: bytes, aux: bytes):
+    hd = np.frombuffer(head[:32], np.float64)
+    nx, ny, words, flags, o_rl, o_ls, o_ll, o_eb = np.frombuffer(head[32:64], np.int32)
     ncell = nx * ny
-
-    def take(n, dt):
-        nonlocal o
-        a = np.frombuffer(blob[o:o + 4 * n], dt)
-        o += (4 * n + 15) // 16 * 16
-        return a
-
-    bits = take(ncell * words, np.uint32).reshape(ncell, words)
-    ebits = take(words, np.uint32)
-    starts = take(ncell + 1, np.int32)
-    lst = take(int(starts[-1]), np.int32)
+    rs = np.frombuffer(aux[:4 * (ncell + 1)], np.int32)
+    rl = np.frombuffer(aux[o_rl:o_rl + 2 * int(rs[-1])], np.uint16)
+    ls = np.frombuffer(aux[o_ls:o_ls + 4 * (ncell + 1)], np.int32)
+    ll = np.frombuffer(aux[o_ll:o_ll + 2 * int(ls[-1])], np.uint16)
     return dict(x0=hd[0], y0=hd[1], cell=hd[2], half=hd[3], nx=nx, ny=ny, words=words, flags=flags,
-                bits=bits, ebits=ebits, starts=starts, lst=lst)
+                road_start=rs, road_list=rl, lane_start=ls, lane_list=ll)
+
+
+def cell_of(ix, px, py):
+    inv = 1.0 / ix["cell"]
+    fx = np.floor((px - ix["x0"]) * inv)
+    fy = np.floor((py - ix["y0"]) * inv)
+    if 0 <= fx < ix["nx"] and 0 <= fy < ix["ny"]:
+        return int(fy) * ix["nx"] + int(fx)
+    return -1
 
 
 def superset(ix, px, py):
-    inv = 1.0 / ix["cell"]
-    cx0 = max(int(np.floor((px - ix["half"] - ix["x0"]) * inv)), 0)
-    cx1 = min(int(np.floor((px + ix["half"] - ix["x0"]) * inv)), ix["nx"] - 1)
-    cy0 = max(int(np.floor((py - ix["half"] - ix["y0"]) * inv)), 0)
-    cy1 = min(int(np.floor((py + ix["half"] - ix["y0"]) * inv)), ix["ny"] - 1)
-    out = set()
-    if cx0 > cx1 or cy0 > cy1:
-        return out
-    for cy in range(cy0, cy1 + 1):
-        for cx in range(cx0, cx1 + 1):
-            for wd, word in enumerate(ix["bits"][cy * ix["nx"] + cx]):
-                for b in range(32):
-                    if int(word) >> b & 1:
-                        out.add(wd * 32 + b)
-    return out
+    c = cell_of(ix, px, py)
+    if c < 0:
+        return set()
+    return set(ix["road_list"][ix["road_start"][c]:ix["road_start"][c + 1]].tolist())
 
 
 def nearest(t: SceneTable, px, py, kks):
@@ -76,9 +66,8 @@ SCENES = [prepare_scene(straight_scene(agent_count=16, agent_gap=8.0, lane_offse
 @pytest.mark.parametrize("scene", SCENES, ids=["straight", "crossroads"])
 def test_index_candidates_are_supersets(scene):
     t = _scene_table(scene_segments(scene))
-    blob = build_scene_index(t.midpoints, t.directions, t.half_lengths, t.half_widths,
-                             t.lane_index, t.edge_index, 10.0, 4.0)
-    ix = parse(blob, t.num_segments)
+    ix = parse(*build_scene_index(t.midpoints, t.directions, t.half_lengths, t.half_widths,
+                                  t.lane_index, t.edge_index, 10.0, 4.0))
     assert ix["flags"] & FLAG_GRID and ix["flags"] & FLAG_LANES
     g = np.random.Generator(np.random.Philox(7))
     pts = np.concatenate([g.uniform(-100, 100, (1500, 2)), g.uniform(-130, 130, (300, 2)),
@@ -93,11 +82,11 @@ def test_index_candidates_are_supersets(scene):
         # edge boxes reachable by a hull (r + d + half_len + half_wid <= 4 m)
         reach = set(q for q in edge if np.hypot(dx[q], dy[q]) <= 4.0)
         assert reach <= sup
-        fx = np.floor((px - ix["x0"]) / ix["cell"])
-        fy = np.floor((py - ix["y0"]) / ix["cell"])
-        if 0 <= fx < ix["nx"] and 0 <= fy < ix["ny"]:
-            c = int(fy) * ix["nx"] + int(fx)
-            cand = ix["lst"][ix["starts"][c]:ix["starts"][c + 1]]
+        c = cell_of(ix, px, py)
+        if c >= 0:
+            rl = ix["road_list"][ix["road_start"][c]:ix["road_start"][c + 1]]
+            assert list(rl) == sorted(rl)
+            cand = ix["lane_list"][ix["lane_start"][c]:ix["lane_start"][c + 1]]
             assert list(cand) == sorted(cand)
             assert nearest(t, px, py, cand) == nearest(t, px, py, range(len(t.lane_index)))
 
@@ -105,9 +94,9 @@ def test_index_candidates_are_supersets(scene):
 def test_index_disabled_when_boxes_outreach_the_grid():
     scene = SCENES[0]
     t = _scene_table(scene_segments(scene))
-    blob = build_scene_index(t.midpoints, t.directions, t.half_lengths, t.half_widths,
-                             t.lane_index, t.edge_index, 10.0, 10.5)
-    assert not parse(blob, t.num_segments)["flags"] & FLAG_GRID
+    head, aux = build_scene_index(t.midpoints, t.directions, t.half_lengths, t.half_widths,
+                                  t.lane_index, t.edge_index, 10.0, 10.5)
+    assert not parse(head, aux)["flags"] & FLAG_GRID
 
 
 def test_default_pool_indexes_build():

@@ -47,4 +47,8 @@ ph = out[:, [1, 17, 18, 19, 2]]
 print("  warp0: loads", np.median(ph[:, 1] - ph[:, 0]), " substeps", np.median(ph[:, 2] - ph[:, 1]),
       " derived+tables", np.median(ph[:, 3] - ph[:, 2]), " zero-fill", np.median(ph[:, 4] - ph[:, 3]))
 print("  substep ends (cycles after state loads):", np.median(out[:, 20:24] - out[:, 17:18], axis=0).astype(int))
+w1 = out[:, [4, 10, 11, 12, 13, 14]]
+print("  warp1 agent1: pairs(2a)", np.median(w1[:, 1] - w1[:, 0]), " road scan", np.median(w1[:, 2] - w1[:, 1]),
+      " road feats", np.median(w1[:, 3] - w1[:, 2]), " edge gap", np.median(w1[:, 4] - w1[:, 3]),
+      " lane", np.median(w1[:, 5] - w1[:, 4]))
 print("  phase2 per-warp end (cycles after phase2 start), median over CTAs:", np.median(wend, axis=0).astype(int))
