@@ -38,6 +38,7 @@
 namespace {
 
 constexpr int kMaxAgents = 16;
+constexpr int kZeroChunk = 4096;   // bytes of zeros in shared memory, source of the TMA row clears
 constexpr unsigned kFull = 0xffffffffu;
 
 enum StateField {
@@ -190,6 +191,16 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
         ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
 }
+// TMA bulk store shared -> global (bulk async-group completion)
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(gdst), "r"(smem_addr(ssrc)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit_and_wait() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -305,6 +316,21 @@ __device__ __forceinline__ double swept_ttc(double dx, double dy, double ux, dou
     if (ce * dx + se * dy < 0.0) return tmax;
     const double a = ux * ux + uy * uy;
     const bool moving = a >= 1e-12;
+    // Far-pair filter: every circle pair's centre offset is p + o with
+    // |o| <= de + dn, so if the closest approach of the hull centres over
+    // t >= 0 stays beyond rsum + de + dn (+1e-4 m of slack over the float64
+    // rounding of the exact test) no pair can hit: the result is tmax.
+    {
+        const double reach = rsum + de + dn + 1e-4;
+        const double R2 = reach * reach;
+        const double pp = dx * dx + dy * dy;
+        if (moving) {
+            const double pu = dx * ux + dy * uy;
+            if (pu >= 0.0 ? pp > R2 : pp * a - pu * pu > R2 * a) return tmax;
+        } else if (pp > R2) {
+            return tmax;
+        }
+    }
     const double a4 = 4.0 * a;
     const double rr = rsum * rsum;
     const double offs[3] = {-1.0, 0.0, 1.0};
@@ -336,24 +362,10 @@ __device__ __forceinline__ double swept_ttc(double dx, double dy, double ux, dou
     return any_overlap ? 0.0 : tmax;
 }
 
-// ----------------------------------------------------------------- observation row
-// The row is mostly zeros (~190 of 1929 values are non-zero): the owning warp
-// streams zeros with 16-byte st.global.cs, then -- ordered by a barrier --
-// the non-zero features are scattered by the lanes that computed them.
-__device__ __forceinline__ void zero_row(float* row, int D, int lane) {
-    const int mis = int((reinterpret_cast<uintptr_t>(row) >> 2) & 3);
-    int head = (4 - mis) & 3;
-    if (head > D) head = D;
-    if (lane < head) row[lane] = 0.0f;
-    const int nvec = (D - head) >> 2;
-    float4* body = reinterpret_cast<float4*>(row + head);
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-    for (int q = lane; q < nvec; q += 32) __stcs(body + q, z);
-    const int tail0 = head + 4 * nvec;
-    if (tail0 + lane < D) row[tail0 + lane] = 0.0f;
-}
-
+// ----------------------------------------------------------------- observation rows
+// A row is mostly zeros (~190 of 1929 values are non-zero): the world's block
+// is cleared by TMA bulk stores, then -- ordered by a barrier -- the non-zero
+// features are scattered by the lanes that computed them.
 // Per-agent results of the warp scans, consumed by the finalize warp.
 struct ScanSm {
     double ttc_min;
@@ -402,6 +414,11 @@ world_step_kernel(const KArgs A) {
     ScanSm* sc = reinterpret_cast<ScanSm*>(ag + kMaxAgents);
     uint64_t* bar = reinterpret_cast<uint64_t*>(sc + kMaxAgents);
     uint16_t* cand_sm = reinterpret_cast<uint16_t*>(bar + 2);   // [M][take_road]
+    float4* zero_sm = reinterpret_cast<float4*>(
+        smem + align16(reinterpret_cast<uint8_t*>(cand_sm + kMaxAgents * A.take_road) - smem));  // [kZeroChunk/16]
+    for (int i = tid; i < kZeroChunk / 16; i += blockDim.x) zero_sm[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
     __shared__ int s_bad;
 
     // ---- phase 0: action scan (the reference rejects before mutating)
@@ -508,7 +525,27 @@ world_step_kernel(const KArgs A) {
         S.spawn = A.spawn_step[am];
         LANE0_MARK(19);
     }
-    for (int m = warp; m < M; m += nwarps) zero_row(obs_w + int64_t(m) * D, D, lane);
+    // the zero background of the world's obs block: TMA bulk stores from a
+    // zeroed shared buffer, issued by one thread of a warp that is idle
+    // during the physics; unaligned head/tail floats by plain stores
+    if (warp == (nwarps > 1 ? 1 : 0)) {
+        const uintptr_t b0 = reinterpret_cast<uintptr_t>(obs_w);
+        const uintptr_t b1 = b0 + uintptr_t(M) * D * 4;
+        const uintptr_t a0 = (b0 + 15) & ~uintptr_t(15), a1 = b1 & ~uintptr_t(15);
+        if (a0 < a1) {
+            for (uintptr_t p = b0 + 4 * lane; p < a0; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
+            for (uintptr_t p = a1 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
+            if (lane == 0) {
+                for (uintptr_t p = a0; p < a1; p += kZeroChunk) {
+                    const uintptr_t n = a1 - p < uintptr_t(kZeroChunk) ? a1 - p : uintptr_t(kZeroChunk);
+                    bulk_store(reinterpret_cast<void*>(p), zero_sm, uint32_t(n));
+                }
+                bulk_commit_and_wait();
+            }
+        } else {
+            for (uintptr_t p = b0 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
+        }
+    }
 
     if (warp == 0) PHASE_MARK(2);
     __syncthreads();  // agent table + zero rows done, mbarrier init visible
@@ -585,7 +622,10 @@ world_step_kernel(const KArgs A) {
             }
             ttc = warp_min(ttc, 16);
             bool touch = false;
-            if (kStep && ego_ok && j < M && j != ii && S.alive && ag[j].alive) {
+            // hull contact; centres sit within d of the position, so a pair
+            // farther apart than r_a + r_b + d_a + d_b (+1e-4 m) cannot touch
+            if (kStep && ego_ok && j < M && j != ii && S.alive && ag[j].alive &&
+                key <= S.r + ag[j].r + S.d + ag[j].d + 1e-4) {
                 const AgentSm& N = ag[j];
                 const double rs = S.r + N.r;
                 const double rs2 = rs * rs;
@@ -1043,6 +1083,7 @@ static size_t step_smem_bytes(const DgDims& d, int take_road) {
     b += sizeof(AgentSm) * kMaxAgents + sizeof(ScanSm) * kMaxAgents;
     b += 16;  // mbarrier
     b += sizeof(uint16_t) * kMaxAgents * size_t(take_road > 0 ? take_road : 1);
+    b = size_t(align16(int64_t(b))) + kZeroChunk;
     return b;
 }
 
