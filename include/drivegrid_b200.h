@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 1
+#define DG_ABI_VERSION 2
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -111,6 +111,7 @@ typedef struct DgEngineDesc {
     double* goal_xy;                /* [W][M][2]  */
     double* start_yaw;              /* [W][M]     */
     int32_t* error_word;            /* [1] DG_NO_ERROR or first bad flat action index */
+    uint8_t* scratch;               /* dg_scratch_bytes(W, M) bytes, or NULL (fused mode only) */
 } DgEngineDesc;
 
 /* Outputs of one control tick (StepOutput, engine.py:70-76, 397-406).
@@ -171,11 +172,17 @@ int dg_lane_follower(dg_engine* eng, const float* obs, double* actions, double s
 /* Kernel launches issued by the last dg_step/dg_observe/dg_reset call. */
 int dg_launch_count(dg_engine* eng);
 
-/* Launch shape: warps per world CTA (1..16, default M; agents are strided
- * over the warps) and the kernel variant's register budget, expressed as
- * resident CTAs per SM (0 = default).  A performance knob only -- results
- * do not depend on it. */
-int dg_tune(dg_engine* eng, int32_t warps_per_world, int32_t ctas_per_sm);
+/* Launch shape -- a performance knob only, results do not depend on it.
+ *   mode 0 (fused): one CTA per world, warps_per_world warps (1..16; agents
+ *                   strided over the warps)
+ *   mode 1 (split): a physics kernel (one warp per world) chained by
+ *                   programmatic dependent launch to a per-agent kernel with
+ *                   warps_per_world (2, 4 or 8) agents per CTA; needs scratch
+ * ctas_per_sm selects the register budget of the kernel variant (0 = default). */
+int dg_tune(dg_engine* eng, int32_t mode, int32_t warps_per_world, int32_t ctas_per_sm);
+
+/* Device scratch the split mode needs (per-agent records between its kernels). */
+size_t dg_scratch_bytes(int32_t W, int32_t M);
 
 const char* dg_last_error(void);
 int dg_abi_version(void);

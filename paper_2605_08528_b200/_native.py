@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class DgDims(ct.Structure):
@@ -61,7 +61,7 @@ class DgEngineDesc(ct.Structure):
     _fields_ = [("dims", DgDims), ("k", DgConsts)] + [(n, _P) for n in (
         "scene_blob", "scene_meta", "scene_of_world", "grid_offset", "mu_eff", "weather", "valid",
         "length", "width", "r_hull", "d_hull", "state", "alive", "reason", "event_seen",
-        "spawn_step", "step_count", "start_xy", "goal_xy", "start_yaw", "error_word")]
+        "spawn_step", "step_count", "start_xy", "goal_xy", "start_yaw", "error_word", "scratch")]
 
 
 class DgStepIO(ct.Structure):
@@ -84,7 +84,8 @@ SIGNATURES = {
     "dg_read_error": (ct.c_int, [_P, ct.POINTER(ct.c_int32), _P]),
     "dg_lane_follower": (ct.c_int, [_P, _P, _P, ct.c_double, ct.c_double, _P]),
     "dg_launch_count": (ct.c_int, [_P]),
-    "dg_tune": (ct.c_int, [_P, ct.c_int32, ct.c_int32]),
+    "dg_tune": (ct.c_int, [_P, ct.c_int32, ct.c_int32, ct.c_int32]),
+    "dg_scratch_bytes": (ct.c_size_t, [ct.c_int32, ct.c_int32]),
 }
 
 

@@ -86,6 +86,7 @@ struct KArgs {
     double* snapshot_out;
     int32_t take_road;   // min(k_road, max_segments) = candidate-list capacity
     int32_t take_veh;    // min(k_vehicles, M)
+    uint8_t* scratch;    // split mode: AgentRec[W*M], int32 world_ok[W], int32 world_step[W]
 };
 
 // ----------------------------------------------------------------- numpy-semantics helpers
@@ -106,6 +107,11 @@ __device__ __forceinline__ double np_sign(double x) {
 }
 __device__ __forceinline__ bool finite(double x) { return isfinite(x); }
 
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
 __device__ __forceinline__ double warp_min(double v, int width = 32) {
     for (int o = width >> 1; o > 0; o >>= 1) v = sel_min(v, __shfl_xor_sync(kFull, v, o, width));
     return v;
@@ -377,16 +383,164 @@ struct ScanSm {
     int pad_;
 };
 
+// ----------------------------------------------------------------- ego block / finalize
+// Both launch modes share these: the ego features of one agent's row
+// (observation.py:51-75) and the reward / event / termination tail of one
+// agent (rewards.py:106-268, engine.py:370-406, 472-509).
+__device__ __forceinline__ void write_ego(float* row, const DgConsts& k, const KArgs& A, int w, double px, double py,
+                                          double c, double s, double vx, double vy, double gx, double gy) {
+    const double gdx = gx - px, gdy = gy - py;
+    const double xb = c * gdx + s * gdy;
+    const double yb = -s * gdx + c * gdy;
+    double sh, ch;
+    sincos(atan2(yb, xb), &sh, &ch);
+    row[0] = __double2float_rn(dg::ddiv(xb, k.bbox_half));
+    row[1] = __double2float_rn(dg::ddiv(yb, k.bbox_half));
+    row[2] = __double2float_rn(sh);
+    row[3] = __double2float_rn(ch);
+    row[4] = __double2float_rn(dg::ddiv(dg::dsqrt(xb * xb + yb * yb), k.bbox_half));
+    row[5] = __double2float_rn(dg::ddiv(vx, k.speed_norm));
+    row[6] = __double2float_rn(dg::ddiv(vy, k.speed_norm));
+    if (A.d.include_weather) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) row[7 + i] = __double2float_rn(A.weather[4 * w + i]);
+    }
+}
+
+struct FinIn {
+    const double* st;                  // post-physics state, 12 fields
+    double px0, py0, gx, gy, sx, sy;   // pre-physics position, goal, start
+    double lane_d2, lane_lat, lane_tx, lane_ty;  // nearest lane (d2 = inf: none)
+    double ttc_min, gap;
+    int edge_hit, touch, alive, valid, reason, seen, spawn;
+};
+
+__device__ __forceinline__ void finalize_agent(const KArgs& A, int w, int m, const FinIn& F, int step_now,
+                                            double ox, double oy) {
+            const DgConsts& k = A.k;
+            const int WM = A.d.W * A.d.M;
+            const int64_t am = int64_t(w) * A.d.M + m;
+            const double px = F.st[SX], py = F.st[SY];
+            const double vx = F.st[SVX], vy = F.st[SVY], yaw = F.st[SYAW];
+            const double dist = dg::dsqrt(F.lane_d2);
+            const bool has_lane = finite(dist);
+            const double lat = has_lane ? F.lane_lat : 0.0;
+            double tx = has_lane ? F.lane_tx : 0.0, ty = has_lane ? F.lane_ty : 0.0;
+            const double tgx = F.gx - px, tgy = F.gy - py;
+            const double flip = (tx * tgx + ty * tgy >= 0.0) ? 1.0 : -1.0;
+            tx = tx * flip;
+            ty = ty * flip;
+            double progress = np_clip((px - F.px0) * tx + (py - F.py0) * ty,
+                                      -k.progress_clamp, k.progress_clamp) * k.progress_weight;
+            const double align = np_max(0.0, cos(yaw - atan2(ty, tx)));
+            const double ls = dg::ddiv(lat, k.lane_sigma);
+            const double quality = exp(-(ls * ls)) * (k.lane_heading_base + k.lane_heading_weight * align);
+            const double lane_t = has_lane ? k.lane_weight * quality : 0.0;
+            progress = has_lane ? progress : 0.0;
+            const double offroad = (has_lane && (fabs(lat) > k.offroad_lat_limit || dist > k.offroad_dist_limit))
+                                       ? -k.offroad_weight : 0.0;
+            const double speed = dg::dsqrt(vx * vx + vy * vy);
+            const double idle = speed < k.idle_speed ? -k.idle_weight : 0.0;
+            const double ttc_v = -np_min(dg::ddiv(k.ttc_vehicle_alpha, np_max(F.ttc_min, k.ttc_floor)), k.ttc_vehicle_pmax);
+            const double tau = F.gap < INFINITY ? dg::ddiv(F.gap, np_max(vx, 0.1)) : F.gap / np_max(vx, 0.1);
+            const double ttc_e = finite(tau) ? -np_min(dg::ddiv(k.ttc_edge_alpha, np_max(tau, k.ttc_floor)), k.ttc_edge_pmax)
+                                             : 0.0;
+            const double total = progress + lane_t + offroad + idle + ttc_v + ttc_e;
+
+            // sparse events, masked by alive and the per-type latch
+            const bool alive = F.alive;
+            const bool goal = dg::dsqrt(tgx * tgx + tgy * tgy) <= k.goal_radius;
+            const double sxd = px - F.sx, syd = py - F.sy;
+            const bool bad = !(finite(px) && finite(py) && finite(vx) && finite(vy));
+            const bool crash = dg::dsqrt(sxd * sxd + syd * syd) > k.crash_drift_limit || bad ||
+                               speed > k.crash_speed_limit;
+            const bool coll = F.touch && step_now - F.spawn >= A.d.collision_warmup;
+            const int seen = F.seen;
+            const bool e_goal = goal && alive && !(seen & 1);
+            const bool e_coll = coll && alive && !(seen & 2);
+            const bool e_crash = crash && alive && !(seen & 4);
+            const bool e_lf = F.edge_hit && alive && !(seen & 8);
+            const int rnow = e_goal ? 1 : (e_crash ? 3 : (e_lf ? 4 : (e_coll ? 2 : 0)));
+            int seen_new = seen | (rnow == 0 ? 0 : 1 << (rnow == 1 ? 0 : rnow == 2 ? 1 : rnow == 3 ? 2 : 3));
+            const double sparse = rnow == 1 ? k.goal_weight
+                                : rnow == 2 ? -k.collision_weight
+                                : rnow == 3 ? -k.crash_weight
+                                : rnow == 4 ? -k.lane_forbidden_weight : 0.0;
+            const double reward = alive ? total + sparse : 0.0;
+            int reason = F.reason;
+            bool done = false;
+            if (!A.d.invincible) {
+                done = rnow != 0;
+                if (done && reason == 0) reason = rnow;
+            }
+            // tail: timeout, park, alive (engine.py:370-393)
+            const int step_new = step_now + 1;
+            const bool timeout = step_new >= A.d.episode_len && alive;
+            const bool finished = done || timeout;
+            if (timeout && reason == 0) reason = 5;
+            const bool park = done && !timeout;
+            int alive_new = alive && !finished;
+
+            A.rewards[am] = reward;
+            A.dones[am] = finished;
+            reinterpret_cast<uint32_t*>(A.events)[am] =
+                uint32_t(rnow == 1) | (uint32_t(rnow == 2) << 8) | (uint32_t(rnow == 3) << 16) |
+                (uint32_t(rnow == 4) << 24);
+            if (A.reason_out) A.reason_out[am] = int8_t(reason);
+            if (A.alive_out) A.alive_out[am] = uint8_t(alive_new);
+            if (A.alive_pre_out) A.alive_pre_out[am] = uint8_t(alive);
+            if (A.ttc_min_out) A.ttc_min_out[am] = F.ttc_min;
+            if (A.terms_out) {
+                const double t7[7] = {progress, lane_t, offroad, idle, ttc_v, ttc_e, total};
+#pragma unroll
+                for (int i = 0; i < 7; ++i) A.terms_out[int64_t(i) * WM + am] = alive ? t7[i] : 0.0;
+            }
+            if (A.snapshot_out) {
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) A.snapshot_out[int64_t(f) * WM + am] = F.st[f];
+            }
+            double x[DG_NUM_STATE];
+#pragma unroll
+            for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = F.st[f];
+            if (park) {
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
+                x[SX] = ox + k.offstage_x;
+                x[SY] = oy;
+            }
+            int spawn = F.spawn;
+            if (A.autoreset && finished && F.valid) {
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
+                x[SX] = F.sx;
+                x[SY] = F.sy;
+                x[SYAW] = A.start_yaw[am];
+                alive_new = 1;
+                reason = 0;
+                spawn = step_new;
+                seen_new = 0;
+            }
+#pragma unroll
+            for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = x[f];
+            A.alive[am] = uint8_t(alive_new);
+            A.reason[am] = int8_t(reason);
+            A.event_seen[am] = uint8_t(seen_new);
+            A.spawn_step[am] = spawn;
+        }
+
 // ----------------------------------------------------------------- optional phase timers
 // Built with -DDG_PHASE_TIMERS: every CTA records clock64() at its phase
 // boundaries (slot 0 start .. 7 end) plus the per-warp end of phase 2.
 #ifdef DG_PHASE_TIMERS
-__device__ long long g_phase_clock[65536][24];
+__device__ long long g_phase_clock[65536][40];
 #define PHASE_MARK(i) do { if (threadIdx.x == 0 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][i] = clock64(); } while (0)
 #define WARP_MARK(i) do { if ((threadIdx.x & 31) == 0 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][8 + (threadIdx.x >> 5)] = clock64(); } while (0)
 #define LANE0_MARK(i) do { if (threadIdx.x == 0 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][i] = clock64(); } while (0)
+__device__ __forceinline__ long long gtimer() { long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
+#define GT_MARK(i) do { if (threadIdx.x == 0 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][i] = gtimer(); } while (0)
 #define W1_MARK(i) do { if (threadIdx.x == 32 && blockIdx.x < 65536) g_phase_clock[blockIdx.x][i] = clock64(); } while (0)
 #else
+#define GT_MARK(i) do { } while (0)
 #define W1_MARK(i) do { } while (0)
 #define LANE0_MARK(i) do { } while (0)
 #define PHASE_MARK(i) do { } while (0)
@@ -422,6 +576,7 @@ world_step_kernel(const KArgs A) {
     __shared__ int s_bad;
 
     // ---- phase 0: action scan (the reference rejects before mutating)
+    GT_MARK(32);
     PHASE_MARK(0);
     int step_now = 0;
     if constexpr (kStep) {
@@ -464,7 +619,7 @@ world_step_kernel(const KArgs A) {
         const int alive = A.alive[am];
         S.px0 = x[SX];
         S.py0 = x[SY];
-        if (alive && x[SX] != -12345.678) LANE0_MARK(17);  // after the state loads landed
+        if (alive && x[SX] != -12345.678) LANE0_MARK(25);  // after the state loads landed
         if (kStep && alive) {
             const int64_t ab = am * 3;
             double raw0, raw1, raw2;
@@ -484,14 +639,14 @@ world_step_kernel(const KArgs A) {
                 for (int i = 0; i < A.d.decimation; ++i) {
                     substep_dynamic(x, act, cap, k);
 #ifdef DG_PHASE_TIMERS
-                    if (i < 4 && x[SX] != -12345.678) LANE0_MARK(20 + i);
+                    if (i < 4 && x[SX] != -12345.678) LANE0_MARK(28 + i);
 #endif
                 }
             } else {
                 step_bicycle(x, act, k);
             }
         }
-        if (x[SX] != -12345.678) LANE0_MARK(18);          // after the substeps
+        if (x[SX] != -12345.678) LANE0_MARK(26);          // after the substeps
 #pragma unroll
         for (int f = 0; f < DG_NUM_STATE; ++f) S.st[f] = x[f];
         double s_, c_;
@@ -523,7 +678,7 @@ world_step_kernel(const KArgs A) {
         S.reason = A.reason[am];
         S.seen = A.event_seen[am];
         S.spawn = A.spawn_step[am];
-        LANE0_MARK(19);
+        LANE0_MARK(27);
     }
     // the zero background of the world's obs block: TMA bulk stores from a
     // zeroed shared buffer, issued by one thread of a warp that is idle
@@ -646,7 +801,7 @@ world_step_kernel(const KArgs A) {
         }
     }
 
-    W1_MARK(10);
+    W1_MARK(34);
     // ---- phase 2b: warp m scans the scene for agent m
     for (int m = warp; m < M; m += nwarps) {
         const AgentSm& S = ag[m];
@@ -716,7 +871,7 @@ world_step_kernel(const KArgs A) {
             for (int p0 = 0; p0 < G.P; p0 += 32) visit(p0 + lane, p0 + lane < G.P, false);
         }
         const int ncand = count < A.take_road ? count : A.take_road;
-        if (m == 1) W1_MARK(11);
+        if (m == 1) W1_MARK(35);
         __syncwarp();
         for (int slot = lane; slot < ncand; slot += 32) {
             const int q = cand[slot];
@@ -731,7 +886,7 @@ world_step_kernel(const KArgs A) {
             o[4] = __double2float_rn(-s * ux + c * uy);
         }
 
-        if (m == 1) W1_MARK(12);
+        if (m == 1) W1_MARK(36);
         if (!rewards_needed) {
             if (kStep && lane == 0) {
                 ScanSm& R = sc[m];
@@ -771,7 +926,7 @@ world_step_kernel(const KArgs A) {
         }
         gap = warp_min(gap);
         edge_hit = __any_sync(kFull, edge_hit);
-        if (m == 1) W1_MARK(13);
+        if (m == 1) W1_MARK(37);
 
         // (c) nearest lane: argmin of point-to-segment d2, lowest index on ties,
         //     over the cell's candidate list when the agent is inside the grid
@@ -799,7 +954,7 @@ world_step_kernel(const KArgs A) {
             const int ok = __shfl_xor_sync(kFull, best_k, o);
             if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
         }
-        if (m == 1) W1_MARK(14);
+        if (m == 1) W1_MARK(38);
         if (lane == 0) {
             ScanSm& R = sc[m];
             R.lane_d2 = best;
@@ -817,148 +972,451 @@ world_step_kernel(const KArgs A) {
     //      warp 1 (or warp 0 afterwards) -> the ego block
     const int ego_warp = nwarps > 1 ? 1 : 0;
     if (warp == ego_warp && lane < M) {
-        const int m = lane;
-        const AgentSm& S = ag[m];
-        float* row = obs_w + int64_t(m) * D;
-        const double px = S.st[SX], py = S.st[SY], c = S.c, s = S.s;
-        const double gdx = S.gx - px, gdy = S.gy - py;
-        const double xb = c * gdx + s * gdy;
-        const double yb = -s * gdx + c * gdy;
-        double sh, ch;
-        sincos(atan2(yb, xb), &sh, &ch);
-        row[0] = __double2float_rn(dg::ddiv(xb, k.bbox_half));
-        row[1] = __double2float_rn(dg::ddiv(yb, k.bbox_half));
-        row[2] = __double2float_rn(sh);
-        row[3] = __double2float_rn(ch);
-        row[4] = __double2float_rn(dg::ddiv(dg::dsqrt(xb * xb + yb * yb), k.bbox_half));
-        row[5] = __double2float_rn(dg::ddiv(S.st[SVX], k.speed_norm));
-        row[6] = __double2float_rn(dg::ddiv(S.st[SVY], k.speed_norm));
-        if (A.d.include_weather) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) row[7 + i] = __double2float_rn(A.weather[4 * w + i]);
-        }
+        const AgentSm& S = ag[lane];
+        write_ego(obs_w + int64_t(lane) * D, k, A, w, S.st[SX], S.st[SY], S.c, S.s, S.st[SVX], S.st[SVY],
+                  S.gx, S.gy);
     }
     if constexpr (kStep) {
         if (warp == 0 && lane < M) {
             const int m = lane;
-            const int64_t am = int64_t(w) * M + m;
             const AgentSm& S = ag[m];
             const ScanSm& R = sc[m];
-            const double px = S.st[SX], py = S.st[SY];
-            const double vx = S.st[SVX], vy = S.st[SVY], yaw = S.st[SYAW];
-            const double dist = dg::dsqrt(R.lane_d2);
-            const bool has_lane = finite(dist);
-            double lat = 0.0, tx = 0.0, ty = 0.0;
-            if (has_lane) {
+            FinIn F;
+            F.st = S.st;
+            F.px0 = S.px0; F.py0 = S.py0; F.gx = S.gx; F.gy = S.gy; F.sx = S.sx; F.sy = S.sy;
+            F.lane_d2 = R.lane_d2;
+            F.lane_lat = 0.0; F.lane_tx = 0.0; F.lane_ty = 0.0;
+            if (R.lane_d2 < INFINITY) {
                 const double4 l4 = G.lane_seg[R.lane_k];
-                const double ex = px - l4.x, ey = py - l4.y;
-                tx = l4.z;
-                ty = l4.w;
-                lat = tx * ey - ty * ex;
+                const double ex = S.st[SX] - l4.x, ey = S.st[SY] - l4.y;
+                F.lane_tx = l4.z;
+                F.lane_ty = l4.w;
+                F.lane_lat = l4.z * ey - l4.w * ex;
             }
-            const double tgx = S.gx - px, tgy = S.gy - py;
-            const double flip = (tx * tgx + ty * tgy >= 0.0) ? 1.0 : -1.0;
-            tx = tx * flip;
-            ty = ty * flip;
-            double progress = np_clip((px - S.px0) * tx + (py - S.py0) * ty,
-                                      -k.progress_clamp, k.progress_clamp) * k.progress_weight;
-            const double align = np_max(0.0, cos(yaw - atan2(ty, tx)));
-            const double ls = dg::ddiv(lat, k.lane_sigma);
-            const double quality = exp(-(ls * ls)) * (k.lane_heading_base + k.lane_heading_weight * align);
-            const double lane_t = has_lane ? k.lane_weight * quality : 0.0;
-            progress = has_lane ? progress : 0.0;
-            const double offroad = (has_lane && (fabs(lat) > k.offroad_lat_limit || dist > k.offroad_dist_limit))
-                                       ? -k.offroad_weight : 0.0;
-            const double speed = dg::dsqrt(vx * vx + vy * vy);
-            const double idle = speed < k.idle_speed ? -k.idle_weight : 0.0;
-            const double ttc_v = -np_min(dg::ddiv(k.ttc_vehicle_alpha, np_max(R.ttc_min, k.ttc_floor)), k.ttc_vehicle_pmax);
-            const double tau = R.gap < INFINITY ? dg::ddiv(R.gap, np_max(vx, 0.1)) : R.gap / np_max(vx, 0.1);
-            const double ttc_e = finite(tau) ? -np_min(dg::ddiv(k.ttc_edge_alpha, np_max(tau, k.ttc_floor)), k.ttc_edge_pmax)
-                                             : 0.0;
-            const double total = progress + lane_t + offroad + idle + ttc_v + ttc_e;
-
-            // sparse events, masked by alive and the per-type latch
-            const bool alive = S.alive;
-            const bool goal = dg::dsqrt(tgx * tgx + tgy * tgy) <= k.goal_radius;
-            const double sxd = px - S.sx, syd = py - S.sy;
-            const bool bad = !(finite(px) && finite(py) && finite(vx) && finite(vy));
-            const bool crash = dg::dsqrt(sxd * sxd + syd * syd) > k.crash_drift_limit || bad ||
-                               speed > k.crash_speed_limit;
-            const bool coll = R.touch && step_now - S.spawn >= A.d.collision_warmup;
-            const int seen = S.seen;
-            const bool e_goal = goal && alive && !(seen & 1);
-            const bool e_coll = coll && alive && !(seen & 2);
-            const bool e_crash = crash && alive && !(seen & 4);
-            const bool e_lf = R.edge_hit && alive && !(seen & 8);
-            const int rnow = e_goal ? 1 : (e_crash ? 3 : (e_lf ? 4 : (e_coll ? 2 : 0)));
-            int seen_new = seen | (rnow == 0 ? 0 : 1 << (rnow == 1 ? 0 : rnow == 2 ? 1 : rnow == 3 ? 2 : 3));
-            const double sparse = rnow == 1 ? k.goal_weight
-                                : rnow == 2 ? -k.collision_weight
-                                : rnow == 3 ? -k.crash_weight
-                                : rnow == 4 ? -k.lane_forbidden_weight : 0.0;
-            const double reward = alive ? total + sparse : 0.0;
-            int reason = S.reason;
-            bool done = false;
-            if (!A.d.invincible) {
-                done = rnow != 0;
-                if (done && reason == 0) reason = rnow;
-            }
-            // tail: timeout, park, alive (engine.py:370-393)
-            const int step_new = step_now + 1;
-            const bool timeout = step_new >= A.d.episode_len && alive;
-            const bool finished = done || timeout;
-            if (timeout && reason == 0) reason = 5;
-            const bool park = done && !timeout;
-            int alive_new = alive && !finished;
-
-            A.rewards[am] = reward;
-            A.dones[am] = finished;
-            reinterpret_cast<uint32_t*>(A.events)[am] =
-                uint32_t(rnow == 1) | (uint32_t(rnow == 2) << 8) | (uint32_t(rnow == 3) << 16) |
-                (uint32_t(rnow == 4) << 24);
-            if (A.reason_out) A.reason_out[am] = int8_t(reason);
-            if (A.alive_out) A.alive_out[am] = uint8_t(alive_new);
-            if (A.alive_pre_out) A.alive_pre_out[am] = uint8_t(alive);
-            if (A.ttc_min_out) A.ttc_min_out[am] = R.ttc_min;
-            if (A.terms_out) {
-                const double t7[7] = {progress, lane_t, offroad, idle, ttc_v, ttc_e, total};
-#pragma unroll
-                for (int i = 0; i < 7; ++i) A.terms_out[int64_t(i) * WM + am] = alive ? t7[i] : 0.0;
-            }
-            if (A.snapshot_out) {
-#pragma unroll
-                for (int f = 0; f < DG_NUM_STATE; ++f) A.snapshot_out[int64_t(f) * WM + am] = S.st[f];
-            }
-            double x[DG_NUM_STATE];
-#pragma unroll
-            for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = S.st[f];
-            if (park) {
-#pragma unroll
-                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
-                x[SX] = ox + k.offstage_x;
-                x[SY] = oy;
-            }
-            int spawn = S.spawn;
-            if (A.autoreset && finished && S.valid) {
-#pragma unroll
-                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
-                x[SX] = S.sx;
-                x[SY] = S.sy;
-                x[SYAW] = A.start_yaw[am];
-                alive_new = 1;
-                reason = 0;
-                spawn = step_new;
-                seen_new = 0;
-            }
-#pragma unroll
-            for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = x[f];
-            A.alive[am] = uint8_t(alive_new);
-            A.reason[am] = int8_t(reason);
-            A.event_seen[am] = uint8_t(seen_new);
-            A.spawn_step[am] = spawn;
+            F.ttc_min = R.ttc_min; F.gap = R.gap;
+            F.edge_hit = R.edge_hit; F.touch = R.touch;
+            F.alive = S.alive; F.valid = S.valid; F.reason = S.reason; F.seen = S.seen; F.spawn = S.spawn;
+            finalize_agent(A, w, m, F, step_now, ox, oy);
         }
         if (tid == 0) A.step_count[w] = step_now + 1;
         PHASE_MARK(6);
+        GT_MARK(33);
+    }
+}
+
+// ----------------------------------------------------------------- split launch mode
+// Two kernels per tick, chained with programmatic dependent launch (PDL):
+//   K1 world_physics_kernel  one warp per world, lane m = agent m: action
+//      scan, decode, 4 substeps (SIMT across agents), derived per-agent
+//      record -> global scratch, post-physics state -> state[], step counter
+//   K2 agent_obs_kernel      one warp per agent, a few agents of one world
+//      per CTA: clears its obs rows with TMA bulk stores *before* waiting on
+//      K1 (griddepcontrol.wait), then pairs / road / edges / lane scans,
+//      the ego block and the agent's own reward / termination tail.
+// Every SM gets many independent agent warps, so the scans of one agent
+// hide the latency chains of another; the physics chain costs one short
+// kernel instead of a CTA-wide barrier stall.
+struct __align__(16) AgentRec {
+    double x, y, yaw, vx, vy, c, s, vwx, vwy, r, d;
+    double hx[3], hy[3];
+    float f_len, f_wid, f_spd;
+    int alive;
+};
+
+// scratch: AgentRec rec[W*M] | int32 world_ok[W], int32 world_step[W] | double2 prev_pos[W*M]
+__host__ __device__ __forceinline__ int64_t split_off_world(int W, int M) {
+    return align16(int64_t(sizeof(AgentRec)) * W * M);
+}
+__host__ __device__ __forceinline__ int64_t split_off_prev(int W, int M) {
+    return split_off_world(W, M) + align16(int64_t(8) * W);
+}
+__host__ __device__ __forceinline__ size_t split_scratch_bytes(int W, int M) {
+    return size_t(split_off_prev(W, M) + align16(int64_t(16) * W * M));
+}
+
+template <bool kStep>
+__global__ void __launch_bounds__(32) world_physics_kernel(const KArgs A) {
+    const int w = blockIdx.x;
+    const int lane = threadIdx.x;
+    const int M = A.d.M;
+    const int WM = A.d.W * M;
+    const DgConsts& k = A.k;
+    AgentRec* rec = reinterpret_cast<AgentRec*>(A.scratch);
+    int32_t* world_ok = reinterpret_cast<int32_t*>(A.scratch + split_off_world(A.d.W, M));
+    int32_t* world_step = world_ok + A.d.W;
+    double2* prev = reinterpret_cast<double2*>(A.scratch + split_off_prev(A.d.W, M));
+    // let the dependent agent kernel start its independent prologue now
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+    if constexpr (kStep) {
+        int bad = DG_NO_ERROR;
+        for (int i = lane; i < 3 * M; i += 32) {
+            const int64_t flat = int64_t(w) * M * 3 + i;
+            const double v = A.actions_f64 ? reinterpret_cast<const double*>(A.actions)[flat]
+                                           : double(reinterpret_cast<const float*>(A.actions)[flat]);
+            if (!finite(v) && int(flat) < bad) bad = int(flat);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const int ob = __shfl_xor_sync(kFull, bad, o);
+            bad = ob < bad ? ob : bad;
+        }
+        if (bad != DG_NO_ERROR) {   // the reference rejects before mutating anything
+            if (lane == 0) {
+                atomicMin(A.error_word, bad);
+                world_ok[w] = 0;
+            }
+            return;
+        }
+        if (lane == 0) {
+            const int step_now = A.step_count[w];
+            world_ok[w] = 1;
+            world_step[w] = step_now;
+            A.step_count[w] = step_now + 1;
+        }
+    }
+    if (lane >= M) return;
+    const int m = lane;
+    const int64_t am = int64_t(w) * M + m;
+    double x[DG_NUM_STATE];
+#pragma unroll
+    for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = A.state[int64_t(f) * WM + am];
+    const int alive = A.alive[am];
+    const double px0 = x[SX], py0 = x[SY];
+    if (kStep && alive) {
+        const int64_t ab = am * 3;
+        double raw0, raw1, raw2;
+        if (A.actions_f64) {
+            const double* a = reinterpret_cast<const double*>(A.actions);
+            raw0 = a[ab]; raw1 = a[ab + 1]; raw2 = a[ab + 2];
+        } else {
+            const float* a = reinterpret_cast<const float*>(A.actions);
+            raw0 = a[ab]; raw1 = a[ab + 1]; raw2 = a[ab + 2];
+        }
+        Act act;
+        act.thr = np_clip(raw0, 0.0, 1.0);
+        act.steer = np_clip(raw1, -1.0, 1.0);
+        act.brk = np_clip(raw2, 0.0, 1.0);
+        if (A.d.dynamic) {
+            const double cap = A.mu_eff[w] * k.f_z;
+            for (int i = 0; i < A.d.decimation; ++i) substep_dynamic(x, act, cap, k);
+        } else {
+            step_bicycle(x, act, k);
+        }
+        // the post-physics state (the info snapshot; the tail parks from here)
+#pragma unroll
+        for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = x[f];
+    }
+    AgentRec R;
+    double s_, c_;
+    sincos(x[SYAW], &s_, &c_);
+    R.x = x[SX]; R.y = x[SY]; R.yaw = x[SYAW]; R.vx = x[SVX]; R.vy = x[SVY];
+    R.c = c_; R.s = s_;
+    R.vwx = x[SVX] * c_ - x[SVY] * s_;
+    R.vwy = x[SVX] * s_ + x[SVY] * c_;
+    R.r = A.r_hull[am];
+    R.d = A.d_hull[am];
+    const double offs[3] = {-1.0, 0.0, 1.0};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double o = offs[i] * R.d;
+        R.hx[i] = x[SX] + o * c_;
+        R.hy[i] = x[SY] + o * s_;
+    }
+    R.f_len = __double2float_rn(dg::ddiv(A.length[am], k.bbox_half));
+    R.f_wid = __double2float_rn(dg::ddiv(A.width[am], k.bbox_half));
+    R.f_spd = __double2float_rn(dg::ddiv(dg::dsqrt(x[SVX] * x[SVX] + x[SVY] * x[SVY]), k.speed_norm));
+    R.alive = alive;
+    rec[am] = R;
+    prev[am] = make_double2(px0, py0);
+}
+
+template <bool kStep, int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const KArgs A) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int apc = blockDim.x >> 5;              // agents (warps) per CTA
+    const int M = A.d.M;
+    const int groups = (M + apc - 1) / apc;
+    const int w = blockIdx.x / groups;
+    const int m0 = (blockIdx.x % groups) * apc;
+    const int mc = M - m0 < apc ? M - m0 : apc;   // agents in this CTA
+    const int WM = A.d.W * M;
+    const int D = A.d.obs_dim;
+    const DgConsts& k = A.k;
+    const AgentRec* rec = reinterpret_cast<const AgentRec*>(A.scratch);
+    const int32_t* world_ok = reinterpret_cast<const int32_t*>(A.scratch + split_off_world(A.d.W, M));
+    const int32_t* world_step = world_ok + A.d.W;
+    const double2* prev = reinterpret_cast<const double2*>(A.scratch + split_off_prev(A.d.W, M));
+
+    AgentRec* ag = reinterpret_cast<AgentRec*>(smem);                          // [M]
+    uint16_t* cand_sm = reinterpret_cast<uint16_t*>(ag + kMaxAgents);        // [apc][take_road]
+    float4* zero_sm = reinterpret_cast<float4*>(
+        smem + align16(reinterpret_cast<uint8_t*>(cand_sm + apc * A.take_road) - smem));
+
+    // ---- prologue, independent of K1: clear this CTA's obs rows (TMA bulk stores)
+    float* rows = A.obs + (int64_t(w) * M + m0) * D;
+    for (int i = tid; i < kZeroChunk / 16; i += blockDim.x) zero_sm[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+        const uintptr_t b0 = reinterpret_cast<uintptr_t>(rows);
+        const uintptr_t b1 = b0 + uintptr_t(mc) * D * 4;
+        const uintptr_t a0 = (b0 + 15) & ~uintptr_t(15), a1 = b1 & ~uintptr_t(15);
+        if (a0 < a1) {
+            for (uintptr_t p = b0 + 4 * lane; p < a0; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
+            for (uintptr_t p = a1 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
+            if (lane == 0) {
+                for (uintptr_t p = a0; p < a1; p += kZeroChunk) {
+                    const uintptr_t n = a1 - p < uintptr_t(kZeroChunk) ? a1 - p : uintptr_t(kZeroChunk);
+                    bulk_store(reinterpret_cast<void*>(p), zero_sm, uint32_t(n));
+                }
+                bulk_commit_and_wait();
+            }
+        } else {
+            for (uintptr_t p = b0 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
+        }
+    }
+    const int scene = A.scene_of_world[w];
+    const int64_t* meta = A.scene_meta + 8 * scene;
+    const uint8_t* gbase = A.scene_blob + meta[0];
+    const double ox = A.grid_offset[2 * w], oy = A.grid_offset[2 * w + 1];
+
+    // ---- wait for the physics kernel (its writes are visible after this)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (kStep && world_ok[w] == 0) return;       // rejected actions: nothing mutates
+    const int step_now = kStep ? world_step[w] : 0;
+    for (int i = tid; i < M * int(sizeof(AgentRec) / 16); i += blockDim.x)
+        reinterpret_cast<int4*>(ag)[i] = reinterpret_cast<const int4*>(rec + int64_t(w) * M)[i];
+    __syncthreads();
+    if (warp >= mc) return;
+
+    const SceneView G = scene_view(const_cast<uint8_t*>(gbase), A.scene_blob + meta[5], int(meta[2]),
+                                   int(meta[3]), int(meta[4]));
+    const int m = m0 + warp;
+    const int64_t am = int64_t(w) * M + m;
+    const AgentRec& S = ag[m];
+    float* row = rows + int64_t(warp) * D;
+    const double px = S.x, py = S.y, c = S.c, s = S.s;
+    const int road0 = A.d.ego_dim;
+    const int veh0 = A.d.ego_dim + 5 * A.d.k_road;
+    const bool rewards_needed = kStep && S.alive;
+
+    // (1) neighbours: lane j <-> agent j (16 lanes), stable distance rank,
+    //     swept TTC, neighbour row, hull contact
+    double ttc_min;
+    bool touch;
+    {
+        const int j = lane;
+        double key = INFINITY, ndx = 0.0, ndy = 0.0;
+        if (j < M) {
+            const AgentRec& N = ag[j];
+            ndx = N.x - px;
+            ndy = N.y - py;
+            const double dist = dg::dsqrt(ndx * ndx + ndy * ndy);
+            key = (N.alive && j != m) ? dist : INFINITY;
+        }
+        int rank = 0;
+        for (int t = 0; t < M; ++t) {
+            const double kt = __shfl_sync(kFull, key, t);
+            rank += (kt < key) || (kt == key && t < j);
+        }
+        const bool nvalid = j < M && finite(key) && rank < A.take_veh;
+        double ttc = k.ttc_max;
+        if (nvalid) {
+            const AgentRec& N = ag[j];
+            ttc = swept_ttc(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c, N.s, N.d, S.r + N.r,
+                            k.ttc_max);
+            double st_, ct_;
+            sincos(N.yaw - S.yaw, &st_, &ct_);
+            const double wrap = atan2(st_, ct_);
+            float* o = row + veh0 + 7 * rank;
+            o[0] = __double2float_rn(dg::ddiv(c * ndx + s * ndy, k.bbox_half));
+            o[1] = __double2float_rn(dg::ddiv(-s * ndx + c * ndy, k.bbox_half));
+            o[2] = N.f_len;
+            o[3] = N.f_wid;
+            o[4] = __double2float_rn(dg::ddiv(wrap, 3.141592653589793));
+            o[5] = N.f_spd;
+            o[6] = __double2float_rn(dg::ddiv(ttc, k.ttc_max));
+        }
+        ttc_min = warp_min(ttc);
+        bool t_ = false;
+        if (kStep && j < M && j != m && S.alive && ag[j].alive &&
+            key <= S.r + ag[j].r + S.d + ag[j].d + 1e-4) {
+            const AgentRec& N = ag[j];
+            const double rs = S.r + N.r;
+            const double rs2 = rs * rs;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    const double ex = S.hx[a] - N.hx[b], ey = S.hy[a] - N.hy[b];
+                    t_ |= ex * ex + ey * ey < rs2;
+                }
+        }
+        touch = __any_sync(kFull, t_);
+    }
+
+    // (2) road context + edge boxes over the cell's superset list
+    const double r2 = S.r * S.r;
+    bool edge_hit = false;
+    uint16_t* cand = cand_sm + warp * A.take_road;
+    int count = 0;
+    auto visit = [&](int q, bool in, bool edge_q) {
+        bool hit = false;
+        if (in) {
+            const double2 m2 = __ldg(G.mid + q);
+            const double mx = m2.x + ox, my = m2.y + oy;
+            const double dx = mx - px, dy = my - py;
+            const double d2 = dx * dx + dy * dy;
+            hit = d2 <= k.road_radius_sq;
+            if (rewards_needed && edge_q) {
+                const double hl = __ldg(G.hl + q), hw = __ldg(G.hw + q);
+                const double reach = S.r + S.d + hl + hw + 1e-6;
+                if (d2 <= reach * reach) {
+                    const double2 u2 = __ldg(G.dir + q);
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        const double qx = S.hx[i] - mx, qy = S.hy[i] - my;
+                        const double along = qx * u2.x + qy * u2.y;
+                        const double lat = u2.x * qy - u2.y * qx;
+                        const double du = along - sel_clip(along, -hl, hl);
+                        const double dv = lat - sel_clip(lat, -hw, hw);
+                        edge_hit |= du * du + dv * dv < r2;
+                    }
+                }
+            }
+        }
+        const unsigned bal = __ballot_sync(kFull, hit);
+        if (hit) {
+            const int slot = count + __popc(bal & ((1u << lane) - 1u));
+            if (slot < A.take_road) cand[slot] = uint16_t(q);
+        }
+        count += __popc(bal);
+    };
+    const bool use_grid = (G.flags & kFlagGrid) != 0;
+    int cell_id = -1;
+    if (G.flags) {
+        const double inv = 1.0 / G.cell;
+        const double fx = floor((px - ox - G.gx0) * inv), fy = floor((py - oy - G.gy0) * inv);
+        if (fx >= 0.0 && fy >= 0.0 && fx < double(G.nx) && fy < double(G.ny)) cell_id = int(fy) * G.nx + int(fx);
+    }
+    if (use_grid) {
+        if (cell_id >= 0) {
+            const int lo = __ldg(G.road_start + cell_id), hi = __ldg(G.road_start + cell_id + 1);
+            for (int b0 = lo; b0 < hi; b0 += 32) {
+                const int i = b0 + lane;
+                const int q = i < hi ? int(__ldg(G.road_list + i)) : 0;
+                const bool edge_q = (__ldg(G.edge_bits + (q >> 5)) >> (q & 31)) & 1u;
+                visit(q, i < hi, edge_q);
+            }
+        }
+    } else {
+        for (int p0 = 0; p0 < G.P; p0 += 32) visit(p0 + lane, p0 + lane < G.P, false);
+    }
+    const int ncand = count < A.take_road ? count : A.take_road;
+    __syncwarp();
+    for (int slot = lane; slot < ncand; slot += 32) {
+        const int q = cand[slot];
+        const double2 m2 = __ldg(G.mid + q), u2 = __ldg(G.dir + q);
+        const double dx = (m2.x + ox) - px, dy = (m2.y + oy) - py;
+        float* o = row + road0 + 5 * slot;
+        o[0] = __double2float_rn(dg::ddiv(c * dx + s * dy, k.road_radius));
+        o[1] = __double2float_rn(dg::ddiv(-s * dx + c * dy, k.road_radius));
+        o[2] = __ldg(G.type_feat + q);
+        o[3] = __double2float_rn(c * u2.x + s * u2.y);
+        o[4] = __double2float_rn(-s * u2.x + c * u2.y);
+    }
+
+    // (3) the ego block (one lane)
+    const double gx = A.goal_xy[2 * am], gy = A.goal_xy[2 * am + 1];
+    if (lane == 0) write_ego(row, k, A, w, px, py, c, s, S.vx, S.vy, gx, gy);
+
+    if constexpr (!kStep) {
+        if (lane == 0 && A.ttc_min_out) A.ttc_min_out[am] = ttc_min;
+        return;
+    }
+
+    // (4) rewards: first edge ahead, nearest lane (alive agents only)
+    double gap = INFINITY, best = INFINITY;
+    int best_k = 0x7fffffff;
+    if (rewards_needed) {
+#pragma unroll 2
+        for (int kk = lane; kk < G.KE; kk += 32) {
+            const double2 m2 = __ldg(G.edge_mid + kk);
+            const double ex = (m2.x + ox) - px, ey = (m2.y + oy) - py;
+            const double xb = c * ex + s * ey;
+            if (xb > 0.0 && xb <= k.edge_range && xb < gap) gap = xb;
+            if (!use_grid) {
+                const int q = __ldg(G.edge + kk);
+                const double2 u2 = __ldg(G.dir + q);
+                const double hl = __ldg(G.hl + q), hw = __ldg(G.hw + q);
+                const double reach = S.r + S.d + hl + hw + 1e-6;
+                if (ex * ex + ey * ey <= reach * reach) {
+                    const double mx = m2.x + ox, my = m2.y + oy;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i) {
+                        const double qx = S.hx[i] - mx, qy = S.hy[i] - my;
+                        const double along = qx * u2.x + qy * u2.y;
+                        const double lat = u2.x * qy - u2.y * qx;
+                        const double du = along - sel_clip(along, -hl, hl);
+                        const double dv = lat - sel_clip(lat, -hw, hw);
+                        edge_hit |= du * du + dv * dv < r2;
+                    }
+                }
+            }
+        }
+        gap = warp_min(gap);
+        auto lane_test = [&](int kk) {
+            const double4 l4 = ldg4(G.lane_seg + kk);
+            const double ex = px - (l4.x + ox), ey = py - (l4.y + oy);
+            const double along = ex * l4.z + ey * l4.w;
+            const double lat = l4.z * ey - l4.w * ex;
+            const double t = fabs(along) - __ldg(G.lane_hl + kk);
+            const double over = t > 0.0 ? t : 0.0;
+            const double d2 = over * over + lat * lat;
+            if (d2 < best) { best = d2; best_k = kk; }
+        };
+        const int lcell = (G.flags & kFlagLanes) ? cell_id : -1;
+        if (lcell >= 0) {
+            const int b0 = __ldg(G.lane_start + lcell), b1 = __ldg(G.lane_start + lcell + 1);
+            for (int i = b0 + lane; i < b1; i += 32) lane_test(__ldg(G.lane_list + i));
+        } else {
+            for (int kk = lane; kk < G.KL; kk += 32) lane_test(kk);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(kFull, best, o);
+            const int ok = __shfl_xor_sync(kFull, best_k, o);
+            if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
+        }
+    }
+    edge_hit = __any_sync(kFull, edge_hit);
+
+    // (5) the agent's reward / event / termination tail
+    if (lane == 0) {
+        double st[DG_NUM_STATE];
+#pragma unroll
+        for (int f = 0; f < DG_NUM_STATE; ++f) st[f] = A.state[int64_t(f) * WM + am];
+        FinIn F;
+        F.st = st;
+        F.px0 = prev[am].x; F.py0 = prev[am].y;
+        F.gx = gx; F.gy = gy;
+        F.sx = A.start_xy[2 * am]; F.sy = A.start_xy[2 * am + 1];
+        F.lane_d2 = best;
+        F.lane_lat = 0.0; F.lane_tx = 0.0; F.lane_ty = 0.0;
+        if (best < INFINITY) {
+            const double4 l4 = ldg4(G.lane_seg + best_k);
+            const double ex = px - (l4.x + ox), ey = py - (l4.y + oy);
+            F.lane_tx = l4.z;
+            F.lane_ty = l4.w;
+            F.lane_lat = l4.z * ey - l4.w * ex;
+        }
+        F.ttc_min = ttc_min; F.gap = gap;
+        F.edge_hit = edge_hit; F.touch = touch;
+        F.alive = S.alive; F.valid = A.valid[am]; F.reason = A.reason[am]; F.seen = A.event_seen[am];
+        F.spawn = A.spawn_step[am];
+        finalize_agent(A, w, m, F, step_now, ox, oy);
     }
 }
 
@@ -1023,8 +1481,10 @@ struct dg_engine {
     KArgs base;
     size_t smem_bytes;
     int launches;
-    int warps_per_world;   // CTA = warps_per_world warps, agents strided over warps
+    int warps_per_world;   // fused: CTA = warps_per_world warps; split: agents (warps) per CTA
     int min_blocks;        // register budget: resident CTAs per SM the variant is built for
+    int mode;              // 0 = fused world kernel, 1 = split physics + per-agent kernels (PDL)
+    size_t smem_split;     // dynamic smem of the per-agent kernel
 };
 
 #define DG_VARIANTS(X)                                                                 \
@@ -1066,6 +1526,58 @@ static bool has_variant(int threads, int blocks) {
     return false;
 }
 
+// split mode: per-agent kernel variants (threads = 32 * agents per CTA)
+#define DG_SPLIT_VARIANTS(X) X(64, 8) X(64, 12) X(64, 16) X(128, 4) X(128, 6) X(128, 8) X(256, 2) X(256, 4)
+
+static bool has_split_variant(int threads, int blocks) {
+#define DG_HAS(T, B) if (threads == T && blocks == B) return true;
+    DG_SPLIT_VARIANTS(DG_HAS)
+#undef DG_HAS
+    return false;
+}
+
+template <bool kStep>
+static cudaError_t set_split_smem_attr(size_t bytes) {
+    cudaError_t e = cudaSuccess;
+#define DG_ATTR(T, B)                                                                    \
+    if (e == cudaSuccess)                                                                \
+        e = cudaFuncSetAttribute(agent_obs_kernel<kStep, T, B>,                          \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    DG_SPLIT_VARIANTS(DG_ATTR)
+#undef DG_ATTR
+    return e;
+}
+
+template <bool kStep>
+static cudaError_t launch_split(const dg_engine* e, const KArgs& A, cudaStream_t st) {
+    world_physics_kernel<kStep><<<A.d.W, 32, 0, st>>>(A);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    const int apc = e->warps_per_world;
+    const int threads = 32 * apc;
+    const int groups = (A.d.M + apc - 1) / apc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(A.d.W * groups);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = e->smem_split;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+#define DG_LAUNCH(T, B)                                                                  \
+    if (threads == T && e->min_blocks == B) return cudaLaunchKernelEx(&cfg, agent_obs_kernel<kStep, T, B>, A);
+    DG_SPLIT_VARIANTS(DG_LAUNCH)
+#undef DG_LAUNCH
+    return cudaErrorInvalidConfiguration;
+}
+
+template <bool kStep>
+static cudaError_t launch_step_any(const dg_engine* e, const KArgs& A, cudaStream_t st) {
+    return e->mode == 1 ? launch_split<kStep>(e, A, st) : launch_world_step<kStep>(e, A, st);
+}
+
 static thread_local char g_err[512] = "";
 
 static int fail(int code, const char* msg) {
@@ -1076,6 +1588,12 @@ static int fail(int code, const char* msg) {
 static int cuda_fail(cudaError_t e, const char* where) {
     std::snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
     return DG_ECUDA;
+}
+
+static size_t split_smem_bytes(int take_road, int apc) {
+    size_t b = sizeof(AgentRec) * kMaxAgents;
+    b += sizeof(uint16_t) * size_t(apc) * size_t(take_road > 0 ? take_road : 1);
+    return size_t(align16(int64_t(b))) + kZeroChunk;
 }
 
 static size_t step_smem_bytes(const DgDims& d, int take_road) {
@@ -1137,6 +1655,7 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
     A.goal_xy = desc->goal_xy;
     A.start_yaw = desc->start_yaw;
     A.error_word = desc->error_word;
+    A.scratch = desc->scratch;
     A.take_road = d.k_road < d.max_segments ? d.k_road : d.max_segments;
     A.take_veh = d.k_vehicles < d.M ? d.k_vehicles : d.M;
     e->smem_bytes = step_smem_bytes(d, A.take_road);
@@ -1144,8 +1663,11 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
         delete e;
         return fail(DG_ENOSUPPORT, "dg_create: scene geometry does not fit in shared memory");
     }
+    e->smem_split = split_smem_bytes(A.take_road, 8);
     cudaError_t err = set_smem_attr<true>(e->smem_bytes);
     if (err == cudaSuccess) err = set_smem_attr<false>(e->smem_bytes);
+    if (err == cudaSuccess) err = set_split_smem_attr<true>(e->smem_split);
+    if (err == cudaSuccess) err = set_split_smem_attr<false>(e->smem_split);
     if (err != cudaSuccess) {
         delete e;
         return cuda_fail(err, "dg_create: cudaFuncSetAttribute");
@@ -1153,6 +1675,7 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
     e->launches = 0;
     e->warps_per_world = d.M;
     e->min_blocks = 1;
+    e->mode = 0;
     *out = e;
     return DG_OK;
 }
@@ -1181,7 +1704,8 @@ int dg_step(dg_engine* eng, const DgStepIO* io, void* stream) {
     A.terms_out = io->terms_out;
     A.snapshot_out = io->snapshot_out;
     eng->launches = 1;
-    const cudaError_t err = launch_world_step<true>(eng, A, static_cast<cudaStream_t>(stream));
+    const cudaError_t err = launch_step_any<true>(eng, A, static_cast<cudaStream_t>(stream));
+    eng->launches = eng->mode == 1 ? 2 : 1;
     return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_step");
 }
 
@@ -1191,7 +1715,8 @@ int dg_observe(dg_engine* eng, float* obs, double* ttc_min_out, void* stream) {
     A.obs = obs;
     A.ttc_min_out = ttc_min_out;
     eng->launches = 1;
-    const cudaError_t err = launch_world_step<false>(eng, A, static_cast<cudaStream_t>(stream));
+    const cudaError_t err = launch_step_any<false>(eng, A, static_cast<cudaStream_t>(stream));
+    eng->launches = eng->mode == 1 ? 2 : 1;
     return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_observe");
 }
 
@@ -1261,13 +1786,25 @@ int dg_launch_count(dg_engine* eng) { return eng ? eng->launches : 0; }
 #ifdef DG_PHASE_TIMERS
 int dg_debug_phase_clocks(long long* host_out, int n_blocks) {
     const int n = n_blocks < 65536 ? n_blocks : 65536;
-    const cudaError_t e = cudaMemcpyFromSymbol(host_out, g_phase_clock, sizeof(long long) * 24 * n);
+    const cudaError_t e = cudaMemcpyFromSymbol(host_out, g_phase_clock, sizeof(long long) * 40 * n);
     return e == cudaSuccess ? DG_OK : cuda_fail(e, "dg_debug_phase_clocks");
 }
 #endif
 
-int dg_tune(dg_engine* eng, int32_t warps_per_world, int32_t ctas_per_sm) {
+int dg_tune(dg_engine* eng, int32_t mode, int32_t warps_per_world, int32_t ctas_per_sm) {
     if (!eng) return fail(DG_EINVAL, "dg_tune: null engine");
+    if (mode == 1) {
+        if (!eng->base.scratch) return fail(DG_EINVAL, "dg_tune: split mode needs the scratch buffer");
+        const int apc = warps_per_world;
+        if (apc != 2 && apc != 4 && apc != 8) return fail(DG_EINVAL, "dg_tune: split mode takes 2, 4 or 8 agents per CTA");
+        const int blocks = ctas_per_sm > 0 ? ctas_per_sm : (apc == 2 ? 8 : apc == 4 ? 4 : 2);
+        if (!has_split_variant(32 * apc, blocks)) return fail(DG_EINVAL, "dg_tune: no split kernel variant for this shape");
+        eng->mode = 1;
+        eng->warps_per_world = apc;
+        eng->min_blocks = blocks;
+        return DG_OK;
+    }
+    if (mode != 0) return fail(DG_EINVAL, "dg_tune: mode must be 0 (fused) or 1 (split)");
     if (warps_per_world < 1 || warps_per_world > kMaxAgents)
         return fail(DG_EINVAL, "dg_tune: warps_per_world must lie in [1, 16]");
     const int nw = warps_per_world < eng->base.d.M ? warps_per_world : eng->base.d.M;
@@ -1276,7 +1813,10 @@ int dg_tune(dg_engine* eng, int32_t warps_per_world, int32_t ctas_per_sm) {
     if (!has_variant(threads, blocks)) return fail(DG_EINVAL, "dg_tune: no kernel variant for this shape");
     eng->warps_per_world = nw;
     eng->min_blocks = blocks;
+    eng->mode = 0;
     return DG_OK;
 }
+
+size_t dg_scratch_bytes(int32_t W, int32_t M) { return split_scratch_bytes(W, M); }
 
 }  // extern "C"

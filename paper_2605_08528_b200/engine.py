@@ -178,7 +178,8 @@ class Engine:
     def __init__(self, worlds, scenes, assignment, frictions, config: SimConfig,
                  obs_config: ObsConfig | None = None, reward_config: RewardConfig | None = None,
                  params: VehicleParams | None = None, bicycle: BicycleParams | None = None,
-                 device=None, spatial_index: bool = True, warps_per_world: int | None = None):
+                 device=None, spatial_index: bool = True, warps_per_world: int | None = None,
+                 launch_mode: int = 0):
         if not torch.cuda.is_available():
             raise RuntimeError("drivegrid-b200 Engine needs a CUDA device (no CPU fallback)")
         self._lib = N.load_library()
@@ -234,6 +235,7 @@ class Engine:
             "goal_xy": up(t.goal_xy, torch.float64),
             "start_yaw": up(t.start_yaw, torch.float64),
             "error_word": torch.full((1,), N.DG_NO_ERROR, dtype=torch.int32, device=dev),
+            "scratch": torch.empty(int(self._lib.dg_scratch_bytes(W, M)), dtype=torch.uint8, device=dev),
         }
         oc = self.obs_config
         dims = N.DgDims(W=W, M=M, obs_dim=oc.obs_dim, ego_dim=oc.ego_dim, k_road=oc.k_road,
@@ -247,13 +249,22 @@ class Engine:
         for name in ("scene_blob", "scene_meta", "scene_of_world", "grid_offset", "mu_eff", "weather",
                      "valid", "length", "width", "r_hull", "d_hull", "state", "alive", "reason",
                      "event_seen", "spawn_step", "step_count", "start_xy", "goal_xy", "start_yaw",
-                     "error_word"):
+                     "error_word", "scratch"):
             setattr(desc, name, d[name].data_ptr())
         handle = ct.c_void_p()
         N.check(self._lib, self._lib.dg_create(ct.byref(desc), ct.byref(handle)), "dg_create")
         self._h = handle
         self._desc = desc
-        self.tune(warps_per_world or min(M, 8))
+        if launch_mode == 1:
+            self.tune(warps_per_world or 4, 0, mode=1)
+        elif warps_per_world:
+            self.tune(warps_per_world)
+        elif W >= 1024:
+            # many worlds per SM: throughput-bound -> 4 warps/world, 4 CTAs/SM
+            self.tune(min(M, 4), 4 if M > 4 else 0)
+        else:
+            # few worlds per SM: latency-bound -> 8 warps/world, 2 CTAs/SM
+            self.tune(min(M, 8))
         self._step_count = 0
         self.phase_seconds = {k: 0.0 for k in PHASES}
         self._act_dev = torch.empty((W, M, 3), dtype=torch.float64, device=dev)
@@ -308,10 +319,18 @@ class Engine:
     def new_step_buffers(self, obs: torch.Tensor | None = None) -> StepBuffers:
         return self._new_buffers(obs)
 
-    def tune(self, warps_per_world: int, ctas_per_sm: int = 0) -> None:
-        """Launch shape knob (warps per world CTA, register budget as resident
-        CTAs per SM); results are unaffected."""
-        N.check(self._lib, self._lib.dg_tune(self._h, int(warps_per_world), int(ctas_per_sm)), "dg_tune")
+    def launch_shape(self) -> dict:
+        return dict(self._shape)
+
+    def tune(self, warps_per_world: int, ctas_per_sm: int = 0, mode: int = 0) -> None:
+        """Launch shape knob; results are unaffected.  mode 0: fused world
+        kernel with ``warps_per_world`` warps; mode 1: split physics + per-agent
+        kernels with ``warps_per_world`` agents per CTA.  ``ctas_per_sm`` picks
+        the register budget of the kernel variant (0 = default)."""
+        N.check(self._lib, self._lib.dg_tune(self._h, int(mode), int(warps_per_world), int(ctas_per_sm)),
+                "dg_tune")
+        self._shape = {"mode": "split" if mode else "fused", "warps": int(warps_per_world),
+                       "ctas_per_sm": int(ctas_per_sm)}
 
     # ------------------------------------------------------------------ device state views
     @property

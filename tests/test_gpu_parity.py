@@ -73,19 +73,20 @@ def compare(dev: Dev, t, g, o, oc):
     dev.f("obs", g.obs, o.obs, rtol=OBS_RTOL, atol=OBS_ATOL)
 
 
-VARIANTS = [(n, True, None) for n in TRAJ_CASES] + [
-    ("traj_events", False, 3), ("traj_wet", True, 16), ("traj_pool", False, 1),
-    ("traj_events_inv", True, 5)]
+VARIANTS = [(n, True, None, 0) for n in TRAJ_CASES] + [(n, True, None, 1) for n in TRAJ_CASES] + [
+    ("traj_events", False, 3, 0), ("traj_wet", True, 16, 0), ("traj_pool", False, 1, 0),
+    ("traj_events_inv", True, 5, 0), ("traj_events", False, 8, 1), ("traj_wet", False, 2, 1)]
 
 
-@pytest.mark.parametrize("name,spatial,warps", VARIANTS,
-                         ids=[f"{n}-{'idx' if s else 'scan'}-w{w}" for n, s, w in VARIANTS])
-def test_trajectory_parity(name, spatial, warps, device):
-    """Launch shape and the spatial index are performance knobs: every
+@pytest.mark.parametrize("name,spatial,warps,mode", VARIANTS,
+                         ids=[f"{n}-{'idx' if s else 'scan'}-w{w}-{'split' if m else 'fused'}"
+                              for n, s, w, m in VARIANTS])
+def test_trajectory_parity(name, spatial, warps, mode, device):
+    """Launch mode/shape and the spatial index are performance knobs: every
     variant must reproduce the oracle."""
     case = case_inputs(name)
     gpu = Engine(**case.inputs.as_kwargs(), device=device, spatial_index=spatial,
-                 warps_per_world=warps)
+                 warps_per_world=warps, launch_mode=mode)
     ora = OracleEngine(**case.inputs.as_kwargs())
     dev = Dev()
     dev.f("obs0", gpu.observe(), ora.observe(), rtol=OBS_RTOL, atol=OBS_ATOL)
@@ -156,10 +157,11 @@ def test_device_lane_follower_equals_host_policy(device):
         obs_d = out.obs
 
 
-def test_fused_autoreset_equals_step_then_teleport(device):
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fused_autoreset_equals_step_then_teleport(mode, device):
     inp = C.build_inputs(cfg_of(8, 16, seed=31))
-    a = Engine(**inp.as_kwargs(), device=device)
-    b = Engine(**inp.as_kwargs(), device=device)
+    a = Engine(**inp.as_kwargs(), device=device, launch_mode=mode)
+    b = Engine(**inp.as_kwargs(), device=device, launch_mode=mode)
     from cases import event_actions
     acts = event_actions(200, 8, 16)
     resets = 0
@@ -194,11 +196,12 @@ def test_nonfinite_action_rejected_before_mutation(device):
         eng.step(np.zeros((2, 3, 3)))
 
 
-def test_device_guard_skips_bad_world(device):
+@pytest.mark.parametrize("mode", [0, 1])
+def test_device_guard_skips_bad_world(mode, device):
     """Without the host-side check the kernel still refuses to step a world
     whose actions are non-finite and reports the first bad element."""
     inp = C.build_inputs(cfg_of(3, 4, assignment="fixed"))
-    eng = Engine(**inp.as_kwargs(), device=device)
+    eng = Engine(**inp.as_kwargs(), device=device, launch_mode=mode)
     st0 = eng.state_tensor.clone()
     acts = torch.zeros((3, 4, 3), dtype=torch.float64, device=device)
     acts[..., 0] = 1.0

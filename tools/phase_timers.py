@@ -33,7 +33,7 @@ for i in range(5):
     eng.lane_follower(bufs.obs if i else obs, out=acts)
     eng.launch_step(acts, bufs, autoreset=True)
 torch.cuda.synchronize()
-out = np.zeros((W, 24), dtype=np.int64)
+out = np.zeros((W, 40), dtype=np.int64)
 assert lib.dg_debug_phase_clocks(out.ctypes.data, W) == 0
 names = ["act-check", "phys+zero(w0)", "bar1", "geo-fixup", "phase2a/2b", "bar3", "finalize"]
 d = np.diff(out[:, :7], axis=1)
@@ -43,12 +43,16 @@ for i, nme in enumerate(names[:6]):
 tot = out[:, 6] - out[:, 0]
 print(f"  total          median {np.median(tot):8.0f}  max {tot.max():8.0f}")
 wend = out[:, 8:8 + nw] - out[:, 4:5]
-ph = out[:, [1, 17, 18, 19, 2]]
+ph = out[:, [1, 25, 26, 27, 2]]
 print("  warp0: loads", np.median(ph[:, 1] - ph[:, 0]), " substeps", np.median(ph[:, 2] - ph[:, 1]),
       " derived+tables", np.median(ph[:, 3] - ph[:, 2]), " zero-fill", np.median(ph[:, 4] - ph[:, 3]))
-print("  substep ends (cycles after state loads):", np.median(out[:, 20:24] - out[:, 17:18], axis=0).astype(int))
-w1 = out[:, [4, 10, 11, 12, 13, 14]]
+print("  substep ends (cycles after state loads):", np.median(out[:, 28:32] - out[:, 25:26], axis=0).astype(int))
+w1 = out[:, [4, 34, 35, 36, 37, 38]]
 print("  warp1 agent1: pairs(2a)", np.median(w1[:, 1] - w1[:, 0]), " road scan", np.median(w1[:, 2] - w1[:, 1]),
       " road feats", np.median(w1[:, 3] - w1[:, 2]), " edge gap", np.median(w1[:, 4] - w1[:, 3]),
       " lane", np.median(w1[:, 5] - w1[:, 4]))
+gs, ge = out[:, 32], out[:, 33]
+t0 = gs.min()
+print(f"  globaltimer: CTA start spread {(gs.max() - t0) / 1e3:.2f} us, first end {(ge.min() - t0) / 1e3:.2f} us, "
+      f"last end {(ge.max() - t0) / 1e3:.2f} us, median CTA duration {np.median(ge - gs) / 1e3:.2f} us")
 print("  phase2 per-warp end (cycles after phase2 start), median over CTAs:", np.median(wend, axis=0).astype(int))
