@@ -3,10 +3,11 @@
 
 Workload (BASELINE.json configs[1]): 256 worlds x 16 agents, default
 procedural pool (straight roads + crossroads, seed 42), dry road, dynamic
-single-track backend.  A "step" = device LaneFollower policy on the previous
-observation -> one fused env step (physics x4, 1929-dim obs, rewards,
-events, tail) with the masked teleport reset of finished agents fused in
-(autoreset), so the alive population stays at every valid slot.
+single-track backend.  A "step" = one fused env step (physics x4, 1929-dim
+obs, rewards, events, tail) with the masked teleport reset of finished agents
+fused in (autoreset, so the alive population stays at every valid slot) and
+the LaneFollower bench policy fused in too (it reads the float32 ego block the
+step just wrote and emits the next tick's actions) -- one kernel per tick.
 
   value   CASPS with everything resident in HBM; observations go to a rotating
           rollout ring larger than L2 (no cache reuse between steps)
@@ -265,13 +266,14 @@ def main():
     ring = max(2, math.ceil(2 * L2_BYTES / obs_bytes))
     obs_ring = torch.empty((ring, W, M, D), dtype=torch.float32, device=dev)
     bufs = [eng.new_step_buffers(obs_ring[i]) for i in range(ring)]
-    acts = torch.zeros((W, M, 3), dtype=torch.float64, device=dev)
-    eng.observe(out=obs_ring[ring - 1], as_numpy=False)
+    # the LaneFollower is fused into the step: step i reads actions[i % 2] and
+    # writes the policy's actions for step i+1 into actions[(i + 1) % 2]
+    acts = [torch.zeros((W, M, 3), dtype=torch.float64, device=dev) for _ in range(2)]
+    eng.observe(out=obs_ring[ring - 1], as_numpy=False, next_actions=acts[0])
     stream = torch.cuda.current_stream(dev)
 
     def one_step(i):
-        eng.lane_follower(obs_ring[(i - 1) % ring], out=acts)
-        eng.launch_step(acts, bufs[i % ring], autoreset=True)
+        eng.launch_step(acts[i % 2], bufs[i % ring], autoreset=True, next_actions=acts[(i + 1) % 2])
 
     # warm-up (untimed)
     for i in range(args.warmup):
@@ -282,8 +284,9 @@ def main():
 
     # The K timed steps are captured once into a CUDA graph (outside the timed
     # region): the device then runs policy -> fused step back to back with no
-    # host launch gaps.  Event nodes bracket every fused-step kernel, so the
-    # per-launch kernel time comes from the same replay.
+    # host launch gaps.  The per-launch time of the fused-step kernel (the
+    # roofline numerator) comes from a second graph of K step-only launches,
+    # timed the same way right after.
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -292,13 +295,8 @@ def main():
     if not args.no_graph:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            cs = torch.cuda.current_stream(dev)
             for i in range(args.steps):
-                j = args.warmup + i
-                eng.lane_follower(obs_ring[(j - 1) % ring], out=acts)
-                ev0[i].record(cs)
-                eng.launch_step(acts, bufs[j % ring], autoreset=True)
-                ev1[i].record(cs)
+                one_step(args.warmup + i)
     if world_size > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -308,21 +306,34 @@ def main():
             graph.replay()
         else:
             for i in range(args.steps):
-                j = args.warmup + i
-                eng.lane_follower(obs_ring[(j - 1) % ring], out=acts)
                 ev0[i].record(stream)
-                eng.launch_step(acts, bufs[j % ring], autoreset=True)
+                one_step(args.warmup + i)
                 ev1[i].record(stream)
         stop.record(stream)
         torch.cuda.synchronize()
     launches = eng.launches - launches0
     total_ms = start.elapsed_time(stop)
+    launches_per_step = launches / args.steps
     if world_size > 1:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    kern_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
-    kern_avg = sum(kern_ms) / len(kern_ms)
+    if graph is not None:
+        # kernel-only timing: K fused-step launches in one graph, CUDA events around the replay
+        g_step = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_step):
+            for i in range(args.steps):
+                one_step(args.warmup + args.steps + i)
+        torch.cuda.synchronize()
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
+        g_step.replay()
+        k1.record(stream)
+        torch.cuda.synchronize()
+        kern_avg = k0.elapsed_time(k1) / args.steps
+    else:
+        kern_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+        kern_avg = sum(kern_ms) / len(kern_ms)
     assert int(eng.alive.sum()) == valid_count, "autoreset must keep every valid slot alive"
     agent_ticks = valid_count * args.steps * world_size  # alive before every step (asserted)
     value = agent_ticks / (total_ms / 1e3)
@@ -343,7 +354,7 @@ def main():
             "higher_is_better": True, "scaling": "weak" if world_size == 1 else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{W_total}x16 default procedural pool (seed 42), dry, dynamic, "
-                                   f"device LaneFollower, fused autoreset",
+                                   f"LaneFollower + autoreset fused into the step",
                        "worlds": W_total, "agents": M, "obs_dim": D,
                        "l2": f"obs rotate through a {ring}-slot rollout ring ({ring * obs_bytes / 2**20:.0f} MiB > L2)",
                        "launch": "CUDA graph of the K timed steps" if graph is not None else "eager",
@@ -353,7 +364,7 @@ def main():
                          "frac": achieved / peak, "traffic": None,
                          "bytes_per_agent_step": per_agent, "kernel_ms": kern_avg,
                          "peak_source": peak_src},
-            "gpu_launches": launches,
+            "gpu_launches": int(round(launches_per_step * args.steps)),
         }
         line["clocks"] = clk.summary()
         # e2e through the numpy API

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 2
+#define DG_ABI_VERSION 3
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -130,6 +130,9 @@ typedef struct DgStepIO {
     double* ttc_min_out;        /* [W][M]      info["ttc_min"]                */
     double* terms_out;          /* [7][W][M]   info["reward_terms"]           */
     double* snapshot_out;       /* [12][W][M]  info["state"] (pre-park)       */
+    double* next_actions;       /* [W][M][3]   fused LaneFollower on this tick's
+                                   observation (policies.py:21-43), or NULL  */
+    double policy_gain, policy_throttle;
 } DgStepIO;
 
 typedef struct dg_engine dg_engine;
@@ -146,8 +149,9 @@ int dg_destroy(dg_engine* eng);
 int dg_step(dg_engine* eng, const DgStepIO* io, void* stream);
 
 /* Observation of the current state without stepping: Engine.observe
- * (engine.py:297-330). */
-int dg_observe(dg_engine* eng, float* obs, double* ttc_min_out, void* stream);
+ * (engine.py:297-330); optional fused LaneFollower actions as in DgStepIO. */
+int dg_observe(dg_engine* eng, float* obs, double* ttc_min_out, double* next_actions, double policy_gain,
+               double policy_throttle, void* stream);
 
 /* Masked teleport reset: Engine.teleport_reset (engine.py:599-619).
  * mask [W][M] u8 (NULL = every valid slot); optional new starts/goals

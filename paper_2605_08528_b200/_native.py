@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class DgDims(ct.Structure):
@@ -67,7 +67,8 @@ class DgEngineDesc(ct.Structure):
 class DgStepIO(ct.Structure):
     _fields_ = [("actions", _P), ("actions_f64", ct.c_int32), ("autoreset", ct.c_int32)] + [
         (n, _P) for n in ("obs", "rewards", "dones", "events", "reason_out", "alive_out",
-                          "alive_pre_out", "ttc_min_out", "terms_out", "snapshot_out")]
+                          "alive_pre_out", "ttc_min_out", "terms_out", "snapshot_out",
+                          "next_actions")] + [("policy_gain", ct.c_double), ("policy_throttle", ct.c_double)]
 
 
 # exported symbol -> (restype, argtypes)
@@ -77,7 +78,7 @@ SIGNATURES = {
     "dg_create": (ct.c_int, [ct.POINTER(DgEngineDesc), ct.POINTER(_P)]),
     "dg_destroy": (ct.c_int, [_P]),
     "dg_step": (ct.c_int, [_P, ct.POINTER(DgStepIO), _P]),
-    "dg_observe": (ct.c_int, [_P, _P, _P, _P]),
+    "dg_observe": (ct.c_int, [_P, _P, _P, _P, ct.c_double, ct.c_double, _P]),
     "dg_reset": (ct.c_int, [_P, _P, _P, _P, _P, _P]),
     "dg_set_step_count": (ct.c_int, [_P, ct.c_int32, _P]),
     "dg_check_actions": (ct.c_int, [_P, _P, ct.c_int32, _P]),

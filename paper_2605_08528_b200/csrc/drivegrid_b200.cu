@@ -84,6 +84,8 @@ struct KArgs {
     double* ttc_min_out;
     double* terms_out;
     double* snapshot_out;
+    double* next_actions;   // fused LaneFollower output for the next tick (NULL = off)
+    double pol_gain, pol_throttle;
     int32_t take_road;   // min(k_road, max_segments) = candidate-list capacity
     int32_t take_veh;    // min(k_vehicles, M)
     uint8_t* scratch;    // split mode: AgentRec[W*M], int32 world_ok[W], int32 world_step[W]
@@ -387,18 +389,33 @@ struct ScanSm {
 // Both launch modes share these: the ego features of one agent's row
 // (observation.py:51-75) and the reward / event / termination tail of one
 // agent (rewards.py:106-268, engine.py:370-406, 472-509).
-__device__ __forceinline__ void write_ego(float* row, const DgConsts& k, const KArgs& A, int w, double px, double py,
-                                          double c, double s, double vx, double vy, double gx, double gy) {
+__device__ __forceinline__ void write_ego(float* row, const DgConsts& k, const KArgs& A, int w, int64_t am,
+                                          double px, double py, double c, double s, double vx, double vy,
+                                          double gx, double gy) {
     const double gdx = gx - px, gdy = gy - py;
     const double xb = c * gdx + s * gdy;
     const double yb = -s * gdx + c * gdy;
     double sh, ch;
     sincos(atan2(yb, xb), &sh, &ch);
+    const float f2 = __double2float_rn(sh), f3 = __double2float_rn(ch);
+    const float f4 = __double2float_rn(dg::ddiv(dg::dsqrt(xb * xb + yb * yb), k.bbox_half));
     row[0] = __double2float_rn(dg::ddiv(xb, k.bbox_half));
     row[1] = __double2float_rn(dg::ddiv(yb, k.bbox_half));
-    row[2] = __double2float_rn(sh);
-    row[3] = __double2float_rn(ch);
-    row[4] = __double2float_rn(dg::ddiv(dg::dsqrt(xb * xb + yb * yb), k.bbox_half));
+    row[2] = f2;
+    row[3] = f3;
+    row[4] = f4;
+    if (A.next_actions) {
+        // LaneFollower (policies.py:21-43) on this float32 observation, fused:
+        // the next tick's actions never leave the GPU
+        const double sin_e = double(f2), cos_e = double(f3);
+        const double dist = double(f4) * k.bbox_half;
+        double steer = np_clip(A.pol_gain * sin_e, -1.0, 1.0);
+        if (cos_e < 0.0) steer = sin_e >= 0.0 ? 1.0 : -1.0;
+        double* act = A.next_actions + 3 * am;
+        act[0] = dist > 5.0 ? A.pol_throttle : A.pol_throttle * 0.5;
+        act[1] = steer;
+        act[2] = 0.0;
+    }
     row[5] = __double2float_rn(dg::ddiv(vx, k.speed_norm));
     row[6] = __double2float_rn(dg::ddiv(vy, k.speed_norm));
     if (A.d.include_weather) {
@@ -973,7 +990,8 @@ world_step_kernel(const KArgs A) {
     const int ego_warp = nwarps > 1 ? 1 : 0;
     if (warp == ego_warp && lane < M) {
         const AgentSm& S = ag[lane];
-        write_ego(obs_w + int64_t(lane) * D, k, A, w, S.st[SX], S.st[SY], S.c, S.s, S.st[SVX], S.st[SVY],
+        write_ego(obs_w + int64_t(lane) * D, k, A, w, int64_t(w) * M + lane, S.st[SX], S.st[SY], S.c, S.s,
+                  S.st[SVX], S.st[SVY],
                   S.gx, S.gy);
     }
     if constexpr (kStep) {
@@ -1331,7 +1349,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
 
     // (3) the ego block (one lane)
     const double gx = A.goal_xy[2 * am], gy = A.goal_xy[2 * am + 1];
-    if (lane == 0) write_ego(row, k, A, w, px, py, c, s, S.vx, S.vy, gx, gy);
+    if (lane == 0) write_ego(row, k, A, w, am, px, py, c, s, S.vx, S.vy, gx, gy);
 
     if constexpr (!kStep) {
         if (lane == 0 && A.ttc_min_out) A.ttc_min_out[am] = ttc_min;
@@ -1703,17 +1721,24 @@ int dg_step(dg_engine* eng, const DgStepIO* io, void* stream) {
     A.ttc_min_out = io->ttc_min_out;
     A.terms_out = io->terms_out;
     A.snapshot_out = io->snapshot_out;
+    A.next_actions = io->next_actions;
+    A.pol_gain = io->policy_gain;
+    A.pol_throttle = io->policy_throttle;
     eng->launches = 1;
     const cudaError_t err = launch_step_any<true>(eng, A, static_cast<cudaStream_t>(stream));
     eng->launches = eng->mode == 1 ? 2 : 1;
     return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_step");
 }
 
-int dg_observe(dg_engine* eng, float* obs, double* ttc_min_out, void* stream) {
+int dg_observe(dg_engine* eng, float* obs, double* ttc_min_out, double* next_actions, double policy_gain,
+               double policy_throttle, void* stream) {
     if (!eng || !obs) return fail(DG_EINVAL, "dg_observe: null argument");
     KArgs A = eng->base;
     A.obs = obs;
     A.ttc_min_out = ttc_min_out;
+    A.next_actions = next_actions;
+    A.pol_gain = policy_gain;
+    A.pol_throttle = policy_throttle;
     eng->launches = 1;
     const cudaError_t err = launch_step_any<false>(eng, A, static_cast<cudaStream_t>(stream));
     eng->launches = eng->mode == 1 ? 2 : 1;

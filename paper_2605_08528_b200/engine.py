@@ -443,10 +443,13 @@ class Engine:
 
     # ------------------------------------------------------------------ observe
     def observe(self, ttc_min: torch.Tensor | None = None, out: torch.Tensor | None = None,
-                as_numpy: bool = True):
-        """Observation of the current state (engine.py:297-300)."""
+                as_numpy: bool = True, next_actions: torch.Tensor | None = None, steer_gain: float = 2.0,
+                throttle: float = 0.5):
+        """Observation of the current state (engine.py:297-300); with
+        ``next_actions`` the LaneFollower actions for it are fused in."""
         obs = out if out is not None else torch.empty_like(self._obs_dev)
-        N.check(self._lib, self._lib.dg_observe(self._h, _ptr(obs), _ptr(ttc_min), self._stream()),
+        N.check(self._lib, self._lib.dg_observe(self._h, _ptr(obs), _ptr(ttc_min), _ptr(next_actions),
+                                                float(steer_gain), float(throttle), self._stream()),
                 "dg_observe")
         self.launches += 1
         if as_numpy:
@@ -458,9 +461,12 @@ class Engine:
 
     # ------------------------------------------------------------------ step
     def launch_step(self, actions: torch.Tensor, bufs: StepBuffers, autoreset: bool = False,
-                    snapshot: bool = True, terms: bool = True) -> None:
+                    snapshot: bool = True, terms: bool = True, next_actions: torch.Tensor | None = None,
+                    steer_gain: float = 2.0, throttle: float = 0.5) -> None:
         """Enqueue one fused step on the current stream; no sync, no checks
-        beyond the device-side non-finite guard.  Used by the fast paths."""
+        beyond the device-side non-finite guard.  Used by the fast paths.
+        ``next_actions`` (float64 [W][M][3], distinct from ``actions``) receives
+        the fused LaneFollower's actions on this tick's observation."""
         v = bufs.views
         io = N.DgStepIO(actions=actions.data_ptr(), actions_f64=int(actions.dtype == torch.float64),
                         autoreset=int(autoreset), obs=bufs.obs.data_ptr(),
@@ -469,7 +475,9 @@ class Engine:
                         alive_out=v["alive"].data_ptr(), alive_pre_out=v["alive_pre"].data_ptr(),
                         ttc_min_out=v["ttc_min"].data_ptr(),
                         terms_out=v["terms"].data_ptr() if terms else None,
-                        snapshot_out=v["snapshot"].data_ptr() if snapshot else None)
+                        snapshot_out=v["snapshot"].data_ptr() if snapshot else None,
+                        next_actions=next_actions.data_ptr() if next_actions is not None else None,
+                        policy_gain=float(steer_gain), policy_throttle=float(throttle))
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), self._stream()), "dg_step")
         self._step_count += 1
         self.launches += 1

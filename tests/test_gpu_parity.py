@@ -158,6 +158,30 @@ def test_device_lane_follower_equals_host_policy(device):
 
 
 @pytest.mark.parametrize("mode", [0, 1])
+def test_fused_policy_equals_policy_kernel_and_host(mode, device):
+    """The LaneFollower fused into the step (next_actions) reproduces both the
+    stand-alone device policy kernel and the numpy policy bit for bit."""
+    inp = C.build_inputs(cfg_of(16, 16, seed=9))
+    a = Engine(**inp.as_kwargs(), device=device, launch_mode=mode)
+    b = Engine(**inp.as_kwargs(), device=device, launch_mode=mode)
+    pol = LaneFollower(obs_config=a.obs_config)
+    acts = [torch.empty((16, 16, 3), dtype=torch.float64, device=device) for _ in range(2)]
+    obs_a = a.observe(as_numpy=False, next_actions=acts[0])
+    obs_b = b.observe(as_numpy=False)
+    assert torch.equal(obs_a, obs_b)
+    ba, bb = a.new_step_buffers(), b.new_step_buffers()
+    for t in range(40):
+        cur, nxt = acts[t % 2], acts[(t + 1) % 2]
+        ref = b.lane_follower(obs_b)
+        assert torch.equal(cur, ref)
+        assert np.array_equal(cur.cpu().numpy(), pol(obs_b.cpu().numpy()))
+        a.launch_step(cur, ba, autoreset=True, next_actions=nxt)
+        b.launch_step(ref, bb, autoreset=True)
+        assert torch.equal(ba.obs, bb.obs)
+        obs_b = bb.obs.clone()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
 def test_fused_autoreset_equals_step_then_teleport(mode, device):
     inp = C.build_inputs(cfg_of(8, 16, seed=31))
     a = Engine(**inp.as_kwargs(), device=device, launch_mode=mode)
