@@ -72,29 +72,10 @@ def root_config(total_worlds, M=16):
 
 
 def shard_inputs(cfg, rank, world_size):
-    """Global host tables (Philox streams over all worlds), sliced to this
-    rank's contiguous world range -- bit-identical to the 1-GPU run."""
+    """Global host tables, sliced to this rank's contiguous world range."""
     from paper_2605_08528_b200 import config as C
-    from paper_2605_08528_b200.params import SimConfig
-    from paper_2605_08528_b200.scenes import WorldBatch
-
-    inp = C.build_inputs(cfg)
-    W = cfg.env.num_envs
-    lo, hi = rank * W // world_size, (rank + 1) * W // world_size
-    if world_size == 1:
-        return inp
-    w = inp.worlds
-    sl = slice(lo, hi)
-    inp.worlds = WorldBatch(w.midpoints[sl], w.directions[sl], w.type_codes[sl], w.half_lengths[sl],
-                            w.half_widths[sl], w.mask[sl], w.grid_offsets[sl], w.scenario_ids[sl],
-                            scene_index=w.scene_index[sl], scene_tables=w.scene_tables)
-    inp.assignment = inp.assignment[sl]
-    inp.frictions = inp.frictions[sl]
-    s = inp.sim
-    inp.sim = SimConfig(num_envs=hi - lo, num_agents=s.num_agents, dynamics_mode=s.dynamics_mode,
-                        episode_len=s.episode_len, seed=s.seed, invincible=s.invincible,
-                        bbox_half=s.bbox_half, goal_radius=s.goal_radius)
-    return inp
+    from paper_2605_08528_b200.sharding import shard_inputs as _shard
+    return _shard(C.build_inputs(cfg), rank, world_size)
 
 
 class ClockSampler:
@@ -272,12 +253,17 @@ def main():
     eng.observe(out=obs_ring[ring - 1], as_numpy=False, next_actions=acts[0])
     stream = torch.cuda.current_stream(dev)
 
-    def one_step(i):
-        eng.launch_step(acts[i % 2], bufs[i % ring], autoreset=True, next_actions=acts[(i + 1) % 2])
+    # per-world episode counters on the device: goal/collision/crash/lane_forbidden
+    # events and alive agent-ticks (the CASPS numerator, counted before each tick)
+    counters = torch.zeros((W, 5), dtype=torch.int32, device=dev)
+
+    def one_step(i, count=True):
+        eng.launch_step(acts[i % 2], bufs[i % ring], autoreset=True, next_actions=acts[(i + 1) % 2],
+                        event_counts=counters if count else None)
 
     # warm-up (untimed)
     for i in range(args.warmup):
-        one_step(i)
+        one_step(i, count=False)
     torch.cuda.synchronize()
     valid_count = int(eng.valid.sum())
     assert int(eng.alive.sum()) == valid_count
@@ -323,7 +309,7 @@ def main():
         g_step = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_step):
             for i in range(args.steps):
-                one_step(args.warmup + args.steps + i)
+                one_step(args.warmup + args.steps + i, count=False)
         torch.cuda.synchronize()
         k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         k0.record(stream)
@@ -334,15 +320,12 @@ def main():
     else:
         kern_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
         kern_avg = sum(kern_ms) / len(kern_ms)
-    assert int(eng.alive.sum()) == valid_count, "autoreset must keep every valid slot alive"
-    agent_ticks = valid_count * args.steps * world_size  # alive before every step (asserted)
+    from paper_2605_08528_b200.sharding import allgather_summaries, combine, episode_summary
+    local = episode_summary(counters.cpu().numpy(), valid_count)
+    # episode statistics: the only cross-rank traffic (one NCCL all-gather)
+    totals = combine(allgather_summaries(local) if world_size > 1 else [local])
+    agent_ticks = totals["alive_ticks"]          # alive agents before each timed tick, device-counted
     value = agent_ticks / (total_ms / 1e3)
-
-    # episode statistics: the only cross-rank traffic (NCCL all-gather, once)
-    stats = torch.tensor([valid_count, args.steps], dtype=torch.float64, device=dev)
-    if world_size > 1:
-        gathered = [torch.empty_like(stats) for _ in range(world_size)]
-        dist.all_gather(gathered, stats)
 
     if rank == 0:
         peak, peak_src = measured_peaks()
@@ -365,6 +348,7 @@ def main():
                          "bytes_per_agent_step": per_agent, "kernel_ms": kern_avg,
                          "peak_source": peak_src},
             "gpu_launches": int(round(launches_per_step * args.steps)),
+            "episode_counters": totals,
         }
         line["clocks"] = clk.summary()
         # e2e through the numpy API

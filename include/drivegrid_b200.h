@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 3
+#define DG_ABI_VERSION 4
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -133,6 +133,9 @@ typedef struct DgStepIO {
     double* next_actions;       /* [W][M][3]   fused LaneFollower on this tick's
                                    observation (policies.py:21-43), or NULL  */
     double policy_gain, policy_throttle;
+    uint32_t* event_counts;     /* [W][5]      += per-world counts of this tick's goal,
+                                   collision, crash, lane_forbidden events and of
+                                   alive agents (CASPS numerator), or NULL     */
 } DgStepIO;
 
 typedef struct dg_engine dg_engine;

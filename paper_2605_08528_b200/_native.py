@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 
 class DgDims(ct.Structure):
@@ -68,7 +68,8 @@ class DgStepIO(ct.Structure):
     _fields_ = [("actions", _P), ("actions_f64", ct.c_int32), ("autoreset", ct.c_int32)] + [
         (n, _P) for n in ("obs", "rewards", "dones", "events", "reason_out", "alive_out",
                           "alive_pre_out", "ttc_min_out", "terms_out", "snapshot_out",
-                          "next_actions")] + [("policy_gain", ct.c_double), ("policy_throttle", ct.c_double)]
+                          "next_actions")] + [("policy_gain", ct.c_double), ("policy_throttle", ct.c_double),
+                                              ("event_counts", _P)]
 
 
 # exported symbol -> (restype, argtypes)

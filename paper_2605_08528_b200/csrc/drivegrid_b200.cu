@@ -85,6 +85,7 @@ struct KArgs {
     double* terms_out;
     double* snapshot_out;
     double* next_actions;   // fused LaneFollower output for the next tick (NULL = off)
+    uint32_t* event_counts; // [W][5] episode counters, accumulated (NULL = off)
     double pol_gain, pol_throttle;
     int32_t take_road;   // min(k_road, max_segments) = candidate-list capacity
     int32_t take_veh;    // min(k_vehicles, M)
@@ -432,8 +433,11 @@ struct FinIn {
     int edge_hit, touch, alive, valid, reason, seen, spawn;
 };
 
-__device__ __forceinline__ void finalize_agent(const KArgs& A, int w, int m, const FinIn& F, int step_now,
-                                            double ox, double oy) {
+// Returns the agent's contribution to the episode counters: bits 0..3 the
+// one-hot event of this tick (goal, collision, crash, lane_forbidden), bit 4
+// alive before the tick.
+__device__ __forceinline__ unsigned finalize_agent(const KArgs& A, int w, int m, const FinIn& F, int step_now,
+                                                double ox, double oy) {
             const DgConsts& k = A.k;
             const int WM = A.d.W * A.d.M;
             const int64_t am = int64_t(w) * A.d.M + m;
@@ -543,7 +547,27 @@ __device__ __forceinline__ void finalize_agent(const KArgs& A, int w, int m, con
             A.reason[am] = int8_t(reason);
             A.event_seen[am] = uint8_t(seen_new);
             A.spawn_step[am] = spawn;
+            return (rnow == 0 ? 0u : 1u << (rnow == 1 ? 0 : rnow == 2 ? 1 : rnow == 3 ? 2 : 3)) |
+                   (alive ? 16u : 0u);
         }
+
+// Episode counters [W][5] (goal, collision, crash, lane_forbidden, alive
+// agent-ticks), accumulated over ticks: warp-reduced, one add per counter.
+__device__ __forceinline__ void count_events(const KArgs& A, int w, unsigned bits, unsigned active_mask, bool leader,
+                                             bool atomic) {
+    if (!A.event_counts) return;
+    unsigned c[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) c[i] = __popc(__ballot_sync(active_mask, (bits >> i) & 1u));
+    if (leader) {
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            if (!c[i]) continue;
+            if (atomic) atomicAdd(A.event_counts + 5 * w + i, c[i]);
+            else A.event_counts[5 * w + i] += c[i];
+        }
+    }
+}
 
 // ----------------------------------------------------------------- optional phase timers
 // Built with -DDG_PHASE_TIMERS: every CTA records clock64() at its phase
@@ -1014,7 +1038,8 @@ world_step_kernel(const KArgs A) {
             F.ttc_min = R.ttc_min; F.gap = R.gap;
             F.edge_hit = R.edge_hit; F.touch = R.touch;
             F.alive = S.alive; F.valid = S.valid; F.reason = S.reason; F.seen = S.seen; F.spawn = S.spawn;
-            finalize_agent(A, w, m, F, step_now, ox, oy);
+            const unsigned bits = finalize_agent(A, w, m, F, step_now, ox, oy);
+            count_events(A, w, bits, __activemask(), lane == 0, false);
         }
         if (tid == 0) A.step_count[w] = step_now + 1;
         PHASE_MARK(6);
@@ -1434,7 +1459,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
         F.edge_hit = edge_hit; F.touch = touch;
         F.alive = S.alive; F.valid = A.valid[am]; F.reason = A.reason[am]; F.seen = A.event_seen[am];
         F.spawn = A.spawn_step[am];
-        finalize_agent(A, w, m, F, step_now, ox, oy);
+        const unsigned bits = finalize_agent(A, w, m, F, step_now, ox, oy);
+        count_events(A, w, bits, 1u, true, true);
     }
 }
 
@@ -1722,6 +1748,7 @@ int dg_step(dg_engine* eng, const DgStepIO* io, void* stream) {
     A.terms_out = io->terms_out;
     A.snapshot_out = io->snapshot_out;
     A.next_actions = io->next_actions;
+    A.event_counts = io->event_counts;
     A.pol_gain = io->policy_gain;
     A.pol_throttle = io->policy_throttle;
     eng->launches = 1;

@@ -462,11 +462,14 @@ class Engine:
     # ------------------------------------------------------------------ step
     def launch_step(self, actions: torch.Tensor, bufs: StepBuffers, autoreset: bool = False,
                     snapshot: bool = True, terms: bool = True, next_actions: torch.Tensor | None = None,
-                    steer_gain: float = 2.0, throttle: float = 0.5) -> None:
+                    steer_gain: float = 2.0, throttle: float = 0.5,
+                    event_counts: torch.Tensor | None = None) -> None:
         """Enqueue one fused step on the current stream; no sync, no checks
         beyond the device-side non-finite guard.  Used by the fast paths.
         ``next_actions`` (float64 [W][M][3], distinct from ``actions``) receives
-        the fused LaneFollower's actions on this tick's observation."""
+        the fused LaneFollower's actions on this tick's observation;
+        ``event_counts`` (int32 [W][5]) accumulates per-world goal / collision /
+        crash / lane_forbidden events and alive agent-ticks on the device."""
         v = bufs.views
         io = N.DgStepIO(actions=actions.data_ptr(), actions_f64=int(actions.dtype == torch.float64),
                         autoreset=int(autoreset), obs=bufs.obs.data_ptr(),
@@ -477,7 +480,8 @@ class Engine:
                         terms_out=v["terms"].data_ptr() if terms else None,
                         snapshot_out=v["snapshot"].data_ptr() if snapshot else None,
                         next_actions=next_actions.data_ptr() if next_actions is not None else None,
-                        policy_gain=float(steer_gain), policy_throttle=float(throttle))
+                        policy_gain=float(steer_gain), policy_throttle=float(throttle),
+                        event_counts=event_counts.data_ptr() if event_counts is not None else None)
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), self._stream()), "dg_step")
         self._step_count += 1
         self.launches += 1

@@ -109,6 +109,28 @@ def test_trajectory_parity(name, spatial, warps, mode, device):
     print(f"\n[{name}] max |gpu - oracle|:", {k: f"{v:.2e}" for k, v in sorted(dev.max.items())})
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_event_counters_match_oracle(mode, device):
+    """Device-accumulated per-world counters (events + alive agent-ticks)
+    equal the host tally of the oracle's outputs."""
+    case = case_inputs("traj_events")
+    gpu = Engine(**case.inputs.as_kwargs(), device=device, launch_mode=mode)
+    ora = OracleEngine(**case.inputs.as_kwargs())
+    W = case.inputs.sim.num_envs
+    counts = torch.zeros((W, 5), dtype=torch.int32, device=device)
+    want = np.zeros((W, 5), dtype=np.int64)
+    bufs = gpu.new_step_buffers()
+    for t in range(case.steps):
+        a = case.actions[t].astype(np.float64)
+        o = ora.step(a)
+        for i, k in enumerate(EVENT_TYPES):
+            want[:, i] += o.events[k].sum(axis=1)
+        want[:, 4] += o.info["alive_pre"].sum(axis=1)
+        gpu.launch_step(torch.from_numpy(a).to(device), bufs, event_counts=counts)
+    assert np.array_equal(counts.cpu().numpy(), want)
+    assert want[:, :4].sum() > 0
+
+
 def test_default_256x16_lane_follower_parity(device):
     """The headline shape (256 worlds x 16 agents, default pool, seed 42),
     LaneFollower closed loop, teacher-forced on the oracle's observations."""
