@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 4
+#define DG_ABI_VERSION 5
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -136,6 +136,20 @@ typedef struct DgStepIO {
     uint32_t* event_counts;     /* [W][5]      += per-world counts of this tick's goal,
                                    collision, crash, lane_forbidden events and of
                                    alive agents (CASPS numerator), or NULL     */
+    int32_t ticks;              /* control ticks in this launch (0/1: one step).  A
+                                   T-tick launch equals T dg_step calls: tick t reads
+                                   actions + t*W*M*3 -- or, when next_actions is set,
+                                   the fused LaneFollower's actions of tick t-1 for
+                                   t >= 1 (env.py:48-65 driven by policies.py:21-43) --
+                                   and writes every per-tick output above at slot
+                                   (ring_start + t) % ring_slots (obs + slot*W*M*D,
+                                   rewards + slot*W*M, events + slot*W*M*4, ...).
+                                   A rejected tick stops its world after the
+                                   previous tick; error_word gets the flat index
+                                   t*W*M*3 + w*M*3 + j.  Fused mode only.       */
+    int32_t ring_slots;         /* 0: ticks                                    */
+    int32_t ring_start;
+    int32_t pad_;
 } DgStepIO;
 
 typedef struct dg_engine dg_engine;

@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 class DgDims(ct.Structure):
@@ -69,7 +69,9 @@ class DgStepIO(ct.Structure):
         (n, _P) for n in ("obs", "rewards", "dones", "events", "reason_out", "alive_out",
                           "alive_pre_out", "ttc_min_out", "terms_out", "snapshot_out",
                           "next_actions")] + [("policy_gain", ct.c_double), ("policy_throttle", ct.c_double),
-                                              ("event_counts", _P)]
+                                              ("event_counts", _P),
+                                              ("ticks", ct.c_int32), ("ring_slots", ct.c_int32),
+                                              ("ring_start", ct.c_int32), ("pad_", ct.c_int32)]
 
 
 # exported symbol -> (restype, argtypes)

@@ -86,6 +86,9 @@ struct KArgs {
     double* snapshot_out;
     double* next_actions;   // fused LaneFollower output for the next tick (NULL = off)
     uint32_t* event_counts; // [W][5] episode counters, accumulated (NULL = off)
+    int32_t ticks;          // control ticks per launch (persistent rollout; 1 = one step)
+    int32_t ring_slots;     // obs ring: tick t writes slot (ring_start + t) % ring_slots
+    int32_t ring_start;
     double pol_gain, pol_throttle;
     int32_t take_road;   // min(k_road, max_segments) = candidate-list capacity
     int32_t take_veh;    // min(k_vehicles, M)
@@ -131,6 +134,11 @@ struct AgentSm {
     double gx, gy, sx, sy;    // goal, start (global)
     float f_len, f_wid, f_spd; // neighbour-row features of this agent: L/100, W/100, speed/10
     int alive, valid, reason, seen, spawn;
+    // persistent rollout: the next tick's state and flags, actions, start heading
+    double st_next[DG_NUM_STATE];
+    double act[3];
+    double start_yaw;
+    int flags_next[4];
 };
 
 struct SceneView {
@@ -392,7 +400,7 @@ struct ScanSm {
 // agent (rewards.py:106-268, engine.py:370-406, 472-509).
 __device__ __forceinline__ void write_ego(float* row, const DgConsts& k, const KArgs& A, int w, int64_t am,
                                           double px, double py, double c, double s, double vx, double vy,
-                                          double gx, double gy) {
+                                          double gx, double gy, double* act_sm = nullptr) {
     const double gdx = gx - px, gdy = gy - py;
     const double xb = c * gdx + s * gdy;
     const double yb = -s * gdx + c * gdy;
@@ -412,10 +420,16 @@ __device__ __forceinline__ void write_ego(float* row, const DgConsts& k, const K
         const double dist = double(f4) * k.bbox_half;
         double steer = np_clip(A.pol_gain * sin_e, -1.0, 1.0);
         if (cos_e < 0.0) steer = sin_e >= 0.0 ? 1.0 : -1.0;
+        const double thr = dist > 5.0 ? A.pol_throttle : A.pol_throttle * 0.5;
         double* act = A.next_actions + 3 * am;
-        act[0] = dist > 5.0 ? A.pol_throttle : A.pol_throttle * 0.5;
+        act[0] = thr;
         act[1] = steer;
         act[2] = 0.0;
+        if (act_sm) {
+            act_sm[0] = thr;
+            act_sm[1] = steer;
+            act_sm[2] = 0.0;
+        }
     }
     row[5] = __double2float_rn(dg::ddiv(vx, k.speed_norm));
     row[6] = __double2float_rn(dg::ddiv(vy, k.speed_norm));
@@ -425,19 +439,51 @@ __device__ __forceinline__ void write_ego(float* row, const DgConsts& k, const K
     }
 }
 
+// Output pointers of one tick (the rollout advances them by one [W][M] plane per tick).
+struct TickOut {
+    double* rewards;
+    uint8_t* dones;
+    uint8_t* events;
+    int8_t* reason_out;
+    uint8_t* alive_out;
+    uint8_t* alive_pre_out;
+    double* ttc_min_out;
+    double* terms_out;
+    double* snapshot_out;
+};
+
+__device__ __forceinline__ TickOut tick_out(const KArgs& A, int t) {
+    const int64_t WM = int64_t(A.d.W) * A.d.M;
+    TickOut o;
+    o.rewards = A.rewards + t * WM;
+    o.dones = A.dones + t * WM;
+    o.events = A.events + t * WM * 4;
+    o.reason_out = A.reason_out ? A.reason_out + t * WM : nullptr;
+    o.alive_out = A.alive_out ? A.alive_out + t * WM : nullptr;
+    o.alive_pre_out = A.alive_pre_out ? A.alive_pre_out + t * WM : nullptr;
+    o.ttc_min_out = A.ttc_min_out ? A.ttc_min_out + t * WM : nullptr;
+    o.terms_out = A.terms_out ? A.terms_out + t * WM * 7 : nullptr;
+    o.snapshot_out = A.snapshot_out ? A.snapshot_out + t * WM * DG_NUM_STATE : nullptr;
+    return o;
+}
+
 struct FinIn {
     const double* st;                  // post-physics state, 12 fields
     double px0, py0, gx, gy, sx, sy;   // pre-physics position, goal, start
     double lane_d2, lane_lat, lane_tx, lane_ty;  // nearest lane (d2 = inf: none)
     double ttc_min, gap;
     int edge_hit, touch, alive, valid, reason, seen, spawn;
+    double start_yaw;
+    bool store_global;                 // write the post-tail state to the engine arrays
+    double* st_out;                    // optional: post-tail state for the next tick (shared memory)
+    int* flags_out;                    // optional: alive, reason, seen, spawn after the tail
 };
 
 // Returns the agent's contribution to the episode counters: bits 0..3 the
 // one-hot event of this tick (goal, collision, crash, lane_forbidden), bit 4
 // alive before the tick.
-__device__ __forceinline__ unsigned finalize_agent(const KArgs& A, int w, int m, const FinIn& F, int step_now,
-                                                double ox, double oy) {
+__device__ __forceinline__ unsigned finalize_agent(const KArgs& A, const TickOut& O, int w, int m, const FinIn& F,
+                                                int step_now, double ox, double oy) {
             const DgConsts& k = A.k;
             const int WM = A.d.W * A.d.M;
             const int64_t am = int64_t(w) * A.d.M + m;
@@ -502,23 +548,23 @@ __device__ __forceinline__ unsigned finalize_agent(const KArgs& A, int w, int m,
             const bool park = done && !timeout;
             int alive_new = alive && !finished;
 
-            A.rewards[am] = reward;
-            A.dones[am] = finished;
-            reinterpret_cast<uint32_t*>(A.events)[am] =
+            O.rewards[am] = reward;
+            O.dones[am] = finished;
+            reinterpret_cast<uint32_t*>(O.events)[am] =
                 uint32_t(rnow == 1) | (uint32_t(rnow == 2) << 8) | (uint32_t(rnow == 3) << 16) |
                 (uint32_t(rnow == 4) << 24);
-            if (A.reason_out) A.reason_out[am] = int8_t(reason);
-            if (A.alive_out) A.alive_out[am] = uint8_t(alive_new);
-            if (A.alive_pre_out) A.alive_pre_out[am] = uint8_t(alive);
-            if (A.ttc_min_out) A.ttc_min_out[am] = F.ttc_min;
-            if (A.terms_out) {
+            if (O.reason_out) O.reason_out[am] = int8_t(reason);
+            if (O.alive_out) O.alive_out[am] = uint8_t(alive_new);
+            if (O.alive_pre_out) O.alive_pre_out[am] = uint8_t(alive);
+            if (O.ttc_min_out) O.ttc_min_out[am] = F.ttc_min;
+            if (O.terms_out) {
                 const double t7[7] = {progress, lane_t, offroad, idle, ttc_v, ttc_e, total};
 #pragma unroll
-                for (int i = 0; i < 7; ++i) A.terms_out[int64_t(i) * WM + am] = alive ? t7[i] : 0.0;
+                for (int i = 0; i < 7; ++i) O.terms_out[int64_t(i) * WM + am] = alive ? t7[i] : 0.0;
             }
-            if (A.snapshot_out) {
+            if (O.snapshot_out) {
 #pragma unroll
-                for (int f = 0; f < DG_NUM_STATE; ++f) A.snapshot_out[int64_t(f) * WM + am] = F.st[f];
+                for (int f = 0; f < DG_NUM_STATE; ++f) O.snapshot_out[int64_t(f) * WM + am] = F.st[f];
             }
             double x[DG_NUM_STATE];
 #pragma unroll
@@ -535,18 +581,28 @@ __device__ __forceinline__ unsigned finalize_agent(const KArgs& A, int w, int m,
                 for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
                 x[SX] = F.sx;
                 x[SY] = F.sy;
-                x[SYAW] = A.start_yaw[am];
+                x[SYAW] = F.start_yaw;
                 alive_new = 1;
                 reason = 0;
                 spawn = step_new;
                 seen_new = 0;
             }
+            if (F.store_global) {
 #pragma unroll
-            for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = x[f];
-            A.alive[am] = uint8_t(alive_new);
-            A.reason[am] = int8_t(reason);
-            A.event_seen[am] = uint8_t(seen_new);
-            A.spawn_step[am] = spawn;
+                for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = x[f];
+                A.alive[am] = uint8_t(alive_new);
+                A.reason[am] = int8_t(reason);
+                A.event_seen[am] = uint8_t(seen_new);
+                A.spawn_step[am] = spawn;
+            }
+            if (F.st_out) {
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) F.st_out[f] = x[f];
+                F.flags_out[0] = alive_new;
+                F.flags_out[1] = reason;
+                F.flags_out[2] = seen_new;
+                F.flags_out[3] = spawn;
+            }
             return (rnow == 0 ? 0u : 1u << (rnow == 1 ? 0 : rnow == 2 ? 1 : rnow == 3 ? 2 : 3)) |
                    (alive ? 16u : 0u);
         }
@@ -615,8 +671,17 @@ world_step_kernel(const KArgs A) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     __shared__ int s_bad;
+    const int T = kStep ? (A.ticks > 0 ? A.ticks : 1) : 1;
+    const int64_t act_tick = int64_t(WM) * 3;      // actions of tick t at A.actions + t * act_tick
+    const bool feedback = kStep && T > 1 && A.next_actions != nullptr;   // fused policy drives ticks >= 1
 
-    // ---- phase 0: action scan (the reference rejects before mutating)
+    // ---- geometry: one bulk async copy of the world's scene blob (TMA engine),
+    //      once per launch; with ticks > 1 it serves the whole rollout
+    const int scene = A.scene_of_world[w];
+    const int64_t* meta = A.scene_meta + 8 * scene;
+    const double ox = A.grid_offset[2 * w], oy = A.grid_offset[2 * w + 1];
+
+    // ---- tick-0 action scan (the reference rejects before mutating anything)
     GT_MARK(32);
     PHASE_MARK(0);
     int step_now = 0;
@@ -636,240 +701,372 @@ world_step_kernel(const KArgs A) {
         }
         step_now = A.step_count[w];
     }
-
-    // ---- geometry: one bulk async copy of the world's scene blob (TMA engine)
-    const int scene = A.scene_of_world[w];
-    const int64_t* meta = A.scene_meta + 8 * scene;
     if (tid == 0) {
         mbar_init(bar, 1);
         bulk_load(geo, A.scene_blob + meta[0], uint32_t(meta[1]), bar);
     }
-    const double ox = A.grid_offset[2 * w], oy = A.grid_offset[2 * w + 1];
-    float* obs_w = A.obs + int64_t(w) * M * D;
 
-    PHASE_MARK(1);
-    // ---- phase 1: warp 0, lane m: agent m load + physics (SIMT across agents);
-    //      every warp streams the zero background of its agents' obs rows
+    // ---- per-agent tables and the initial state -> shared memory (once)
     if (warp == 0 && lane < M) {
         const int m = lane;
         const int64_t am = int64_t(w) * M + m;
         AgentSm& S = ag[m];
-        double x[DG_NUM_STATE];
 #pragma unroll
-        for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = A.state[int64_t(f) * WM + am];
-        const int alive = A.alive[am];
-        S.px0 = x[SX];
-        S.py0 = x[SY];
-        if (alive && x[SX] != -12345.678) LANE0_MARK(25);  // after the state loads landed
-        if (kStep && alive) {
-            const int64_t ab = am * 3;
-            double raw0, raw1, raw2;
-            if (A.actions_f64) {
-                const double* a = reinterpret_cast<const double*>(A.actions);
-                raw0 = a[ab]; raw1 = a[ab + 1]; raw2 = a[ab + 2];
-            } else {
-                const float* a = reinterpret_cast<const float*>(A.actions);
-                raw0 = a[ab]; raw1 = a[ab + 1]; raw2 = a[ab + 2];
-            }
-            Act act;
-            act.thr = np_clip(raw0, 0.0, 1.0);
-            act.steer = np_clip(raw1, -1.0, 1.0);
-            act.brk = np_clip(raw2, 0.0, 1.0);
-            if (A.d.dynamic) {
-                const double cap = A.mu_eff[w] * k.f_z;
-                for (int i = 0; i < A.d.decimation; ++i) {
-                    substep_dynamic(x, act, cap, k);
-#ifdef DG_PHASE_TIMERS
-                    if (i < 4 && x[SX] != -12345.678) LANE0_MARK(28 + i);
-#endif
-                }
-            } else {
-                step_bicycle(x, act, k);
-            }
-        }
-        if (x[SX] != -12345.678) LANE0_MARK(26);          // after the substeps
-#pragma unroll
-        for (int f = 0; f < DG_NUM_STATE; ++f) S.st[f] = x[f];
-        double s_, c_;
-        sincos(x[SYAW], &s_, &c_);
-        S.c = c_;
-        S.s = s_;
-        S.vwx = x[SVX] * c_ - x[SVY] * s_;
-        S.vwy = x[SVX] * s_ + x[SVY] * c_;
+        for (int f = 0; f < DG_NUM_STATE; ++f) S.st_next[f] = A.state[int64_t(f) * WM + am];
+        S.flags_next[0] = A.alive[am];
+        S.flags_next[1] = A.reason[am];
+        S.flags_next[2] = A.event_seen[am];
+        S.flags_next[3] = A.spawn_step[am];
         S.r = A.r_hull[am];
         S.d = A.d_hull[am];
         S.len = A.length[am];
         S.wid = A.width[am];
         S.f_len = __double2float_rn(dg::ddiv(S.len, k.bbox_half));
         S.f_wid = __double2float_rn(dg::ddiv(S.wid, k.bbox_half));
-        S.f_spd = __double2float_rn(dg::ddiv(dg::dsqrt(x[SVX] * x[SVX] + x[SVY] * x[SVY]), k.speed_norm));
-        const double offs[3] = {-1.0, 0.0, 1.0};
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const double o = offs[i] * S.d;
-            S.hx[i] = x[SX] + o * c_;
-            S.hy[i] = x[SY] + o * s_;
-        }
         S.gx = A.goal_xy[2 * am];
         S.gy = A.goal_xy[2 * am + 1];
         S.sx = A.start_xy[2 * am];
         S.sy = A.start_xy[2 * am + 1];
-        S.alive = alive;
+        S.start_yaw = A.start_yaw[am];
         S.valid = A.valid[am];
-        S.reason = A.reason[am];
-        S.seen = A.event_seen[am];
-        S.spawn = A.spawn_step[am];
-        LANE0_MARK(27);
     }
-    // the zero background of the world's obs block: TMA bulk stores from a
-    // zeroed shared buffer, issued by one thread of a warp that is idle
-    // during the physics; unaligned head/tail floats by plain stores
-    if (warp == (nwarps > 1 ? 1 : 0)) {
-        const uintptr_t b0 = reinterpret_cast<uintptr_t>(obs_w);
-        const uintptr_t b1 = b0 + uintptr_t(M) * D * 4;
-        const uintptr_t a0 = (b0 + 15) & ~uintptr_t(15), a1 = b1 & ~uintptr_t(15);
-        if (a0 < a1) {
-            for (uintptr_t p = b0 + 4 * lane; p < a0; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
-            for (uintptr_t p = a1 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
-            if (lane == 0) {
-                for (uintptr_t p = a0; p < a1; p += kZeroChunk) {
-                    const uintptr_t n = a1 - p < uintptr_t(kZeroChunk) ? a1 - p : uintptr_t(kZeroChunk);
-                    bulk_store(reinterpret_cast<void*>(p), zero_sm, uint32_t(n));
+    SceneView G;
+    for (int t = 0; t < T; ++t) {
+        const int slot = A.ring_slots > 0 ? (A.ring_start + t) % A.ring_slots : t;
+        float* obs_w = A.obs + (int64_t(slot) * WM + int64_t(w) * M) * D;
+        const TickOut O = tick_out(A, slot);
+        if (kStep && t > 0) {
+            // every tick gets the same rejection as a separate step call
+            if (tid == 0) s_bad = DG_NO_ERROR;
+            __syncthreads();
+            if (tid < 3 * M) {
+                const int64_t flat = t * act_tick + int64_t(w) * M * 3 + tid;
+                const double v = feedback ? ag[tid / 3].act[tid % 3]
+                               : A.actions_f64 ? reinterpret_cast<const double*>(A.actions)[flat]
+                                               : double(reinterpret_cast<const float*>(A.actions)[flat]);
+                if (!finite(v)) atomicMin(&s_bad, int(flat));
+            }
+            __syncthreads();
+            if (s_bad != DG_NO_ERROR) {
+                // ticks 0..t-1 stand (as t separate step calls would leave them)
+                if (warp == 0 && lane < M) {
+                    const int64_t am = int64_t(w) * M + lane;
+                    const AgentSm& S = ag[lane];
+#pragma unroll
+                    for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = S.st_next[f];
+                    A.alive[am] = uint8_t(S.flags_next[0]);
+                    A.reason[am] = int8_t(S.flags_next[1]);
+                    A.event_seen[am] = uint8_t(S.flags_next[2]);
+                    A.spawn_step[am] = S.flags_next[3];
                 }
-                bulk_commit_and_wait();
+                if (tid == 0) {
+                    atomicMin(A.error_word, s_bad);
+                    A.step_count[w] = step_now + t;
+                }
+                return;
             }
-        } else {
-            for (uintptr_t p = b0 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
         }
-    }
 
-    if (warp == 0) PHASE_MARK(2);
-    __syncthreads();  // agent table + zero rows done, mbarrier init visible
-    PHASE_MARK(3);
-    mbar_wait(bar, 0);
-    // the view reads the index header from the copied blob: only after the wait
-    const SceneView G = scene_view(geo, A.scene_blob + meta[5], int(meta[2]), int(meta[3]), int(meta[4]));
-    {   // scene-local midpoints -> global, exactly midpoints + grid offset
-        for (int i = tid; i < G.P; i += blockDim.x) {
-            double2 m2 = G.mid[i];
-            m2.x = m2.x + ox;
-            m2.y = m2.y + oy;
-            G.mid[i] = m2;
-        }
-        for (int i = tid; i < G.KL; i += blockDim.x) {
-            double4 l4 = G.lane_seg[i];
-            l4.x = l4.x + ox;
-            l4.y = l4.y + oy;
-            G.lane_seg[i] = l4;
-        }
-        for (int i = tid; i < G.KE; i += blockDim.x) {
-            double2 e2 = G.edge_mid[i];
-            e2.x = e2.x + ox;
-            e2.y = e2.y + oy;
-            G.edge_mid[i] = e2;
-        }
-    }
-    __syncthreads();
-
-    PHASE_MARK(4);
-    // ---- phase 2a: agent pairs, 16 lanes per ego agent (lane j <-> other agent j):
-    //      stable distance rank, swept-circle TTC, neighbour rows, hull contact
-    const int road0 = A.d.ego_dim;
-    const int veh0 = A.d.ego_dim + 5 * A.d.k_road;
-    {
-        const int half_id = lane >> 4;          // two ego agents per warp
-        const int j = lane & 15;
-        const unsigned gmask = half_id ? 0xffff0000u : 0x0000ffffu;
-        for (int i = 2 * warp + half_id; i - half_id < M; i += 2 * nwarps) {
-            const bool ego_ok = i < M;
-            const int ii = ego_ok ? i : 0;
-            const AgentSm& S = ag[ii];
-            const double px = S.st[SX], py = S.st[SY], c = S.c, s = S.s;
-            double key = INFINITY, ndx = 0.0, ndy = 0.0;
-            if (ego_ok && j < M) {
-                const AgentSm& N = ag[j];
-                ndx = N.st[SX] - px;
-                ndy = N.st[SY] - py;
-                const double dist = dg::dsqrt(ndx * ndx + ndy * ndy);
-                key = (N.alive && j != ii) ? dist : INFINITY;
-            }
-            int rank = 0;
-            for (int t = 0; t < M; ++t) {
-                const double kt = __shfl_sync(kFull, key, t, 16);
-                rank += (kt < key) || (kt == key && t < j);
-            }
-            const bool nvalid = ego_ok && j < M && finite(key) && rank < A.take_veh;
-            double ttc = k.ttc_max;
-            if (nvalid) {
-                const AgentSm& N = ag[j];
-                ttc = swept_ttc(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c, N.s, N.d,
-                                S.r + N.r, k.ttc_max);
-                double st_, ct_;
-                sincos(N.st[SYAW] - S.st[SYAW], &st_, &ct_);
-                const double wrap = atan2(st_, ct_);
-                float* o = obs_w + int64_t(ii) * D + veh0 + 7 * rank;
-                o[0] = __double2float_rn(dg::ddiv(c * ndx + s * ndy, k.bbox_half));
-                o[1] = __double2float_rn(dg::ddiv(-s * ndx + c * ndy, k.bbox_half));
-                o[2] = N.f_len;
-                o[3] = N.f_wid;
-                o[4] = __double2float_rn(dg::ddiv(wrap, 3.141592653589793));
-                o[5] = N.f_spd;
-                o[6] = __double2float_rn(dg::ddiv(ttc, k.ttc_max));
-            }
-            ttc = warp_min(ttc, 16);
-            bool touch = false;
-            // hull contact; centres sit within d of the position, so a pair
-            // farther apart than r_a + r_b + d_a + d_b (+1e-4 m) cannot touch
-            if (kStep && ego_ok && j < M && j != ii && S.alive && ag[j].alive &&
-                key <= S.r + ag[j].r + S.d + ag[j].d + 1e-4) {
-                const AgentSm& N = ag[j];
-                const double rs = S.r + N.r;
-                const double rs2 = rs * rs;
+        PHASE_MARK(1);
+        // ---- phase 1: warp 0, lane m: agent m physics (SIMT across agents)
+        if (warp == 0 && lane < M) {
+            const int m = lane;
+            const int64_t am = int64_t(w) * M + m;
+            AgentSm& S = ag[m];
+            double x[DG_NUM_STATE];
 #pragma unroll
-                for (int a = 0; a < 3; ++a)
-#pragma unroll
-                    for (int b = 0; b < 3; ++b) {
-                        const double ex = S.hx[a] - N.hx[b], ey = S.hy[a] - N.hy[b];
-                        touch |= ex * ex + ey * ey < rs2;
+            for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = S.st_next[f];
+            const int alive = S.flags_next[0];
+            S.reason = S.flags_next[1];
+            S.seen = S.flags_next[2];
+            S.spawn = S.flags_next[3];
+            S.px0 = x[SX];
+            S.py0 = x[SY];
+            if (alive && x[SX] != -12345.678) LANE0_MARK(25);  // after the state loads landed
+            if (kStep && alive) {
+                double raw0, raw1, raw2;
+                if (t > 0 && feedback) {
+                    raw0 = S.act[0]; raw1 = S.act[1]; raw2 = S.act[2];
+                } else {
+                    const int64_t ab = t * act_tick + am * 3;
+                    if (A.actions_f64) {
+                        const double* a = reinterpret_cast<const double*>(A.actions);
+                        raw0 = a[ab]; raw1 = a[ab + 1]; raw2 = a[ab + 2];
+                    } else {
+                        const float* a = reinterpret_cast<const float*>(A.actions);
+                        raw0 = a[ab]; raw1 = a[ab + 1]; raw2 = a[ab + 2];
                     }
+                }
+                Act act;
+                act.thr = np_clip(raw0, 0.0, 1.0);
+                act.steer = np_clip(raw1, -1.0, 1.0);
+                act.brk = np_clip(raw2, 0.0, 1.0);
+                if (A.d.dynamic) {
+                    const double cap = A.mu_eff[w] * k.f_z;
+                    for (int i = 0; i < A.d.decimation; ++i) {
+                        substep_dynamic(x, act, cap, k);
+#ifdef DG_PHASE_TIMERS
+                        if (i < 4 && x[SX] != -12345.678) LANE0_MARK(28 + i);
+#endif
+                    }
+                } else {
+                    step_bicycle(x, act, k);
+                }
             }
-            touch = (__ballot_sync(kFull, touch) & gmask) != 0;
-            if (ego_ok && j == 0) {
-                sc[ii].ttc_min = ttc;
-                sc[ii].touch = touch;
-                if (!kStep && A.ttc_min_out) A.ttc_min_out[int64_t(w) * M + ii] = ttc;
+            if (x[SX] != -12345.678) LANE0_MARK(26);          // after the substeps
+#pragma unroll
+            for (int f = 0; f < DG_NUM_STATE; ++f) S.st[f] = x[f];
+            double s_, c_;
+            sincos(x[SYAW], &s_, &c_);
+            S.c = c_;
+            S.s = s_;
+            S.vwx = x[SVX] * c_ - x[SVY] * s_;
+            S.vwy = x[SVX] * s_ + x[SVY] * c_;
+            S.f_spd = __double2float_rn(dg::ddiv(dg::dsqrt(x[SVX] * x[SVX] + x[SVY] * x[SVY]), k.speed_norm));
+            const double offs[3] = {-1.0, 0.0, 1.0};
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const double o = offs[i] * S.d;
+                S.hx[i] = x[SX] + o * c_;
+                S.hy[i] = x[SY] + o * s_;
+            }
+            S.alive = alive;
+            LANE0_MARK(27);
+        }
+        // the zero background of the world's obs block: TMA bulk stores from a
+        // zeroed shared buffer, issued by one thread of a warp that is idle
+        // during the physics; unaligned head/tail floats by plain stores
+        if (warp == (nwarps > 1 ? 1 : 0)) {
+            const uintptr_t b0 = reinterpret_cast<uintptr_t>(obs_w);
+            const uintptr_t b1 = b0 + uintptr_t(M) * D * 4;
+            const uintptr_t a0 = (b0 + 15) & ~uintptr_t(15), a1 = b1 & ~uintptr_t(15);
+            if (a0 < a1) {
+                for (uintptr_t p = b0 + 4 * lane; p < a0; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
+                for (uintptr_t p = a1 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
+                if (lane == 0) {
+                    for (uintptr_t p = a0; p < a1; p += kZeroChunk) {
+                        const uintptr_t n = a1 - p < uintptr_t(kZeroChunk) ? a1 - p : uintptr_t(kZeroChunk);
+                        bulk_store(reinterpret_cast<void*>(p), zero_sm, uint32_t(n));
+                    }
+                    bulk_commit_and_wait();
+                }
+            } else {
+                for (uintptr_t p = b0 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
             }
         }
-    }
 
-    W1_MARK(34);
-    // ---- phase 2b: warp m scans the scene for agent m
-    for (int m = warp; m < M; m += nwarps) {
-        const AgentSm& S = ag[m];
-        float* row = obs_w + int64_t(m) * D;
-        const double px = S.st[SX], py = S.st[SY];
-        const double c = S.c, s = S.s;
-        const bool rewards_needed = kStep && S.alive;   // dead agents: rewards/events masked
-        const double r2 = S.r * S.r;
-        bool edge_hit = false;
+        if (warp == 0) PHASE_MARK(2);
+        __syncthreads();  // agent table + zero rows done, mbarrier init visible
+        PHASE_MARK(3);
+        if (t == 0) {
+            mbar_wait(bar, 0);
+            // the view reads the index header from the copied blob: only after the wait
+            G = scene_view(geo, A.scene_blob + meta[5], int(meta[2]), int(meta[3]), int(meta[4]));
+            // scene-local midpoints -> global, exactly midpoints + grid offset
+            for (int i = tid; i < G.P; i += blockDim.x) {
+                double2 m2 = G.mid[i];
+                m2.x = m2.x + ox;
+                m2.y = m2.y + oy;
+                G.mid[i] = m2;
+            }
+            for (int i = tid; i < G.KL; i += blockDim.x) {
+                double4 l4 = G.lane_seg[i];
+                l4.x = l4.x + ox;
+                l4.y = l4.y + oy;
+                G.lane_seg[i] = l4;
+            }
+            for (int i = tid; i < G.KE; i += blockDim.x) {
+                double2 e2 = G.edge_mid[i];
+                e2.x = e2.x + ox;
+                e2.y = e2.y + oy;
+                G.edge_mid[i] = e2;
+            }
+            __syncthreads();
+        }
 
-        // (a) road context: exact d2 <= r^2 over the candidate superset, ordered
-        //     compaction into shared memory; edge boxes tested on the same pass
-        uint16_t* cand = cand_sm + m * A.take_road;
-        int count = 0;
-        auto visit = [&](int q, bool in, bool edge_q) {
-            bool hit = false;
-            if (in) {
-                const double2 m2 = G.mid[q];
+        PHASE_MARK(4);
+        // ---- phase 2a: agent pairs, 16 lanes per ego agent (lane j <-> other agent j):
+        //      stable distance rank, swept-circle TTC, neighbour rows, hull contact
+        const int road0 = A.d.ego_dim;
+        const int veh0 = A.d.ego_dim + 5 * A.d.k_road;
+        {
+            const int half_id = lane >> 4;          // two ego agents per warp
+            const int j = lane & 15;
+            const unsigned gmask = half_id ? 0xffff0000u : 0x0000ffffu;
+            for (int i = 2 * warp + half_id; i - half_id < M; i += 2 * nwarps) {
+                const bool ego_ok = i < M;
+                const int ii = ego_ok ? i : 0;
+                const AgentSm& S = ag[ii];
+                const double px = S.st[SX], py = S.st[SY], c = S.c, s = S.s;
+                double key = INFINITY, ndx = 0.0, ndy = 0.0;
+                if (ego_ok && j < M) {
+                    const AgentSm& N = ag[j];
+                    ndx = N.st[SX] - px;
+                    ndy = N.st[SY] - py;
+                    const double dist = dg::dsqrt(ndx * ndx + ndy * ndy);
+                    key = (N.alive && j != ii) ? dist : INFINITY;
+                }
+                int rank = 0;
+                for (int t = 0; t < M; ++t) {
+                    const double kt = __shfl_sync(kFull, key, t, 16);
+                    rank += (kt < key) || (kt == key && t < j);
+                }
+                const bool nvalid = ego_ok && j < M && finite(key) && rank < A.take_veh;
+                double ttc = k.ttc_max;
+                if (nvalid) {
+                    const AgentSm& N = ag[j];
+                    ttc = swept_ttc(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c, N.s, N.d,
+                                    S.r + N.r, k.ttc_max);
+                    double st_, ct_;
+                    sincos(N.st[SYAW] - S.st[SYAW], &st_, &ct_);
+                    const double wrap = atan2(st_, ct_);
+                    float* o = obs_w + int64_t(ii) * D + veh0 + 7 * rank;
+                    o[0] = __double2float_rn(dg::ddiv(c * ndx + s * ndy, k.bbox_half));
+                    o[1] = __double2float_rn(dg::ddiv(-s * ndx + c * ndy, k.bbox_half));
+                    o[2] = N.f_len;
+                    o[3] = N.f_wid;
+                    o[4] = __double2float_rn(dg::ddiv(wrap, 3.141592653589793));
+                    o[5] = N.f_spd;
+                    o[6] = __double2float_rn(dg::ddiv(ttc, k.ttc_max));
+                }
+                ttc = warp_min(ttc, 16);
+                bool touch = false;
+                // hull contact; centres sit within d of the position, so a pair
+                // farther apart than r_a + r_b + d_a + d_b (+1e-4 m) cannot touch
+                if (kStep && ego_ok && j < M && j != ii && S.alive && ag[j].alive &&
+                    key <= S.r + ag[j].r + S.d + ag[j].d + 1e-4) {
+                    const AgentSm& N = ag[j];
+                    const double rs = S.r + N.r;
+                    const double rs2 = rs * rs;
+    #pragma unroll
+                    for (int a = 0; a < 3; ++a)
+    #pragma unroll
+                        for (int b = 0; b < 3; ++b) {
+                            const double ex = S.hx[a] - N.hx[b], ey = S.hy[a] - N.hy[b];
+                            touch |= ex * ex + ey * ey < rs2;
+                        }
+                }
+                touch = (__ballot_sync(kFull, touch) & gmask) != 0;
+                if (ego_ok && j == 0) {
+                    sc[ii].ttc_min = ttc;
+                    sc[ii].touch = touch;
+                    if (!kStep && A.ttc_min_out) A.ttc_min_out[int64_t(w) * M + ii] = ttc;
+                }
+            }
+        }
+
+        W1_MARK(34);
+        // ---- phase 2b: warp m scans the scene for agent m
+        for (int m = warp; m < M; m += nwarps) {
+            const AgentSm& S = ag[m];
+            float* row = obs_w + int64_t(m) * D;
+            const double px = S.st[SX], py = S.st[SY];
+            const double c = S.c, s = S.s;
+            const bool rewards_needed = kStep && S.alive;   // dead agents: rewards/events masked
+            const double r2 = S.r * S.r;
+            bool edge_hit = false;
+
+            // (a) road context: exact d2 <= r^2 over the candidate superset, ordered
+            //     compaction into shared memory; edge boxes tested on the same pass
+            uint16_t* cand = cand_sm + m * A.take_road;
+            int count = 0;
+            auto visit = [&](int q, bool in, bool edge_q) {
+                bool hit = false;
+                if (in) {
+                    const double2 m2 = G.mid[q];
+                    const double dx = m2.x - px, dy = m2.y - py;
+                    const double d2 = dx * dx + dy * dy;
+                    hit = d2 <= k.road_radius_sq;
+                    if (rewards_needed && edge_q) {
+                        const double hl = G.hl[q], hw = G.hw[q];
+                        const double reach = S.r + S.d + hl + hw + 1e-6;
+                        if (d2 <= reach * reach) {
+                            const double2 u2 = G.dir[q];
+    #pragma unroll
+                            for (int i = 0; i < 3; ++i) {
+                                const double qx = S.hx[i] - m2.x, qy = S.hy[i] - m2.y;
+                                const double along = qx * u2.x + qy * u2.y;
+                                const double lat = u2.x * qy - u2.y * qx;
+                                const double du = along - sel_clip(along, -hl, hl);
+                                const double dv = lat - sel_clip(lat, -hw, hw);
+                                edge_hit |= du * du + dv * dv < r2;
+                            }
+                        }
+                    }
+                }
+                const unsigned bal = __ballot_sync(kFull, hit);
+                if (hit) {
+                    const int slot = count + __popc(bal & ((1u << lane) - 1u));
+                    if (slot < A.take_road) cand[slot] = uint16_t(q);
+                }
+                count += __popc(bal);
+            };
+            const bool use_grid = (G.flags & kFlagGrid) != 0;
+            // the agent's grid cell (scene-local coordinates); -1 off the grid
+            int cell_id = -1;
+            if (G.flags) {
+                const double inv = 1.0 / G.cell;
+                const double fx = floor((px - ox - G.gx0) * inv), fy = floor((py - oy - G.gy0) * inv);
+                if (fx >= 0.0 && fy >= 0.0 && fx < double(G.nx) && fy < double(G.ny)) cell_id = int(fy) * G.nx + int(fx);
+            }
+            if (use_grid) {
+                // the cell's superset list (ascending) -> exact predicates, index order;
+                // off the grid nothing is within the road radius or an edge box
+                if (cell_id >= 0) {
+                    const int lo = __ldg(G.road_start + cell_id), hi = __ldg(G.road_start + cell_id + 1);
+                    for (int b0 = lo; b0 < hi; b0 += 32) {
+                        const int i = b0 + lane;
+                        const int q = i < hi ? int(__ldg(G.road_list + i)) : 0;
+                        const bool edge_q = (__ldg(G.edge_bits + (q >> 5)) >> (q & 31)) & 1u;
+                        visit(q, i < hi, edge_q);
+                    }
+                }
+            } else {
+                for (int p0 = 0; p0 < G.P; p0 += 32) visit(p0 + lane, p0 + lane < G.P, false);
+            }
+            const int ncand = count < A.take_road ? count : A.take_road;
+            if (m == 1) W1_MARK(35);
+            __syncwarp();
+            for (int slot = lane; slot < ncand; slot += 32) {
+                const int q = cand[slot];
+                const double2 m2 = G.mid[q], u2 = G.dir[q];
                 const double dx = m2.x - px, dy = m2.y - py;
-                const double d2 = dx * dx + dy * dy;
-                hit = d2 <= k.road_radius_sq;
-                if (rewards_needed && edge_q) {
+                const double ux = u2.x, uy = u2.y;
+                float* o = row + road0 + 5 * slot;
+                o[0] = __double2float_rn(dg::ddiv(c * dx + s * dy, k.road_radius));
+                o[1] = __double2float_rn(dg::ddiv(-s * dx + c * dy, k.road_radius));
+                o[2] = G.type_feat[q];
+                o[3] = __double2float_rn(c * ux + s * uy);
+                o[4] = __double2float_rn(-s * ux + c * uy);
+            }
+
+            if (m == 1) W1_MARK(36);
+            if (!rewards_needed) {
+                if (kStep && lane == 0) {
+                    ScanSm& R = sc[m];
+                    R.lane_d2 = INFINITY;
+                    R.lane_k = 0;
+                    R.gap = INFINITY;
+                    R.edge_hit = 0;
+                }
+                continue;
+            }
+            // (b) first road edge ahead over every edge (xb in (0, edge_range]); the
+            //     edge boxes when the grid could not take them
+            double gap = INFINITY;
+    #pragma unroll 2
+            for (int kk = lane; kk < G.KE; kk += 32) {
+                const double2 m2 = G.edge_mid[kk];
+                const double ex = m2.x - px, ey = m2.y - py;
+                const double xb = c * ex + s * ey;
+                if (xb > 0.0 && xb <= k.edge_range && xb < gap) gap = xb;
+                if (!use_grid) {
+                    const int q = G.edge[kk];
+                    const double2 u2 = G.dir[q];
                     const double hl = G.hl[q], hw = G.hw[q];
                     const double reach = S.r + S.d + hl + hw + 1e-6;
-                    if (d2 <= reach * reach) {
-                        const double2 u2 = G.dir[q];
-#pragma unroll
+                    if (ex * ex + ey * ey <= reach * reach) {
+    #pragma unroll
                         for (int i = 0; i < 3; ++i) {
                             const double qx = S.hx[i] - m2.x, qy = S.hy[i] - m2.y;
                             const double along = qx * u2.x + qy * u2.y;
@@ -881,169 +1078,90 @@ world_step_kernel(const KArgs A) {
                     }
                 }
             }
-            const unsigned bal = __ballot_sync(kFull, hit);
-            if (hit) {
-                const int slot = count + __popc(bal & ((1u << lane) - 1u));
-                if (slot < A.take_road) cand[slot] = uint16_t(q);
-            }
-            count += __popc(bal);
-        };
-        const bool use_grid = (G.flags & kFlagGrid) != 0;
-        // the agent's grid cell (scene-local coordinates); -1 off the grid
-        int cell_id = -1;
-        if (G.flags) {
-            const double inv = 1.0 / G.cell;
-            const double fx = floor((px - ox - G.gx0) * inv), fy = floor((py - oy - G.gy0) * inv);
-            if (fx >= 0.0 && fy >= 0.0 && fx < double(G.nx) && fy < double(G.ny)) cell_id = int(fy) * G.nx + int(fx);
-        }
-        if (use_grid) {
-            // the cell's superset list (ascending) -> exact predicates, index order;
-            // off the grid nothing is within the road radius or an edge box
-            if (cell_id >= 0) {
-                const int lo = __ldg(G.road_start + cell_id), hi = __ldg(G.road_start + cell_id + 1);
-                for (int b0 = lo; b0 < hi; b0 += 32) {
-                    const int i = b0 + lane;
-                    const int q = i < hi ? int(__ldg(G.road_list + i)) : 0;
-                    const bool edge_q = (__ldg(G.edge_bits + (q >> 5)) >> (q & 31)) & 1u;
-                    visit(q, i < hi, edge_q);
-                }
-            }
-        } else {
-            for (int p0 = 0; p0 < G.P; p0 += 32) visit(p0 + lane, p0 + lane < G.P, false);
-        }
-        const int ncand = count < A.take_road ? count : A.take_road;
-        if (m == 1) W1_MARK(35);
-        __syncwarp();
-        for (int slot = lane; slot < ncand; slot += 32) {
-            const int q = cand[slot];
-            const double2 m2 = G.mid[q], u2 = G.dir[q];
-            const double dx = m2.x - px, dy = m2.y - py;
-            const double ux = u2.x, uy = u2.y;
-            float* o = row + road0 + 5 * slot;
-            o[0] = __double2float_rn(dg::ddiv(c * dx + s * dy, k.road_radius));
-            o[1] = __double2float_rn(dg::ddiv(-s * dx + c * dy, k.road_radius));
-            o[2] = G.type_feat[q];
-            o[3] = __double2float_rn(c * ux + s * uy);
-            o[4] = __double2float_rn(-s * ux + c * uy);
-        }
+            gap = warp_min(gap);
+            edge_hit = __any_sync(kFull, edge_hit);
+            if (m == 1) W1_MARK(37);
 
-        if (m == 1) W1_MARK(36);
-        if (!rewards_needed) {
-            if (kStep && lane == 0) {
+            // (c) nearest lane: argmin of point-to-segment d2, lowest index on ties,
+            //     over the cell's candidate list when the agent is inside the grid
+            double best = INFINITY;
+            int best_k = 0x7fffffff;
+            auto lane_test = [&](int kk) {
+                const double4 l4 = G.lane_seg[kk];
+                const double ex = px - l4.x, ey = py - l4.y;
+                const double along = ex * l4.z + ey * l4.w;
+                const double lat = l4.z * ey - l4.w * ex;
+                const double t = fabs(along) - G.lane_hl[kk];
+                const double over = t > 0.0 ? t : 0.0;   // NaN along -> NaN lat, d2 NaN either way
+                const double d2 = over * over + lat * lat;
+                if (d2 < best) { best = d2; best_k = kk; }
+            };
+            const int lcell = (G.flags & kFlagLanes) ? cell_id : -1;
+            if (lcell >= 0) {
+                const int b0 = __ldg(G.lane_start + lcell), b1 = __ldg(G.lane_start + lcell + 1);
+                for (int i = b0 + lane; i < b1; i += 32) lane_test(__ldg(G.lane_list + i));
+            } else {
+                for (int kk = lane; kk < G.KL; kk += 32) lane_test(kk);
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(kFull, best, o);
+                const int ok = __shfl_xor_sync(kFull, best_k, o);
+                if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
+            }
+            if (m == 1) W1_MARK(38);
+            if (lane == 0) {
                 ScanSm& R = sc[m];
-                R.lane_d2 = INFINITY;
-                R.lane_k = 0;
-                R.gap = INFINITY;
-                R.edge_hit = 0;
+                R.lane_d2 = best;
+                R.lane_k = best_k;
+                R.gap = gap;
+                R.edge_hit = edge_hit;
             }
-            continue;
         }
-        // (b) first road edge ahead over every edge (xb in (0, edge_range]); the
-        //     edge boxes when the grid could not take them
-        double gap = INFINITY;
-#pragma unroll 2
-        for (int kk = lane; kk < G.KE; kk += 32) {
-            const double2 m2 = G.edge_mid[kk];
-            const double ex = m2.x - px, ey = m2.y - py;
-            const double xb = c * ex + s * ey;
-            if (xb > 0.0 && xb <= k.edge_range && xb < gap) gap = xb;
-            if (!use_grid) {
-                const int q = G.edge[kk];
-                const double2 u2 = G.dir[q];
-                const double hl = G.hl[q], hw = G.hw[q];
-                const double reach = S.r + S.d + hl + hw + 1e-6;
-                if (ex * ex + ey * ey <= reach * reach) {
-#pragma unroll
-                    for (int i = 0; i < 3; ++i) {
-                        const double qx = S.hx[i] - m2.x, qy = S.hy[i] - m2.y;
-                        const double along = qx * u2.x + qy * u2.y;
-                        const double lat = u2.x * qy - u2.y * qx;
-                        const double du = along - sel_clip(along, -hl, hl);
-                        const double dv = lat - sel_clip(lat, -hw, hw);
-                        edge_hit |= du * du + dv * dv < r2;
-                    }
+        WARP_MARK(0);
+        __syncthreads();
+        PHASE_MARK(5);
+
+        // ---- phase 3: one lane per agent (SIMT across the world's agents):
+        //      warp 0 -> rewards, events, termination, state for the next tick;
+        //      warp 1 (or warp 0 afterwards) -> the ego block (+ fused policy)
+        const int ego_warp = nwarps > 1 ? 1 : 0;
+        if (warp == ego_warp && lane < M) {
+            AgentSm& S = ag[lane];
+            write_ego(obs_w + int64_t(lane) * D, k, A, w, int64_t(w) * M + lane, S.st[SX], S.st[SY], S.c, S.s,
+                      S.st[SVX], S.st[SVY], S.gx, S.gy, feedback ? S.act : nullptr);
+        }
+        if constexpr (kStep) {
+            if (warp == 0 && lane < M) {
+                const int m = lane;
+                AgentSm& S = ag[m];
+                const ScanSm& R = sc[m];
+                FinIn F;
+                F.st = S.st;
+                F.px0 = S.px0; F.py0 = S.py0; F.gx = S.gx; F.gy = S.gy; F.sx = S.sx; F.sy = S.sy;
+                F.lane_d2 = R.lane_d2;
+                F.lane_lat = 0.0; F.lane_tx = 0.0; F.lane_ty = 0.0;
+                if (R.lane_d2 < INFINITY) {
+                    const double4 l4 = G.lane_seg[R.lane_k];
+                    const double ex = S.st[SX] - l4.x, ey = S.st[SY] - l4.y;
+                    F.lane_tx = l4.z;
+                    F.lane_ty = l4.w;
+                    F.lane_lat = l4.z * ey - l4.w * ex;
                 }
+                F.ttc_min = R.ttc_min; F.gap = R.gap;
+                F.edge_hit = R.edge_hit; F.touch = R.touch;
+                F.alive = S.alive; F.valid = S.valid; F.reason = S.reason; F.seen = S.seen; F.spawn = S.spawn;
+                F.start_yaw = S.start_yaw;
+                F.store_global = t + 1 == T;
+                F.st_out = S.st_next;
+                F.flags_out = S.flags_next;
+                const unsigned bits = finalize_agent(A, O, w, m, F, step_now + t, ox, oy);
+                count_events(A, w, bits, __activemask(), lane == 0, false);
             }
+            if (tid == 0) A.step_count[w] = step_now + t + 1;
+            PHASE_MARK(6);
+            GT_MARK(33);
         }
-        gap = warp_min(gap);
-        edge_hit = __any_sync(kFull, edge_hit);
-        if (m == 1) W1_MARK(37);
-
-        // (c) nearest lane: argmin of point-to-segment d2, lowest index on ties,
-        //     over the cell's candidate list when the agent is inside the grid
-        double best = INFINITY;
-        int best_k = 0x7fffffff;
-        auto lane_test = [&](int kk) {
-            const double4 l4 = G.lane_seg[kk];
-            const double ex = px - l4.x, ey = py - l4.y;
-            const double along = ex * l4.z + ey * l4.w;
-            const double lat = l4.z * ey - l4.w * ex;
-            const double t = fabs(along) - G.lane_hl[kk];
-            const double over = t > 0.0 ? t : 0.0;   // NaN along -> NaN lat, d2 NaN either way
-            const double d2 = over * over + lat * lat;
-            if (d2 < best) { best = d2; best_k = kk; }
-        };
-        const int lcell = (G.flags & kFlagLanes) ? cell_id : -1;
-        if (lcell >= 0) {
-            const int b0 = __ldg(G.lane_start + lcell), b1 = __ldg(G.lane_start + lcell + 1);
-            for (int i = b0 + lane; i < b1; i += 32) lane_test(__ldg(G.lane_list + i));
-        } else {
-            for (int kk = lane; kk < G.KL; kk += 32) lane_test(kk);
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ob = __shfl_xor_sync(kFull, best, o);
-            const int ok = __shfl_xor_sync(kFull, best_k, o);
-            if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
-        }
-        if (m == 1) W1_MARK(38);
-        if (lane == 0) {
-            ScanSm& R = sc[m];
-            R.lane_d2 = best;
-            R.lane_k = best_k;
-            R.gap = gap;
-            R.edge_hit = edge_hit;
-        }
-    }
-    WARP_MARK(0);
-    __syncthreads();
-    PHASE_MARK(5);
-
-    // ---- phase 3: one lane per agent (SIMT across the world's agents):
-    //      warp 0 -> rewards, events, termination, state write-back;
-    //      warp 1 (or warp 0 afterwards) -> the ego block
-    const int ego_warp = nwarps > 1 ? 1 : 0;
-    if (warp == ego_warp && lane < M) {
-        const AgentSm& S = ag[lane];
-        write_ego(obs_w + int64_t(lane) * D, k, A, w, int64_t(w) * M + lane, S.st[SX], S.st[SY], S.c, S.s,
-                  S.st[SVX], S.st[SVY],
-                  S.gx, S.gy);
-    }
-    if constexpr (kStep) {
-        if (warp == 0 && lane < M) {
-            const int m = lane;
-            const AgentSm& S = ag[m];
-            const ScanSm& R = sc[m];
-            FinIn F;
-            F.st = S.st;
-            F.px0 = S.px0; F.py0 = S.py0; F.gx = S.gx; F.gy = S.gy; F.sx = S.sx; F.sy = S.sy;
-            F.lane_d2 = R.lane_d2;
-            F.lane_lat = 0.0; F.lane_tx = 0.0; F.lane_ty = 0.0;
-            if (R.lane_d2 < INFINITY) {
-                const double4 l4 = G.lane_seg[R.lane_k];
-                const double ex = S.st[SX] - l4.x, ey = S.st[SY] - l4.y;
-                F.lane_tx = l4.z;
-                F.lane_ty = l4.w;
-                F.lane_lat = l4.z * ey - l4.w * ex;
-            }
-            F.ttc_min = R.ttc_min; F.gap = R.gap;
-            F.edge_hit = R.edge_hit; F.touch = R.touch;
-            F.alive = S.alive; F.valid = S.valid; F.reason = S.reason; F.seen = S.seen; F.spawn = S.spawn;
-            const unsigned bits = finalize_agent(A, w, m, F, step_now, ox, oy);
-            count_events(A, w, bits, __activemask(), lane == 0, false);
-        }
-        if (tid == 0) A.step_count[w] = step_now + 1;
-        PHASE_MARK(6);
-        GT_MARK(33);
+        if (t + 1 < T) __syncthreads();   // next tick reads st_next / act written above
     }
 }
 
@@ -1459,7 +1577,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
         F.edge_hit = edge_hit; F.touch = touch;
         F.alive = S.alive; F.valid = A.valid[am]; F.reason = A.reason[am]; F.seen = A.event_seen[am];
         F.spawn = A.spawn_step[am];
-        const unsigned bits = finalize_agent(A, w, m, F, step_now, ox, oy);
+        F.start_yaw = A.start_yaw[am];
+        F.store_global = true;
+        F.st_out = nullptr;
+        F.flags_out = nullptr;
+        const unsigned bits = finalize_agent(A, tick_out(A, 0), w, m, F, step_now, ox, oy);
         count_events(A, w, bits, 1u, true, true);
     }
 }
@@ -1532,7 +1654,7 @@ struct dg_engine {
 };
 
 #define DG_VARIANTS(X)                                                                 \
-    X(512, 1) X(256, 2) X(256, 3) X(256, 4) X(128, 4) X(128, 6) X(128, 8)
+    X(512, 1) X(512, 2) X(256, 2) X(256, 3) X(256, 4) X(128, 4) X(128, 6) X(128, 8)
 
 // Kernel variants: (threads per CTA, min resident CTAs per SM) bounds trade
 // registers for occupancy; dg_tune picks one.
@@ -1751,6 +1873,13 @@ int dg_step(dg_engine* eng, const DgStepIO* io, void* stream) {
     A.event_counts = io->event_counts;
     A.pol_gain = io->policy_gain;
     A.pol_throttle = io->policy_throttle;
+    A.ticks = io->ticks > 0 ? io->ticks : 1;
+    A.ring_slots = io->ring_slots > 0 ? io->ring_slots : A.ticks;
+    A.ring_start = io->ring_start;
+    if (A.ring_start < 0 || A.ring_start >= A.ring_slots)
+        return fail(DG_EINVAL, "dg_step: ring_start must lie in [0, ring_slots)");
+    if (A.ticks > 1 && eng->mode == 1)
+        return fail(DG_ENOSUPPORT, "dg_step: ticks > 1 needs the fused launch mode");
     eng->launches = 1;
     const cudaError_t err = launch_step_any<true>(eng, A, static_cast<cudaStream_t>(stream));
     eng->launches = eng->mode == 1 ? 2 : 1;
@@ -1766,6 +1895,9 @@ int dg_observe(dg_engine* eng, float* obs, double* ttc_min_out, double* next_act
     A.next_actions = next_actions;
     A.pol_gain = policy_gain;
     A.pol_throttle = policy_throttle;
+    A.ticks = 1;
+    A.ring_slots = 1;
+    A.ring_start = 0;
     eng->launches = 1;
     const cudaError_t err = launch_step_any<false>(eng, A, static_cast<cudaStream_t>(stream));
     eng->launches = eng->mode == 1 ? 2 : 1;

@@ -152,9 +152,9 @@ class StepOutput:
             self._info = {
                 "alive": as_bool(s["alive"]),
                 "alive_pre": as_bool(s["alive_pre"]),
-                "state": {k: s["snapshot"][i] for i, k in enumerate(STATE_FIELDS)},
+                "state": {k: s["snapshot"][..., i, :, :] for i, k in enumerate(STATE_FIELDS)},
                 "reason": s["reason"],
-                "reward_terms": {k: s["terms"][i] for i, k in enumerate(TERM_NAMES)},
+                "reward_terms": {k: s["terms"][..., i, :, :] for i, k in enumerate(TERM_NAMES)},
                 "ttc_min": s["ttc_min"],
                 "step": s["step"],
             }
@@ -286,10 +286,12 @@ class Engine:
     def _stream(self):
         return ct.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
-    def _aux_layout(self):
+    def _aux_layout(self, slots: int | None = None):
         W, M = self.W, self.M
         WM = W * M
         lay, off = {}, 0
+        k = 1 if slots is None else int(slots)
+        lead = () if slots is None else (k,)
         for name, nbytes, dtype, shape in (
                 ("rewards", 8 * WM, torch.float64, (W, M)),
                 ("ttc_min", 8 * WM, torch.float64, (W, M)),
@@ -300,12 +302,12 @@ class Engine:
                 ("reason", WM, torch.int8, (W, M)),
                 ("alive", WM, torch.uint8, (W, M)),
                 ("alive_pre", WM, torch.uint8, (W, M))):
-            lay[name] = (off, nbytes, dtype, shape)
-            off = _align16(off + nbytes)
+            lay[name] = (off, k * nbytes, dtype, lead + shape)
+            off = _align16(off + k * nbytes)
         return lay, off
 
-    def _views(self, aux: torch.Tensor) -> dict:
-        lay, _ = self._aux_layout()
+    def _views(self, aux: torch.Tensor, slots: int | None = None) -> dict:
+        lay, _ = self._aux_layout(slots)
         return {name: aux[o:o + n].view(dt).view(shape) for name, (o, n, dt, shape) in lay.items()}
 
     def _new_buffers(self, obs: torch.Tensor | None = None) -> StepBuffers:
@@ -318,6 +320,15 @@ class Engine:
 
     def new_step_buffers(self, obs: torch.Tensor | None = None) -> StepBuffers:
         return self._new_buffers(obs)
+
+    def new_rollout_buffers(self, slots: int) -> StepBuffers:
+        """Ring of ``slots`` per-tick outputs for ``launch_step(ticks=...)``:
+        obs [S][W][M][D] and every aux view with a leading slot axis."""
+        _, total = self._aux_layout(slots)
+        aux = torch.empty(total, dtype=torch.uint8, device=self.device)
+        obs = torch.empty((slots, self.W, self.M, self.obs_config.obs_dim), dtype=torch.float32,
+                          device=self.device)
+        return StepBuffers(obs, aux, self._views(aux, slots))
 
     def launch_shape(self) -> dict:
         return dict(self._shape)
@@ -424,7 +435,7 @@ class Engine:
 
     # ------------------------------------------------------------------ errors
     def _raise_nonfinite(self, flat: int):
-        w, m = flat // (3 * self.M), (flat // 3) % self.M
+        w, m = (flat // (3 * self.M)) % self.W, (flat // 3) % self.M
         raise ValueError(f"non-finite action for world {w} agent {m}")
 
     def check_actions(self, actions: torch.Tensor) -> None:
@@ -463,14 +474,22 @@ class Engine:
     def launch_step(self, actions: torch.Tensor, bufs: StepBuffers, autoreset: bool = False,
                     snapshot: bool = True, terms: bool = True, next_actions: torch.Tensor | None = None,
                     steer_gain: float = 2.0, throttle: float = 0.5,
-                    event_counts: torch.Tensor | None = None) -> None:
-        """Enqueue one fused step on the current stream; no sync, no checks
+                    event_counts: torch.Tensor | None = None, ticks: int = 1, ring_start: int = 0) -> None:
+        """Enqueue one fused launch on the current stream; no sync, no checks
         beyond the device-side non-finite guard.  Used by the fast paths.
-        ``next_actions`` (float64 [W][M][3], distinct from ``actions``) receives
-        the fused LaneFollower's actions on this tick's observation;
+        ``next_actions`` (float64 [W][M][3], may alias ``actions``) receives
+        the fused LaneFollower's actions on the last tick's observation;
         ``event_counts`` (int32 [W][5]) accumulates per-world goal / collision /
-        crash / lane_forbidden events and alive agent-ticks on the device."""
+        crash / lane_forbidden events and alive agent-ticks on the device.
+
+        ``ticks`` > 1 runs that many control ticks in the same launch (each
+        world's CTA keeps its scene and agents in shared memory across them):
+        tick t reads ``actions[t]`` ([T][W][M][3]) -- or, with ``next_actions``,
+        ``actions`` ([W][M][3]) at tick 0 and the fused policy's actions after
+        -- and writes slot ``(ring_start + t) % S`` of rollout buffers with S
+        slots (``new_rollout_buffers``)."""
         v = bufs.views
+        slots = bufs.obs.shape[0] if bufs.obs.dim() == 4 else 1
         io = N.DgStepIO(actions=actions.data_ptr(), actions_f64=int(actions.dtype == torch.float64),
                         autoreset=int(autoreset), obs=bufs.obs.data_ptr(),
                         rewards=v["rewards"].data_ptr(), dones=v["dones"].data_ptr(),
@@ -481,10 +500,65 @@ class Engine:
                         snapshot_out=v["snapshot"].data_ptr() if snapshot else None,
                         next_actions=next_actions.data_ptr() if next_actions is not None else None,
                         policy_gain=float(steer_gain), policy_throttle=float(throttle),
-                        event_counts=event_counts.data_ptr() if event_counts is not None else None)
+                        event_counts=event_counts.data_ptr() if event_counts is not None else None,
+                        ticks=int(ticks), ring_slots=int(slots), ring_start=int(ring_start))
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), self._stream()), "dg_step")
-        self._step_count += 1
+        self._step_count += int(ticks)
         self.launches += 1
+
+    def rollout(self, actions, ticks: int | None = None, autoreset: bool = False, policy: str | None = None,
+                steer_gain: float = 2.0, throttle: float = 0.5, bufs: StepBuffers | None = None,
+                next_actions: torch.Tensor | None = None) -> StepOutput:
+        """T control ticks in ONE kernel launch -- the same results as T
+        ``step`` calls (env.py:48-65 in a loop).
+
+        ``actions``: a [T][W][M][3] stream replayed tick by tick, or with
+        ``policy="lane_follower"`` the [W][M][3] actions of the first tick,
+        the fused LaneFollower (policies.py:21-43) driving every later tick
+        from that tick's observation (``ticks`` required).  A replayed stream
+        is validated before anything runs and raises like ``step``.  Returns a
+        device StepOutput whose arrays carry a leading tick axis; the policy's
+        actions for the tick after the last are in ``next_actions``."""
+        dev = self.device
+        a = actions if isinstance(actions, torch.Tensor) else torch.as_tensor(np.asarray(actions, np.float64))
+        if a.dtype not in (torch.float32, torch.float64):
+            a = a.to(torch.float64)
+        a = a.to(dev).contiguous()
+        if policy is None:
+            if a.dim() != 4 or tuple(a.shape[1:]) != (self.W, self.M, 3):
+                raise ValueError(f"actions shape {tuple(a.shape)}, expected (T, {self.W}, {self.M}, 3)")
+            T = a.shape[0] if ticks is None else int(ticks)
+            if T > a.shape[0]:
+                raise ValueError(f"{T} ticks but only {a.shape[0]} action frames")
+            bad = ~torch.isfinite(a[:T])
+            if bool(bad.any()):
+                t, w, m, _ = (int(i) for i in bad.nonzero()[0])
+                raise ValueError(f"non-finite action for world {w} agent {m}")
+        elif policy == "lane_follower":
+            if tuple(a.shape) != (self.W, self.M, 3):
+                raise ValueError(f"actions shape {tuple(a.shape)}, expected {(self.W, self.M, 3)}")
+            if ticks is None:
+                raise ValueError("rollout with a policy needs ticks")
+            T = int(ticks)
+            self.check_actions(a)
+            if next_actions is None:
+                next_actions = torch.empty((self.W, self.M, 3), dtype=torch.float64, device=dev)
+        else:
+            raise ValueError(f"unknown rollout policy {policy!r}")
+        if T < 1:
+            raise ValueError("ticks must be >= 1")
+        if bufs is None:
+            bufs = self.new_rollout_buffers(T)
+        self.launch_step(a, bufs, autoreset=autoreset, ticks=T,
+                         next_actions=next_actions if policy else None,
+                         steer_gain=steer_gain, throttle=throttle)
+        self.raise_pending_error()
+        v = bufs.views
+        src = dict(v)
+        src["step"] = self._step_count
+        out = StepOutput(bufs.obs, v["rewards"], v["dones"].bool(), v["events"], src, to_host=False)
+        out.next_actions = next_actions
+        return out
 
     def step(self, actions, autoreset: bool = False) -> StepOutput:
         """One 30 Hz control tick (engine.py:334-406)."""
