@@ -42,6 +42,7 @@ import numpy as np  # noqa: E402
 L2_BYTES = 126 * 1024 * 1024
 HEADLINE = (256, 16)
 SCALE_TOTAL_WORLDS = 4096
+DEFAULT_TICKS_PER_LAUNCH = 16
 
 
 def parse():
@@ -55,6 +56,8 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly from the host (slower)")
+    ap.add_argument("--ticks-per-launch", type=int, default=0,
+                    help="control ticks per persistent kernel launch (0 = default for the shape)")
     return ap.parse_args()
 
 
@@ -245,44 +248,49 @@ def main():
     W, M, D = eng.W, eng.M, eng.obs_config.obs_dim
     obs_bytes = W * M * D * 4
     ring = max(2, math.ceil(2 * L2_BYTES / obs_bytes))
-    obs_ring = torch.empty((ring, W, M, D), dtype=torch.float32, device=dev)
-    bufs = [eng.new_step_buffers(obs_ring[i]) for i in range(ring)]
-    # the LaneFollower is fused into the step: step i reads actions[i % 2] and
-    # writes the policy's actions for step i+1 into actions[(i + 1) % 2]
-    acts = [torch.zeros((W, M, 3), dtype=torch.float64, device=dev) for _ in range(2)]
-    eng.observe(out=obs_ring[ring - 1], as_numpy=False, next_actions=acts[0])
+    # every tick writes its own ring slot (obs + the per-tick aux outputs)
+    rbufs = eng.new_rollout_buffers(ring)
+    R = args.ticks_per_launch or DEFAULT_TICKS_PER_LAUNCH
+    # the LaneFollower is fused into the step: a launch reads actions (tick 0),
+    # feeds the policy's actions to its later ticks through shared memory and
+    # leaves the next launch's actions in next_actions (in place: a world's
+    # CTA reads its rows before it overwrites them)
+    acts = torch.zeros((W, M, 3), dtype=torch.float64, device=dev)
+    eng.observe(out=rbufs.obs[ring - 1], as_numpy=False, next_actions=acts)
     stream = torch.cuda.current_stream(dev)
 
     # per-world episode counters on the device: goal/collision/crash/lane_forbidden
     # events and alive agent-ticks (the CASPS numerator, counted before each tick)
     counters = torch.zeros((W, 5), dtype=torch.int32, device=dev)
+    tick = [0]
 
-    def one_step(i, count=True):
-        eng.launch_step(acts[i % 2], bufs[i % ring], autoreset=True, next_actions=acts[(i + 1) % 2],
-                        event_counts=counters if count else None)
+    def run_ticks(n, count=True):
+        """n control ticks in ceil(n / R) launches of up to R ticks each."""
+        done = 0
+        while done < n:
+            r = min(R, n - done)
+            eng.launch_step(acts, rbufs, autoreset=True, next_actions=acts, ticks=r,
+                            ring_start=tick[0] % ring, event_counts=counters if count else None)
+            tick[0] += r
+            done += r
 
     # warm-up (untimed)
-    for i in range(args.warmup):
-        one_step(i, count=False)
+    run_ticks(args.warmup, count=False)
     torch.cuda.synchronize()
     valid_count = int(eng.valid.sum())
     assert int(eng.alive.sum()) == valid_count
 
-    # The K timed steps are captured once into a CUDA graph (outside the timed
-    # region): the device then runs policy -> fused step back to back with no
-    # host launch gaps.  The per-launch time of the fused-step kernel (the
-    # roofline numerator) comes from a second graph of K step-only launches,
-    # timed the same way right after.
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    # The K timed ticks are captured once into a CUDA graph (outside the timed
+    # region) so the device runs the launches back to back with no host gaps.
+    # The per-launch kernel time (the roofline numerator) comes from a second
+    # graph of the same launches without the counters, timed right after.
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = eng.launches
     graph = None
     if not args.no_graph:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            for i in range(args.steps):
-                one_step(args.warmup + i)
+            run_ticks(args.steps)
     if world_size > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -291,35 +299,31 @@ def main():
         if graph is not None:
             graph.replay()
         else:
-            for i in range(args.steps):
-                ev0[i].record(stream)
-                one_step(args.warmup + i)
-                ev1[i].record(stream)
+            run_ticks(args.steps)
         stop.record(stream)
         torch.cuda.synchronize()
     launches = eng.launches - launches0
     total_ms = start.elapsed_time(stop)
-    launches_per_step = launches / args.steps
     if world_size > 1:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
+    n_launch = math.ceil(args.steps / R)
     if graph is not None:
-        # kernel-only timing: K fused-step launches in one graph, CUDA events around the replay
         g_step = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_step):
-            for i in range(args.steps):
-                one_step(args.warmup + args.steps + i, count=False)
+            run_ticks(args.steps, count=False)
         torch.cuda.synchronize()
         k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         k0.record(stream)
         g_step.replay()
         k1.record(stream)
         torch.cuda.synchronize()
-        kern_avg = k0.elapsed_time(k1) / args.steps
+        kern_total = k0.elapsed_time(k1)
     else:
-        kern_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
-        kern_avg = sum(kern_ms) / len(kern_ms)
+        kern_total = total_ms
+    kern_avg = kern_total / n_launch            # ms per launch
+    ticks_per_launch = args.steps / n_launch
     from paper_2605_08528_b200.sharding import allgather_summaries, combine, episode_summary
     local = episode_summary(counters.cpu().numpy(), valid_count)
     # episode statistics: the only cross-rank traffic (one NCCL all-gather)
@@ -330,7 +334,7 @@ def main():
     if rank == 0:
         peak, peak_src = measured_peaks()
         per_agent = algorithmic_bytes_per_agent(D)
-        achieved = per_agent * W * M / (kern_avg / 1e3) / 1e9
+        achieved = per_agent * W * M * ticks_per_launch / (kern_avg / 1e3) / 1e9
         line = {
             "metric": "CASPS", "value": value, "unit": "agent-steps/s", "n_gpus": world_size,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -340,14 +344,17 @@ def main():
                                    f"LaneFollower + autoreset fused into the step",
                        "worlds": W_total, "agents": M, "obs_dim": D,
                        "l2": f"obs rotate through a {ring}-slot rollout ring ({ring * obs_bytes / 2**20:.0f} MiB > L2)",
-                       "launch": "CUDA graph of the K timed steps" if graph is not None else "eager",
+                       "launch": (f"{n_launch} persistent launches of {R} ticks"
+                                  + (", one CUDA graph" if graph is not None else ", eager")),
+                       "ticks_per_launch": R,
                        "kernel_shape": eng.launch_shape(),
                        "parallelism": f"world-shard x{world_size}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
                          "bytes_per_agent_step": per_agent, "kernel_ms": kern_avg,
+                         "kernel_ms_per_tick": kern_avg / ticks_per_launch,
                          "peak_source": peak_src},
-            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "gpu_launches": launches,
             "episode_counters": totals,
         }
         line["clocks"] = clk.summary()
