@@ -144,6 +144,16 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic(W, M, ticks):
+    """dram read+write bytes of one launch of this shape from the committed
+    ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    rec = json.loads(p.read_text()).get(f"{W}x{M}x{ticks}")
+    return None if rec is None else float(rec["traffic_bytes"])
+
+
 def algorithmic_bytes_per_agent(obs_dim: int) -> int:
     """Bytes one agent-step must move to/from HBM (roofline):
     obs row write + state read/write + actions + the per-agent outputs and
@@ -350,7 +360,9 @@ def main():
                        "kernel_shape": eng.launch_shape(),
                        "parallelism": f"world-shard x{world_size}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": ncu_traffic(W, M, R) if world_size == 1 else None,
+                         "traffic_unit": "bytes per launch (ncu dram read+write, profiles/ncu_traffic.json)",
+                         "algorithmic_bytes_per_launch": per_agent * W * M * ticks_per_launch,
                          "bytes_per_agent_step": per_agent, "kernel_ms": kern_avg,
                          "kernel_ms_per_tick": kern_avg / ticks_per_launch,
                          "peak_source": peak_src},

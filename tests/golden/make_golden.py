@@ -19,6 +19,9 @@ Cases (each an .npz under tests/golden/):
   traj_reset        2x4: steps, EnvHandle.reset quirk, overlapping teleport starts
   traj_events       4x16, scripted throttle/steer/brake: goal, edge, crash, collision
   traj_events_inv   same actions, invincible mode (latched events, no termination)
+  drac_wet          traj_wet's run through Engine.run_episode(record=True): per-step
+                    pairwise_drac + episode_metrics (metrics.py:33-125)
+  drac_events       traj_events' run, same records (collisions, DRAC > 3.4)
 """
 
 from __future__ import annotations
@@ -259,9 +262,59 @@ def traj_events_inv():
     rec.save("traj_events_inv")
 
 
+def _drac_record(name, eng, acts):
+    """Engine.run_episode(record=True) -> pairwise_drac per logged step and
+    episode_metrics over the log, exactly as the reference's eval does."""
+    from drivegrid.metrics import episode_metrics, pairwise_drac
+
+    it = iter(range(len(acts)))
+    log = eng.run_episode(lambda obs: acts[next(it)].astype(np.float64), record=True,
+                          max_steps=len(acts))
+    per = {k: [] for k in ("x", "y", "yaw", "v_x", "v_y", "alive_pre", "drac", "goal", "collision")}
+    for rec in log.steps:
+        st = rec["state"]
+        c, s = np.cos(st["yaw"]), np.sin(st["yaw"])
+        vel = np.stack([st["v_x"] * c - st["v_y"] * s, st["v_x"] * s + st["v_y"] * c], axis=-1)
+        pos = np.stack([st["x"], st["y"]], axis=-1)
+        per["drac"].append(pairwise_drac(pos, st["yaw"], vel, eng.r_hull, eng.d_hull, rec["alive_pre"]))
+        for k in ("x", "y", "yaw", "v_x", "v_y"):
+            per[k].append(st[k])
+        per["alive_pre"].append(rec["alive_pre"])
+        per["goal"].append(rec["events"]["goal"])
+        per["collision"].append(rec["events"]["collision"])
+    em = episode_metrics(log, eng.valid, eng.length, eng.width)
+    np.savez_compressed(
+        OUT / f"{name}.npz", actions=acts[:len(log.steps)], r_hull=eng.r_hull, d_hull=eng.d_hull,
+        valid=eng.valid, length=eng.length, width=eng.width,
+        per_agent_max_drac=em.per_agent_max_drac, sr=em.sr, cr=em.cr,
+        mean_max_drac=em.mean_max_drac, goals=em.goals, collisions=em.collisions,
+        **{"step_" + k: np.stack(v) for k, v in per.items()})
+    print(name, len(log.steps), "steps", em.to_dict())
+
+
+def drac_wet():
+    from drivegrid.config import load_scene_pool
+    from drivegrid.engine import Engine, SimConfig
+    from drivegrid.world import build_world_batch
+
+    W, M = 12, 16
+    cfg = cfg_of(W, M, seed=5)
+    pool = load_scene_pool(cfg.scene_factory)
+    worlds, assignment = build_world_batch(pool, W, mode="random_fill", seed=5)
+    eng = Engine(worlds, pool, assignment, wet_frictions(W), SimConfig(num_envs=W, num_agents=M, seed=5))
+    acts = philox_actions(9, 80, W, M)
+    acts[..., 0] = np.abs(acts[..., 0])
+    _drac_record("drac_wet", eng, acts)
+
+
+def drac_events():
+    eng = build_engine(cfg_of(4, 16, seed=31))
+    _drac_record("drac_events", eng, event_actions(420, 4, 16))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv"]
+                             "traj_events_inv", "drac_wet", "drac_events"]
     for name in which:
         globals()[name]()
