@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 5
+#define DG_ABI_VERSION 6
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -150,6 +150,13 @@ typedef struct DgStepIO {
     int32_t ring_slots;         /* 0: ticks                                    */
     int32_t ring_start;
     int32_t pad_;
+    double* drac_max;           /* [W][M]      episode safety metric, accumulated:
+                                   drac_max = max(drac_max, pairwise DRAC of this
+                                   tick's post-physics state over the agents alive
+                                   before it) -- episode_metrics' per-agent max
+                                   (metrics.py:33-62, 101-108), or NULL        */
+    uint8_t* metric_seen;       /* [W][M]      |= bit 0 goal event, bit 1 collision
+                                   event of this tick (metrics.py:100-101), or NULL */
 } DgStepIO;
 
 typedef struct dg_engine dg_engine;
@@ -189,6 +196,19 @@ int dg_read_error(dg_engine* eng, int32_t* flat_index, void* stream);
  * [W][M][3], the same values the host numpy policy produces. */
 int dg_lane_follower(dg_engine* eng, const float* obs, double* actions, double steer_gain,
                      double throttle, void* stream);
+
+/* Pairwise DRAC of logged states (metrics.py:33-62 pairwise_drac, applied per
+ * record by episode_metrics, metrics.py:86-125), no engine needed.
+ * x, y, yaw, v_x, v_y, alive: [steps][W][M]; v_x/v_y are the body-frame
+ * velocity of STATE_FIELDS (rotated by yaw as metrics.py:104-107 does) or,
+ * with world_velocity != 0, pairwise_drac's vel_world argument as is;
+ * r_hull, d_hull: [W][M].  out [W][M] = max over the steps of each record's
+ * per-agent max DRAC, also max'ed with the incoming out when accumulate != 0.
+ * M <= 16.  Device pointers; asynchronous on stream. */
+int dg_pairwise_drac(const double* x, const double* y, const double* yaw, const double* v_x,
+                     const double* v_y, const uint8_t* alive, const double* r_hull,
+                     const double* d_hull, int32_t steps, int32_t W, int32_t M, double* out,
+                     int32_t accumulate, int32_t world_velocity, void* stream);
 
 /* Kernel launches issued by the last dg_step/dg_observe/dg_reset call. */
 int dg_launch_count(dg_engine* eng);

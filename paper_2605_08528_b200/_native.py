@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 
 class DgDims(ct.Structure):
@@ -71,7 +71,8 @@ class DgStepIO(ct.Structure):
                           "next_actions")] + [("policy_gain", ct.c_double), ("policy_throttle", ct.c_double),
                                               ("event_counts", _P),
                                               ("ticks", ct.c_int32), ("ring_slots", ct.c_int32),
-                                              ("ring_start", ct.c_int32), ("pad_", ct.c_int32)]
+                                              ("ring_start", ct.c_int32), ("pad_", ct.c_int32),
+                                              ("drac_max", _P), ("metric_seen", _P)]
 
 
 # exported symbol -> (restype, argtypes)
@@ -90,6 +91,7 @@ SIGNATURES = {
     "dg_launch_count": (ct.c_int, [_P]),
     "dg_tune": (ct.c_int, [_P, ct.c_int32, ct.c_int32, ct.c_int32]),
     "dg_scratch_bytes": (ct.c_size_t, [ct.c_int32, ct.c_int32]),
+    "dg_pairwise_drac": (ct.c_int, [_P] * 8 + [ct.c_int32, ct.c_int32, ct.c_int32, _P, ct.c_int32, ct.c_int32, _P]),
 }
 
 

@@ -93,6 +93,8 @@ struct KArgs {
     int32_t take_road;   // min(k_road, max_segments) = candidate-list capacity
     int32_t take_veh;    // min(k_vehicles, M)
     uint8_t* scratch;    // split mode: AgentRec[W*M], int32 world_ok[W], int32 world_step[W]
+    double* drac_max;    // [W][M] running max of the per-step pairwise DRAC (NULL = off)
+    uint8_t* metric_seen; // [W][M] |= goal (bit 0) / collision (bit 1) events (NULL = off)
 };
 
 // ----------------------------------------------------------------- numpy-semantics helpers
@@ -121,6 +123,39 @@ __device__ __forceinline__ double4 ldg4(const double4* p) {
 __device__ __forceinline__ double warp_min(double v, int width = 32) {
     for (int o = width >> 1; o > 0; o >>= 1) v = sel_min(v, __shfl_xor_sync(kFull, v, o, width));
     return v;
+}
+
+__device__ __forceinline__ double warp_max_nn(double v, int width = 32) {   // non-negative values
+    for (int o = width >> 1; o > 0; o >>= 1) {
+        const double u = __shfl_xor_sync(kFull, v, o, width);
+        v = u > v ? u : v;
+    }
+    return v;
+}
+
+// DRAC of the ordered pair (ego e, other n), metrics.py:33-62: d = p_n - p_e,
+// u = v_n - v_e (world frame), closing = -(d.u) / max(|d|, 1e-9), clearance =
+// min over the 3x3 hull-circle pairs of the centre distance - (r_e + r_n);
+// closing^2 / (2 max(clearance, 1e-2)) if closing > 0 and clearance > 1e-2,
+// else 0.  The caller masks dead agents and e == n.  IEEE / and sqrt (not the
+// fast-path helpers): squared clearances can be arbitrarily small.  min of
+// square roots == square root of the min (sqrt is correctly rounded, hence
+// monotone), so one sqrt replaces nine.
+__device__ __forceinline__ double pair_drac(double dx, double dy, double ux, double uy, const double* ehx,
+                                            const double* ehy, const double* nhx, const double* nhy,
+                                            double rsum) {
+    const double dist = sqrt(dx * dx + dy * dy);
+    const double closing = -(dx * ux + dy * uy) / np_max(dist, 1e-9);
+    double m2 = INFINITY;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const double ex = ehx[a] - nhx[b], ey = ehy[a] - nhy[b];
+            m2 = sel_min(m2, ex * ex + ey * ey);
+        }
+    const double clear = sqrt(m2) - rsum;
+    return (closing > 0.0 && clear > 1e-2) ? closing * closing / (2.0 * np_max(clear, 1e-2)) : 0.0;
 }
 
 // ----------------------------------------------------------------- shared-memory layout
@@ -548,6 +583,7 @@ __device__ __forceinline__ unsigned finalize_agent(const KArgs& A, const TickOut
             const bool park = done && !timeout;
             int alive_new = alive && !finished;
 
+            if (A.metric_seen && (rnow == 1 || rnow == 2)) A.metric_seen[am] |= uint8_t(rnow == 1 ? 1 : 2);
             O.rewards[am] = reward;
             O.dones[am] = finished;
             reinterpret_cast<uint32_t*>(O.events)[am] =
@@ -947,6 +983,21 @@ world_step_kernel(const KArgs A) {
                         }
                 }
                 touch = (__ballot_sync(kFull, touch) & gmask) != 0;
+                if (kStep && A.drac_max) {
+                    // episode safety metric on the post-physics state, agents alive before the tick
+                    double dr = 0.0;
+                    if (ego_ok && j < M && j != ii && S.alive && ag[j].alive) {
+                        const AgentSm& N = ag[j];
+                        dr = pair_drac(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, S.hx, S.hy, N.hx, N.hy,
+                                       S.r + N.r);
+                    }
+                    dr = warp_max_nn(dr, 16);
+                    if (ego_ok && j == 0) {
+                        double* p = A.drac_max + int64_t(w) * M + ii;
+                        const double prev = *p;
+                        *p = dr > prev ? dr : prev;
+                    }
+                }
                 if (ego_ok && j == 0) {
                     sc[ii].ttc_min = ttc;
                     sc[ii].touch = touch;
@@ -1417,6 +1468,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
                 }
         }
         touch = __any_sync(kFull, t_);
+        if (kStep && A.drac_max) {
+            double dr = 0.0;
+            if (j < M && j != m && S.alive && ag[j].alive) {
+                const AgentRec& N = ag[j];
+                dr = pair_drac(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, S.hx, S.hy, N.hx, N.hy, S.r + N.r);
+            }
+            dr = warp_max_nn(dr);
+            if (lane == 0) {
+                const double prev = A.drac_max[am];
+                A.drac_max[am] = dr > prev ? dr : prev;
+            }
+        }
     }
 
     // (2) road context + edge boxes over the cell's superset list
@@ -1624,6 +1687,57 @@ __global__ void set_step_kernel(int32_t* step_count, int W, int32_t value) {
 }
 
 // policies.py:21-43 on the device, float64 like the numpy policy
+// Standalone pairwise DRAC over logged states (metrics.py:33-62, 101-108):
+// one CTA per world, 16 lanes per ego agent (lane j <-> other agent j), the
+// world's records visited in order, the per-agent max kept in a register.
+__global__ void __launch_bounds__(256) pairwise_drac_kernel(const double* x, const double* y, const double* yaw,
+                                                            const double* vx, const double* vy,
+                                                            const uint8_t* alive, const double* r_hull,
+                                                            const double* d_hull, int steps, int W, int M,
+                                                            double* out, int accumulate, int world_vel) {
+    __shared__ double s_px[kMaxAgents], s_py[kMaxAgents], s_ux[kMaxAgents], s_uy[kMaxAgents];
+    __shared__ double s_hx[kMaxAgents][3], s_hy[kMaxAgents][3];
+    __shared__ int s_alive[kMaxAgents];
+    const int w = blockIdx.x;
+    const int i = threadIdx.x >> 4, j = threadIdx.x & 15;
+    const int64_t WM = int64_t(W) * M;
+    double best = 0.0;
+    for (int t = 0; t < steps; ++t) {
+        if (threadIdx.x < M) {
+            const int m = threadIdx.x;
+            const int64_t q = t * WM + int64_t(w) * M + m;
+            const double px = x[q], py = y[q], th = yaw[q], bx = vx[q], by = vy[q];
+            const double c = cos(th), sn = sin(th);                 // metrics.py:104
+            s_px[m] = px;
+            s_py[m] = py;
+            s_ux[m] = world_vel ? bx : bx * c - by * sn;             // metrics.py:105-106
+            s_uy[m] = world_vel ? by : bx * sn + by * c;
+            const double d = d_hull[int64_t(w) * M + m];
+            const double oc = d * c, os = d * sn;                    // metrics.py:46-49
+            s_hx[m][0] = px + -1.0 * oc; s_hx[m][1] = px + 0.0 * oc; s_hx[m][2] = px + 1.0 * oc;
+            s_hy[m][0] = py + -1.0 * os; s_hy[m][1] = py + 0.0 * os; s_hy[m][2] = py + 1.0 * os;
+            s_alive[m] = alive[q];
+        }
+        __syncthreads();
+        double dr = 0.0;
+        if (i < M && j < M && i != j && s_alive[i] && s_alive[j]) {
+            dr = pair_drac(s_px[j] - s_px[i], s_py[j] - s_py[i], s_ux[j] - s_ux[i], s_uy[j] - s_uy[i], s_hx[i],
+                           s_hy[i], s_hx[j], s_hy[j], r_hull[int64_t(w) * M + i] + r_hull[int64_t(w) * M + j]);
+        }
+        dr = warp_max_nn(dr, 16);
+        best = dr > best ? dr : best;
+        __syncthreads();
+    }
+    if (i < M && j == 0) {
+        double* p = out + int64_t(w) * M + i;
+        if (accumulate) {
+            const double prev = *p;
+            best = best > prev ? best : prev;
+        }
+        *p = best;
+    }
+}
+
 __global__ void lane_follower_kernel(const float* obs, double* actions, int64_t n, int D, double gain,
                                      double throttle, double bbox_half) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
@@ -1873,6 +1987,8 @@ int dg_step(dg_engine* eng, const DgStepIO* io, void* stream) {
     A.event_counts = io->event_counts;
     A.pol_gain = io->policy_gain;
     A.pol_throttle = io->policy_throttle;
+    A.drac_max = io->drac_max;
+    A.metric_seen = io->metric_seen;
     A.ticks = io->ticks > 0 ? io->ticks : 1;
     A.ring_slots = io->ring_slots > 0 ? io->ring_slots : A.ticks;
     A.ring_start = io->ring_start;
@@ -1963,6 +2079,20 @@ int dg_lane_follower(dg_engine* eng, const float* obs, double* actions, double s
     eng->launches = 1;
     const cudaError_t err = cudaGetLastError();
     return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_lane_follower");
+}
+
+int dg_pairwise_drac(const double* x, const double* y, const double* yaw, const double* v_x, const double* v_y,
+                     const uint8_t* alive, const double* r_hull, const double* d_hull, int32_t steps, int32_t W,
+                     int32_t M, double* out, int32_t accumulate, int32_t world_velocity, void* stream) {
+    if (!x || !y || !yaw || !v_x || !v_y || !alive || !r_hull || !d_hull || !out)
+        return fail(DG_EINVAL, "dg_pairwise_drac: null argument");
+    if (W < 1 || M < 1 || M > kMaxAgents || steps < 0)
+        return fail(DG_EINVAL, "dg_pairwise_drac: need W >= 1, 1 <= M <= 16, steps >= 0");
+    pairwise_drac_kernel<<<W, 256, 0, static_cast<cudaStream_t>(stream)>>>(x, y, yaw, v_x, v_y, alive, r_hull,
+                                                                           d_hull, steps, W, M, out, accumulate,
+                                                                           world_velocity);
+    const cudaError_t err = cudaGetLastError();
+    return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_pairwise_drac");
 }
 
 int dg_launch_count(dg_engine* eng) { return eng ? eng->launches : 0; }

@@ -272,6 +272,9 @@ class Engine:
         self._obs_dev = torch.empty((W, M, oc.obs_dim), dtype=torch.float32, device=dev)
         self._host_bufs = self._new_buffers(self._obs_dev)
         self.launches = 0
+        self._metrics_on = False
+        self._drac_max = None
+        self._metric_seen = None
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -474,7 +477,8 @@ class Engine:
     def launch_step(self, actions: torch.Tensor, bufs: StepBuffers, autoreset: bool = False,
                     snapshot: bool = True, terms: bool = True, next_actions: torch.Tensor | None = None,
                     steer_gain: float = 2.0, throttle: float = 0.5,
-                    event_counts: torch.Tensor | None = None, ticks: int = 1, ring_start: int = 0) -> None:
+                    event_counts: torch.Tensor | None = None, ticks: int = 1, ring_start: int = 0,
+                    drac_max: torch.Tensor | None = None, metric_seen: torch.Tensor | None = None) -> None:
         """Enqueue one fused launch on the current stream; no sync, no checks
         beyond the device-side non-finite guard.  Used by the fast paths.
         ``next_actions`` (float64 [W][M][3], may alias ``actions``) receives
@@ -487,7 +491,14 @@ class Engine:
         tick t reads ``actions[t]`` ([T][W][M][3]) -- or, with ``next_actions``,
         ``actions`` ([W][M][3]) at tick 0 and the fused policy's actions after
         -- and writes slot ``(ring_start + t) % S`` of rollout buffers with S
-        slots (``new_rollout_buffers``)."""
+        slots (``new_rollout_buffers``).
+
+        ``drac_max`` (float64 [W][M]) / ``metric_seen`` (uint8 [W][M]) are the
+        in-kernel episode-metric accumulators (default: the engine's own when
+        ``track_episode_metrics`` is on)."""
+        if self._metrics_on:
+            drac_max = self._drac_max if drac_max is None else drac_max
+            metric_seen = self._metric_seen if metric_seen is None else metric_seen
         v = bufs.views
         slots = bufs.obs.shape[0] if bufs.obs.dim() == 4 else 1
         io = N.DgStepIO(actions=actions.data_ptr(), actions_f64=int(actions.dtype == torch.float64),
@@ -501,7 +512,8 @@ class Engine:
                         next_actions=next_actions.data_ptr() if next_actions is not None else None,
                         policy_gain=float(steer_gain), policy_throttle=float(throttle),
                         event_counts=event_counts.data_ptr() if event_counts is not None else None,
-                        ticks=int(ticks), ring_slots=int(slots), ring_start=int(ring_start))
+                        ticks=int(ticks), ring_slots=int(slots), ring_start=int(ring_start),
+                        drac_max=_ptr(drac_max), metric_seen=_ptr(metric_seen))
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), self._stream()), "dg_step")
         self._step_count += int(ticks)
         self.launches += 1
@@ -642,22 +654,110 @@ class Engine:
         self.launches += 1
         return acts
 
-    def run_episode(self, policy, record: bool = False, max_steps: int | None = None) -> list:
+    # ------------------------------------------------------------------ episode metrics
+    def track_episode_metrics(self, enable: bool = True) -> None:
+        """Accumulate the episode safety metrics inside the step kernel: per
+        agent, the running max of the pairwise DRAC of every tick's
+        post-physics state over the agents alive before the tick, and goal /
+        collision event latches (what episode_metrics derives from a recorded
+        log, metrics.py:86-125).  Zeroes the accumulators."""
+        self._metrics_on = bool(enable)
+        if enable:
+            W, M = self.W, self.M
+            self._drac_max = torch.zeros((W, M), dtype=torch.float64, device=self.device)
+            self._metric_seen = torch.zeros((W, M), dtype=torch.uint8, device=self.device)
+
+    def reset_episode_metrics(self) -> None:
+        if self._metrics_on:
+            self._drac_max.zero_()
+            self._metric_seen.zero_()
+
+    def episode_metrics(self, threshold: float = 3.4):
+        """SR / CR / mean peak DRAC from the in-kernel accumulators
+        (metrics.EpisodeMetrics, the reference's episode_metrics result)."""
+        from .metrics import aggregate
+        if not self._metrics_on:
+            raise RuntimeError("episode metrics are not tracked: call track_episode_metrics() first")
+        seen = self._metric_seen.cpu().numpy()
+        return aggregate(seen & 1 != 0, seen & 2 != 0, self._drac_max.cpu().numpy(), self.valid, threshold)
+
+    def run_episode(self, policy, record: bool = False, max_steps: int | None = None) -> "EpisodeLog":
         """Step until every agent terminated or the episode times out
-        (engine.py:621-643); returns the per-step records when ``record``."""
-        log = []
+        (engine.py:621-643); the log holds the per-step records when ``record``."""
+        log = EpisodeLog(control_dt=self.config.control_dt)
+        log.initial_state = {k: v.copy() for k, v in self.state.items() if k in LOG_STATE_FIELDS}
         limit = max_steps if max_steps is not None else self.config.episode_len
         obs = self.observe()
         for _ in range(limit):
             actions = policy(obs)
             out = self.step(actions)
             if record:
-                log.append({"step": self._step_count, "state": out.info["state"],
-                            "actions": np.array(actions, dtype=np.float64), "rewards": out.rewards,
-                            "terms": out.info["reward_terms"], "events": out.events,
-                            "dones": out.dones, "alive": out.info["alive"],
-                            "alive_pre": out.info["alive_pre"]})
+                log.append(self._step_count, out.info["state"], actions, out.rewards,
+                           out.info["reward_terms"], out.events, out.dones, out.info["alive"],
+                           out.info["alive_pre"])
             obs = out.obs
             if not out.info["alive"].any() or self._step_count >= self.config.episode_len:
                 break
         return log
+
+
+LOG_STATE_FIELDS = ("x", "y", "yaw", "v_x", "v_y", "yaw_rate", "steer_angle", "wheel_front", "wheel_rear")
+
+
+class EpisodeLog:
+    """Control-rate record of an episode (engine.py:83-145): per-step state
+    snapshots taken before the teleport write-back, actions, rewards, terms,
+    events, dones and alive masks."""
+
+    def __init__(self, control_dt: float, initial_state: dict | None = None):
+        self.control_dt = control_dt
+        self.initial_state = initial_state
+        self.steps = []
+
+    def append(self, step, state, actions, rewards, terms, events, dones, alive, alive_pre):
+        self.steps.append({
+            "step": step,
+            "state": {k: np.array(state[k]) for k in LOG_STATE_FIELDS},
+            "actions": np.array(actions, dtype=np.float64),
+            "rewards": np.array(rewards),
+            "terms": {k: np.array(v) for k, v in terms.items()},
+            "events": {k: np.array(v) for k, v in events.items()},
+            "dones": np.array(dones),
+            "alive": np.array(alive),
+            "alive_pre": np.array(alive_pre),
+        })
+
+    def __len__(self):
+        return len(self.steps)
+
+    def resample_60hz(self) -> list:
+        """States at twice the control rate by midpoint interpolation (engine.py:111-121)."""
+        out, prev = [], self.initial_state
+        for rec in self.steps:
+            cur = rec["state"]
+            if prev is not None:
+                out.append({k: 0.5 * (prev[k] + cur[k]) for k in LOG_STATE_FIELDS})
+            out.append({k: cur[k].copy() for k in LOG_STATE_FIELDS})
+            prev = cur
+        return out
+
+    def to_jsonl(self, path):
+        """One JSON record per (step, world, agent), full float precision (engine.py:123-145)."""
+        import json
+        with open(path, "w", encoding="utf-8") as fh:
+            for rec in self.steps:
+                W, M = rec["alive"].shape
+                st = rec["state"]
+                for w in range(W):
+                    for m in range(M):
+                        fh.write(json.dumps({
+                            "step": rec["step"], "world": w, "agent": m,
+                            "pose": [float(st["x"][w, m]), float(st["y"][w, m]), float(st["yaw"][w, m])],
+                            "vel": [float(st["v_x"][w, m]), float(st["v_y"][w, m]),
+                                    float(st["yaw_rate"][w, m])],
+                            "action": rec["actions"][w, m].tolist(),
+                            "reward": float(rec["rewards"][w, m]),
+                            "terms": {k: float(v[w, m]) for k, v in rec["terms"].items()},
+                            "events": [k for k, v in rec["events"].items() if v[w, m]],
+                            "alive": bool(rec["alive"][w, m]),
+                        }) + "\n")

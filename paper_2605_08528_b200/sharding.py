@@ -81,3 +81,52 @@ def combine(summaries: list) -> dict:
     tot["success_rate_events"] = tot["goal"] / tot["valid_agents"] if tot["valid_agents"] else 0.0
     tot["collision_rate_events"] = tot["collision"] / tot["valid_agents"] if tot["valid_agents"] else 0.0
     return tot
+
+
+# ---------------------------------------------------------------- safety metrics
+METRIC_INT_KEYS = ("valid_agents", "goals", "collisions", "n_drac_over")
+
+
+def metric_summary(per_agent_max_drac, valid, goals: int, collisions: int, threshold: float = 3.4) -> dict:
+    """Sufficient statistics of one rank's episode metrics (metrics.py:110-125):
+    goal / collision agent counts, valid agents, and the count and sum of the
+    per-agent peak DRACs over ``threshold``."""
+    valid = np.asarray(valid, dtype=bool)
+    over = np.asarray(per_agent_max_drac)[valid & (np.asarray(per_agent_max_drac) > threshold)]
+    return {"valid_agents": int(valid.sum()), "goals": int(goals), "collisions": int(collisions),
+            "n_drac_over": int(over.size), "sum_drac_over": float(over.sum())}
+
+
+def allgather_metric_summaries(local: dict, group=None) -> list:
+    """Rank-ordered metric summaries: one all_gather of four int64 counts and
+    one of the float64 DRAC sum (NCCL on GPU ranks, gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    n = dist.get_world_size(group)
+    ti = torch.tensor([local[k] for k in METRIC_INT_KEYS], dtype=torch.int64, device=dev)
+    tf = torch.tensor([local["sum_drac_over"]], dtype=torch.float64, device=dev)
+    pi = [torch.empty_like(ti) for _ in range(n)]
+    pf = [torch.empty_like(tf) for _ in range(n)]
+    dist.all_gather(pi, ti, group=group)
+    dist.all_gather(pf, tf, group=group)
+    out = []
+    for a, b in zip(pi, pf):
+        d = {k: int(v) for k, v in zip(METRIC_INT_KEYS, a.cpu().tolist())}
+        d["sum_drac_over"] = float(b.cpu().item())
+        out.append(d)
+    return out
+
+
+def combine_metrics(summaries: list) -> dict:
+    """SR / CR / mean peak DRAC of the whole job from rank-ordered summaries
+    (the rank order fixes the float summation order: deterministic)."""
+    tot = {k: sum(s[k] for s in summaries) for k in METRIC_INT_KEYS}
+    sdr = 0.0
+    for s in summaries:
+        sdr += s["sum_drac_over"]
+    n = tot["valid_agents"]
+    return {"sr": tot["goals"] / n if n else 0.0, "cr": tot["collisions"] / n if n else 0.0,
+            "mean_max_drac": sdr / tot["n_drac_over"] if tot["n_drac_over"] else 0.0, **tot}

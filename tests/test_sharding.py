@@ -15,7 +15,9 @@ from cases import cfg_of, philox_actions
 from oracle import OracleEngine
 from paper_2605_08528_b200 import config as C
 from paper_2605_08528_b200.params import EVENT_TYPES, STATE_FIELDS
-from paper_2605_08528_b200.sharding import (allgather_summaries, combine, episode_summary,
+from oracle.metrics import aggregate, drac_of_snapshot
+from paper_2605_08528_b200.sharding import (allgather_metric_summaries, allgather_summaries, combine,
+                                            combine_metrics, episode_summary, metric_summary,
                                             shard_inputs, shard_range)
 
 W, M, T = 6, 16, 30
@@ -60,12 +62,33 @@ def _worker(rank, port, result_q):
     acts = philox_actions(2, T, W, M).astype(np.float64)
     lo, hi = shard_range(W, rank, 2)
     counts = np.zeros((hi - lo, 5), dtype=np.int64)
+    acc = _MetricAcc(hi - lo)
     for t in range(T):
-        _counts(eng.step(acts[t][lo:hi]), counts)
+        out = eng.step(acts[t][lo:hi])
+        _counts(out, counts)
+        acc.add(out, eng)
     gathered = allgather_summaries(episode_summary(counts, int(eng.valid.sum())))
+    mg = allgather_metric_summaries(acc.summary(eng.valid))
     if rank == 0:
-        result_q.put(combine(gathered))
+        result_q.put((combine(gathered), combine_metrics(mg)))
     dist.destroy_process_group()
+
+
+class _MetricAcc:
+    def __init__(self, Wl):
+        self.mx = np.zeros((Wl, M))
+        self.goal = np.zeros((Wl, M), dtype=bool)
+        self.coll = np.zeros((Wl, M), dtype=bool)
+
+    def add(self, out, eng):
+        self.mx = np.maximum(self.mx, drac_of_snapshot(out.info["state"], out.info["alive_pre"],
+                                                       eng.r_hull, eng.d_hull))
+        self.goal |= out.events["goal"]
+        self.coll |= out.events["collision"]
+
+    def summary(self, valid):
+        return metric_summary(self.mx, valid, int((self.goal & valid).sum()), int((self.coll & valid).sum()),
+                              threshold=0.0)
 
 
 def test_gloo_allgather_of_episode_counters():
@@ -77,7 +100,7 @@ def test_gloo_allgather_of_episode_counters():
     procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got = q.get(timeout=300)
+    got, got_m = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -86,8 +109,17 @@ def test_gloo_allgather_of_episode_counters():
     eng = OracleEngine(**inp.as_kwargs())
     acts = philox_actions(2, T, W, M).astype(np.float64)
     counts = np.zeros((W, 5), dtype=np.int64)
+    acc = _MetricAcc(W)
     for t in range(T):
-        _counts(eng.step(acts[t]), counts)
+        out = eng.step(acts[t])
+        _counts(out, counts)
+        acc.add(out, eng)
     want = combine([episode_summary(counts, int(eng.valid.sum()))])
     assert got == want
     assert want["alive_ticks"] > 0
+    # the gathered safety metrics equal the single-process episode_metrics reduction
+    ref = aggregate(acc.goal, acc.coll, acc.mx, eng.valid, threshold=0.0)
+    for k in ("goals", "collisions", "valid_agents", "sr", "cr"):
+        assert got_m[k] == ref[k], k
+    assert got_m["n_drac_over"] == int((acc.mx[eng.valid] > 0.0).sum()) > 0
+    np.testing.assert_allclose(got_m["mean_max_drac"], ref["mean_max_drac"], rtol=1e-12)
