@@ -225,6 +225,50 @@ int dg_tune(dg_engine* eng, int32_t mode, int32_t warps_per_world, int32_t ctas_
 /* Device scratch the split mode needs (per-agent records between its kernels). */
 size_t dg_scratch_bytes(int32_t W, int32_t M);
 
+/* ------------------------------------------------------------------------
+ * Policy MLP (BASELINE configs[4]: the rollout's batched policy forward,
+ * fused into the env loop on the device).  The reference has no policy code;
+ * the network is the paper's App. E: per-net ego
+ * 11->64->64, road 5->96->96 and vehicle 7->96->96 encoders with masked
+ * max-pool over the observation's valid slots, trunk 256->128->64 (ELU),
+ * actor head 64->3 (mean), critic head 64->1; actor and critic do not share
+ * weights.  Runs on tcgen05 tensor cores (bf16 operands, fp32 accumulate).
+ *
+ * Weights: one blob per net (net 0 = actor, 1 = critic), net n at
+ * weights + n * net_stride; off[] = byte offsets of the sections below inside
+ * a net's blob (16-byte aligned).  W_* sections are bf16 tiles [out][in] in
+ * the canonical K-major UMMA layout (8x8 core matrices, element (r, k) at
+ * ((r/8)*(K/8) + k/8)*128 + (r%8)*16 + (k%8)*2, K = in padded to 16 for the
+ * first layers); B_* and W_HEAD / B_HEAD are float32 (W_HEAD [out][64]). */
+enum {
+    DG_POL_W_EGO1 = 0, DG_POL_W_EGO2, DG_POL_W_T1, DG_POL_W_T2,
+    DG_POL_W_ROAD1, DG_POL_W_ROAD2, DG_POL_W_VEH1, DG_POL_W_VEH2,
+    DG_POL_B_EGO1, DG_POL_B_EGO2, DG_POL_B_ROAD1, DG_POL_B_ROAD2, DG_POL_B_VEH1, DG_POL_B_VEH2,
+    DG_POL_B_T1, DG_POL_B_T2, DG_POL_W_HEAD, DG_POL_B_HEAD,
+    DG_POL_NUM_SECTIONS
+};
+
+typedef struct DgPolicyDesc {
+    int32_t n_agents;           /* rows of obs (W * M)                              */
+    int32_t obs_dim, ego_dim, k_road, k_vehicles;
+    int32_t critic;             /* 1: also run net 1 (value head)                   */
+    const float* obs;           /* [n_agents][obs_dim] float32, device              */
+    const uint8_t* weights;     /* net blobs, device                                */
+    int64_t net_stride;
+    int64_t off[DG_POL_NUM_SECTIONS];
+    uint16_t* emb;              /* scratch: dg_policy_scratch_bytes(n_agents, nets)  */
+    float* mean;                /* [n_agents][3] actor mean, or NULL                */
+    double* actions;            /* [n_agents][3] the same mean as float64 env actions
+                                   (the next tick's input), or NULL                */
+    float* value;               /* [n_agents] critic value, or NULL                 */
+} DgPolicyDesc;
+
+/* One forward of the policy over every agent's observation row: 2 kernel
+ * launches (encoders, trunk + heads), asynchronous on stream. */
+int dg_policy_forward(const DgPolicyDesc* desc, void* stream);
+size_t dg_policy_scratch_bytes(int32_t n_agents, int32_t nets);
+const char* dg_policy_last_error(void);
+
 const char* dg_last_error(void);
 int dg_abi_version(void);
 

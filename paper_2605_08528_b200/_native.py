@@ -16,8 +16,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB_PATH = PKG / "libdrivegrid_b200.so"
-SOURCES = [PKG / "csrc" / "drivegrid_b200.cu"]
-DEPS = [PKG / "csrc" / "dg_fastmath.cuh"]
+SOURCES = [PKG / "csrc" / "drivegrid_b200.cu", PKG / "csrc" / "dg_policy.cu"]
+DEPS = [PKG / "csrc" / "dg_fastmath.cuh", PKG / "csrc" / "dg_umma.cuh"]
 HEADER = ROOT / "include" / "drivegrid_b200.h"
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-fmad=false", "-Xcompiler", "-fPIC", "-shared"]
@@ -64,6 +64,17 @@ class DgEngineDesc(ct.Structure):
         "spawn_step", "step_count", "start_xy", "goal_xy", "start_yaw", "error_word", "scratch")]
 
 
+POL_SECTIONS = ("W_EGO1", "W_EGO2", "W_T1", "W_T2", "W_ROAD1", "W_ROAD2", "W_VEH1", "W_VEH2",
+                "B_EGO1", "B_EGO2", "B_ROAD1", "B_ROAD2", "B_VEH1", "B_VEH2", "B_T1", "B_T2",
+                "W_HEAD", "B_HEAD")
+
+
+class DgPolicyDesc(ct.Structure):
+    _fields_ = [(n, ct.c_int32) for n in ("n_agents", "obs_dim", "ego_dim", "k_road", "k_vehicles", "critic")] + [
+        ("obs", _P), ("weights", _P), ("net_stride", ct.c_int64), ("off", ct.c_int64 * len(POL_SECTIONS)),
+        ("emb", _P), ("mean", _P), ("actions", _P), ("value", _P)]
+
+
 class DgStepIO(ct.Structure):
     _fields_ = [("actions", _P), ("actions_f64", ct.c_int32), ("autoreset", ct.c_int32)] + [
         (n, _P) for n in ("obs", "rewards", "dones", "events", "reason_out", "alive_out",
@@ -91,6 +102,9 @@ SIGNATURES = {
     "dg_launch_count": (ct.c_int, [_P]),
     "dg_tune": (ct.c_int, [_P, ct.c_int32, ct.c_int32, ct.c_int32]),
     "dg_scratch_bytes": (ct.c_size_t, [ct.c_int32, ct.c_int32]),
+    "dg_policy_forward": (ct.c_int, [ct.POINTER(DgPolicyDesc), _P]),
+    "dg_policy_scratch_bytes": (ct.c_size_t, [ct.c_int32, ct.c_int32]),
+    "dg_policy_last_error": (ct.c_char_p, []),
     "dg_pairwise_drac": (ct.c_int, [_P] * 8 + [ct.c_int32, ct.c_int32, ct.c_int32, _P, ct.c_int32, ct.c_int32, _P]),
 }
 
