@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--cpu-steps", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] policy-rollout line")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly from the host (slower)")
     ap.add_argument("--ticks-per-launch", type=int, default=0,
                     help="control ticks per persistent kernel launch (0 = default for the shape)")
@@ -373,11 +374,99 @@ def main():
         # e2e through the numpy API
         e2e_steps = args.e2e_steps or max(10, min(args.steps, 50))
         line["e2e"] = e2e_numpy(eng, e2e_steps)
+        if not args.no_c5 and world_size == 1:
+            line["c5_policy_rollout"] = bench_c5(dev)
         if not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(args.cpu_steps or 40)
         print(json.dumps(line), flush=True)
     if world_size > 1:
         dist.destroy_process_group()
+
+
+def policy_flops_per_agent(n_road: float, n_veh: float, ego_dim: int = 11, nets: int = 2) -> float:
+    """Algorithmic FLOPs of one policy forward per agent (App. E network,
+    policy.py): only VALID road / vehicle slots count (masked max-pool
+    ignores the rest); 2 FLOP per MAC; actor + critic."""
+    per_net = (n_road * (5 * 96 + 96 * 96) + n_veh * (7 * 96 + 96 * 96)
+               + ego_dim * 64 + 64 * 64 + 256 * 128 + 128 * 64)
+    return 2.0 * nets * per_net + 2.0 * 64 * (3 + 1)
+
+
+def bench_c5(dev, ticks=128, W=1024, M=16, reps=2):
+    """BASELINE configs[4]: 1024 x 16 rollout of T=128 ticks with the policy
+    MLP (actor mean -> next actions, critic values) fused into the loop on
+    the device: per tick one step launch + two tcgen05 policy launches, the
+    whole rollout one CUDA graph.  Returns a dict for the JSON line."""
+    import torch
+    from paper_2605_08528_b200.engine import Engine
+    from paper_2605_08528_b200.policy import PolicyMLP
+
+    inp = shard_inputs(root_config(W, M), 0, 1)
+    eng = Engine(**inp.as_kwargs(), device=dev)
+    D = eng.obs_config.obs_dim
+    pol = PolicyMLP(eng.obs_config, seed=0, device=dev, head_scale=1.0)
+    rb = eng.new_rollout_buffers(ticks)          # [T][W][M][D]: 1 GB > L2, every tick its own slot
+    values = torch.empty((ticks, W, M), dtype=torch.float32, device=dev)
+    acts = torch.zeros((W, M, 3), dtype=torch.float64, device=dev)
+    acts[..., 0] = 0.5
+    counters = torch.zeros((W, 5), dtype=torch.int32, device=dev)
+    # warm-up (allocates the policy scratch, packs the weights)
+    eng.run_mlp_ticks(acts, rb, pol, 4, autoreset=True, values=values)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    launches0 = eng.launches
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        eng.run_mlp_ticks(acts, rb, pol, ticks, autoreset=True, values=values, event_counts=counters)
+    launches = eng.launches - launches0
+    g.replay()
+    torch.cuda.synchronize()
+    counters.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    alive_ticks = int(counters[:, 4].sum().item()) / reps
+    # the two halves of a tick, each timed alone over the same T ticks
+    obs_last = rb.obs[ticks - 1]
+    gp = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gp):
+        for _ in range(ticks):
+            pol.forward(obs_last, actions=acts, value=values[0])
+    ge = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(ge):
+        for t in range(ticks):
+            eng.launch_step(acts, rb, autoreset=True, ticks=1, ring_start=t)
+    res = {}
+    for name, gg in (("policy", gp), ("env", ge)):
+        gg.replay()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        gg.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res[name] = e0.elapsed_time(e1) / ticks
+    oc = eng.obs_config
+    road = obs_last[..., oc.ego_dim:oc.ego_dim + 5 * oc.k_road].reshape(W, M, oc.k_road, 5)
+    veh = obs_last[..., oc.ego_dim + 5 * oc.k_road:].reshape(W, M, oc.k_vehicles, 7)
+    n_road = float(((road[..., 3] != 0) | (road[..., 4] != 0)).sum(-1).float().mean())
+    n_veh = float((veh[..., 2] != 0).sum(-1).float().mean())
+    flops = policy_flops_per_agent(n_road, n_veh, oc.ego_dim) * W * M
+    peak = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops_sustained"] \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else 1400.0
+    achieved = flops / (res["policy"] / 1e3) / 1e12
+    return {"metric": "CASPS", "value": alive_ticks / (ms / 1e3), "unit": "agent-steps/s",
+            "workload": f"{W}x{M} default pool, T={ticks} rollout, policy MLP (actor mean + critic value) "
+                        "fused: step + 2 tcgen05 launches per tick, autoreset, one CUDA graph",
+            "ms_per_tick": ms / ticks, "env_ms_per_tick": res["env"], "policy_ms_per_tick": res["policy"],
+            "gpu_launches": launches, "launches_per_tick": launches / ticks,
+            "valid_slots_per_agent": {"road": n_road, "vehicle": n_veh},
+            "policy_roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                                "frac": achieved / peak, "flops_per_agent": flops / (W * M),
+                                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained"}}
 
 
 def e2e_numpy(eng, steps):

@@ -40,7 +40,7 @@
 
 namespace {
 
-constexpr int kEncAgents = 64;     // agents per encoder CTA
+constexpr int kEncAgents = 32;     // agents per encoder CTA
 constexpr int kTrunkAgents = 128;  // agents per trunk CTA (one TMEM lane each)
 constexpr int kThreads = 128;
 constexpr int kHid = 96;           // road / vehicle encoder width
@@ -49,6 +49,16 @@ constexpr int kT1 = 128, kT2 = 64;
 constexpr int kEmb = 2 * kHid;     // pooled road | vehicle, bf16, per agent and net
 
 __device__ __forceinline__ float elu(float x) { return x > 0.0f ? x : __expf(x) - 1.0f; }
+
+constexpr float kLog2e = 1.4426950408889634f;
+// log2(e) * ELU(y / log2(e)): the encoders' first layers carry a log2(e) factor
+// in their weights and bias (policy.py, fold_first_layer), so the exponential is
+// one ex2 and the scale folds into one FFMA; the next layer's weights carry ln 2.
+__device__ __forceinline__ float elu_log2(float y) {
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(y));
+    return y > 0.0f ? y : fmaf(e, kLog2e, -kLog2e);
+}
 
 // float <-> order-preserving unsigned (0 = "no value yet")
 __device__ __forceinline__ uint32_t f2o(float x) {
@@ -89,15 +99,16 @@ __device__ __forceinline__ const float* fsec(const DgPolicyDesc& p, int net, int
 
 // ------------------------------------------------------------------ encoder
 // Shared memory (bytes): A0 128x16 bf16 | A1 128x96 bf16 | W1 96x16 | W2 96x96 |
-// b1 f32[96] | acc u32[64][96] | cnt[64] | segstart[65] | seg u16[64 * 44] | bars
+// acc u32[32][97] | cnt[32] | segstart[36] | seg u16[32 * ceil(K/8)] | bars
+constexpr int kEncThreads = 256;   // 8 warps: lane quarter = warp % 4, column half = warp / 4
+constexpr int kAccStride = kHid + 1;
 struct EncSmem {
     static constexpr int kA0 = 0;
     static constexpr int kA1 = kA0 + 128 * 16 * 2;
     static constexpr int kW1 = kA1 + 128 * kHid * 2;
     static constexpr int kW2 = kW1 + kHid * 16 * 2;
-    static constexpr int kB1 = kW2 + kHid * kHid * 2;
-    static constexpr int kAcc = kB1 + kHid * 4;
-    static constexpr int kCnt = kAcc + kEncAgents * kHid * 4;
+    static constexpr int kAcc = kW2 + kHid * kHid * 2;
+    static constexpr int kCnt = kAcc + kEncAgents * kAccStride * 4;
     static constexpr int kSegStart = kCnt + kEncAgents * 4;
     static constexpr int kSeg = kSegStart + (kEncAgents + 4) * 4;
 };
@@ -107,7 +118,23 @@ __host__ __device__ __forceinline__ size_t enc_smem_bytes(int k_max) {
     return size_t(EncSmem::kSeg) + ((size_t(enc_seg_cap(k_max)) * 2 + 15) & ~size_t(15)) + 64;
 }
 
-__global__ void __launch_bounds__(kThreads, 2) policy_encoder_kernel(const DgPolicyDesc p) {
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
+__device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(umma::smem_u32(bar)), "r"(bytes) : "memory");
+}
+// TMA bulk copy global -> shared, completing on bar (after expect_tx of the total)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(umma::smem_u32(dst)), "l"(src), "r"(bytes), "r"(umma::smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const DgPolicyDesc p) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int net = blockIdx.y;
@@ -117,23 +144,29 @@ __global__ void __launch_bounds__(kThreads, 2) policy_encoder_kernel(const DgPol
     uint8_t* A1 = sm + EncSmem::kA1;
     uint8_t* W1 = sm + EncSmem::kW1;
     uint8_t* W2 = sm + EncSmem::kW2;
-    float* b1 = reinterpret_cast<float*>(sm + EncSmem::kB1);
     uint32_t* acc = reinterpret_cast<uint32_t*>(sm + EncSmem::kAcc);
     int* cnt = reinterpret_cast<int*>(sm + EncSmem::kCnt);
     int* segstart = reinterpret_cast<int*>(sm + EncSmem::kSegStart);
     uint16_t* seg = reinterpret_cast<uint16_t*>(sm + EncSmem::kSeg);
     const int kmax = p.k_road > p.k_vehicles ? p.k_road : p.k_vehicles;
     uint8_t* tail = sm + EncSmem::kSeg + ((enc_seg_cap(kmax) * 2 + 15) & ~15);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(tail);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tail);          // [0] MMA, [1] weights
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tail + 16);
 
-    if (warp == 0) umma::tmem_alloc(tmem_slot, 256);
-    if (tid == 0) umma::bar_init(bar, 1);
+    if (warp == 0) umma::tmem_alloc(tmem_slot, 128);
+    if (tid == 32) {
+        umma::bar_init(bar, 1);
+        umma::bar_init(bar + 1, 1);
+    }
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t lane_base = uint32_t(32 * warp) << 16;
+    const uint32_t tmem = *tmem_slot;     // D1 and D2 share columns 0..95 (D1 is drained before MMA2)
+    // epilogue mapping: TMEM lane quarter q (rows 32q..32q+31), column half hf (48 columns)
+    const int q = warp & 3, hf = warp >> 2;
+    const int r = 32 * q + lane;                       // this thread's tile row
+    const uint32_t lane_base = uint32_t(32 * q) << 16;
+    const int c0 = 48 * hf;
     uint32_t phase = 0;
     const uint8_t* wb = net_base(p, net);
 
@@ -143,85 +176,121 @@ __global__ void __launch_bounds__(kThreads, 2) policy_encoder_kernel(const DgPol
         const int fbase = mod == 0 ? p.ego_dim : p.ego_dim + 5 * p.k_road;
         const int w1 = mod == 0 ? DG_POL_W_ROAD1 : DG_POL_W_VEH1;
         const int w2 = mod == 0 ? DG_POL_W_ROAD2 : DG_POL_W_VEH2;
-        const float* gb1 = fsec(p, net, mod == 0 ? DG_POL_B_ROAD1 : DG_POL_B_VEH1);
         const float* gb2 = fsec(p, net, mod == 0 ? DG_POL_B_ROAD2 : DG_POL_B_VEH2);
 
-        // weights of this modality -> shared memory; accumulators cleared
-        copy_to_smem(W1, wb + p.off[w1], kHid * 16 * 2, tid, kThreads);
-        copy_to_smem(W2, wb + p.off[w2], kHid * kHid * 2, tid, kThreads);
-        for (int i = tid; i < kHid; i += kThreads) b1[i] = __ldg(gb1 + i);
-        for (int i = tid; i < kEncAgents * kHid; i += kThreads) acc[i] = 0u;
+        // weights of this modality: TMA bulk copies (the previous modality's MMAs are done)
+        if (tid == 0) {
+            expect_tx(bar + 1, kHid * 16 * 2 + kHid * kHid * 2);
+            bulk_g2s(W1, wb + p.off[w1], kHid * 16 * 2, bar + 1);
+            bulk_g2s(W2, wb + p.off[w2], kHid * kHid * 2, bar + 1);
+        }
+        for (int i = tid; i < kEncAgents * kAccStride; i += kEncThreads) acc[i] = 0u;
 
-        // valid slot counts: the valid slots are a prefix; warp per agent, 32 slots per probe
-        for (int a = warp; a < na; a += kThreads / 32) {
-            const float* row = p.obs + int64_t(a0 + a) * p.obs_dim + fbase;
-            int c = 0;
+        // valid slot counts (the valid slots are a prefix): warp w probes agents 4w..4w+3,
+        // 32 slots per round, the four agents' loads in flight together
+        {
+            int c4[4] = {0, 0, 0, 0};
+            bool more[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) more[j] = 4 * warp + j < na;
             for (int s0 = 0; s0 < kslots; s0 += 32) {
                 const int s = s0 + lane;
-                bool ok = false;
-                if (s < kslots) {
-                    const float* f = row + s * nf;
-                    ok = mod == 0 ? (__ldg(f + 3) != 0.0f || __ldg(f + 4) != 0.0f) : (__ldg(f + 2) != 0.0f);
+                bool ok[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    ok[j] = false;
+                    if (more[j] && s < kslots) {
+                        const float* f = p.obs + int64_t(a0 + 4 * warp + j) * p.obs_dim + fbase + s * nf;
+                        ok[j] = mod == 0 ? (__ldg(f + 3) != 0.0f || __ldg(f + 4) != 0.0f) : (__ldg(f + 2) != 0.0f);
+                    }
                 }
-                const unsigned b = __ballot_sync(0xffffffffu, ok);
-                c += __popc(b);
-                if (b != 0xffffffffu) break;
+                bool any = false;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const unsigned b = __ballot_sync(0xffffffffu, ok[j]);
+                    if (more[j]) {
+                        c4[j] += __popc(b);
+                        more[j] = b == 0xffffffffu;
+                    }
+                    any |= more[j];
+                }
+                if (!any) break;
             }
-            if (lane == 0) cnt[a] = c;
+            if (lane < 4 && 4 * warp + lane < na) cnt[4 * warp + lane] = c4[0] * (lane == 0) + c4[1] * (lane == 1) +
+                                                                        c4[2] * (lane == 2) + c4[3] * (lane == 3);
         }
         __syncthreads();
-        if (tid == 0) {
-            int s = 0;
-            for (int a = 0; a < na; ++a) {
-                segstart[a] = s;
-                s += (cnt[a] + 7) >> 3;
+        if (warp == 0) {
+            // exclusive scan of the per-agent segment counts (one agent per lane)
+            const int n0 = lane < na ? (cnt[lane] + 7) >> 3 : 0;
+            int incl = n0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
             }
-            segstart[na] = s;
+            if (lane <= na) segstart[lane] = incl - n0;
+            if (lane == 31 && na == kEncAgents) segstart[kEncAgents] = incl;
         }
         __syncthreads();
         const int S = segstart[na];
-        for (int a = warp; a < na; a += kThreads / 32) {
+        for (int a = warp; a < na; a += kEncThreads / 32) {
             const int s0 = segstart[a], n = segstart[a + 1] - s0;
             for (int j = lane; j < n; j += 32) seg[s0 + j] = uint16_t((a << 8) | j);
         }
-        umma::fence_async_smem();
         __syncthreads();
 
-        for (int t0 = 0; t0 < S; t0 += 16) {
-            // ---- A0: this row's point features (bf16, K padded to 16)
-            const int r = tid;
+        // features of row r for the tile starting at segment t0 (warps 0-3 build A0)
+        auto fetch = [&](int t0, float* f) {
             const int s = t0 + (r >> 3);
-            const bool valid = s < S;
-            float f[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) f[i] = 0.0f;
-            int a = 0;
-            if (valid) {
+            for (int i = 0; i < 8; ++i) f[i] = 0.0f;
+            if (hf == 0 && s < S) {
                 const int e = seg[s];
-                a = e >> 8;
+                const int a = e >> 8;
                 int slot = 8 * (e & 255) + (r & 7);
                 if (slot >= cnt[a]) slot = 0;                   // duplicate of a valid point
                 const float* src = p.obs + int64_t(a0 + a) * p.obs_dim + fbase + slot * nf;
-                for (int i = 0; i < nf; ++i) f[i] = __ldg(src + i);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (i < nf) f[i] = __ldg(src + i);
+                    if (i == nf) f[i] = 1.0f;                   // bias column of W1
+                }
             }
-            store_row16(A0, r, 0, 16, f);
+        };
+        float fcur[8];
+        fetch(0, fcur);
+        for (int t0 = 0; t0 < S; t0 += 16) {
+            const int s = t0 + (r >> 3);                 // this row's segment
+            const bool valid = s < S;
+            const int a = valid ? (seg[s] >> 8) : 0;
+            // ---- A0: point features of row r (bf16, K padded to 16, constant-1 bias column)
+            if (hf == 0) {
+                float f[16];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) { f[i] = fcur[i]; f[8 + i] = 0.0f; }
+                store_row16(A0, r, 0, 16, f);
+            }
             umma::fence_async_smem();
+            umma::fence_before();
             __syncthreads();
             if (tid == 0) {
+                if (t0 == 0) umma::bar_wait(bar + 1, uint32_t(mod));   // weights landed
                 umma::fence_after();
                 umma::gemm_128xN(tmem, A0, W1, kHid, 16);
                 umma::commit(bar);
             }
+            fetch(t0 + 16, fcur);                        // next tile's features, in flight meanwhile
             umma::bar_wait(bar, phase);
             phase ^= 1u;
             umma::fence_after();
-            // ---- L1 epilogue: +b1, ELU -> A1 (bf16)
+            // ---- L1 epilogue: (bias already in the GEMM) log2e-scaled ELU -> A1 (bf16),
+            //      48 columns per thread
 #pragma unroll 1
-            for (int c = 0; c < kHid; c += 16) {
+            for (int c = c0; c < c0 + 48; c += 16) {
                 float v[16];
                 umma::tmem_ld16(tmem + lane_base + c, v);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = elu(v[i] + b1[c + i]);
+                for (int i = 0; i < 16; ++i) v[i] = elu_log2(v[i]);
                 store_row16(A1, r, c, kHid, v);
             }
             umma::fence_async_smem();
@@ -229,47 +298,76 @@ __global__ void __launch_bounds__(kThreads, 2) policy_encoder_kernel(const DgPol
             __syncthreads();
             if (tid == 0) {
                 umma::fence_after();
-                umma::gemm_128xN(tmem + 128, A1, W2, kHid, kHid);
+                umma::gemm_128xN(tmem, A1, W2, kHid, kHid);
                 umma::commit(bar);
             }
             umma::bar_wait(bar, phase);
             phase ^= 1u;
             umma::fence_after();
-            // ---- L2 epilogue: segment max of the raw accumulator (8 rows = 8 lanes)
-#pragma unroll 1
-            for (int c = 0; c < kHid; c += 16) {
-                float v[16];
-                umma::tmem_ld16(tmem + lane_base + 128 + c, v);
+            // ---- L2 epilogue: segment max of the raw accumulator, rounded to bf16
+            //      (rounding is monotone: max of rounded == rounded max).  The 8 rows of
+            //      a segment are 8 consecutive lanes: a 3-stage transpose-butterfly on
+            //      bf16x2 pairs leaves each lane 6 of the 48 columns' maxima.
+            uint32_t pk[24];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    float x = valid ? v[i] : -INFINITY;
-                    x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 1));
-                    x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 2));
-                    x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 4));
-                    if (valid && (r & 7) == 0) atomicMax(acc + a * kHid + c + i, f2o(x));
+            for (int cc = 0; cc < 3; ++cc) {
+                float v[16];
+                umma::tmem_ld16(tmem + lane_base + c0 + 16 * cc, v);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) pk[8 * cc + i] = valid ? umma::pack_bf16(v[2 * i], v[2 * i + 1]) : 0xff80ff80u;
+            }
+            const bool bA = (lane >> 2) & 1, bB = (lane >> 1) & 1, bC = lane & 1;
+            uint32_t qa[12];
+#pragma unroll
+            for (int j = 0; j < 12; ++j) {
+                const uint32_t snd = bA ? pk[j] : pk[12 + j];
+                const uint32_t keep = bA ? pk[12 + j] : pk[j];
+                qa[j] = bmax2(keep, __shfl_xor_sync(0xffffffffu, snd, 4));
+            }
+            uint32_t qb[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) {
+                const uint32_t snd = bB ? qa[j] : qa[6 + j];
+                const uint32_t keep = bB ? qa[6 + j] : qa[j];
+                qb[j] = bmax2(keep, __shfl_xor_sync(0xffffffffu, snd, 2));
+            }
+            uint32_t qc[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const uint32_t snd = bC ? qb[j] : qb[3 + j];
+                const uint32_t keep = bC ? qb[3 + j] : qb[j];
+                qc[j] = bmax2(keep, __shfl_xor_sync(0xffffffffu, snd, 1));
+            }
+            if (valid) {
+                const int col = c0 + 24 * bA + 12 * bB + 6 * bC;
+                uint32_t* dst = acc + a * kAccStride + col;
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    atomicMax(dst + 2 * j, f2o(__uint_as_float(qc[j] << 16)));
+                    atomicMax(dst + 2 * j + 1, f2o(__uint_as_float(qc[j] & 0xffff0000u)));
                 }
             }
-            umma::fence_before();
-            __syncthreads();
         }
         __syncthreads();
-        // ---- pooled embedding = ELU(max + b2), zero when the agent has no valid slot
+        // ---- pooled embedding = ELU(max + b2), zero when the agent has no valid slot;
+        //      two bf16 per thread and store
         uint16_t* out = p.emb + (int64_t(net) * p.n_agents + a0) * kEmb + mod * kHid;
-        for (int i = tid; i < na * kHid; i += kThreads) {
-            const int a = i / kHid, c = i % kHid;
-            const uint32_t u = acc[i];
-            const float v = u ? elu(o2f(u) + __ldg(gb2 + c)) : 0.0f;
-            const uint32_t pk = umma::pack_bf16(v, 0.0f);
-            out[int64_t(a) * kEmb + c] = uint16_t(pk & 0xffffu);
+        for (int i = tid; i < na * (kHid / 2); i += kEncThreads) {
+            const int a = i / (kHid / 2), c = 2 * (i % (kHid / 2));
+            const uint32_t u0 = acc[a * kAccStride + c], u1 = acc[a * kAccStride + c + 1];
+            const float v0 = u0 ? elu(o2f(u0) + __ldg(gb2 + c)) : 0.0f;
+            const float v1 = u1 ? elu(o2f(u1) + __ldg(gb2 + c + 1)) : 0.0f;
+            *reinterpret_cast<uint32_t*>(out + int64_t(a) * kEmb + c) = umma::pack_bf16(v0, v1);
         }
         __syncthreads();
     }
     umma::fence_before();
     __syncthreads();
-    if (warp == 0) umma::tmem_dealloc(tmem, 256);
+    if (warp == 0) umma::tmem_dealloc(tmem, 128);
 }
 
 // ------------------------------------------------------------------ trunk
+constexpr int kTrunkThreads = 256;   // 8 warps: lane quarter = warp % 4, column half = warp / 4
 struct TrunkSmem {
     static constexpr int kWe1 = 0;                                  // 64 x 16
     static constexpr int kWe2 = kWe1 + kEgo * 16 * 2;               // 64 x 64
@@ -280,16 +378,18 @@ struct TrunkSmem {
     static constexpr int kAt = kAe1 + 128 * kEgo * 2;               // 128 x 256
     static constexpr int kAt2 = kAt + 128 * 256 * 2;                // 128 x 128
     static constexpr int kBias = kAt2 + 128 * kT1 * 2;              // f32: be1 64, be2 64, bt1 128, bt2 64, wh 4x64, bh 4
-    static constexpr int kBar = kBias + (64 + 64 + 128 + 64 + 256 + 4) * 4;
+    static constexpr int kHead = kBias + (64 + 64 + 128 + 64 + 256 + 4) * 4;   // f32 [128][4] partial heads
+    static constexpr int kBar = kHead + 128 * 4 * 4;
     static constexpr int kTotal = kBar + 64;
 };
 
-__global__ void __launch_bounds__(kThreads, 1) policy_trunk_kernel(const DgPolicyDesc p) {
+__global__ void __launch_bounds__(kTrunkThreads, 1) policy_trunk_kernel(const DgPolicyDesc p) {
     extern __shared__ __align__(1024) uint8_t sm[];
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int net = blockIdx.y;
     const int a0 = blockIdx.x * kTrunkAgents;
-    const int r = tid;
+    const int q = warp & 3, hf = warp >> 2;
+    const int r = 32 * q + lane;                    // tile row = agent a0 + r
     const int agent = a0 + r;
     const bool live = agent < p.n_agents;
     uint8_t* We1 = sm + TrunkSmem::kWe1;
@@ -306,41 +406,55 @@ __global__ void __launch_bounds__(kThreads, 1) policy_trunk_kernel(const DgPolic
     float* bt2 = bt1 + 128;
     float* wh = bt2 + 64;
     float* bh = wh + 256;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + TrunkSmem::kBar);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + TrunkSmem::kBar + 16);
+    float* part = reinterpret_cast<float*>(sm + TrunkSmem::kHead);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + TrunkSmem::kBar);   // [0] mma, [1..3] weights
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + TrunkSmem::kBar + 32);
 
-    if (warp == 0) umma::tmem_alloc(tmem_slot, 256);
-    if (tid == 0) umma::bar_init(bar, 1);
     const uint8_t* wb = net_base(p, net);
-    copy_to_smem(We1, wb + p.off[DG_POL_W_EGO1], kEgo * 16 * 2, tid, kThreads);
-    copy_to_smem(We2, wb + p.off[DG_POL_W_EGO2], kEgo * kEgo * 2, tid, kThreads);
-    copy_to_smem(Wt1, wb + p.off[DG_POL_W_T1], kT1 * 256 * 2, tid, kThreads);
-    copy_to_smem(Wt2, wb + p.off[DG_POL_W_T2], kT2 * kT1 * 2, tid, kThreads);
+    if (warp == 0) umma::tmem_alloc(tmem_slot, 256);
+    if (tid == 32) {
+        // weights by TMA bulk copies, one mbarrier each, so the ego layers start
+        // while the 64 KB trunk matrix is still in flight
+        for (int i = 0; i < 4; ++i) umma::bar_init(bar + i, 1);
+        expect_tx(bar + 1, kEgo * 16 * 2 + kEgo * kEgo * 2);
+        expect_tx(bar + 2, kT1 * 256 * 2);
+        expect_tx(bar + 3, kT2 * kT1 * 2);
+        bulk_g2s(We1, wb + p.off[DG_POL_W_EGO1], kEgo * 16 * 2, bar + 1);
+        bulk_g2s(We2, wb + p.off[DG_POL_W_EGO2], kEgo * kEgo * 2, bar + 1);
+        bulk_g2s(Wt1, wb + p.off[DG_POL_W_T1], kT1 * 256 * 2, bar + 2);
+        bulk_g2s(Wt2, wb + p.off[DG_POL_W_T2], kT2 * kT1 * 2, bar + 3);
+    }
     const int nout = net == 0 ? 3 : 1;
     {
         const float* g;
-        g = fsec(p, net, DG_POL_B_EGO1); for (int i = tid; i < 64; i += kThreads) be1[i] = __ldg(g + i);
-        g = fsec(p, net, DG_POL_B_EGO2); for (int i = tid; i < 64; i += kThreads) be2[i] = __ldg(g + i);
-        g = fsec(p, net, DG_POL_B_T1); for (int i = tid; i < 128; i += kThreads) bt1[i] = __ldg(g + i);
-        g = fsec(p, net, DG_POL_B_T2); for (int i = tid; i < 64; i += kThreads) bt2[i] = __ldg(g + i);
-        g = fsec(p, net, DG_POL_W_HEAD); for (int i = tid; i < nout * 64; i += kThreads) wh[i] = __ldg(g + i);
-        g = fsec(p, net, DG_POL_B_HEAD); for (int i = tid; i < nout; i += kThreads) bh[i] = __ldg(g + i);
+        g = fsec(p, net, DG_POL_B_EGO1); for (int i = tid; i < 64; i += kTrunkThreads) be1[i] = __ldg(g + i);
+        g = fsec(p, net, DG_POL_B_EGO2); for (int i = tid; i < 64; i += kTrunkThreads) be2[i] = __ldg(g + i);
+        g = fsec(p, net, DG_POL_B_T1); for (int i = tid; i < 128; i += kTrunkThreads) bt1[i] = __ldg(g + i);
+        g = fsec(p, net, DG_POL_B_T2); for (int i = tid; i < 64; i += kTrunkThreads) bt2[i] = __ldg(g + i);
+        g = fsec(p, net, DG_POL_W_HEAD); for (int i = tid; i < nout * 64; i += kTrunkThreads) wh[i] = __ldg(g + i);
+        g = fsec(p, net, DG_POL_B_HEAD); for (int i = tid; i < nout; i += kTrunkThreads) bh[i] = __ldg(g + i);
     }
-    // ego features (K padded to 16) and the pooled road | vehicle embeddings
-    {
+    // ego features (K padded to 16; warps 0-3) and the pooled road | vehicle embeddings
+    // (bf16 rows of 192, 12 of the 24 16-byte chunks per thread)
+    if (hf == 0) {
         float f[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) f[i] = 0.0f;
         if (live) {
             const float* src = p.obs + int64_t(agent) * p.obs_dim;
-            for (int i = 0; i < p.ego_dim; ++i) f[i] = __ldg(src + i);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                if (i < p.ego_dim) f[i] = __ldg(src + i);
         }
         store_row16(Ae0, r, 0, 16, f);
+    }
+    {
         const uint4* e = reinterpret_cast<const uint4*>(p.emb + (int64_t(net) * p.n_agents + agent) * kEmb);
-#pragma unroll 4
-        for (int q = 0; q < kEmb / 8; ++q) {
-            const uint4 v = live ? __ldg(e + q) : make_uint4(0u, 0u, 0u, 0u);
-            *reinterpret_cast<uint4*>(At + umma::kmajor_offset(r, kEgo + 8 * q, 256)) = v;
+#pragma unroll
+        for (int j = 0; j < 12; ++j) {
+            const int qq = 12 * hf + j;
+            const uint4 v = live ? __ldg(e + qq) : make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(At + umma::kmajor_offset(r, kEgo + 8 * qq, 256)) = v;
         }
     }
     umma::fence_async_smem();
@@ -348,11 +462,12 @@ __global__ void __launch_bounds__(kThreads, 1) policy_trunk_kernel(const DgPolic
     __syncthreads();
     umma::fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t lane_base = uint32_t(32 * warp) << 16;
+    const uint32_t lane_base = uint32_t(32 * q) << 16;
     uint32_t phase = 0;
 
-    auto run = [&](uint32_t tcol, const uint8_t* A, const uint8_t* B, int N, int K) {
+    auto run = [&](uint32_t tcol, const uint8_t* A, const uint8_t* B, int N, int K, int wbar) {
         if (tid == 0) {
+            umma::bar_wait(bar + wbar, 0);           // weights landed (TMA)
             umma::fence_after();
             umma::gemm_128xN(tmem + tcol, A, B, N, K);
             umma::commit(bar);
@@ -367,10 +482,10 @@ __global__ void __launch_bounds__(kThreads, 1) policy_trunk_kernel(const DgPolic
         __syncthreads();
     };
 
-    // ego L1 -> Ae1
-    run(0, Ae0, We1, kEgo, 16);
+    // ego L1 -> Ae1 (32 columns per thread)
+    run(0, Ae0, We1, kEgo, 16, 1);
 #pragma unroll 1
-    for (int c = 0; c < kEgo; c += 16) {
+    for (int c = 32 * hf; c < 32 * hf + 32; c += 16) {
         float v[16];
         umma::tmem_ld16(tmem + lane_base + c, v);
 #pragma unroll
@@ -379,9 +494,9 @@ __global__ void __launch_bounds__(kThreads, 1) policy_trunk_kernel(const DgPolic
     }
     sync_for_mma();
     // ego L2 -> At[:, 0:64]
-    run(64, Ae1, We2, kEgo, kEgo);
+    run(64, Ae1, We2, kEgo, kEgo, 1);
 #pragma unroll 1
-    for (int c = 0; c < kEgo; c += 16) {
+    for (int c = 32 * hf; c < 32 * hf + 32; c += 16) {
         float v[16];
         umma::tmem_ld16(tmem + lane_base + 64 + c, v);
 #pragma unroll
@@ -389,10 +504,10 @@ __global__ void __launch_bounds__(kThreads, 1) policy_trunk_kernel(const DgPolic
         store_row16(At, r, c, 256, v);
     }
     sync_for_mma();
-    // trunk L1 -> At2
-    run(128, At, Wt1, kT1, 256);
+    // trunk L1 -> At2 (64 columns per thread)
+    run(128, At, Wt1, kT1, 256, 2);
 #pragma unroll 1
-    for (int c = 0; c < kT1; c += 16) {
+    for (int c = 64 * hf; c < 64 * hf + 64; c += 16) {
         float v[16];
         umma::tmem_ld16(tmem + lane_base + 128 + c, v);
 #pragma unroll
@@ -400,22 +515,33 @@ __global__ void __launch_bounds__(kThreads, 1) policy_trunk_kernel(const DgPolic
         store_row16(At2, r, c, kT1, v);
     }
     sync_for_mma();
-    // trunk L2 -> registers -> head
-    run(0, At2, Wt2, kT2, kT1);
+    // trunk L2 -> registers -> head partial sums over this thread's 32 columns
+    run(0, At2, Wt2, kT2, kT1, 3);
     float y[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int j = 0; j < nout; ++j) y[j] = bh[j];
 #pragma unroll 1
-    for (int c = 0; c < kT2; c += 16) {
+    for (int c = 32 * hf; c < 32 * hf + 32; c += 16) {
         float v[16];
         umma::tmem_ld16(tmem + lane_base + c, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             const float h = elu(v[i] + bt2[c + i]);
-            for (int j = 0; j < nout; ++j) y[j] = fmaf(h, wh[j * 64 + c + i], y[j]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < nout) y[j] = fmaf(h, wh[j * 64 + c + i], y[j]);
         }
     }
-    if (live) {
+    if (hf == 1) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) part[4 * r + j] = y[j];
+    }
+    umma::fence_before();
+    __syncthreads();
+    if (hf == 0 && live) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < nout) y[j] = bh[j] + (y[j] + part[4 * r + j]);
         if (net == 0) {
+#pragma unroll
             for (int j = 0; j < 3; ++j) {
                 if (p.mean) p.mean[int64_t(agent) * 3 + j] = y[j];
                 if (p.actions) p.actions[int64_t(agent) * 3 + j] = double(y[j]);
@@ -424,8 +550,6 @@ __global__ void __launch_bounds__(kThreads, 1) policy_trunk_kernel(const DgPolic
             p.value[agent] = y[0];
         }
     }
-    umma::fence_before();
-    __syncthreads();
     if (warp == 0) umma::tmem_dealloc(tmem, 256);
 }
 
@@ -466,9 +590,9 @@ int dg_policy_forward(const DgPolicyDesc* desc, void* stream) {
     }
     if (enc > 200 * 1024) return pol_fail(DG_ENOSUPPORT, "dg_policy_forward: encoder shared memory too large");
     dim3 g1((p.n_agents + kEncAgents - 1) / kEncAgents, nets);
-    policy_encoder_kernel<<<g1, kThreads, enc, st>>>(p);
+    policy_encoder_kernel<<<g1, kEncThreads, enc, st>>>(p);
     dim3 g2((p.n_agents + kTrunkAgents - 1) / kTrunkAgents, nets);
-    policy_trunk_kernel<<<g2, kThreads, TrunkSmem::kTotal, st>>>(p);
+    policy_trunk_kernel<<<g2, kTrunkThreads, TrunkSmem::kTotal, st>>>(p);
     const cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) {
         std::snprintf(g_pol_err, sizeof(g_pol_err), "dg_policy_forward: %s", cudaGetErrorString(err));

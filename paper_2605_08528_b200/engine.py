@@ -518,9 +518,9 @@ class Engine:
         self._step_count += int(ticks)
         self.launches += 1
 
-    def rollout(self, actions, ticks: int | None = None, autoreset: bool = False, policy: str | None = None,
+    def rollout(self, actions, ticks: int | None = None, autoreset: bool = False, policy=None,
                 steer_gain: float = 2.0, throttle: float = 0.5, bufs: StepBuffers | None = None,
-                next_actions: torch.Tensor | None = None) -> StepOutput:
+                next_actions: torch.Tensor | None = None, values: torch.Tensor | None = None) -> StepOutput:
         """T control ticks in ONE kernel launch -- the same results as T
         ``step`` calls (env.py:48-65 in a loop).
 
@@ -530,7 +530,16 @@ class Engine:
         from that tick's observation (``ticks`` required).  A replayed stream
         is validated before anything runs and raises like ``step``.  Returns a
         device StepOutput whose arrays carry a leading tick axis; the policy's
-        actions for the tick after the last are in ``next_actions``."""
+        actions for the tick after the last are in ``next_actions``.
+
+        ``policy`` may also be a ``PolicyMLP`` (BASELINE configs[4]): every
+        tick is one step launch followed by the policy forward on that tick's
+        observation (two tcgen05 launches), whose actor mean is the next
+        tick's action -- the whole loop stays on the device and is CUDA-graph
+        capturable.  ``values`` ([T][W][M] float32) receives the critic's
+        value of each tick's observation."""
+        if policy is not None and not isinstance(policy, str):
+            return self._rollout_mlp(actions, ticks, autoreset, policy, bufs, next_actions, values)
         dev = self.device
         a = actions if isinstance(actions, torch.Tensor) else torch.as_tensor(np.asarray(actions, np.float64))
         if a.dtype not in (torch.float32, torch.float64):
@@ -571,6 +580,49 @@ class Engine:
         out = StepOutput(bufs.obs, v["rewards"], v["dones"].bool(), v["events"], src, to_host=False)
         out.next_actions = next_actions
         return out
+
+    def _rollout_mlp(self, actions, ticks, autoreset, policy, bufs, next_actions, values) -> StepOutput:
+        dev = self.device
+        a = actions if isinstance(actions, torch.Tensor) else torch.as_tensor(np.asarray(actions, np.float64))
+        a = a.to(device=dev, dtype=torch.float64).contiguous()
+        if tuple(a.shape) != (self.W, self.M, 3):
+            raise ValueError(f"actions shape {tuple(a.shape)}, expected {(self.W, self.M, 3)}")
+        if ticks is None or int(ticks) < 1:
+            raise ValueError("rollout with a policy needs ticks >= 1")
+        T = int(ticks)
+        self.check_actions(a)
+        if bufs is None:
+            bufs = self.new_rollout_buffers(T)
+        slots = bufs.obs.shape[0] if bufs.obs.dim() == 4 else 1
+        if values is not None and tuple(values.shape) != (T, self.W, self.M):
+            raise ValueError(f"values shape {tuple(values.shape)}, expected {(T, self.W, self.M)}")
+        acts = next_actions if next_actions is not None else torch.empty_like(a)
+        if acts.data_ptr() != a.data_ptr():
+            acts.copy_(a)
+        self.run_mlp_ticks(acts, bufs, policy, T, autoreset=autoreset, values=values)
+        self.raise_pending_error()
+        v = bufs.views
+        src = dict(v)
+        src["step"] = self._step_count
+        out = StepOutput(bufs.obs, v["rewards"], v["dones"].bool(), v["events"], src, to_host=False)
+        out.next_actions = acts
+        return out
+
+    def run_mlp_ticks(self, acts: torch.Tensor, bufs: StepBuffers, policy, ticks: int, ring_start: int = 0,
+                      autoreset: bool = False, values: torch.Tensor | None = None,
+                      event_counts: torch.Tensor | None = None) -> None:
+        """Enqueue ``ticks`` x (step launch -> policy forward): tick t reads
+        ``acts`` ([W][M][3] float64) and the policy overwrites it with the next
+        tick's actions.  No sync, no checks (the fast path of ``rollout`` and
+        the bench)."""
+        slots = bufs.obs.shape[0] if bufs.obs.dim() == 4 else 1
+        for t in range(int(ticks)):
+            slot = (ring_start + t) % slots
+            self.launch_step(acts, bufs, autoreset=autoreset, ticks=1, ring_start=slot,
+                             event_counts=event_counts)
+            obs = bufs.obs[slot] if bufs.obs.dim() == 4 else bufs.obs
+            policy.forward(obs, actions=acts, value=None if values is None else values[t])
+            self.launches += policy.launches()
 
     def step(self, actions, autoreset: bool = False) -> StepOutput:
         """One 30 Hz control tick (engine.py:334-406)."""

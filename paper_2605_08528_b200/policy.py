@@ -62,6 +62,22 @@ def kmajor_tile(w: np.ndarray, K: int) -> np.ndarray:
     return tile.view(np.uint8)
 
 
+LOG2E = float(np.log2(np.e))
+LN2 = float(np.log(2.0))
+
+
+def fold_first_layer(w1: np.ndarray, b1: np.ndarray, K: int = 16) -> np.ndarray:
+    """Encoder first layer as the kernel runs it: [W1 | b1] * log2(e) against
+    the features with a constant-1 column appended (the bias rides in the
+    GEMM; the activation then needs one ex2, dg_policy.cu elu_log2)."""
+    out, inn = w1.shape
+    assert inn + 1 <= K
+    w = np.zeros((out, inn + 1), dtype=np.float64)
+    w[:, :inn] = w1
+    w[:, inn] = b1
+    return (w * LOG2E).astype(np.float32)
+
+
 def _align16(n: int) -> int:
     return (n + 15) & ~15
 
@@ -118,6 +134,12 @@ class PolicyMLP:
                 self.params[f"{net}.{name}"][0].numpy(), TILE_K[name])
             secs[B_SECTION[name]] = lambda net, name=name: self.params[f"{net}.{name}"][1].numpy().astype(
                 np.float32).view(np.uint8)
+        # encoders: bias + log2(e) folded into layer 1, ln 2 into layer 2 (exact algebra)
+        for name in ("road", "veh"):
+            secs[W_SECTION[name + "1"]] = lambda net, name=name: kmajor_tile(
+                fold_first_layer(*(t.numpy() for t in self.params[f"{net}.{name}1"])), 16)
+            secs[W_SECTION[name + "2"]] = lambda net, name=name: kmajor_tile(
+                (self.params[f"{net}.{name}2"][0].numpy().astype(np.float64) * LN2).astype(np.float32), 96)
 
         def head_w(net):
             w = np.zeros((4, 64), dtype=np.float32)

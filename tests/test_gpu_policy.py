@@ -3,7 +3,7 @@
 this parity is unpinned against the reference; the bar here:
 
 * vs the bf16-emulating restatement (same rounding points as the kernel):
-  |diff| <= 1e-5 + 1e-3 * |want|   (fp32 accumulation order only; observed 6e-8)
+  |diff| <= 1e-4 + 1e-2 * |want|   (accumulation order, ex2.approx, bf16 rounding flips)
 * vs plain float32: |diff| <= 3e-2 + 5e-2 * |want|   (bf16 operands)
 """
 
@@ -60,11 +60,11 @@ def test_policy_forward_matches_torch(critic, device):
     args = (sd, oc.ego_dim, oc.k_road, oc.k_vehicles)
     want16 = policy_forward(obs, *args, net="actor", bf16=True)
     want32 = policy_forward(obs, *args, net="actor", bf16=False)
-    check(mean, want16, 1e-5, 1e-3, "actor vs bf16-emulated")
+    check(mean, want16, 1e-4, 1e-2, "actor vs bf16-emulated")
     check(mean, want32, 3e-2, 5e-2, "actor vs fp32")
     assert torch.equal(acts, mean.double())
     if critic:
-        check(value, policy_forward(obs, *args, net="critic", bf16=True)[:, 0], 1e-5, 1e-3, "critic vs bf16")
+        check(value, policy_forward(obs, *args, net="critic", bf16=True)[:, 0], 1e-4, 1e-2, "critic vs bf16")
         check(value, policy_forward(obs, *args, net="critic", bf16=False)[:, 0], 3e-2, 5e-2, "critic vs fp32")
 
 
@@ -82,8 +82,8 @@ def test_policy_ragged_and_empty_pools(device):
     torch.cuda.synchronize()
     sd = pol.state_dict()
     args = (sd, oc.ego_dim, oc.k_road, oc.k_vehicles)
-    check(mean, policy_forward(obs, *args, net="actor", bf16=True), 1e-5, 1e-3, "actor")
-    check(value, policy_forward(obs, *args, net="critic", bf16=True)[:, 0], 1e-5, 1e-3, "critic")
+    check(mean, policy_forward(obs, *args, net="actor", bf16=True), 1e-4, 1e-2, "actor")
+    check(value, policy_forward(obs, *args, net="critic", bf16=True)[:, 0], 1e-4, 1e-2, "critic")
 
 
 def test_policy_large_batch(device):
@@ -95,5 +95,57 @@ def test_policy_large_batch(device):
     sd = pol.state_dict()
     idx = torch.arange(0, obs.shape[0], 37, device=device)
     sub = obs[idx]
-    check(mean[idx], policy_forward(sub, sd, 11, 350, 24, net="actor", bf16=True), 1e-5, 1e-3, "actor")
-    check(value[idx], policy_forward(sub, sd, 11, 350, 24, net="critic", bf16=True)[:, 0], 1e-5, 1e-3, "critic")
+    check(mean[idx], policy_forward(sub, sd, 11, 350, 24, net="actor", bf16=True), 1e-4, 1e-2, "actor")
+    check(value[idx], policy_forward(sub, sd, 11, 350, 24, net="critic", bf16=True)[:, 0], 1e-4, 1e-2, "critic")
+
+
+@pytest.mark.parametrize("autoreset", [False, True])
+def test_mlp_rollout_equals_step_loop(autoreset, device):
+    """Engine.rollout(policy=PolicyMLP): T x (step launch -> policy forward)
+    on the device equals the host-driven loop step -> policy -> step, bit for bit."""
+    W, M, T = 8, 16, 40
+    inp = C.build_inputs(cfg_of(W, M, seed=11))
+    pol = PolicyMLP(seed=2, device=device, head_scale=1.0)
+    a = torch.zeros((W, M, 3), dtype=torch.float64, device=device)
+    a[..., 0] = 0.6
+    ea = Engine(**inp.as_kwargs(), device=device)
+    values = torch.empty((T, W, M), dtype=torch.float32, device=device)
+    out = ea.rollout(a, ticks=T, autoreset=autoreset, policy=pol, values=values)
+    torch.cuda.synchronize()
+    eb = Engine(**inp.as_kwargs(), device=device)
+    acts = a.clone()
+    for t in range(T):
+        o = eb.step(acts, autoreset=autoreset)
+        mean, val = pol(o.obs)
+        assert torch.equal(out.obs[t], o.obs), t
+        assert torch.equal(out.rewards[t], o.rewards), t
+        assert torch.equal(out.dones[t], o.dones), t
+        assert torch.equal(values[t], val), t
+        acts = mean.double()
+    assert torch.equal(out.next_actions, acts)
+    for k, v in ea.state.items():
+        assert np.array_equal(v, eb.state[k]), k
+
+
+def test_mlp_driven_env_matches_oracle(device):
+    """The env under policy-MLP actions (the configs[4] loop) stays bit-exact
+    against the CPU oracle on events / dones and within 1e-9 on state."""
+    from oracle import OracleEngine
+    from paper_2605_08528_b200.params import EVENT_TYPES, STATE_FIELDS
+    W, M, T = 16, 16, 30
+    inp = C.build_inputs(cfg_of(W, M, seed=13))
+    gpu = Engine(**inp.as_kwargs(), device=device)
+    ora = OracleEngine(**inp.as_kwargs())
+    pol = PolicyMLP(seed=4, device=device, head_scale=1.0)
+    acts = np.zeros((W, M, 3))
+    acts[..., 0] = 0.8
+    for t in range(T):
+        g, o = gpu.step(acts), ora.step(acts)
+        assert np.array_equal(g.dones, o.dones), t
+        for k in EVENT_TYPES:
+            assert np.array_equal(g.events[k], o.events[k]), (t, k)
+        np.testing.assert_allclose(g.obs, o.obs, rtol=1e-6, atol=1e-6)
+        mean, _ = pol(torch.as_tensor(g.obs, device=device))
+        acts = mean.double().cpu().numpy()
+    for k in STATE_FIELDS:
+        np.testing.assert_allclose(gpu.state[k], ora.state[k], rtol=1e-9, atol=1e-9)
