@@ -42,7 +42,6 @@ namespace {
 
 constexpr int kEncAgents = 32;     // agents per encoder CTA
 constexpr int kTrunkAgents = 128;  // agents per trunk CTA (one TMEM lane each)
-constexpr int kThreads = 128;
 constexpr int kHid = 96;           // road / vehicle encoder width
 constexpr int kEgo = 64;
 constexpr int kT1 = 128, kT2 = 64;
@@ -79,16 +78,6 @@ __device__ __forceinline__ void store_row16(uint8_t* tile, int r, int c, int K, 
     *reinterpret_cast<uint4*>(tile + umma::kmajor_offset(r, c, K)) = lo;
     *reinterpret_cast<uint4*>(tile + umma::kmajor_offset(r, c + 8, K)) = hi;
 }
-
-__device__ __forceinline__ void copy_to_smem(void* dst, const void* src, int bytes, int tid, int nthreads) {
-    const uint4* s = reinterpret_cast<const uint4*>(src);
-    uint4* d = reinterpret_cast<uint4*>(dst);
-    for (int i = tid; i < bytes / 16; i += nthreads) d[i] = __ldg(s + i);
-}
-
-struct PolArgs {
-    DgPolicyDesc p;
-};
 
 __device__ __forceinline__ const uint8_t* net_base(const DgPolicyDesc& p, int net) {
     return p.weights + int64_t(net) * p.net_stride;
