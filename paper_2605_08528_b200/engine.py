@@ -273,6 +273,8 @@ class Engine:
         self._host_bufs = self._new_buffers(self._obs_dev)
         self.launches = 0
         self._metrics_on = False
+        self._host_lay = None
+        self._host_io = {}
         self._drac_max = None
         self._metric_seen = None
 
@@ -308,6 +310,14 @@ class Engine:
             lay[name] = (off, k * nbytes, dtype, lead + shape)
             off = _align16(off + k * nbytes)
         return lay, off
+
+    def _host_views(self, aux: np.ndarray) -> dict:
+        """numpy views of a host copy of the packed aux buffer (one tick)."""
+        lay = self._host_lay
+        if lay is None:
+            lay = self._host_lay = [(name, o, n, torch.empty((), dtype=dt).numpy().dtype, shape)
+                                    for name, (o, n, dt, shape) in self._aux_layout()[0].items()]
+        return {name: aux[o:o + n].view(dt).reshape(shape) for name, o, n, dt, shape in lay}
 
     def _views(self, aux: torch.Tensor, slots: int | None = None) -> dict:
         lay, _ = self._aux_layout(slots)
@@ -496,6 +506,15 @@ class Engine:
         ``drac_max`` (float64 [W][M]) / ``metric_seen`` (uint8 [W][M]) are the
         in-kernel episode-metric accumulators (default: the engine's own when
         ``track_episode_metrics`` is on)."""
+        io = self._step_io(actions, bufs, autoreset, snapshot, terms, next_actions, steer_gain, throttle,
+                           event_counts, ticks, ring_start, drac_max, metric_seen)
+        N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), self._stream()), "dg_step")
+        self._step_count += int(ticks)
+        self.launches += 1
+
+    def _step_io(self, actions, bufs, autoreset=False, snapshot=True, terms=True, next_actions=None,
+                 steer_gain=2.0, throttle=0.5, event_counts=None, ticks=1, ring_start=0, drac_max=None,
+                 metric_seen=None):
         if self._metrics_on:
             drac_max = self._drac_max if drac_max is None else drac_max
             metric_seen = self._metric_seen if metric_seen is None else metric_seen
@@ -514,9 +533,7 @@ class Engine:
                         event_counts=event_counts.data_ptr() if event_counts is not None else None,
                         ticks=int(ticks), ring_slots=int(slots), ring_start=int(ring_start),
                         drac_max=_ptr(drac_max), metric_seen=_ptr(metric_seen))
-        N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), self._stream()), "dg_step")
-        self._step_count += int(ticks)
-        self.launches += 1
+        return io
 
     def rollout(self, actions, ticks: int | None = None, autoreset: bool = False, policy=None,
                 steer_gain: float = 2.0, throttle: float = 0.5, bufs: StepBuffers | None = None,
@@ -660,14 +677,22 @@ class Engine:
         self._act_dev.copy_(self._act_host, non_blocking=True)
         t1 = time.perf_counter()
         bufs = self._host_bufs
-        self.launch_step(self._act_dev, bufs, autoreset=autoreset)
+        key = (bool(autoreset), self._metrics_on)
+        io = self._host_io.get(key)
+        if io is None:
+            # the host path always uses the same device buffers: build its DgStepIO once
+            io = self._host_io[key] = self._step_io(self._act_dev, bufs, autoreset=autoreset)
+        stream = torch.cuda.current_stream(self.device)
+        N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), ct.c_void_p(stream.cuda_stream)), "dg_step")
+        self._step_count += 1
+        self.launches += 1
         obs = torch.empty(bufs.obs.shape, dtype=torch.float32, pin_memory=True)
         aux = torch.empty(bufs.aux.shape, dtype=torch.uint8, pin_memory=True)
         obs.copy_(bufs.obs, non_blocking=True)
         aux.copy_(bufs.aux, non_blocking=True)
-        torch.cuda.current_stream(self.device).synchronize()
+        stream.synchronize()
         t2 = time.perf_counter()
-        hv = {k: t.numpy() for k, t in self._views(aux).items()}
+        hv = self._host_views(aux.numpy())
         src = dict(hv)
         src["step"] = self._step_count
         self.phase_seconds["action"] += t1 - t0
@@ -714,6 +739,7 @@ class Engine:
         collision event latches (what episode_metrics derives from a recorded
         log, metrics.py:86-125).  Zeroes the accumulators."""
         self._metrics_on = bool(enable)
+        self._host_io.clear()            # cached DgStepIO hold the accumulator pointers
         if enable:
             W, M = self.W, self.M
             self._drac_max = torch.zeros((W, M), dtype=torch.float64, device=self.device)
