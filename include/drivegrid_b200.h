@@ -210,6 +210,18 @@ int dg_pairwise_drac(const double* x, const double* y, const double* yaw, const 
                      const double* d_hull, int32_t steps, int32_t W, int32_t M, double* out,
                      int32_t accumulate, int32_t world_velocity, void* stream);
 
+/* Batched system-identification rollouts (sysid.py:201-228 rollout_channels,
+ * evaluated for every candidate x maneuver of a CEM generation at once):
+ * consts [B] DgConsts (device, one per candidate parameter vector, built like
+ * dg_create's), mu [B][3] effective friction per surface (dry, wet, gravel),
+ * tick_start [n_maneuvers + 1] offsets into actions [ticks][3] (decoded
+ * throttle / steer / brake per 30 Hz tick) and surface [ticks] (0..2);
+ * out + out_offset[m] receives maneuver m's channels [7][2 * ticks_m][B]
+ * (x, y, yaw, speed, yaw_rate, wheel_speed, steer_angle at 60 Hz). */
+int dg_sysid_rollout(const void* consts, const double* mu, const int32_t* tick_start, const double* actions,
+                     const uint8_t* surface, const int64_t* out_offset, int32_t B, int32_t n_maneuvers,
+                     double* out, void* stream);
+
 /* Kernel launches issued by the last dg_step/dg_observe/dg_reset call. */
 int dg_launch_count(dg_engine* eng);
 

@@ -102,6 +102,7 @@ SIGNATURES = {
     "dg_launch_count": (ct.c_int, [_P]),
     "dg_tune": (ct.c_int, [_P, ct.c_int32, ct.c_int32, ct.c_int32]),
     "dg_scratch_bytes": (ct.c_size_t, [ct.c_int32, ct.c_int32]),
+    "dg_sysid_rollout": (ct.c_int, [_P] * 6 + [ct.c_int32, ct.c_int32, _P, _P]),
     "dg_policy_forward": (ct.c_int, [ct.POINTER(DgPolicyDesc), _P]),
     "dg_policy_scratch_bytes": (ct.c_size_t, [ct.c_int32, ct.c_int32]),
     "dg_policy_last_error": (ct.c_char_p, []),

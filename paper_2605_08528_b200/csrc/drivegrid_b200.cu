@@ -1738,6 +1738,50 @@ __global__ void __launch_bounds__(256) pairwise_drac_kernel(const double* x, con
     }
 }
 
+// Batched system-identification rollouts (sysid.py:201-228): thread (b, m) rolls
+// maneuver m for candidate parameter vector b -- the step kernel's 120 Hz
+// substep with that candidate's constant block -- and records the 7 channels
+// after every second substep (60 Hz).  out + out_offset[m] holds [7][2 T_m][B].
+__global__ void __launch_bounds__(64) sysid_rollout_kernel(const DgConsts* consts, const double* mu,
+                                                           const int32_t* tick_start, const double* actions,
+                                                           const uint8_t* surface, const int64_t* out_offset,
+                                                           int B, double* out) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m = blockIdx.y;
+    if (b >= B) return;
+    const DgConsts k = consts[b];
+    double x[DG_NUM_STATE];
+#pragma unroll
+    for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = 0.0;
+    x[SBF] = 1.0;
+    x[SBR] = 1.0;
+    const int t0 = tick_start[m], t1 = tick_start[m + 1];
+    const int64_t T60 = 2 * int64_t(t1 - t0);
+    double* o = out + out_offset[m];
+    int64_t rec = 0;
+    for (int t = t0; t < t1; ++t) {
+        Act a;
+        a.thr = actions[3 * t];
+        a.steer = actions[3 * t + 1];
+        a.brk = actions[3 * t + 2];
+        const double cap = mu[3 * b + surface[t]] * k.f_z;
+        for (int sub = 0; sub < 4; ++sub) {
+            substep_dynamic(x, a, cap, k);
+            if (sub & 1) {
+                double* r = o + rec * B + b;
+                r[0 * T60 * B] = x[SX];
+                r[1 * T60 * B] = x[SY];
+                r[2 * T60 * B] = x[SYAW];
+                r[3 * T60 * B] = sqrt(x[SVX] * x[SVX] + x[SVY] * x[SVY]);
+                r[4 * T60 * B] = x[SOM];
+                r[5 * T60 * B] = 0.5 * (x[SWF] + x[SWR]);
+                r[6 * T60 * B] = x[SANG];
+                ++rec;
+            }
+        }
+    }
+}
+
 __global__ void lane_follower_kernel(const float* obs, double* actions, int64_t n, int D, double gain,
                                      double throttle, double bbox_half) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
@@ -2093,6 +2137,20 @@ int dg_pairwise_drac(const double* x, const double* y, const double* yaw, const 
                                                                            world_velocity);
     const cudaError_t err = cudaGetLastError();
     return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_pairwise_drac");
+}
+
+int dg_sysid_rollout(const void* consts, const double* mu, const int32_t* tick_start, const double* actions,
+                     const uint8_t* surface, const int64_t* out_offset, int32_t B, int32_t n_maneuvers,
+                     double* out, void* stream) {
+    if (!consts || !mu || !tick_start || !actions || !surface || !out_offset || !out)
+        return fail(DG_EINVAL, "dg_sysid_rollout: null argument");
+    if (B < 1 || n_maneuvers < 1 || n_maneuvers > 65535)
+        return fail(DG_EINVAL, "dg_sysid_rollout: need B >= 1 and 1 <= n_maneuvers <= 65535");
+    const dim3 grid((B + 63) / 64, n_maneuvers);
+    sysid_rollout_kernel<<<grid, 64, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const DgConsts*>(consts), mu, tick_start, actions, surface, out_offset, B, out);
+    const cudaError_t err = cudaGetLastError();
+    return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_sysid_rollout");
 }
 
 int dg_launch_count(dg_engine* eng) { return eng ? eng->launches : 0; }

@@ -22,6 +22,9 @@ Cases (each an .npz under tests/golden/):
   drac_wet          traj_wet's run through Engine.run_episode(record=True): per-step
                     pairwise_drac + episode_metrics (metrics.py:33-125)
   drac_events       traj_events' run, same records (collisions, DRAC > 3.4)
+  sysid             sysid.py: maneuver sets, 60 Hz channel rollouts of 6 candidate
+                    parameter vectors on one maneuver of every kind, sysid_loss,
+                    and a small five-stage run_cem (population 8, 40 trials)
 """
 
 from __future__ import annotations
@@ -312,9 +315,50 @@ def drac_events():
     _drac_record("drac_events", eng, event_actions(420, 4, 16))
 
 
+def sysid():
+    import json
+    from drivegrid import sysid as S
+    from drivegrid.vehicle import VehicleParams, params_to_vector
+
+    base = VehicleParams()
+    lo, hi = S.default_bounds(base)
+    rng = np.random.Generator(np.random.Philox(77))
+    vectors = lo + (hi - lo) * rng.uniform(0.1, 0.9, (6, lo.size))
+    vectors[0] = params_to_vector(base)
+    teacher = VehicleParams(tau_drive_max=700.0, lambda_lat=120.0, kp_steer=1700.0, f_lat_wet=0.85)
+    mans = {sc: S.generate_maneuvers(sc) for sc in (1.0, 0.2, 0.1)}
+    pick, seen = [], set()
+    for m in mans[1.0]:
+        if m.kind not in seen:
+            seen.add(m.kind)
+            pick.append(m)
+    batch = S.ParamBatch(base, vectors)
+    tbatch = S.ParamBatch(teacher, params_to_vector(teacher)[None, :])
+    arrays = {"vectors": vectors, "lo": lo, "hi": hi, "teacher": params_to_vector(teacher)}
+    for i, m in enumerate(pick):
+        st = S.rollout_channels(batch, m)
+        te = S.rollout_channels(tbatch, m)
+        for k, v in st.items():
+            arrays[f"m{i}_{k}"] = v
+            arrays[f"m{i}_teacher_{k}"] = te[k]
+        arrays[f"m{i}_loss"] = S.sysid_loss(st, te)
+    cem = S.CEMConfig(population=8, total_trials=40)
+    res = S.run_cem(teacher, cem, scale=0.1, seed=3)
+    meta = {
+        "maneuvers": {str(sc): [[m.id, m.tier, m.kind, m.duration, m.params] for m in ms]
+                      for sc, ms in mans.items()},
+        "picked": [m.id for m in pick],
+        "run_cem": res.to_dict(),
+        "run_cem_args": {"population": 8, "total_trials": 40, "scale": 0.1, "seed": 3},
+    }
+    arrays["meta_json"] = np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)
+    np.savez_compressed(OUT / "sysid.npz", **arrays)
+    print("sysid", len(pick), "maneuver kinds; run_cem best", res.stages[-1]["best_loss"])
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid"]
     for name in which:
         globals()[name]()
