@@ -40,7 +40,10 @@
 
 namespace {
 
-constexpr int kEncAgents = 32;     // agents per encoder CTA
+#ifndef DG_ENC_AGENTS
+#define DG_ENC_AGENTS 32
+#endif
+constexpr int kEncAgents = DG_ENC_AGENTS;   // agents per encoder CTA (<= 32: one per lane in the scan)
 constexpr int kTrunkAgents = 128;  // agents per trunk CTA (one TMEM lane each)
 constexpr int kHid = 96;           // road / vehicle encoder width
 constexpr int kEgo = 64;
@@ -570,12 +573,21 @@ int dg_policy_forward(const DgPolicyDesc* desc, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int kmax = p.k_road > p.k_vehicles ? p.k_road : p.k_vehicles;
     const size_t enc = enc_smem_bytes(kmax);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(policy_encoder_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(policy_trunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             TrunkSmem::kTotal);
-        attr_set = true;
+    // the shared-memory opt-in is per device: remember it per device ordinal
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(policy_encoder_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             200 * 1024);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(policy_trunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     TrunkSmem::kTotal);
+        if (e != cudaSuccess) {
+            std::snprintf(g_pol_err, sizeof(g_pol_err), "dg_policy_forward: %s", cudaGetErrorString(e));
+            return DG_ECUDA;
+        }
+        if (dev >= 0 && dev < 64) attr_set[dev] = true;
     }
     if (enc > 200 * 1024) return pol_fail(DG_ENOSUPPORT, "dg_policy_forward: encoder shared memory too large");
     dim3 g1((p.n_agents + kEncAgents - 1) / kEncAgents, nets);
