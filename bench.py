@@ -342,6 +342,25 @@ def main():
     agent_ticks = totals["alive_ticks"]          # alive agents before each timed tick, device-counted
     value = agent_ticks / (total_ms / 1e3)
 
+    # e2e through the numpy API on every rank at once; whole-job value =
+    # all ranks' agent-ticks / the slowest rank's wall time
+    e2e_steps = args.e2e_steps or max(10, min(args.steps, 50))
+    if world_size > 1:
+        dist.barrier()
+    e2e = e2e_numpy(eng, e2e_steps)
+    if world_size > 1:
+        t = torch.tensor([float(e2e["ticks"]), e2e["wall_s"], float(e2e["h2d_bytes_per_step"]),
+                          float(e2e["d2h_bytes_per_step"])], dtype=torch.float64, device=dev)
+        parts = [torch.empty_like(t) for _ in range(world_size)]
+        dist.all_gather(parts, t)
+        parts = torch.stack(parts).cpu().numpy()
+        e2e["ticks"] = int(parts[:, 0].sum())
+        e2e["wall_s"] = float(parts[:, 1].max())
+        e2e["value"] = e2e["ticks"] / e2e["wall_s"]
+        e2e["h2d_bytes_per_step"] = int(parts[:, 2].sum())
+        e2e["d2h_bytes_per_step"] = int(parts[:, 3].sum())
+        e2e["ranks"] = world_size
+
     if rank == 0:
         peak, peak_src = measured_peaks()
         per_agent = algorithmic_bytes_per_agent(D)
@@ -371,9 +390,7 @@ def main():
             "episode_counters": totals,
         }
         line["clocks"] = clk.summary()
-        # e2e through the numpy API
-        e2e_steps = args.e2e_steps or max(10, min(args.steps, 50))
-        line["e2e"] = e2e_numpy(eng, e2e_steps)
+        line["e2e"] = e2e
         if not args.no_c5 and world_size == 1:
             line["c5_policy_rollout"] = bench_c5(dev)
         if not args.no_cpu:
@@ -490,7 +507,7 @@ def e2e_numpy(eng, steps):
     W, M, D = eng.W, eng.M, eng.obs_config.obs_dim
     _, aux_bytes = eng._aux_layout()
     return {"value": ticks / wall, "unit": "agent-steps/s", "h2d_bytes_per_step": W * M * 3 * 8,
-            "d2h_bytes_per_step": W * M * D * 4 + aux_bytes, "steps": steps,
+            "d2h_bytes_per_step": W * M * D * 4 + aux_bytes, "steps": steps, "ticks": ticks, "wall_s": wall,
             "api": "Engine.step(numpy) with fused autoreset + host numpy LaneFollower"}
 
 
