@@ -246,10 +246,18 @@ def main():
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # DG_BENCH_DIST_BACKEND=gloo + DG_BENCH_ONE_DEVICE=1 exercise the N-rank code
+    # path with every rank on cuda:0 (a one-GPU box); the real runs use NCCL
+    backend = os.environ.get("DG_BENCH_DIST_BACKEND", "nccl")
+    gpu = 0 if os.environ.get("DG_BENCH_ONE_DEVICE") == "1" else local_rank
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world_size > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    cdev = dev if backend == "nccl" else torch.device("cpu")   # collective tensors
 
     from paper_2605_08528_b200.engine import Engine
 
@@ -316,7 +324,7 @@ def main():
     launches = eng.launches - launches0
     total_ms = start.elapsed_time(stop)
     if world_size > 1:
-        t = torch.tensor([total_ms], device=dev)
+        t = torch.tensor([total_ms], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     n_launch = math.ceil(args.steps / R)
@@ -350,7 +358,7 @@ def main():
     e2e = e2e_numpy(eng, e2e_steps)
     if world_size > 1:
         t = torch.tensor([float(e2e["ticks"]), e2e["wall_s"], float(e2e["h2d_bytes_per_step"]),
-                          float(e2e["d2h_bytes_per_step"])], dtype=torch.float64, device=dev)
+                          float(e2e["d2h_bytes_per_step"])], dtype=torch.float64, device=cdev)
         parts = [torch.empty_like(t) for _ in range(world_size)]
         dist.all_gather(parts, t)
         parts = torch.stack(parts).cpu().numpy()
@@ -393,11 +401,57 @@ def main():
         line["e2e"] = e2e
         if not args.no_c5 and world_size == 1:
             line["c5_policy_rollout"] = bench_c5(dev)
-        if not args.no_cpu:
+        if not args.no_c5 and world_size == 1:
+            line["c4_single_gpu"] = bench_c4(dev, steps=max(64, args.steps), R=R)
+        if not args.no_cpu and world_size == 1:
             line["cpu_baseline"] = cpu_baseline(args.cpu_steps or 40)
         print(json.dumps(line), flush=True)
     if world_size > 1:
         dist.destroy_process_group()
+
+
+def bench_c4(dev, steps=200, R=DEFAULT_TICKS_PER_LAUNCH, W=SCALE_TOTAL_WORLDS, M=16):
+    """BASELINE configs[3] at N=1: the 4096 x 16 batch the multi-GPU runs shard
+    (the N-GPU lines divide these worlds), timed exactly like the headline:
+    fused LaneFollower + autoreset, persistent launches of R ticks, one CUDA
+    graph, obs ring > L2, device-counted alive agent-ticks."""
+    import torch
+    from paper_2605_08528_b200.engine import Engine
+
+    eng = Engine(**shard_inputs(root_config(W, M), 0, 1).as_kwargs(), device=dev)
+    D = eng.obs_config.obs_dim
+    ring = max(2, math.ceil(2 * L2_BYTES / (W * M * D * 4)))
+    rb = eng.new_rollout_buffers(ring)
+    acts = torch.zeros((W, M, 3), dtype=torch.float64, device=dev)
+    eng.observe(out=rb.obs[ring - 1], as_numpy=False, next_actions=acts)
+    counters = torch.zeros((W, 5), dtype=torch.int32, device=dev)
+    tick = [0]
+
+    def run(n, count):
+        done = 0
+        while done < n:
+            r = min(R, n - done)
+            eng.launch_step(acts, rb, autoreset=True, next_actions=acts, ticks=r, ring_start=tick[0] % ring,
+                            event_counts=counters if count else None)
+            tick[0] += r
+            done += r
+
+    run(2 * R, False)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        run(steps, True)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    ticks = int(counters[:, 4].sum().item())
+    return {"metric": "CASPS", "value": ticks / (ms / 1e3), "unit": "agent-steps/s", "n_gpus": 1,
+            "workload": f"{W}x{M} default pool (the batch the N-GPU runs shard), LaneFollower + autoreset",
+            "steps": steps, "ms_per_step": ms / steps, "ticks_per_launch": R}
 
 
 def policy_flops_per_agent(n_road: float, n_veh: float, ego_dim: int = 11, nets: int = 2) -> float:
