@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--cpu-steps", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] policy-rollout line")
+    ap.add_argument("--no-c5", action="store_true", help="skip the configs[3] single-GPU and configs[4] policy-rollout sub-lines")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly from the host (slower)")
     ap.add_argument("--ticks-per-launch", type=int, default=0,
                     help="control ticks per persistent kernel launch (0 = default for the shape)")
