@@ -433,16 +433,41 @@ struct ScanSm {
 // Both launch modes share these: the ego features of one agent's row
 // (observation.py:51-75) and the reward / event / termination tail of one
 // agent (rewards.py:106-268, engine.py:370-406, 472-509).
+// atan2(sin t, cos t) (observation.py:246-247, the neighbour heading feature):
+// t itself reduced by whole turns.  Off the +-pi seam the two agree to ~1e-14
+// (far below the float32 the feature is stored in); near the seam, where the
+// sign of the result depends on the last bits of sin t, the exact composition
+// runs instead.
+__device__ __forceinline__ double wrap_angle(double t) {
+    const double r = t - 6.283185307179586 * rint(t * 0.15915494309189535);
+    if (fabs(r) < 3.1415) return r;
+    double st, ct;
+    sincos(t, &st, &ct);
+    return atan2(st, ct);
+}
+
+// (sin, cos) of atan2(y, x) (observation.py:58-64): y / r, x / r; the exact
+// composition where r is 0 or not finite (signed-zero quadrants).
+__device__ __forceinline__ void sincos_of_bearing(double y, double x, double r, double* sh, double* ch) {
+    if (r > 0.0 && r < INFINITY) {
+        *sh = dg::ddiv(y, r);
+        *ch = dg::ddiv(x, r);
+    } else {
+        sincos(atan2(y, x), sh, ch);
+    }
+}
+
 __device__ __forceinline__ void write_ego(float* row, const DgConsts& k, const KArgs& A, int w, int64_t am,
                                           double px, double py, double c, double s, double vx, double vy,
                                           double gx, double gy, double* act_sm = nullptr) {
     const double gdx = gx - px, gdy = gy - py;
     const double xb = c * gdx + s * gdy;
     const double yb = -s * gdx + c * gdy;
+    const double dist = dg::dsqrt(xb * xb + yb * yb);
     double sh, ch;
-    sincos(atan2(yb, xb), &sh, &ch);
+    sincos_of_bearing(yb, xb, dist, &sh, &ch);
     const float f2 = __double2float_rn(sh), f3 = __double2float_rn(ch);
-    const float f4 = __double2float_rn(dg::ddiv(dg::dsqrt(xb * xb + yb * yb), k.bbox_half));
+    const float f4 = __double2float_rn(dg::ddiv(dist, k.bbox_half));
     row[0] = __double2float_rn(dg::ddiv(xb, k.bbox_half));
     row[1] = __double2float_rn(dg::ddiv(yb, k.bbox_half));
     row[2] = f2;
@@ -504,6 +529,7 @@ __device__ __forceinline__ TickOut tick_out(const KArgs& A, int t) {
 
 struct FinIn {
     const double* st;                  // post-physics state, 12 fields
+    double c, s;                       // cos / sin of the post-physics yaw
     double px0, py0, gx, gy, sx, sy;   // pre-physics position, goal, start
     double lane_d2, lane_lat, lane_tx, lane_ty;  // nearest lane (d2 = inf: none)
     double ttc_min, gap;
@@ -534,7 +560,10 @@ __device__ __forceinline__ unsigned finalize_agent(const KArgs& A, const TickOut
             ty = ty * flip;
             double progress = np_clip((px - F.px0) * tx + (py - F.py0) * ty,
                                       -k.progress_clamp, k.progress_clamp) * k.progress_weight;
-            const double align = np_max(0.0, cos(yaw - atan2(ty, tx)));
+            // cos(yaw - atan2(ty, tx)) (rewards.py:127-128) as the dot product of the
+            // heading with the unit lane tangent: same value to ~1e-16, no atan2 / cos
+            // on the tail's critical path (yaw NaN -> NaN, as numpy)
+            const double align = np_max(0.0, F.c * tx + F.s * ty);
             const double ls = dg::ddiv(lat, k.lane_sigma);
             const double quality = exp(-(ls * ls)) * (k.lane_heading_base + k.lane_heading_weight * align);
             const double lane_t = has_lane ? k.lane_weight * quality : 0.0;
@@ -953,9 +982,7 @@ world_step_kernel(const KArgs A) {
                     const AgentSm& N = ag[j];
                     ttc = swept_ttc(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c, N.s, N.d,
                                     S.r + N.r, k.ttc_max);
-                    double st_, ct_;
-                    sincos(N.st[SYAW] - S.st[SYAW], &st_, &ct_);
-                    const double wrap = atan2(st_, ct_);
+                    const double wrap = wrap_angle(N.st[SYAW] - S.st[SYAW]);
                     float* o = obs_w + int64_t(ii) * D + veh0 + 7 * rank;
                     o[0] = __double2float_rn(dg::ddiv(c * ndx + s * ndy, k.bbox_half));
                     o[1] = __double2float_rn(dg::ddiv(-s * ndx + c * ndy, k.bbox_half));
@@ -1188,6 +1215,8 @@ world_step_kernel(const KArgs A) {
                 const ScanSm& R = sc[m];
                 FinIn F;
                 F.st = S.st;
+                F.c = S.c;
+                F.s = S.s;
                 F.px0 = S.px0; F.py0 = S.py0; F.gx = S.gx; F.gy = S.gy; F.sx = S.sx; F.sy = S.sy;
                 F.lane_d2 = R.lane_d2;
                 F.lane_lat = 0.0; F.lane_tx = 0.0; F.lane_ty = 0.0;
@@ -1440,9 +1469,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
             const AgentRec& N = ag[j];
             ttc = swept_ttc(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c, N.s, N.d, S.r + N.r,
                             k.ttc_max);
-            double st_, ct_;
-            sincos(N.yaw - S.yaw, &st_, &ct_);
-            const double wrap = atan2(st_, ct_);
+            const double wrap = wrap_angle(N.yaw - S.yaw);
             float* o = row + veh0 + 7 * rank;
             o[0] = __double2float_rn(dg::ddiv(c * ndx + s * ndy, k.bbox_half));
             o[1] = __double2float_rn(dg::ddiv(-s * ndx + c * ndy, k.bbox_half));
@@ -1624,6 +1651,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
         for (int f = 0; f < DG_NUM_STATE; ++f) st[f] = A.state[int64_t(f) * WM + am];
         FinIn F;
         F.st = st;
+        F.c = S.c;
+        F.s = S.s;
         F.px0 = prev[am].x; F.py0 = prev[am].y;
         F.gx = gx; F.gy = gy;
         F.sx = A.start_xy[2 * am]; F.sy = A.start_xy[2 * am + 1];
