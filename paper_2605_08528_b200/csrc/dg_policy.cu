@@ -102,7 +102,8 @@ struct EncSmem {
     static constexpr int kAcc = kW2 + kHid * kHid * 2;
     static constexpr int kCnt = kAcc + kEncAgents * kAccStride * 4;
     static constexpr int kSegStart = kCnt + kEncAgents * 4;
-    static constexpr int kSeg = kSegStart + (kEncAgents + 4) * 4;
+    static constexpr int kB2 = kSegStart + (kEncAgents + 4) * 4;
+    static constexpr int kSeg = kB2 + kHid * 4;
 };
 
 __host__ __device__ __forceinline__ int enc_seg_cap(int k_slots) { return kEncAgents * ((k_slots + 7) / 8); }
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
     int* cnt = reinterpret_cast<int*>(sm + EncSmem::kCnt);
     int* segstart = reinterpret_cast<int*>(sm + EncSmem::kSegStart);
     uint16_t* seg = reinterpret_cast<uint16_t*>(sm + EncSmem::kSeg);
+    float* b2 = reinterpret_cast<float*>(sm + EncSmem::kB2);
     const int kmax = p.k_road > p.k_vehicles ? p.k_road : p.k_vehicles;
     uint8_t* tail = sm + EncSmem::kSeg + ((enc_seg_cap(kmax) * 2 + 15) & ~15);
     uint64_t* bar = reinterpret_cast<uint64_t*>(tail);          // [0] MMA, [1] weights
@@ -177,32 +179,37 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
             bulk_g2s(W2, wb + p.off[w2], kHid * kHid * 2, bar + 1);
         }
         for (int i = tid; i < kEncAgents * kAccStride; i += kEncThreads) acc[i] = 0u;
+        for (int i = tid; i < kHid; i += kEncThreads) b2[i] = __ldg(gb2 + i);
 
         // valid slot counts (the valid slots are a prefix): warp w probes agents 4w..4w+3,
-        // 32 slots per round, the four agents' loads in flight together
+        // 64 slots per round (two per lane), all eight loads per lane in flight together
         {
             int c4[4] = {0, 0, 0, 0};
             bool more[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) more[j] = 4 * warp + j < na;
-            for (int s0 = 0; s0 < kslots; s0 += 32) {
-                const int s = s0 + lane;
-                bool ok[4];
+            for (int s0 = 0; s0 < kslots; s0 += 64) {
+                bool ok[4][2];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    ok[j] = false;
-                    if (more[j] && s < kslots) {
-                        const float* f = p.obs + int64_t(a0 + 4 * warp + j) * p.obs_dim + fbase + s * nf;
-                        ok[j] = mod == 0 ? (__ldg(f + 3) != 0.0f || __ldg(f + 4) != 0.0f) : (__ldg(f + 2) != 0.0f);
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int s = s0 + 32 * h + lane;
+                        ok[j][h] = false;
+                        if (more[j] && s < kslots) {
+                            const float* f = p.obs + int64_t(a0 + 4 * warp + j) * p.obs_dim + fbase + s * nf;
+                            ok[j][h] = mod == 0 ? (__ldg(f + 3) != 0.0f || __ldg(f + 4) != 0.0f)
+                                                : (__ldg(f + 2) != 0.0f);
+                        }
                     }
-                }
                 bool any = false;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    const unsigned b = __ballot_sync(0xffffffffu, ok[j]);
+                    const unsigned b0 = __ballot_sync(0xffffffffu, ok[j][0]);
+                    const unsigned b1 = __ballot_sync(0xffffffffu, ok[j][1]);
                     if (more[j]) {
-                        c4[j] += __popc(b);
-                        more[j] = b == 0xffffffffu;
+                        c4[j] += __popc(b0) + (b0 == 0xffffffffu ? __popc(b1) : 0);
+                        more[j] = b0 == 0xffffffffu && b1 == 0xffffffffu;
                     }
                     any |= more[j];
                 }
@@ -347,8 +354,8 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
         for (int i = tid; i < na * (kHid / 2); i += kEncThreads) {
             const int a = i / (kHid / 2), c = 2 * (i % (kHid / 2));
             const uint32_t u0 = acc[a * kAccStride + c], u1 = acc[a * kAccStride + c + 1];
-            const float v0 = u0 ? elu(o2f(u0) + __ldg(gb2 + c)) : 0.0f;
-            const float v1 = u1 ? elu(o2f(u1) + __ldg(gb2 + c + 1)) : 0.0f;
+            const float v0 = u0 ? elu(o2f(u0) + b2[c]) : 0.0f;
+            const float v1 = u1 ? elu(o2f(u1) + b2[c + 1]) : 0.0f;
             *reinterpret_cast<uint32_t*>(out + int64_t(a) * kEmb + c) = umma::pack_bf16(v0, v1);
         }
         __syncthreads();
