@@ -478,18 +478,25 @@ def bench_c5(dev, ticks=128, W=1024, M=16, reps=2):
     pol = PolicyMLP(eng.obs_config, seed=0, device=dev, head_scale=1.0)
     rb = eng.new_rollout_buffers(ticks)          # [T][W][M][D]: 1 GB > L2, every tick its own slot
     values = torch.empty((ticks, W, M), dtype=torch.float32, device=dev)
+    log_probs = torch.empty((ticks, W, M), dtype=torch.float32, device=dev)
+    actions_out = torch.empty((ticks, W, M, 3), dtype=torch.float32, device=dev)
+    ppo = dict(sample=True, seed=1234, log_probs=log_probs, actions_out=actions_out)
+    from paper_2605_08528_b200.policy import gae
     acts = torch.zeros((W, M, 3), dtype=torch.float64, device=dev)
     acts[..., 0] = 0.5
     counters = torch.zeros((W, 5), dtype=torch.int32, device=dev)
     # warm-up (allocates the policy scratch, packs the weights)
-    eng.run_mlp_ticks(acts, rb, pol, 4, autoreset=True, values=values)
+    eng.run_mlp_ticks(acts, rb, pol, 4, autoreset=True, values=values, **ppo)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
     launches0 = eng.launches
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
-        eng.run_mlp_ticks(acts, rb, pol, ticks, autoreset=True, values=values, event_counts=counters)
-    launches = eng.launches - launches0
+        # the PPO collection: T ticks of (step -> sampled actions, log-probs, values),
+        # then GAE over the T-1 complete transitions
+        eng.run_mlp_ticks(acts, rb, pol, ticks, autoreset=True, values=values, event_counts=counters, **ppo)
+        adv, ret = gae(rb.views["rewards"][1:], rb.views["dones"][1:], values, 0.99, 0.98)
+    launches = eng.launches - launches0 + 1
     g.replay()
     torch.cuda.synchronize()
     counters.zero_()
@@ -506,7 +513,8 @@ def bench_c5(dev, ticks=128, W=1024, M=16, reps=2):
     gp = torch.cuda.CUDAGraph()
     with torch.cuda.graph(gp):
         for _ in range(ticks):
-            pol.forward(obs_last, actions=acts, value=values[0])
+            pol.forward(obs_last, actions=acts, value=values[0], sample=True, seed=1, log_prob=log_probs[0],
+                        actions_f32=actions_out[0])
     ge = torch.cuda.CUDAGraph()
     with torch.cuda.graph(ge):
         for t in range(ticks):
@@ -530,8 +538,9 @@ def bench_c5(dev, ticks=128, W=1024, M=16, reps=2):
         if (ROOT / "MEASURED_PEAKS.json").exists() else 1400.0
     achieved = flops / (res["policy"] / 1e3) / 1e12
     return {"metric": "CASPS", "value": alive_ticks / (ms / 1e3), "unit": "agent-steps/s",
-            "workload": f"{W}x{M} default pool, T={ticks} rollout, policy MLP (actor mean + critic value) "
-                        "fused: step + 2 tcgen05 launches per tick, autoreset, one CUDA graph",
+            "workload": f"{W}x{M} default pool, T={ticks} PPO rollout: policy MLP fused into the loop "
+                        "(actor sample + log-prob, critic value: step + 2 tcgen05 launches per tick), "
+                        "autoreset, GAE at the end, one CUDA graph",
             "ms_per_tick": ms / ticks, "env_ms_per_tick": res["env"], "policy_ms_per_tick": res["policy"],
             "gpu_launches": launches, "launches_per_tick": launches / ticks,
             "valid_slots_per_agent": {"road": n_road, "vehicle": n_veh},

@@ -257,6 +257,7 @@ enum {
     DG_POL_W_ROAD1, DG_POL_W_ROAD2, DG_POL_W_VEH1, DG_POL_W_VEH2,
     DG_POL_B_EGO1, DG_POL_B_EGO2, DG_POL_B_ROAD1, DG_POL_B_ROAD2, DG_POL_B_VEH1, DG_POL_B_VEH2,
     DG_POL_B_T1, DG_POL_B_T2, DG_POL_W_HEAD, DG_POL_B_HEAD,
+    DG_POL_LOG_STD,             /* actor only: float32 [4] (3 used), the state-independent log sigma */
     DG_POL_NUM_SECTIONS
 };
 
@@ -273,12 +274,32 @@ typedef struct DgPolicyDesc {
     double* actions;            /* [n_agents][3] the same mean as float64 env actions
                                    (the next tick's input), or NULL                */
     float* value;               /* [n_agents] critic value, or NULL                 */
+    int32_t sample;             /* 0: actions = the actor mean; 1: PPO sampling,
+                                   actions = mean + exp(log_std) * eps with eps ~ N(0, 1)
+                                   from Philox4x32-10 (key = seed, counter = {agent
+                                   index, counter}) and Box-Muller in float64        */
+    int32_t pad_;
+    uint64_t seed;
+    uint64_t counter;           /* e.g. the rollout tick: a fresh draw per tick      */
+    float* log_prob;            /* [n_agents] log pi(actions | obs) (diagonal Gaussian), or NULL */
+    float* actions_f32;         /* [n_agents][3] the written actions as float32 (the
+                                   rollout's action record), or NULL                */
 } DgPolicyDesc;
 
 /* One forward of the policy over every agent's observation row: 2 kernel
  * launches (encoders, trunk + heads), asynchronous on stream. */
 int dg_policy_forward(const DgPolicyDesc* desc, void* stream);
 size_t dg_policy_scratch_bytes(int32_t n_agents, int32_t nets);
+
+/* Generalised advantage estimation over a rollout of T transitions for N
+ * agents (the PPO batch of BASELINE configs[4]): with
+ * done_t = the transition ended the episode,
+ *   delta_t = r_t + gamma * V_{t+1} * (1 - done_t) - V_t
+ *   A_t     = delta_t + gamma * lambda * (1 - done_t) * A_{t+1}
+ * rewards [T][N] f64, dones [T][N] u8, values [T+1][N] f32 (row T = bootstrap);
+ * advantages, returns (= A + V) [T][N] f32.  Float64 accumulation. */
+int dg_gae(const double* rewards, const uint8_t* dones, const float* values, int32_t T, int64_t N,
+           double gamma, double lambda, float* advantages, float* returns, void* stream);
 const char* dg_policy_last_error(void);
 
 const char* dg_last_error(void);

@@ -72,3 +72,50 @@ def policy_forward(obs: torch.Tensor, sd: dict, ego_dim: int, k_road: int, k_veh
     x = torch.cat([e, r, v], dim=-1)
     h = F.elu(_lin(F.elu(_lin(x, *p["t1"], bf16)), *p["t2"], bf16))
     return h @ p["head"][0].t() + p["head"][1]
+
+
+# ---------------------------------------------------------------- PPO sampling / GAE
+M0, M1, W0, W1 = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85
+MASK = 0xFFFFFFFF
+
+
+def philox4x32_10(counter: "np.ndarray", key: tuple) -> "np.ndarray":
+    """Philox4x32-10 (Salmon et al. 2011) over rows of uint32 counters [n, 4]."""
+    import numpy as np
+    c = counter.astype(np.uint64)
+    k0, k1 = np.uint64(key[0]), np.uint64(key[1])
+    for _ in range(10):
+        p0 = np.uint64(M0) * c[:, 0]
+        p1 = np.uint64(M1) * c[:, 2]
+        hi0, lo0 = p0 >> np.uint64(32), p0 & np.uint64(MASK)
+        hi1, lo1 = p1 >> np.uint64(32), p1 & np.uint64(MASK)
+        c = np.stack([hi1 ^ c[:, 1] ^ k0, lo1, hi0 ^ c[:, 3] ^ k1, lo0], axis=1)
+        k0 = (k0 + np.uint64(W0)) & np.uint64(MASK)
+        k1 = (k1 + np.uint64(W1)) & np.uint64(MASK)
+    return c.astype(np.uint32)
+
+
+def gaussian3(n: int, seed: int, counter: int) -> "np.ndarray":
+    """The three standard normals the kernel draws for rows 0..n-1 (Box-Muller, float64)."""
+    import numpy as np
+    rows = np.arange(n, dtype=np.uint64)
+    ctr = np.stack([rows & np.uint64(MASK), rows >> np.uint64(32),
+                    np.full(n, counter & MASK, dtype=np.uint64), np.full(n, counter >> 32, dtype=np.uint64)], axis=1)
+    u = (philox4x32_10(ctr, (seed & MASK, seed >> 32)).astype(np.float64) + 0.5) * 2.0 ** -32
+    r0, r1 = np.sqrt(-2.0 * np.log(u[:, 0])), np.sqrt(-2.0 * np.log(u[:, 2]))
+    return np.stack([r0 * np.cos(2.0 * np.pi * u[:, 1]), r0 * np.sin(2.0 * np.pi * u[:, 1]),
+                     r1 * np.cos(2.0 * np.pi * u[:, 3])], axis=1)
+
+
+def gae(rewards, dones, values, gamma=0.99, lam=0.98):
+    """delta_t = r_t + g V_{t+1} (1 - d_t) - V_t;  A_t = delta_t + g l (1 - d_t) A_{t+1} (float64)."""
+    import numpy as np
+    T = rewards.shape[0]
+    adv = np.zeros(rewards.shape)
+    a = np.zeros(rewards.shape[1:])
+    for t in range(T - 1, -1, -1):
+        nt = 1.0 - dones[t].astype(np.float64)
+        delta = rewards[t] + gamma * values[t + 1].astype(np.float64) * nt - values[t].astype(np.float64)
+        a = delta + gamma * lam * nt * a
+        adv[t] = a
+    return adv, adv + values[:T].astype(np.float64)

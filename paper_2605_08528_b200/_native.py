@@ -66,13 +66,15 @@ class DgEngineDesc(ct.Structure):
 
 POL_SECTIONS = ("W_EGO1", "W_EGO2", "W_T1", "W_T2", "W_ROAD1", "W_ROAD2", "W_VEH1", "W_VEH2",
                 "B_EGO1", "B_EGO2", "B_ROAD1", "B_ROAD2", "B_VEH1", "B_VEH2", "B_T1", "B_T2",
-                "W_HEAD", "B_HEAD")
+                "W_HEAD", "B_HEAD", "LOG_STD")
 
 
 class DgPolicyDesc(ct.Structure):
     _fields_ = [(n, ct.c_int32) for n in ("n_agents", "obs_dim", "ego_dim", "k_road", "k_vehicles", "critic")] + [
         ("obs", _P), ("weights", _P), ("net_stride", ct.c_int64), ("off", ct.c_int64 * len(POL_SECTIONS)),
-        ("emb", _P), ("mean", _P), ("actions", _P), ("value", _P)]
+        ("emb", _P), ("mean", _P), ("actions", _P), ("value", _P),
+        ("sample", ct.c_int32), ("pad_", ct.c_int32), ("seed", ct.c_uint64), ("counter", ct.c_uint64),
+        ("log_prob", _P), ("actions_f32", _P)]
 
 
 class DgStepIO(ct.Structure):
@@ -106,6 +108,7 @@ SIGNATURES = {
     "dg_policy_forward": (ct.c_int, [ct.POINTER(DgPolicyDesc), _P]),
     "dg_policy_scratch_bytes": (ct.c_size_t, [ct.c_int32, ct.c_int32]),
     "dg_policy_last_error": (ct.c_char_p, []),
+    "dg_gae": (ct.c_int, [_P, _P, _P, ct.c_int32, ct.c_int64, ct.c_double, ct.c_double, _P, _P, _P]),
     "dg_pairwise_drac": (ct.c_int, [_P] * 8 + [ct.c_int32, ct.c_int32, ct.c_int32, _P, ct.c_int32, ct.c_int32, _P]),
 }
 

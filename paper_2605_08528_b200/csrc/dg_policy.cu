@@ -365,6 +365,39 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
     if (warp == 0) umma::tmem_dealloc(tmem, 128);
 }
 
+// ------------------------------------------------------------------ sampling
+// Philox4x32-10 (Salmon et al., SC'11): counter (agent, 0, counter lo, counter hi),
+// key (seed lo, seed hi) -> four uniforms -> Box-Muller (float64) -> 3 normals.
+__device__ __forceinline__ void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const uint32_t lo0 = 0xD2511F53u * c[0], hi0 = __umulhi(0xD2511F53u, c[0]);
+        const uint32_t lo1 = 0xCD9E8D57u * c[2], hi1 = __umulhi(0xCD9E8D57u, c[2]);
+        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0;
+        c[1] = lo1;
+        c[2] = n2;
+        c[3] = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+__device__ __forceinline__ void gaussian3(uint64_t agent, uint64_t seed, uint64_t counter, double* z) {
+    uint32_t c[4] = {uint32_t(agent), uint32_t(agent >> 32), uint32_t(counter), uint32_t(counter >> 32)};
+    philox4x32_10(c, uint32_t(seed), uint32_t(seed >> 32));
+    double u[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) u[i] = (double(c[i]) + 0.5) * 2.3283064365386963e-10;   // 2^-32
+    const double r0 = sqrt(-2.0 * log(u[0])), r1 = sqrt(-2.0 * log(u[2]));
+    double s0, c0, s1, c1;
+    sincospi(2.0 * u[1], &s0, &c0);
+    sincospi(2.0 * u[3], &s1, &c1);
+    z[0] = r0 * c0;
+    z[1] = r0 * s0;
+    z[2] = r1 * c1;
+}
+
 // ------------------------------------------------------------------ trunk
 constexpr int kTrunkThreads = 256;   // 8 warps: lane quarter = warp % 4, column half = warp / 4
 struct TrunkSmem {
@@ -540,16 +573,53 @@ __global__ void __launch_bounds__(kTrunkThreads, 1) policy_trunk_kernel(const Dg
         for (int j = 0; j < 4; ++j)
             if (j < nout) y[j] = bh[j] + (y[j] + part[4 * r + j]);
         if (net == 0) {
+            double act[3], lp = 0.0;
+            if (p.sample) {
+                // a = mu + sigma * eps;  log N(a; mu, sigma) = sum -eps^2/2 - log sigma - log(2 pi)/2
+                const float* ls = fsec(p, 0, DG_POL_LOG_STD);
+                double z[3];
+                gaussian3(uint64_t(agent), p.seed, p.counter, z);
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const double l = double(__ldg(ls + j));
+                    act[j] = double(y[j]) + exp(l) * z[j];
+                    lp += -0.5 * z[j] * z[j] - l - 0.9189385332046727;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) act[j] = double(y[j]);
+            }
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
                 if (p.mean) p.mean[int64_t(agent) * 3 + j] = y[j];
-                if (p.actions) p.actions[int64_t(agent) * 3 + j] = double(y[j]);
+                if (p.actions) p.actions[int64_t(agent) * 3 + j] = act[j];
+                if (p.actions_f32) p.actions_f32[int64_t(agent) * 3 + j] = float(act[j]);
             }
+            if (p.log_prob && p.sample) p.log_prob[agent] = float(lp);
         } else if (p.value) {
             p.value[agent] = y[0];
         }
     }
     if (warp == 0) umma::tmem_dealloc(tmem, 256);
+}
+
+// ------------------------------------------------------------------ GAE
+__global__ void gae_kernel(const double* rewards, const uint8_t* dones, const float* values, int T, int64_t N,
+                           double gamma, double lam, float* adv, float* ret) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    double a = 0.0;
+    double v_next = double(values[int64_t(T) * N + i]);
+    for (int t = T - 1; t >= 0; --t) {
+        const int64_t q = int64_t(t) * N + i;
+        const double nonterm = dones[q] ? 0.0 : 1.0;
+        const double v = double(values[q]);
+        const double delta = rewards[q] + gamma * v_next * nonterm - v;
+        a = delta + gamma * lam * nonterm * a;
+        adv[q] = float(a);
+        ret[q] = float(a + v);
+        v_next = v;
+    }
 }
 
 thread_local char g_pol_err[256] = "";
@@ -604,6 +674,21 @@ int dg_policy_forward(const DgPolicyDesc* desc, void* stream) {
     const cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) {
         std::snprintf(g_pol_err, sizeof(g_pol_err), "dg_policy_forward: %s", cudaGetErrorString(err));
+        return DG_ECUDA;
+    }
+    return DG_OK;
+}
+
+int dg_gae(const double* rewards, const uint8_t* dones, const float* values, int32_t T, int64_t N, double gamma,
+           double lambda, float* advantages, float* returns, void* stream) {
+    if (!rewards || !dones || !values || !advantages || !returns) return pol_fail(DG_EINVAL, "dg_gae: null argument");
+    if (T < 1 || N < 1) return pol_fail(DG_EINVAL, "dg_gae: need T >= 1 and N >= 1");
+    const int threads = 256;
+    gae_kernel<<<unsigned((N + threads - 1) / threads), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+        rewards, dones, values, T, N, gamma, lambda, advantages, returns);
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) {
+        std::snprintf(g_pol_err, sizeof(g_pol_err), "dg_gae: %s", cudaGetErrorString(err));
         return DG_ECUDA;
     }
     return DG_OK;

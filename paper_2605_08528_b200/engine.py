@@ -537,7 +537,9 @@ class Engine:
 
     def rollout(self, actions, ticks: int | None = None, autoreset: bool = False, policy=None,
                 steer_gain: float = 2.0, throttle: float = 0.5, bufs: StepBuffers | None = None,
-                next_actions: torch.Tensor | None = None, values: torch.Tensor | None = None) -> StepOutput:
+                next_actions: torch.Tensor | None = None, values: torch.Tensor | None = None,
+                sample: bool = False, seed: int = 0, counter0: int = 0, log_probs: torch.Tensor | None = None,
+                actions_out: torch.Tensor | None = None) -> StepOutput:
         """T control ticks in ONE kernel launch -- the same results as T
         ``step`` calls (env.py:48-65 in a loop).
 
@@ -554,9 +556,13 @@ class Engine:
         observation (two tcgen05 launches), whose actor mean is the next
         tick's action -- the whole loop stays on the device and is CUDA-graph
         capturable.  ``values`` ([T][W][M] float32) receives the critic's
-        value of each tick's observation."""
+        value of each tick's observation; with ``sample`` the actions are PPO
+        draws (Philox, ``seed``, counter ``counter0 + t``) recorded in
+        ``actions_out`` ([T][W][M][3] f32) with their ``log_probs``."""
         if policy is not None and not isinstance(policy, str):
-            return self._rollout_mlp(actions, ticks, autoreset, policy, bufs, next_actions, values)
+            return self._rollout_mlp(actions, ticks, autoreset, policy, bufs, next_actions, values,
+                                     dict(sample=sample, seed=seed, counter0=counter0, log_probs=log_probs,
+                                          actions_out=actions_out))
         dev = self.device
         a = actions if isinstance(actions, torch.Tensor) else torch.as_tensor(np.asarray(actions, np.float64))
         if a.dtype not in (torch.float32, torch.float64):
@@ -598,7 +604,7 @@ class Engine:
         out.next_actions = next_actions
         return out
 
-    def _rollout_mlp(self, actions, ticks, autoreset, policy, bufs, next_actions, values) -> StepOutput:
+    def _rollout_mlp(self, actions, ticks, autoreset, policy, bufs, next_actions, values, ppo) -> StepOutput:
         dev = self.device
         a = actions if isinstance(actions, torch.Tensor) else torch.as_tensor(np.asarray(actions, np.float64))
         a = a.to(device=dev, dtype=torch.float64).contiguous()
@@ -616,7 +622,10 @@ class Engine:
         acts = next_actions if next_actions is not None else torch.empty_like(a)
         if acts.data_ptr() != a.data_ptr():
             acts.copy_(a)
-        self.run_mlp_ticks(acts, bufs, policy, T, autoreset=autoreset, values=values)
+        for name, shape in (("log_probs", (T, self.W, self.M)), ("actions_out", (T, self.W, self.M, 3))):
+            if ppo[name] is not None and tuple(ppo[name].shape) != shape:
+                raise ValueError(f"{name} shape {tuple(ppo[name].shape)}, expected {shape}")
+        self.run_mlp_ticks(acts, bufs, policy, T, autoreset=autoreset, values=values, **ppo)
         self.raise_pending_error()
         v = bufs.views
         src = dict(v)
@@ -627,18 +636,25 @@ class Engine:
 
     def run_mlp_ticks(self, acts: torch.Tensor, bufs: StepBuffers, policy, ticks: int, ring_start: int = 0,
                       autoreset: bool = False, values: torch.Tensor | None = None,
-                      event_counts: torch.Tensor | None = None) -> None:
+                      event_counts: torch.Tensor | None = None, sample: bool = False, seed: int = 0,
+                      counter0: int = 0, log_probs: torch.Tensor | None = None,
+                      actions_out: torch.Tensor | None = None) -> None:
         """Enqueue ``ticks`` x (step launch -> policy forward): tick t reads
         ``acts`` ([W][M][3] float64) and the policy overwrites it with the next
-        tick's actions.  No sync, no checks (the fast path of ``rollout`` and
-        the bench)."""
+        tick's actions (the mean, or a Philox draw with ``sample``, counter
+        ``counter0 + t``); per tick t: ``values[t]``, ``log_probs[t]``,
+        ``actions_out[t]`` (the action chosen on tick t's observation).  No
+        sync, no checks (the fast path of ``rollout`` and the bench)."""
         slots = bufs.obs.shape[0] if bufs.obs.dim() == 4 else 1
         for t in range(int(ticks)):
             slot = (ring_start + t) % slots
             self.launch_step(acts, bufs, autoreset=autoreset, ticks=1, ring_start=slot,
                              event_counts=event_counts)
             obs = bufs.obs[slot] if bufs.obs.dim() == 4 else bufs.obs
-            policy.forward(obs, actions=acts, value=None if values is None else values[t])
+            policy.forward(obs, actions=acts, value=None if values is None else values[t], sample=sample,
+                           seed=seed, counter=counter0 + t,
+                           log_prob=None if log_probs is None else log_probs[t],
+                           actions_f32=None if actions_out is None else actions_out[t])
             self.launches += policy.launches()
 
     def step(self, actions, autoreset: bool = False) -> StepOutput:

@@ -153,7 +153,13 @@ class PolicyMLP:
             b[:hb.shape[0]] = hb
             return b.view(np.uint8)
 
-        secs["W_HEAD"], secs["B_HEAD"] = head_w, head_b
+        def log_std(net):
+            v = np.zeros(4, dtype=np.float32)
+            if net == "actor":
+                v[:3] = self.log_std.numpy()
+            return v.view(np.uint8)
+
+        secs["W_HEAD"], secs["B_HEAD"], secs["LOG_STD"] = head_w, head_b, log_std
         blobs, offs = [], None
         for net in NETS:
             parts, off, cur = [], [], 0
@@ -178,10 +184,15 @@ class PolicyMLP:
 
     # ---------------------------------------------------------------- forward
     def forward(self, obs: torch.Tensor, actions: torch.Tensor | None = None,
-                mean: torch.Tensor | None = None, value: torch.Tensor | None = None) -> None:
+                mean: torch.Tensor | None = None, value: torch.Tensor | None = None,
+                sample: bool = False, seed: int = 0, counter: int = 0,
+                log_prob: torch.Tensor | None = None, actions_f32: torch.Tensor | None = None) -> None:
         """Enqueue the forward over every observation row of ``obs``
         ([..., obs_dim] float32, CUDA).  ``actions`` ([..., 3] float64) gets
-        the actor mean as the next tick's env input; ``mean`` ([..., 3] f32),
+        the next tick's env input: the actor mean, or with ``sample`` a draw
+        mean + exp(log_std) * eps (eps from Philox4x32-10 keyed by ``seed``,
+        counter (row, ``counter``)); ``log_prob`` ([...] f32) its log-density,
+        ``actions_f32`` ([..., 3]) a float32 copy; ``mean`` ([..., 3] f32),
         ``value`` ([...] f32, needs critic=True)."""
         oc = self.obs_config
         if not obs.is_cuda or obs.dtype != torch.float32 or obs.shape[-1] != oc.obs_dim:
@@ -204,10 +215,15 @@ class PolicyMLP:
                            emb=self._emb.data_ptr(),
                            mean=mean.data_ptr() if mean is not None else None,
                            actions=actions.data_ptr() if actions is not None else None,
-                           value=value.data_ptr() if value is not None else None)
+                           value=value.data_ptr() if value is not None else None,
+                           sample=int(bool(sample)), seed=int(seed) & (2 ** 64 - 1),
+                           counter=int(counter) & (2 ** 64 - 1),
+                           log_prob=log_prob.data_ptr() if log_prob is not None else None,
+                           actions_f32=actions_f32.data_ptr() if actions_f32 is not None else None)
         for i, o in enumerate(self._offs):
             d.off[i] = o
-        for t, dt in ((actions, torch.float64), (mean, torch.float32), (value, torch.float32)):
+        for t, dt in ((actions, torch.float64), (mean, torch.float32), (value, torch.float32),
+                      (log_prob, torch.float32), (actions_f32, torch.float32)):
             if t is not None and (t.dtype != dt or not t.is_cuda or not t.is_contiguous()):
                 raise ValueError("policy outputs must be contiguous CUDA tensors of the documented dtype")
         st = ct.c_void_p(torch.cuda.current_stream(obs.device).cuda_stream)
@@ -225,3 +241,27 @@ class PolicyMLP:
 
     def launches(self) -> int:
         return 2
+
+
+def gae(rewards: torch.Tensor, dones: torch.Tensor, values: torch.Tensor, gamma: float = 0.99,
+        lam: float = 0.98):
+    """Generalised advantage estimation on the device (``dg_gae``; PPO
+    hyper-parameters of PAPER.md:1214-1244 as defaults).  rewards [T][...]
+    float64, dones [T][...] (done_t: transition t ended the episode), values
+    [T+1][...] float32 with the bootstrap value in row T.  Returns
+    (advantages, returns) [T][...] float32."""
+    T = rewards.shape[0]
+    if tuple(values.shape) != (T + 1,) + tuple(rewards.shape[1:]) or tuple(dones.shape) != tuple(rewards.shape):
+        raise ValueError("gae: rewards / dones [T][...], values [T+1][...]")
+    r = rewards.to(torch.float64).contiguous()
+    d = dones.to(torch.uint8).contiguous()
+    v = values.to(torch.float32).contiguous()
+    adv = torch.empty(r.shape, dtype=torch.float32, device=r.device)
+    ret = torch.empty_like(adv)
+    lib = N.load_library()
+    st = ct.c_void_p(torch.cuda.current_stream(r.device).cuda_stream)
+    rc = lib.dg_gae(r.data_ptr(), d.data_ptr(), v.data_ptr(), T, r[0].numel(), float(gamma), float(lam),
+                    adv.data_ptr(), ret.data_ptr(), st)
+    if rc != N.DG_OK:
+        raise RuntimeError(f"dg_gae failed ({rc}): {lib.dg_policy_last_error().decode()}")
+    return adv, ret

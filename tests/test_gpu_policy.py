@@ -149,3 +149,80 @@ def test_mlp_driven_env_matches_oracle(device):
         acts = mean.double().cpu().numpy()
     for k in STATE_FIELDS:
         np.testing.assert_allclose(gpu.state[k], ora.state[k], rtol=1e-9, atol=1e-9)
+
+
+def test_ppo_sampling_matches_philox_restatement(device):
+    """sample=True: actions = mean + exp(log_std) * eps with eps from the
+    oracle's own Philox4x32-10 + Box-Muller; log-probabilities; statistics."""
+    from oracle.policy import gaussian3
+    _, obs = env_obs(device, W=64, M=16, ticks=4)
+    pol = PolicyMLP(seed=6, device=device, head_scale=1.0)
+    pol.log_std = torch.tensor([-0.5, 0.0, 0.3])
+    n = obs.shape[0]
+    mean = torch.empty((n, 3), dtype=torch.float32, device=device)
+    acts = torch.empty((n, 3), dtype=torch.float64, device=device)
+    a32 = torch.empty((n, 3), dtype=torch.float32, device=device)
+    lp = torch.empty((n,), dtype=torch.float32, device=device)
+    seed, ctr = 0x1234_5678_9ABC, 77
+    pol.forward(obs, actions=acts, mean=mean, sample=True, seed=seed, counter=ctr, log_prob=lp, actions_f32=a32)
+    torch.cuda.synchronize()
+    z = gaussian3(n, seed, ctr)
+    ls = pol.log_std.double().numpy()
+    want = mean.double().cpu().numpy() + np.exp(ls) * z
+    np.testing.assert_allclose(acts.cpu().numpy(), want, rtol=1e-12, atol=1e-12)
+    assert torch.equal(a32, acts.float())
+    want_lp = (-0.5 * z * z - ls - 0.5 * np.log(2 * np.pi)).sum(1)
+    np.testing.assert_allclose(lp.double().cpu().numpy(), want_lp, rtol=1e-6, atol=1e-5)
+    assert abs(z.mean()) < 0.05 and abs(z.std() - 1.0) < 0.05
+    # a different counter draws afresh; the same counter reproduces
+    acts2 = torch.empty_like(acts)
+    pol.forward(obs, actions=acts2, sample=True, seed=seed, counter=ctr + 1)
+    acts3 = torch.empty_like(acts)
+    pol.forward(obs, actions=acts3, sample=True, seed=seed, counter=ctr)
+    torch.cuda.synchronize()
+    assert not torch.equal(acts2, acts) and torch.equal(acts3, acts)
+
+
+def test_gae_matches_numpy(device):
+    from oracle.policy import gae as gae_ref
+    from paper_2605_08528_b200.policy import gae
+    rng = np.random.default_rng(3)
+    T, N = 33, 1000
+    r = rng.normal(size=(T, N))
+    d = rng.uniform(size=(T, N)) < 0.05
+    v = rng.normal(size=(T + 1, N)).astype(np.float32)
+    adv, ret = gae(torch.as_tensor(r, device=device), torch.as_tensor(d, device=device),
+                   torch.as_tensor(v, device=device), 0.99, 0.98)
+    wa, wr = gae_ref(r, d, v, 0.99, 0.98)
+    np.testing.assert_allclose(adv.cpu().numpy(), wa, rtol=1e-5, atol=1e-5)
+    np.testing.assert_allclose(ret.cpu().numpy(), wr, rtol=1e-5, atol=1e-5)
+
+
+def test_ppo_rollout_records_a_batch(device):
+    """configs[4] as a PPO collection: T ticks with sampled actions, their
+    log-probs and values recorded per tick, then GAE over the batch; the
+    recorded actions replayed through step() reproduce the rollout."""
+    from paper_2605_08528_b200.policy import gae
+    W, M, T = 16, 16, 24
+    inp = C.build_inputs(cfg_of(W, M, seed=21))
+    pol = PolicyMLP(seed=8, device=device, head_scale=1.0)
+    a0 = torch.zeros((W, M, 3), dtype=torch.float64, device=device)
+    ea = Engine(**inp.as_kwargs(), device=device)
+    vals = torch.empty((T, W, M), dtype=torch.float32, device=device)
+    lps = torch.empty((T, W, M), dtype=torch.float32, device=device)
+    acts = torch.empty((T, W, M, 3), dtype=torch.float32, device=device)
+    out = ea.rollout(a0, ticks=T, policy=pol, values=vals, sample=True, seed=5, log_probs=lps, actions_out=acts,
+                     autoreset=True)
+    torch.cuda.synchronize()
+    eb = Engine(**inp.as_kwargs(), device=device)
+    a = a0.clone()
+    for t in range(T):
+        o = eb.step(a, autoreset=True)
+        assert torch.equal(o.obs, out.obs[t]) and torch.equal(o.rewards, out.rewards[t]), t
+        _, val = pol(o.obs)
+        assert torch.equal(val, vals[t])
+        a = torch.empty((W, M, 3), dtype=torch.float64, device=device)
+        pol.forward(o.obs, actions=a, sample=True, seed=5, counter=t)
+        assert torch.equal(a.float(), acts[t])
+    adv, ret = gae(out.rewards[1:], out.dones[1:], vals, 0.99, 0.98)
+    assert adv.shape == (T - 1, W, M) and bool(torch.isfinite(adv).all())
