@@ -183,6 +183,13 @@ int dg_observe(dg_engine* eng, float* obs, double* ttc_min_out, double* next_act
 int dg_reset(dg_engine* eng, const uint8_t* mask, const double* new_starts,
              const double* new_goals, const double* new_headings, void* stream);
 
+/* Copy of the 12-field state [12][W][M] f64 out of / into the engine
+ * (Engine.state / set_state; the teacher-forced parity harness).  `dst` /
+ * `src` may be host (pinned or pageable) or device memory; asynchronous on
+ * stream for device and pinned memory. */
+int dg_get_state(dg_engine* eng, double* dst, void* stream);
+int dg_set_state(dg_engine* eng, const double* src, void* stream);
+
 /* step_count assignment (EnvHandle.reset sets it to 0, env.py:42). */
 int dg_set_step_count(dg_engine* eng, int32_t value, void* stream);
 

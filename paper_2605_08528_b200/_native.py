@@ -97,6 +97,8 @@ SIGNATURES = {
     "dg_step": (ct.c_int, [_P, ct.POINTER(DgStepIO), _P]),
     "dg_observe": (ct.c_int, [_P, _P, _P, _P, ct.c_double, ct.c_double, _P]),
     "dg_reset": (ct.c_int, [_P, _P, _P, _P, _P, _P]),
+    "dg_get_state": (ct.c_int, [_P, _P, _P]),
+    "dg_set_state": (ct.c_int, [_P, _P, _P]),
     "dg_set_step_count": (ct.c_int, [_P, ct.c_int32, _P]),
     "dg_check_actions": (ct.c_int, [_P, _P, ct.c_int32, _P]),
     "dg_read_error": (ct.c_int, [_P, ct.POINTER(ct.c_int32), _P]),

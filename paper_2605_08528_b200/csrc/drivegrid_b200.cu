@@ -2213,6 +2213,20 @@ int dg_sysid_rollout(const void* consts, const double* mu, const int32_t* tick_s
     return err == cudaSuccess ? DG_OK : cuda_fail(err, "dg_sysid_rollout");
 }
 
+int dg_get_state(dg_engine* eng, double* dst, void* stream) {
+    if (!eng || !dst) return fail(DG_EINVAL, "dg_get_state: null argument");
+    const size_t n = size_t(DG_NUM_STATE) * eng->base.d.W * eng->base.d.M * sizeof(double);
+    const cudaError_t e = cudaMemcpyAsync(dst, eng->base.state, n, cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DG_OK : cuda_fail(e, "dg_get_state");
+}
+
+int dg_set_state(dg_engine* eng, const double* src, void* stream) {
+    if (!eng || !src) return fail(DG_EINVAL, "dg_set_state: null argument");
+    const size_t n = size_t(DG_NUM_STATE) * eng->base.d.W * eng->base.d.M * sizeof(double);
+    const cudaError_t e = cudaMemcpyAsync(eng->base.state, src, n, cudaMemcpyDefault, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? DG_OK : cuda_fail(e, "dg_set_state");
+}
+
 int dg_launch_count(dg_engine* eng) { return eng ? eng->launches : 0; }
 
 #ifdef DG_PHASE_TIMERS

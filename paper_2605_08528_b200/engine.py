@@ -380,8 +380,20 @@ class Engine:
 
     @property
     def state(self) -> dict:
-        st = self._d["state"].cpu().numpy()
+        st = torch.empty(self._d["state"].shape, dtype=torch.float64, pin_memory=True)
+        N.check(self._lib, self._lib.dg_get_state(self._h, st.data_ptr(), self._stream()), "dg_get_state")
+        torch.cuda.current_stream(self.device).synchronize()
+        st = st.numpy()
         return {k: st[i].copy() for i, k in enumerate(STATE_FIELDS)}
+
+    def load_state_tensor(self, state: torch.Tensor) -> None:
+        """Replace the whole [12][W][M] float64 state (device or host tensor) via dg_set_state."""
+        if tuple(state.shape) != tuple(self._d["state"].shape) or state.dtype != torch.float64:
+            raise ValueError(f"state must be float64 {tuple(self._d['state'].shape)}")
+        state = state.contiguous()
+        N.check(self._lib, self._lib.dg_set_state(self._h, state.data_ptr(), self._stream()), "dg_set_state")
+        if not state.is_cuda:
+            torch.cuda.current_stream(self.device).synchronize()
 
     def set_state(self, values: dict) -> None:
         """Overwrite state fields (host or device arrays, global coordinates)."""

@@ -296,3 +296,24 @@ def test_make_env_default_shapes(device):
     assert obs.shape == (256, 16, 1929) and obs.dtype == np.float32
     with pytest.raises(FileNotFoundError):
         make_env("/nonexistent/config.yaml")
+
+
+def test_state_get_set_through_the_c_abi(device):
+    """dg_get_state / dg_set_state: a state saved after k steps and loaded back
+    into a fresh engine reproduces the next steps (teacher forcing)."""
+    inp = C.build_inputs(cfg_of(4, 16, seed=3))
+    a = Engine(**inp.as_kwargs(), device=device)
+    acts = np.random.Generator(np.random.Philox(1)).uniform(-1, 1, (12, 4, 16, 3))
+    for t in range(6):
+        a.step(acts[t])
+    saved = torch.tensor(np.stack([a.state[k] for k in STATE_FIELDS]))
+    b = Engine(**inp.as_kwargs(), device=device)
+    b.load_state_tensor(saved.to(device))
+    for k in ("alive", "reason", "event_seen", "spawn_step"):
+        b.device_tables()[k].copy_(a.device_tables()[k])
+    b.step_count = a.step_count
+    for t in range(6, 12):
+        oa, ob = a.step(acts[t]), b.step(acts[t])
+        assert np.array_equal(oa.obs, ob.obs) and np.array_equal(oa.rewards, ob.rewards)
+    for k in STATE_FIELDS:
+        assert np.array_equal(a.state[k], b.state[k])
