@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the configs[3] single-GPU and configs[4] policy-rollout sub-lines")
     ap.add_argument("--no-graph", action="store_true", help="launch eagerly from the host (slower)")
+    ap.add_argument("--shape", default="", help="launch shape '<warps>x<ctas/SM>' (default: the engine's choice)")
     ap.add_argument("--ticks-per-launch", type=int, default=0,
                     help="control ticks per persistent kernel launch (0 = default for the shape)")
     return ap.parse_args()
@@ -264,6 +265,9 @@ def main():
     W_total = args.worlds or (HEADLINE[0] if world_size == 1 else SCALE_TOTAL_WORLDS)
     inp = shard_inputs(root_config(W_total), rank, world_size)
     eng = Engine(**inp.as_kwargs(), device=dev)
+    if args.shape:
+        nw, cps = (int(v) for v in args.shape.split("x"))
+        eng.tune(nw, cps)
     W, M, D = eng.W, eng.M, eng.obs_config.obs_dim
     obs_bytes = W * M * D * 4
     ring = max(2, math.ceil(2 * L2_BYTES / obs_bytes))
