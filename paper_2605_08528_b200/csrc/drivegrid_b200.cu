@@ -191,7 +191,8 @@ struct SceneView {
     double gx0, gy0, cell, half;
     int nx, ny, words, flags;
     const int32_t* road_start;  // [nx*ny + 1]
-    const uint16_t* road_list;  // segments with midpoint within `half` of the cell, ascending
+    const uint16_t* road_list;  // segments with midpoint within `half` of the cell, ascending;
+                                // bit 15 set when the segment is a road edge
     const int32_t* lane_start;  // [nx*ny + 1]
     const uint16_t* lane_list;  // lane-subset indices that can be the nearest lane, ascending
     const uint32_t* edge_bits;  // [words] bit q: segment q is a road edge
@@ -1118,15 +1119,28 @@ world_step_kernel(const KArgs A) {
                 const double fx = floor((px - ox - G.gx0) * inv), fy = floor((py - oy - G.gy0) * inv);
                 if (fx >= 0.0 && fy >= 0.0 && fx < double(G.nx) && fy < double(G.ny)) cell_id = int(fy) * G.nx + int(fx);
             }
+            // the cell's list bounds and the first lane candidate, loaded together up
+            // front (independent of the road pass; consumed by the lane pass below)
+            const int lcell = (G.flags & kFlagLanes) ? cell_id : -1;
+            int lo = 0, hi = 0, lb0 = 0, lb1 = 0, lfirst = 0;
+            if (use_grid && cell_id >= 0) {
+                lo = __ldg(G.road_start + cell_id);
+                hi = __ldg(G.road_start + cell_id + 1);
+            }
+            if (lcell >= 0) {
+                lb0 = __ldg(G.lane_start + lcell);
+                lb1 = __ldg(G.lane_start + lcell + 1);
+                if (lb0 + lane < lb1) lfirst = __ldg(G.lane_list + lb0 + lane);
+            }
             if (use_grid) {
                 // the cell's superset list (ascending) -> exact predicates, index order;
                 // off the grid nothing is within the road radius or an edge box
                 if (cell_id >= 0) {
-                    const int lo = __ldg(G.road_start + cell_id), hi = __ldg(G.road_start + cell_id + 1);
                     for (int b0 = lo; b0 < hi; b0 += 32) {
                         const int i = b0 + lane;
-                        const int q = i < hi ? int(__ldg(G.road_list + i)) : 0;
-                        const bool edge_q = (__ldg(G.edge_bits + (q >> 5)) >> (q & 31)) & 1u;
+                        const int e = i < hi ? int(__ldg(G.road_list + i)) : 0;
+                        const int q = e & 0x7fff;
+                        const bool edge_q = (e >> 15) != 0;
                         visit(q, i < hi, edge_q);
                     }
                 }
@@ -1205,10 +1219,9 @@ world_step_kernel(const KArgs A) {
                 const double d2 = over * over + lat * lat;
                 if (d2 < best) { best = d2; best_k = kk; }
             };
-            const int lcell = (G.flags & kFlagLanes) ? cell_id : -1;
             if (lcell >= 0) {
-                const int b0 = __ldg(G.lane_start + lcell), b1 = __ldg(G.lane_start + lcell + 1);
-                for (int i = b0 + lane; i < b1; i += 32) lane_test(__ldg(G.lane_list + i));
+                if (lb0 + lane < lb1) lane_test(lfirst);
+                for (int i = lb0 + 32 + lane; i < lb1; i += 32) lane_test(__ldg(G.lane_list + i));
             } else {
                 for (int kk = lane; kk < G.KL; kk += 32) lane_test(kk);
             }
@@ -1589,8 +1602,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
             const int lo = __ldg(G.road_start + cell_id), hi = __ldg(G.road_start + cell_id + 1);
             for (int b0 = lo; b0 < hi; b0 += 32) {
                 const int i = b0 + lane;
-                const int q = i < hi ? int(__ldg(G.road_list + i)) : 0;
-                const bool edge_q = (__ldg(G.edge_bits + (q >> 5)) >> (q & 31)) & 1u;
+                const int e = i < hi ? int(__ldg(G.road_list + i)) : 0;
+                const int q = e & 0x7fff;
+                const bool edge_q = (e >> 15) != 0;
                 visit(q, i < hi, edge_q);
             }
         }

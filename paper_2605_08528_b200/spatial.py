@@ -104,7 +104,8 @@ def build_scene_index(mid, dirs, hl, hw, lane_index, edge_index, road_radius: fl
     ``header`` (64 bytes) rides in the shared-memory scene blob:
     f64 x0, y0, cell, half; i32 nx, ny, words, flags; i32 byte offsets in aux
     of road_list, lane_start, lane_list, edge_bits.  ``aux`` stays in global
-    memory (read through L1): i32 road_start[ncell+1], u16 road_list[],
+    memory (read through L1): i32 road_start[ncell+1], u16 road_list[] (segment
+    index | is-edge << 15),
     i32 lane_start[ncell+1], u16 lane_list[], u32 edge_bits[words].
     Cell c = cy * nx + cx covers [x0 + cell*cx, +cell) x [y0 + cell*cy, +cell).
     """
@@ -114,7 +115,7 @@ def build_scene_index(mid, dirs, hl, hw, lane_index, edge_index, road_radius: fl
     cell = half / cells_per_radius
     head = np.zeros(4, dtype=np.float64)
     ints = np.zeros(8, dtype=np.int32)
-    if P == 0 or P > 65535:
+    if P == 0 or P > 32767:
         return head.tobytes() + ints.tobytes(), b""
     x0 = float(mid[:, 0].min()) - half
     y0 = float(mid[:, 1].min()) - half
@@ -157,6 +158,11 @@ def build_scene_index(mid, dirs, hl, hw, lane_index, edge_index, road_radius: fl
     edge_bits = np.zeros(words, dtype=np.uint32)
     for q in edge_index:
         edge_bits[int(q) >> 5] |= np.uint32(1 << (int(q) & 31))
+    # the road list carries the edge flag in bit 15 (segment index < 32768): the
+    # scan gets "is this candidate a road edge" with the index, no dependent load
+    is_edge = np.zeros(P, dtype=bool)
+    is_edge[np.asarray(edge_index, dtype=np.int64)] = True
+    road_list = road_list | (is_edge[road_list].astype(np.uint16) << np.uint16(15))
 
     aux = b""
     offs = []

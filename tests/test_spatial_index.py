@@ -21,11 +21,12 @@ def parse(head: bytes, aux: bytes):
     nx, ny, words, flags, o_rl, o_ls, o_ll, o_eb = np.frombuffer(head[32:64], np.int32)
     ncell = nx * ny
     rs = np.frombuffer(aux[:4 * (ncell + 1)], np.int32)
-    rl = np.frombuffer(aux[o_rl:o_rl + 2 * int(rs[-1])], np.uint16)
+    rl_raw = np.frombuffer(aux[o_rl:o_rl + 2 * int(rs[-1])], np.uint16)
+    rl = rl_raw & np.uint16(0x7FFF)
     ls = np.frombuffer(aux[o_ls:o_ls + 4 * (ncell + 1)], np.int32)
     ll = np.frombuffer(aux[o_ll:o_ll + 2 * int(ls[-1])], np.uint16)
     return dict(x0=hd[0], y0=hd[1], cell=hd[2], half=hd[3], nx=nx, ny=ny, words=words, flags=flags,
-                road_start=rs, road_list=rl, lane_start=ls, lane_list=ll)
+                road_start=rs, road_list=rl, road_edge=(rl_raw >> 15).astype(bool), lane_start=ls, lane_list=ll)
 
 
 def cell_of(ix, px, py):
@@ -102,3 +103,16 @@ def test_index_disabled_when_boxes_outreach_the_grid():
 def test_default_pool_indexes_build():
     inp = C.build_inputs(C.RootConfig())
     assert inp.worlds.scene_tables is not None
+
+
+def test_road_list_edge_flags():
+    """bit 15 of every road-list entry == the segment is a road edge."""
+    for scene in SCENES:
+        t = _scene_table(scene_segments(scene))
+        head, aux = build_scene_index(t.midpoints, t.directions, t.half_lengths, t.half_widths,
+                                      t.lane_index, t.edge_index, 10.0, 4.0)
+        ix = parse(head, aux)
+        edge = set(int(q) for q in t.edge_index)
+        assert ix["road_list"].size
+        for q, e in zip(ix["road_list"], ix["road_edge"]):
+            assert bool(e) == (int(q) in edge)
