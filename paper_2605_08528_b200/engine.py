@@ -326,7 +326,7 @@ class Engine:
 
     def _new_buffers(self, obs: torch.Tensor | None = None) -> StepBuffers:
         _, total = self._aux_layout()
-        aux = torch.empty(total, dtype=torch.uint8, device=self.device)
+        aux = torch.zeros(total, dtype=torch.uint8, device=self.device)   # padding defined (initcheck)
         if obs is None:
             obs = torch.empty((self.W, self.M, self.obs_config.obs_dim), dtype=torch.float32,
                               device=self.device)
@@ -339,7 +339,7 @@ class Engine:
         """Ring of ``slots`` per-tick outputs for ``launch_step(ticks=...)``:
         obs [S][W][M][D] and every aux view with a leading slot axis."""
         _, total = self._aux_layout(slots)
-        aux = torch.empty(total, dtype=torch.uint8, device=self.device)
+        aux = torch.zeros(total, dtype=torch.uint8, device=self.device)   # padding defined (initcheck)
         obs = torch.empty((slots, self.W, self.M, self.obs_config.obs_dim), dtype=torch.float32,
                           device=self.device)
         return StepBuffers(obs, aux, self._views(aux, slots))
