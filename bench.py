@@ -42,6 +42,7 @@ import numpy as np  # noqa: E402
 L2_BYTES = 126 * 1024 * 1024
 HEADLINE = (256, 16)
 SCALE_TOTAL_WORLDS = 4096
+REF_SAMPLE_WORLDS = 1024
 DEFAULT_TICKS_PER_LAUNCH = 16
 
 
@@ -182,6 +183,13 @@ def run_reference(args, rank, world_size):
     W = args.worlds or (HEADLINE[0] if world_size == 1 else SCALE_TOTAL_WORLDS)
     cfg = root_config(W)
     inp = C.build_inputs(cfg)
+    # bounded sample: the first REF_SAMPLE_WORLDS worlds of the (globally built)
+    # batch per step, so a K-step run stays within minutes at 4096 worlds; CASPS
+    # is per agent-tick, and the numpy path's per-agent cost is flat at this size
+    Ws = min(W, REF_SAMPLE_WORLDS)
+    if Ws < W:
+        from paper_2605_08528_b200.sharding import shard_inputs as _shard
+        inp = _shard(inp, 0, W // Ws)
     eng = OracleEngine(**inp.as_kwargs(), num_workers=cores)
     pol = LaneFollower(obs_config=eng.obs_config)
     obs = eng.observe()
@@ -206,7 +214,8 @@ def run_reference(args, rank, world_size):
         "data": "synthetic", "config": {"workload": f"{W}x16 default procedural pool, LaneFollower, autoreset",
                                         "worlds": W, "agents": 16},
         "cpu_baseline": {"value": v, "unit": "agent-steps/s", "cores": cores, "kind": "port",
-                         "sample": f"{W}x16, {args.steps} steps after {args.warmup} warmup, numpy {np.__version__}"},
+                         "sample": f"{Ws} of the {W} worlds x16 (contiguous range 0..{Ws - 1}), {args.steps} steps "
+                                   f"after {args.warmup} warmup, oracle/ numpy port, numpy {np.__version__}"},
         "e2e": {"value": v, "unit": "agent-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
