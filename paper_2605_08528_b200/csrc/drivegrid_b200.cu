@@ -1066,19 +1066,27 @@ world_step_kernel(const KArgs A) {
         }
 
         W1_MARK(34);
-        // ---- phase 2b: warp m scans the scene for agent m
-        for (int m = warp; m < M; m += nwarps) {
-            const AgentSm& S = ag[m];
-            float* row = obs_w + int64_t(m) * D;
+        // ---- phase 2b: each half-warp scans the scene for one agent -- a warp takes the
+        //      agent pair (2p, 2p+1), so the two agents' dependent load / reduction chains
+        //      overlap in one instruction stream.  Lists are walked in 16-entry chunks
+        //      (both halves iterate to the longer list, predicated); collectives are
+        //      full-warp with per-half masks, reductions are 16-lane shuffles.
+        for (int pr = warp; 2 * pr < M; pr += nwarps) {
+            const int half = lane >> 4, hl = lane & 15;
+            const unsigned hshift = 16u * unsigned(half);
+            const int m = 2 * pr + half;
+            const bool act = m < M;                     // an odd last agent leaves half 1 idle
+            const AgentSm& S = ag[act ? m : 2 * pr];
+            float* row = obs_w + int64_t(act ? m : 2 * pr) * D;
             const double px = S.st[SX], py = S.st[SY];
             const double c = S.c, s = S.s;
-            const bool rewards_needed = kStep && S.alive;   // dead agents: rewards/events masked
+            const bool rewards_needed = kStep && act && S.alive;   // dead agents: rewards/events masked
             const double r2 = S.r * S.r;
             bool edge_hit = false;
 
             // (a) road context: exact d2 <= r^2 over the candidate superset, ordered
             //     compaction into shared memory; edge boxes tested on the same pass
-            uint16_t* cand = cand_sm + m * A.take_road;
+            uint16_t* cand = cand_sm + (act ? m : 2 * pr) * A.take_road;
             int count = 0;
             auto visit = [&](int q, bool in, bool edge_q) {
                 bool hit = false;
@@ -1088,8 +1096,8 @@ world_step_kernel(const KArgs A) {
                     const double d2 = dx * dx + dy * dy;
                     hit = d2 <= k.road_radius_sq;
                     if (rewards_needed && edge_q) {
-                        const double hl = G.hl[q], hw = G.hw[q];
-                        const double reach = S.r + S.d + hl + hw + 1e-6;
+                        const double hl_ = G.hl[q], hw_ = G.hw[q];
+                        const double reach = S.r + S.d + hl_ + hw_ + 1e-6;
                         if (d2 <= reach * reach) {
                             const double2 u2 = G.dir[q];
     #pragma unroll
@@ -1097,16 +1105,16 @@ world_step_kernel(const KArgs A) {
                                 const double qx = S.hx[i] - m2.x, qy = S.hy[i] - m2.y;
                                 const double along = qx * u2.x + qy * u2.y;
                                 const double lat = u2.x * qy - u2.y * qx;
-                                const double du = along - sel_clip(along, -hl, hl);
-                                const double dv = lat - sel_clip(lat, -hw, hw);
+                                const double du = along - sel_clip(along, -hl_, hl_);
+                                const double dv = lat - sel_clip(lat, -hw_, hw_);
                                 edge_hit |= du * du + dv * dv < r2;
                             }
                         }
                     }
                 }
-                const unsigned bal = __ballot_sync(kFull, hit);
+                const unsigned bal = (__ballot_sync(kFull, hit) >> hshift) & 0xffffu;
                 if (hit) {
-                    const int slot = count + __popc(bal & ((1u << lane) - 1u));
+                    const int slot = count + __popc(bal & ((1u << hl) - 1u));
                     if (slot < A.take_road) cand[slot] = uint16_t(q);
                 }
                 count += __popc(bal);
@@ -1114,12 +1122,12 @@ world_step_kernel(const KArgs A) {
             const bool use_grid = (G.flags & kFlagGrid) != 0;
             // the agent's grid cell (scene-local coordinates); -1 off the grid
             int cell_id = -1;
-            if (G.flags) {
+            if (G.flags && act) {
                 const double inv = 1.0 / G.cell;
                 const double fx = floor((px - ox - G.gx0) * inv), fy = floor((py - oy - G.gy0) * inv);
                 if (fx >= 0.0 && fy >= 0.0 && fx < double(G.nx) && fy < double(G.ny)) cell_id = int(fy) * G.nx + int(fx);
             }
-            // the cell's list bounds and the first lane candidate, loaded together up
+            // the cell's list bounds and the first lane candidates, loaded together up
             // front (independent of the road pass; consumed by the lane pass below)
             const int lcell = (G.flags & kFlagLanes) ? cell_id : -1;
             int lo = 0, hi = 0, lb0 = 0, lb1 = 0, lfirst = 0;
@@ -1130,42 +1138,41 @@ world_step_kernel(const KArgs A) {
             if (lcell >= 0) {
                 lb0 = __ldg(G.lane_start + lcell);
                 lb1 = __ldg(G.lane_start + lcell + 1);
-                if (lb0 + lane < lb1) lfirst = __ldg(G.lane_list + lb0 + lane);
+                if (lb0 + hl < lb1) lfirst = __ldg(G.lane_list + lb0 + hl);
             }
             if (use_grid) {
                 // the cell's superset list (ascending) -> exact predicates, index order;
                 // off the grid nothing is within the road radius or an edge box
-                if (cell_id >= 0) {
-                    for (int b0 = lo; b0 < hi; b0 += 32) {
-                        const int i = b0 + lane;
-                        const int e = i < hi ? int(__ldg(G.road_list + i)) : 0;
-                        const int q = e & 0x7fff;
-                        const bool edge_q = (e >> 15) != 0;
-                        visit(q, i < hi, edge_q);
-                    }
+                const int nt = (hi - lo + 15) >> 4;
+                const int nt_max = max(nt, __shfl_xor_sync(kFull, nt, 16));
+                for (int it = 0; it < nt_max; ++it) {
+                    const int i = lo + 16 * it + hl;
+                    const bool in = i < hi;
+                    const int e = in ? int(__ldg(G.road_list + i)) : 0;
+                    visit(e & 0x7fff, in, (e >> 15) != 0);
                 }
             } else {
-                for (int p0 = 0; p0 < G.P; p0 += 32) visit(p0 + lane, p0 + lane < G.P, false);
+                for (int p0 = 0; p0 < G.P; p0 += 16) visit(p0 + hl, act && p0 + hl < G.P, false);
             }
             const int ncand = count < A.take_road ? count : A.take_road;
-            if (m == 1) W1_MARK(35);
             __syncwarp();
-            for (int slot = lane; slot < ncand; slot += 32) {
-                const int q = cand[slot];
-                const double2 m2 = G.mid[q], u2 = G.dir[q];
-                const double dx = m2.x - px, dy = m2.y - py;
-                const double ux = u2.x, uy = u2.y;
-                float* o = row + road0 + 5 * slot;
-                o[0] = __double2float_rn(dg::ddiv(c * dx + s * dy, k.road_radius));
-                o[1] = __double2float_rn(dg::ddiv(-s * dx + c * dy, k.road_radius));
-                o[2] = G.type_feat[q];
-                o[3] = __double2float_rn(c * ux + s * uy);
-                o[4] = __double2float_rn(-s * ux + c * uy);
+            if (act) {
+                for (int slot = hl; slot < ncand; slot += 16) {
+                    const int q = cand[slot];
+                    const double2 m2 = G.mid[q], u2 = G.dir[q];
+                    const double dx = m2.x - px, dy = m2.y - py;
+                    const double ux = u2.x, uy = u2.y;
+                    float* o = row + road0 + 5 * slot;
+                    o[0] = __double2float_rn(dg::ddiv(c * dx + s * dy, k.road_radius));
+                    o[1] = __double2float_rn(dg::ddiv(-s * dx + c * dy, k.road_radius));
+                    o[2] = G.type_feat[q];
+                    o[3] = __double2float_rn(c * ux + s * uy);
+                    o[4] = __double2float_rn(-s * ux + c * uy);
+                }
             }
-
-            if (m == 1) W1_MARK(36);
-            if (!rewards_needed) {
-                if (kStep && lane == 0) {
+            // both agents dead (or absent): no rewards / events -> skip the rest
+            if (!__any_sync(kFull, rewards_needed)) {
+                if (kStep && act && hl == 0) {
                     ScanSm& R = sc[m];
                     R.lane_d2 = INFINITY;
                     R.lane_k = 0;
@@ -1178,32 +1185,31 @@ world_step_kernel(const KArgs A) {
             //     edge boxes when the grid could not take them
             double gap = INFINITY;
     #pragma unroll 2
-            for (int kk = lane; kk < G.KE; kk += 32) {
+            for (int kk = hl; kk < G.KE; kk += 16) {
                 const double2 m2 = G.edge_mid[kk];
                 const double ex = m2.x - px, ey = m2.y - py;
                 const double xb = c * ex + s * ey;
                 if (xb > 0.0 && xb <= k.edge_range && xb < gap) gap = xb;
-                if (!use_grid) {
+                if (!use_grid && rewards_needed) {
                     const int q = G.edge[kk];
                     const double2 u2 = G.dir[q];
-                    const double hl = G.hl[q], hw = G.hw[q];
-                    const double reach = S.r + S.d + hl + hw + 1e-6;
+                    const double hl_ = G.hl[q], hw_ = G.hw[q];
+                    const double reach = S.r + S.d + hl_ + hw_ + 1e-6;
                     if (ex * ex + ey * ey <= reach * reach) {
     #pragma unroll
                         for (int i = 0; i < 3; ++i) {
                             const double qx = S.hx[i] - m2.x, qy = S.hy[i] - m2.y;
                             const double along = qx * u2.x + qy * u2.y;
                             const double lat = u2.x * qy - u2.y * qx;
-                            const double du = along - sel_clip(along, -hl, hl);
-                            const double dv = lat - sel_clip(lat, -hw, hw);
+                            const double du = along - sel_clip(along, -hl_, hl_);
+                            const double dv = lat - sel_clip(lat, -hw_, hw_);
                             edge_hit |= du * du + dv * dv < r2;
                         }
                     }
                 }
             }
-            gap = warp_min(gap);
-            edge_hit = __any_sync(kFull, edge_hit);
-            if (m == 1) W1_MARK(37);
+            gap = warp_min(gap, 16);
+            edge_hit = ((__ballot_sync(kFull, edge_hit) >> hshift) & 0xffffu) != 0;
 
             // (c) nearest lane: argmin of point-to-segment d2, lowest index on ties,
             //     over the cell's candidate list when the agent is inside the grid
@@ -1220,23 +1226,29 @@ world_step_kernel(const KArgs A) {
                 if (d2 < best) { best = d2; best_k = kk; }
             };
             if (lcell >= 0) {
-                if (lb0 + lane < lb1) lane_test(lfirst);
-                for (int i = lb0 + 32 + lane; i < lb1; i += 32) lane_test(__ldg(G.lane_list + i));
-            } else {
-                for (int kk = lane; kk < G.KL; kk += 32) lane_test(kk);
+                if (lb0 + hl < lb1) lane_test(lfirst);
+                for (int i = lb0 + 16 + hl; i < lb1; i += 16) lane_test(__ldg(G.lane_list + i));
+            } else if (act) {
+                for (int kk = hl; kk < G.KL; kk += 16) lane_test(kk);
             }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ob = __shfl_xor_sync(kFull, best, o);
-                const int ok = __shfl_xor_sync(kFull, best_k, o);
+            for (int o = 8; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(kFull, best, o, 16);
+                const int ok = __shfl_xor_sync(kFull, best_k, o, 16);
                 if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
             }
-            if (m == 1) W1_MARK(38);
-            if (lane == 0) {
+            if (kStep && act && hl == 0) {
                 ScanSm& R = sc[m];
-                R.lane_d2 = best;
-                R.lane_k = best_k;
-                R.gap = gap;
-                R.edge_hit = edge_hit;
+                if (rewards_needed) {
+                    R.lane_d2 = best;
+                    R.lane_k = best_k;
+                    R.gap = gap;
+                    R.edge_hit = edge_hit;
+                } else {
+                    R.lane_d2 = INFINITY;
+                    R.lane_k = 0;
+                    R.gap = INFINITY;
+                    R.edge_hit = 0;
+                }
             }
         }
         WARP_MARK(0);
