@@ -1066,18 +1066,22 @@ world_step_kernel(const KArgs A) {
         }
 
         W1_MARK(34);
-        // ---- phase 2b: each half-warp scans the scene for one agent -- a warp takes the
-        //      agent pair (2p, 2p+1), so the two agents' dependent load / reduction chains
-        //      overlap in one instruction stream.  Lists are walked in 16-entry chunks
-        //      (both halves iterate to the longer list, predicated); collectives are
-        //      full-warp with per-half masks, reductions are 16-lane shuffles.
-        for (int pr = warp; 2 * pr < M; pr += nwarps) {
-            const int half = lane >> 4, hl = lane & 15;
-            const unsigned hshift = 16u * unsigned(half);
-            const int m = 2 * pr + half;
-            const bool act = m < M;                     // an odd last agent leaves half 1 idle
-            const AgentSm& S = ag[act ? m : 2 * pr];
-            float* row = obs_w + int64_t(act ? m : 2 * pr) * D;
+        // ---- phase 2b: each lane group scans the scene for one agent -- a warp takes
+        //      kAPW consecutive agents (16 lanes x 2 at 8 warps per world, 8 lanes x 4 at
+        //      4 warps), so the agents' dependent load / reduction chains overlap in one
+        //      instruction stream.  Lists are walked in kGL-entry chunks (every group
+        //      iterates to the longest list, predicated); collectives are full-warp with
+        //      per-group masks, reductions are kGL-lane shuffles.
+        constexpr int kGL = kThreads <= 128 ? 8 : 16;       // lanes per agent
+        constexpr int kAPW = 32 / kGL;                      // agents per warp
+        constexpr unsigned kGMask = (1u << kGL) - 1u;
+        for (int pr = warp; kAPW * pr < M; pr += nwarps) {
+            const int half = lane / kGL, hl = lane % kGL;
+            const unsigned hshift = unsigned(kGL) * unsigned(half);
+            const int m = kAPW * pr + half;
+            const bool act = m < M;                     // a short last group leaves lanes idle
+            const AgentSm& S = ag[act ? m : kAPW * pr];
+            float* row = obs_w + int64_t(act ? m : kAPW * pr) * D;
             const double px = S.st[SX], py = S.st[SY];
             const double c = S.c, s = S.s;
             const bool rewards_needed = kStep && act && S.alive;   // dead agents: rewards/events masked
@@ -1086,7 +1090,7 @@ world_step_kernel(const KArgs A) {
 
             // (a) road context: exact d2 <= r^2 over the candidate superset, ordered
             //     compaction into shared memory; edge boxes tested on the same pass
-            uint16_t* cand = cand_sm + (act ? m : 2 * pr) * A.take_road;
+            uint16_t* cand = cand_sm + (act ? m : kAPW * pr) * A.take_road;
             int count = 0;
             auto visit = [&](int q, bool in, bool edge_q) {
                 bool hit = false;
@@ -1112,7 +1116,7 @@ world_step_kernel(const KArgs A) {
                         }
                     }
                 }
-                const unsigned bal = (__ballot_sync(kFull, hit) >> hshift) & 0xffffu;
+                const unsigned bal = (__ballot_sync(kFull, hit) >> hshift) & kGMask;
                 if (hit) {
                     const int slot = count + __popc(bal & ((1u << hl) - 1u));
                     if (slot < A.take_road) cand[slot] = uint16_t(q);
@@ -1143,21 +1147,21 @@ world_step_kernel(const KArgs A) {
             if (use_grid) {
                 // the cell's superset list (ascending) -> exact predicates, index order;
                 // off the grid nothing is within the road radius or an edge box
-                const int nt = (hi - lo + 15) >> 4;
-                const int nt_max = max(nt, __shfl_xor_sync(kFull, nt, 16));
+                int nt_max = (hi - lo + kGL - 1) / kGL;
+                for (int o = kGL; o < 32; o <<= 1) nt_max = max(nt_max, __shfl_xor_sync(kFull, nt_max, o));
                 for (int it = 0; it < nt_max; ++it) {
-                    const int i = lo + 16 * it + hl;
+                    const int i = lo + kGL * it + hl;
                     const bool in = i < hi;
                     const int e = in ? int(__ldg(G.road_list + i)) : 0;
                     visit(e & 0x7fff, in, (e >> 15) != 0);
                 }
             } else {
-                for (int p0 = 0; p0 < G.P; p0 += 16) visit(p0 + hl, act && p0 + hl < G.P, false);
+                for (int p0 = 0; p0 < G.P; p0 += kGL) visit(p0 + hl, act && p0 + hl < G.P, false);
             }
             const int ncand = count < A.take_road ? count : A.take_road;
             __syncwarp();
             if (act) {
-                for (int slot = hl; slot < ncand; slot += 16) {
+                for (int slot = hl; slot < ncand; slot += kGL) {
                     const int q = cand[slot];
                     const double2 m2 = G.mid[q], u2 = G.dir[q];
                     const double dx = m2.x - px, dy = m2.y - py;
@@ -1185,7 +1189,7 @@ world_step_kernel(const KArgs A) {
             //     edge boxes when the grid could not take them
             double gap = INFINITY;
     #pragma unroll 2
-            for (int kk = hl; kk < G.KE; kk += 16) {
+            for (int kk = hl; kk < G.KE; kk += kGL) {
                 const double2 m2 = G.edge_mid[kk];
                 const double ex = m2.x - px, ey = m2.y - py;
                 const double xb = c * ex + s * ey;
@@ -1208,8 +1212,8 @@ world_step_kernel(const KArgs A) {
                     }
                 }
             }
-            gap = warp_min(gap, 16);
-            edge_hit = ((__ballot_sync(kFull, edge_hit) >> hshift) & 0xffffu) != 0;
+            gap = warp_min(gap, kGL);
+            edge_hit = ((__ballot_sync(kFull, edge_hit) >> hshift) & kGMask) != 0;
 
             // (c) nearest lane: argmin of point-to-segment d2, lowest index on ties,
             //     over the cell's candidate list when the agent is inside the grid
@@ -1227,13 +1231,13 @@ world_step_kernel(const KArgs A) {
             };
             if (lcell >= 0) {
                 if (lb0 + hl < lb1) lane_test(lfirst);
-                for (int i = lb0 + 16 + hl; i < lb1; i += 16) lane_test(__ldg(G.lane_list + i));
+                for (int i = lb0 + kGL + hl; i < lb1; i += kGL) lane_test(__ldg(G.lane_list + i));
             } else if (act) {
-                for (int kk = hl; kk < G.KL; kk += 16) lane_test(kk);
+                for (int kk = hl; kk < G.KL; kk += kGL) lane_test(kk);
             }
-            for (int o = 8; o > 0; o >>= 1) {
-                const double ob = __shfl_xor_sync(kFull, best, o, 16);
-                const int ok = __shfl_xor_sync(kFull, best_k, o, 16);
+            for (int o = kGL / 2; o > 0; o >>= 1) {
+                const double ob = __shfl_xor_sync(kFull, best, o, kGL);
+                const int ok = __shfl_xor_sync(kFull, best_k, o, kGL);
                 if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
             }
             if (kStep && act && hl == 0) {
