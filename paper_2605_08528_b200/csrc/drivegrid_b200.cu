@@ -982,82 +982,110 @@ world_step_kernel(const KArgs A) {
         }
 
         PHASE_MARK(4);
-        // ---- phase 2a: agent pairs, 16 lanes per ego agent (lane j <-> other agent j):
-        //      stable distance rank, swept-circle TTC, neighbour rows, hull contact
+        // ---- phase 2a: agent pairs.  kPL lanes per ego agent, each lane owns the other
+        //      agents j = jl + kPL * u (u < 16 / kPL): 16 lanes x 1 at 8 warps per world,
+        //      8 lanes x 2 at 4 warps (four egos per warp in one pass).  Stable distance
+        //      rank, swept-circle TTC, neighbour rows, hull contact, optional DRAC.
         const int road0 = A.d.ego_dim;
         const int veh0 = A.d.ego_dim + 5 * A.d.k_road;
         {
-            const int half_id = lane >> 4;          // two ego agents per warp
-            const int j = lane & 15;
-            const unsigned gmask = half_id ? 0xffff0000u : 0x0000ffffu;
-            for (int i = 2 * warp + half_id; i - half_id < M; i += 2 * nwarps) {
+            constexpr int kPL = 16;                           // lanes per ego (8 measured slower at 4 warps)
+            constexpr int kOPL = kMaxAgents / kPL;            // other agents per lane
+            constexpr int kEPW = 32 / kPL;                    // egos per warp
+            const int grp = lane / kPL, jl = lane % kPL;
+            const unsigned gmask = ((1u << kPL) - 1u) << (kPL * grp);
+            for (int i = kEPW * warp + grp; i - grp < M; i += kEPW * nwarps) {
                 const bool ego_ok = i < M;
                 const int ii = ego_ok ? i : 0;
                 const AgentSm& S = ag[ii];
                 const double px = S.st[SX], py = S.st[SY], c = S.c, s = S.s;
-                double key = INFINITY, ndx = 0.0, ndy = 0.0;
-                if (ego_ok && j < M) {
-                    const AgentSm& N = ag[j];
-                    ndx = N.st[SX] - px;
-                    ndy = N.st[SY] - py;
-                    const double dist = dg::dsqrt(ndx * ndx + ndy * ndy);
-                    key = (N.alive && j != ii) ? dist : INFINITY;
+                double key[kOPL], ndx[kOPL], ndy[kOPL];
+#pragma unroll
+                for (int u = 0; u < kOPL; ++u) {
+                    const int j = jl + kPL * u;
+                    key[u] = INFINITY;
+                    ndx[u] = 0.0;
+                    ndy[u] = 0.0;
+                    if (ego_ok && j < M) {
+                        const AgentSm& N = ag[j];
+                        ndx[u] = N.st[SX] - px;
+                        ndy[u] = N.st[SY] - py;
+                        const double dist = dg::dsqrt(ndx[u] * ndx[u] + ndy[u] * ndy[u]);
+                        key[u] = (N.alive && j != ii) ? dist : INFINITY;
+                    }
                 }
-                int rank = 0;
-                for (int t = 0; t < M; ++t) {
-                    const double kt = __shfl_sync(kFull, key, t, 16);
-                    rank += (kt < key) || (kt == key && t < j);
-                }
-                const bool nvalid = ego_ok && j < M && finite(key) && rank < A.take_veh;
-                double ttc = k.ttc_max;
-                if (nvalid) {
-                    const AgentSm& N = ag[j];
-                    ttc = swept_ttc(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c, N.s, N.d,
-                                    S.r + N.r, k.ttc_max);
-                    const double wrap = wrap_angle(N.st[SYAW] - S.st[SYAW]);
-                    float* o = obs_w + int64_t(ii) * D + veh0 + 7 * rank;
-                    o[0] = __double2float_rn(dg::ddiv(c * ndx + s * ndy, k.bbox_half));
-                    o[1] = __double2float_rn(dg::ddiv(-s * ndx + c * ndy, k.bbox_half));
-                    o[2] = N.f_len;
-                    o[3] = N.f_wid;
-                    o[4] = __double2float_rn(dg::ddiv(wrap, 3.141592653589793));
-                    o[5] = N.f_spd;
-                    o[6] = __double2float_rn(dg::ddiv(ttc, k.ttc_max));
-                }
-                ttc = warp_min(ttc, 16);
-                bool touch = false;
-                // hull contact; centres sit within d of the position, so a pair
-                // farther apart than r_a + r_b + d_a + d_b (+1e-4 m) cannot touch
-                if (kStep && ego_ok && j < M && j != ii && S.alive && ag[j].alive &&
-                    key <= S.r + ag[j].r + S.d + ag[j].d + 1e-4) {
-                    const AgentSm& N = ag[j];
-                    const double rs = S.r + N.r;
-                    const double rs2 = rs * rs;
-    #pragma unroll
-                    for (int a = 0; a < 3; ++a)
-    #pragma unroll
-                        for (int b = 0; b < 3; ++b) {
-                            const double ex = S.hx[a] - N.hx[b], ey = S.hy[a] - N.hy[b];
-                            touch |= ex * ex + ey * ey < rs2;
+                int rank[kOPL];
+#pragma unroll
+                for (int u = 0; u < kOPL; ++u) rank[u] = 0;
+#pragma unroll
+                for (int v = 0; v < kOPL; ++v)
+                    for (int sl = 0; sl < kPL; ++sl) {
+                        const int t = sl + kPL * v;
+                        const double kt = __shfl_sync(kFull, key[v], sl, kPL);
+                        if (t < M) {
+#pragma unroll
+                            for (int u = 0; u < kOPL; ++u) {
+                                const int j = jl + kPL * u;
+                                rank[u] += (kt < key[u]) || (kt == key[u] && t < j);
+                            }
                         }
+                    }
+                double ttc = k.ttc_max;
+                bool touch = false;
+                double dr = 0.0;
+#pragma unroll
+                for (int u = 0; u < kOPL; ++u) {
+                    const int j = jl + kPL * u;
+                    const bool nvalid = ego_ok && j < M && finite(key[u]) && rank[u] < A.take_veh;
+                    if (nvalid) {
+                        const AgentSm& N = ag[j];
+                        const double tj = swept_ttc(ndx[u], ndy[u], N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c,
+                                                    N.s, N.d, S.r + N.r, k.ttc_max);
+                        ttc = sel_min(ttc, tj);
+                        const double wrap = wrap_angle(N.st[SYAW] - S.st[SYAW]);
+                        float* o = obs_w + int64_t(ii) * D + veh0 + 7 * rank[u];
+                        o[0] = __double2float_rn(dg::ddiv(c * ndx[u] + s * ndy[u], k.bbox_half));
+                        o[1] = __double2float_rn(dg::ddiv(-s * ndx[u] + c * ndy[u], k.bbox_half));
+                        o[2] = N.f_len;
+                        o[3] = N.f_wid;
+                        o[4] = __double2float_rn(dg::ddiv(wrap, 3.141592653589793));
+                        o[5] = N.f_spd;
+                        o[6] = __double2float_rn(dg::ddiv(tj, k.ttc_max));
+                    }
+                    // hull contact; centres sit within d of the position, so a pair
+                    // farther apart than r_a + r_b + d_a + d_b (+1e-4 m) cannot touch
+                    if (kStep && ego_ok && j < M && j != ii && S.alive && ag[j].alive &&
+                        key[u] <= S.r + ag[j].r + S.d + ag[j].d + 1e-4) {
+                        const AgentSm& N = ag[j];
+                        const double rs = S.r + N.r;
+                        const double rs2 = rs * rs;
+    #pragma unroll
+                        for (int a = 0; a < 3; ++a)
+    #pragma unroll
+                            for (int b = 0; b < 3; ++b) {
+                                const double ex = S.hx[a] - N.hx[b], ey = S.hy[a] - N.hy[b];
+                                touch |= ex * ex + ey * ey < rs2;
+                            }
+                    }
+                    if (kStep && A.drac_max && ego_ok && j < M && j != ii && S.alive && ag[j].alive) {
+                        // episode safety metric on the post-physics state, agents alive before the tick
+                        const AgentSm& N = ag[j];
+                        const double d1 = pair_drac(ndx[u], ndy[u], N.vwx - S.vwx, N.vwy - S.vwy, S.hx, S.hy,
+                                                    N.hx, N.hy, S.r + N.r);
+                        dr = d1 > dr ? d1 : dr;
+                    }
                 }
+                ttc = warp_min(ttc, kPL);
                 touch = (__ballot_sync(kFull, touch) & gmask) != 0;
                 if (kStep && A.drac_max) {
-                    // episode safety metric on the post-physics state, agents alive before the tick
-                    double dr = 0.0;
-                    if (ego_ok && j < M && j != ii && S.alive && ag[j].alive) {
-                        const AgentSm& N = ag[j];
-                        dr = pair_drac(ndx, ndy, N.vwx - S.vwx, N.vwy - S.vwy, S.hx, S.hy, N.hx, N.hy,
-                                       S.r + N.r);
-                    }
-                    dr = warp_max_nn(dr, 16);
-                    if (ego_ok && j == 0) {
+                    dr = warp_max_nn(dr, kPL);
+                    if (ego_ok && jl == 0) {
                         double* p = A.drac_max + int64_t(w) * M + ii;
                         const double prev = *p;
                         *p = dr > prev ? dr : prev;
                     }
                 }
-                if (ego_ok && j == 0) {
+                if (ego_ok && jl == 0) {
                     sc[ii].ttc_min = ttc;
                     sc[ii].touch = touch;
                     if (!kStep && A.ttc_min_out) A.ttc_min_out[int64_t(w) * M + ii] = ttc;
