@@ -47,10 +47,8 @@ ph = out[:, [1, 25, 26, 27, 2]]
 print("  warp0: loads", np.median(ph[:, 1] - ph[:, 0]), " substeps", np.median(ph[:, 2] - ph[:, 1]),
       " derived+tables", np.median(ph[:, 3] - ph[:, 2]), " zero-fill", np.median(ph[:, 4] - ph[:, 3]))
 print("  substep ends (cycles after state loads):", np.median(out[:, 28:32] - out[:, 25:26], axis=0).astype(int))
-w1 = out[:, [4, 34, 35, 36, 37, 38]]
-print("  warp1 agent1: pairs(2a)", np.median(w1[:, 1] - w1[:, 0]), " road scan", np.median(w1[:, 2] - w1[:, 1]),
-      " road feats", np.median(w1[:, 3] - w1[:, 2]), " edge gap", np.median(w1[:, 4] - w1[:, 3]),
-      " lane", np.median(w1[:, 5] - w1[:, 4]))
+w1 = out[:, [4, 34]]
+print("  warp1: pairs (phase 2a)", np.median(w1[:, 1] - w1[:, 0]))
 gs, ge = out[:, 32], out[:, 33]
 t0 = gs.min()
 print(f"  globaltimer: CTA start spread {(gs.max() - t0) / 1e3:.2f} us, first end {(ge.min() - t0) / 1e3:.2f} us, "
