@@ -833,9 +833,8 @@ world_step_kernel(const KArgs A) {
         float* obs_w = A.obs + (int64_t(slot) * WM + int64_t(w) * M) * D;
         const TickOut O = tick_out(A, slot);
         if (kStep && t > 0) {
-            // every tick gets the same rejection as a separate step call
-            if (tid == 0) s_bad = DG_NO_ERROR;
-            __syncthreads();
+            // every tick gets the same rejection as a separate step call (s_bad was
+            // reset at the end of the previous tick, before its closing barrier)
             if (tid < 3 * M) {
                 const int64_t flat = t * act_tick + int64_t(w) * M * 3 + tid;
                 const double v = feedback ? ag[tid / 3].act[tid % 3]
@@ -1329,6 +1328,7 @@ world_step_kernel(const KArgs A) {
             PHASE_MARK(6);
             GT_MARK(33);
         }
+        if (kStep && tid == 0) s_bad = DG_NO_ERROR;   // for the next tick's action check
         if (t + 1 < T) __syncthreads();   // next tick reads st_next / act written above
     }
 }
