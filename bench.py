@@ -43,7 +43,7 @@ L2_BYTES = 126 * 1024 * 1024
 HEADLINE = (256, 16)
 SCALE_TOTAL_WORLDS = 4096
 REF_SAMPLE_WORLDS = 1024
-DEFAULT_TICKS_PER_LAUNCH = 16
+DEFAULT_TICKS_PER_LAUNCH = 64
 
 
 def parse():
