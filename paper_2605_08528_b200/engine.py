@@ -270,8 +270,14 @@ class Engine:
         self.phase_seconds = {k: 0.0 for k in PHASES}
         self._act_dev = torch.empty((W, M, 3), dtype=torch.float64, device=dev)
         self._act_host = torch.empty((W, M, 3), dtype=torch.float64).pin_memory()
-        self._obs_dev = torch.empty((W, M, oc.obs_dim), dtype=torch.float32, device=dev)
-        self._host_bufs = self._new_buffers(self._obs_dev)
+        # host-path outputs in ONE device allocation [obs | pad | aux] -> one D2H copy per step
+        obs_bytes = W * M * oc.obs_dim * 4
+        self._host_obs_bytes = _align16(obs_bytes)
+        _, aux_total = self._aux_layout()
+        self._host_blob = torch.zeros(self._host_obs_bytes + aux_total, dtype=torch.uint8, device=dev)
+        self._obs_dev = self._host_blob[:obs_bytes].view(torch.float32).view(W, M, oc.obs_dim)
+        aux_dev = self._host_blob[self._host_obs_bytes:]
+        self._host_bufs = StepBuffers(self._obs_dev, aux_dev, self._views(aux_dev))
         self.launches = 0
         self._metrics_on = False
         self._host_lay = None
@@ -715,19 +721,18 @@ class Engine:
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), ct.c_void_p(stream.cuda_stream)), "dg_step")
         self._step_count += 1
         self.launches += 1
-        obs = torch.empty(bufs.obs.shape, dtype=torch.float32, pin_memory=True)
-        aux = torch.empty(bufs.aux.shape, dtype=torch.uint8, pin_memory=True)
-        obs.copy_(bufs.obs, non_blocking=True)
-        aux.copy_(bufs.aux, non_blocking=True)
+        host = torch.empty(self._host_blob.shape, dtype=torch.uint8, pin_memory=True)
+        host.copy_(self._host_blob, non_blocking=True)          # obs + every per-tick output, one copy
         stream.synchronize()
         t2 = time.perf_counter()
-        hv = self._host_views(aux.numpy())
+        hb = host.numpy()
+        obs = hb[:self.W * self.M * self.obs_config.obs_dim * 4].view(np.float32).reshape(bufs.obs.shape)
+        hv = self._host_views(hb[self._host_obs_bytes:])
         src = dict(hv)
         src["step"] = self._step_count
         self.phase_seconds["action"] += t1 - t0
         self.phase_seconds["physics"] += t2 - t1  # the fused kernel covers every phase
-        return StepOutput(obs.numpy(), hv["rewards"], hv["dones"].astype(bool), hv["events"], src,
-                          to_host=True)
+        return StepOutput(obs, hv["rewards"], hv["dones"].astype(bool), hv["events"], src, to_host=True)
 
     # ------------------------------------------------------------------ resets
     def teleport_reset(self, mask, new_starts=None, new_goals=None, new_headings=None):
