@@ -285,7 +285,8 @@ typedef struct DgPolicyDesc {
                                    actions = mean + exp(log_std) * eps with eps ~ N(0, 1)
                                    from Philox4x32-10 (key = seed, counter = {agent
                                    index, counter}) and Box-Muller in float64        */
-    int32_t pad_;
+    int32_t first_net;          /* 0: nets 0 (actor) [and 1 with critic]; 1: the critic alone --
+                                   a trainer can run the value head on a side stream */
     uint64_t seed;
     uint64_t counter;           /* e.g. the rollout tick: a fresh draw per tick      */
     float* log_prob;            /* [n_agents] log pi(actions | obs) (diagonal Gaussian), or NULL */

@@ -73,7 +73,7 @@ class DgPolicyDesc(ct.Structure):
     _fields_ = [(n, ct.c_int32) for n in ("n_agents", "obs_dim", "ego_dim", "k_road", "k_vehicles", "critic")] + [
         ("obs", _P), ("weights", _P), ("net_stride", ct.c_int64), ("off", ct.c_int64 * len(POL_SECTIONS)),
         ("emb", _P), ("mean", _P), ("actions", _P), ("value", _P),
-        ("sample", ct.c_int32), ("pad_", ct.c_int32), ("seed", ct.c_uint64), ("counter", ct.c_uint64),
+        ("sample", ct.c_int32), ("first_net", ct.c_int32), ("seed", ct.c_uint64), ("counter", ct.c_uint64),
         ("log_prob", _P), ("actions_f32", _P)]
 
 

@@ -130,7 +130,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const DgPolicyDesc p) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int net = blockIdx.y;
+    const int net = blockIdx.y + p.first_net;
     const int a0 = blockIdx.x * kEncAgents;
     const int na = min(kEncAgents, p.n_agents - a0);
     uint8_t* A0 = sm + EncSmem::kA0;
@@ -418,7 +418,7 @@ struct TrunkSmem {
 __global__ void __launch_bounds__(kTrunkThreads, 1) policy_trunk_kernel(const DgPolicyDesc p) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int net = blockIdx.y;
+    const int net = blockIdx.y + p.first_net;
     const int a0 = blockIdx.x * kTrunkAgents;
     const int q = warp & 3, hf = warp >> 2;
     const int r = 32 * q + lane;                    // tile row = agent a0 + r
@@ -646,7 +646,8 @@ int dg_policy_forward(const DgPolicyDesc* desc, void* stream) {
     if (p.obs_dim != p.ego_dim + 5 * p.k_road + 7 * p.k_vehicles || p.ego_dim > 16)
         return pol_fail(DG_EINVAL, "dg_policy_forward: observation layout mismatch");
     if (p.k_road > 8 * 255 || p.k_vehicles > 8 * 255) return pol_fail(DG_ENOSUPPORT, "dg_policy_forward: too many slots");
-    const int nets = p.critic ? 2 : 1;
+    if (p.first_net != 0 && p.first_net != 1) return pol_fail(DG_EINVAL, "dg_policy_forward: first_net must be 0 or 1");
+    const int nets = p.first_net == 1 ? 1 : (p.critic ? 2 : 1);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int kmax = p.k_road > p.k_vehicles ? p.k_road : p.k_vehicles;
     const size_t enc = enc_smem_bytes(kmax);

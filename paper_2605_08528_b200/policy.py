@@ -186,14 +186,23 @@ class PolicyMLP:
     def forward(self, obs: torch.Tensor, actions: torch.Tensor | None = None,
                 mean: torch.Tensor | None = None, value: torch.Tensor | None = None,
                 sample: bool = False, seed: int = 0, counter: int = 0,
-                log_prob: torch.Tensor | None = None, actions_f32: torch.Tensor | None = None) -> None:
+                log_prob: torch.Tensor | None = None, actions_f32: torch.Tensor | None = None,
+                nets: str = "both") -> None:
         """Enqueue the forward over every observation row of ``obs``
         ([..., obs_dim] float32, CUDA).  ``actions`` ([..., 3] float64) gets
         the next tick's env input: the actor mean, or with ``sample`` a draw
         mean + exp(log_std) * eps (eps from Philox4x32-10 keyed by ``seed``,
         counter (row, ``counter``)); ``log_prob`` ([...] f32) its log-density,
         ``actions_f32`` ([..., 3]) a float32 copy; ``mean`` ([..., 3] f32),
-        ``value`` ([...] f32, needs critic=True)."""
+        ``value`` ([...] f32, needs critic=True).  ``nets``: "both" (default),
+        "actor" (no value) or "critic" (value only) -- the two halves can run
+        on different streams."""
+        if nets not in ("both", "actor", "critic"):
+            raise ValueError(f"nets must be 'both', 'actor' or 'critic', not {nets!r}")
+        if nets == "actor":
+            value = None
+        if nets == "critic" and value is None:
+            raise ValueError("nets='critic' needs a value output")
         oc = self.obs_config
         if not obs.is_cuda or obs.dtype != torch.float32 or obs.shape[-1] != oc.obs_dim:
             raise ValueError(f"obs must be float32 CUDA [..., {oc.obs_dim}]")
@@ -211,6 +220,7 @@ class PolicyMLP:
             self._emb = torch.empty(need // 2, dtype=torch.int16, device=self.device)
         d = N.DgPolicyDesc(n_agents=n, obs_dim=oc.obs_dim, ego_dim=oc.ego_dim, k_road=oc.k_road,
                            k_vehicles=oc.k_vehicles, critic=int(self.critic and value is not None),
+                           first_net=1 if nets == "critic" else 0,
                            obs=obs.data_ptr(), weights=self._blob.data_ptr(), net_stride=self._stride,
                            emb=self._emb.data_ptr(),
                            mean=mean.data_ptr() if mean is not None else None,
