@@ -284,13 +284,18 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
             umma::fence_after();
             // ---- L1 epilogue: (bias already in the GEMM) log2e-scaled ELU -> A1 (bf16),
             //      48 columns per thread
-#pragma unroll 1
-            for (int c = c0; c < c0 + 48; c += 16) {
-                float v[16];
-                umma::tmem_ld16(tmem + lane_base + c, v);
+            {
+                uint32_t raw[48];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = elu_log2(v[i]);
-                store_row16(A1, r, c, kHid, v);
+                for (int cc = 0; cc < 3; ++cc) umma::tmem_ld16_issue(tmem + lane_base + c0 + 16 * cc, raw + 16 * cc);
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) {
+                    umma::tmem_wait16(raw + 16 * cc);
+                    float v[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] = elu_log2(__uint_as_float(raw[16 * cc + i]));
+                    store_row16(A1, r, c0 + 16 * cc, kHid, v);
+                }
             }
             umma::fence_async_smem();
             umma::fence_before();
@@ -308,12 +313,17 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
             //      a segment are 8 consecutive lanes: a 3-stage transpose-butterfly on
             //      bf16x2 pairs leaves each lane 6 of the 48 columns' maxima.
             uint32_t pk[24];
+            {
+                // the three 16-column loads in flight together, one wait
+                uint32_t raw[48];
 #pragma unroll
-            for (int cc = 0; cc < 3; ++cc) {
-                float v[16];
-                umma::tmem_ld16(tmem + lane_base + c0 + 16 * cc, v);
+                for (int cc = 0; cc < 3; ++cc) umma::tmem_ld16_issue(tmem + lane_base + c0 + 16 * cc, raw + 16 * cc);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) pk[8 * cc + i] = valid ? umma::pack_bf16(v[2 * i], v[2 * i + 1]) : 0xff80ff80u;
+                for (int cc = 0; cc < 3; ++cc) umma::tmem_wait16(raw + 16 * cc);
+#pragma unroll
+                for (int i = 0; i < 24; ++i)
+                    pk[i] = valid ? umma::pack_bf16(__uint_as_float(raw[2 * i]), __uint_as_float(raw[2 * i + 1]))
+                                  : 0xff80ff80u;
             }
             const bool bA = (lane >> 2) & 1, bB = (lane >> 1) & 1, bC = lane & 1;
             uint32_t qa[12];
