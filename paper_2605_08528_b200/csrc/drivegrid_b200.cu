@@ -110,6 +110,19 @@ __device__ __forceinline__ double sel_clip(double x, double lo, double hi) {
 __device__ __forceinline__ double np_clip(double x, double lo, double hi) {
     return np_min(np_max(x, lo), hi);
 }
+// The same with a bound that cannot be NaN (constants): one unordered compare
+// (a NaN `a` still propagates) instead of two -- shorter float64 dependency chains.
+__device__ __forceinline__ double np_max_k(double a, double b) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.gtu.f64 p, %1, %2;\n\tselp.f64 %0, %1, %2, p;\n\t}" : "=d"(r) : "d"(a), "d"(b));
+    return r;
+}
+__device__ __forceinline__ double np_min_k(double a, double b) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.ltu.f64 p, %1, %2;\n\tselp.f64 %0, %1, %2, p;\n\t}" : "=d"(r) : "d"(a), "d"(b));
+    return r;
+}
+__device__ __forceinline__ double np_clip_k(double x, double lo, double hi) { return np_min_k(np_max_k(x, lo), hi); }
 __device__ __forceinline__ double np_sign(double x) {
     return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : (x == 0.0 ? 0.0 : x));
 }
@@ -302,11 +315,11 @@ __device__ __forceinline__ void sincos_steer(double x, double* s, double* c) {
 // One 120 Hz substep of the single-track model (vehicle.py:237-336), with the
 // reference's expression order; x[] is the 12-field state.
 __device__ __forceinline__ void substep_dynamic(double* x, const Act a, double cap, const DgConsts& k) {
-    double tau_s = np_clip(k.kp_steer * (k.theta_max * a.steer - x[SANG]) - k.kd_steer * x[SRATE],
+    double tau_s = np_clip_k(k.kp_steer * (k.theta_max * a.steer - x[SANG]) - k.kd_steer * x[SRATE],
                            -k.tau_steer_max, k.tau_steer_max);
     double rate = x[SRATE] + dg::ddiv(tau_s, k.steer_inertia) * k.physics_dt;
     double ang = x[SANG] + rate * k.physics_dt;
-    double ang_c = np_clip(ang, -k.steer_limit, k.steer_limit);
+    double ang_c = np_clip_k(ang, -k.steer_limit, k.steer_limit);
     rate = (ang_c == ang) ? rate : 0.0;
     ang = ang_c;
 
@@ -320,15 +333,15 @@ __device__ __forceinline__ void substep_dynamic(double* x, const Act a, double c
     double t_rear = 2.0 * tbr;
     double fxf0 = dg::ddiv(t_front, k.wheel_radius);
     double fxr0 = dg::ddiv(t_rear, k.wheel_radius);
-    double den = np_max(vx, 0.5);
+    double den = np_max_k(vx, 0.5);
     double fyf0 = k.cornering_stiffness * (ang - dg::ddiv(vy + k.a_f * om, den));
     double fyr0 = k.cornering_stiffness * dg::ddiv(-(vy - k.b_r * om), den);
 
     double nf = dg::dsqrt(fxf0 * fxf0 + fyf0 * fyf0);
     double nr = dg::dsqrt(fxr0 * fxr0 + fyr0 * fyr0);
     bool satf = nf > cap, satr = nr > cap;
-    double kf = satf ? dg::ddiv(cap, np_max(nf, 1e-12)) : 1.0;
-    double kr = satr ? dg::ddiv(cap, np_max(nr, 1e-12)) : 1.0;
+    double kf = satf ? dg::ddiv(cap, np_max_k(nf, 1e-12)) : 1.0;
+    double kr = satr ? dg::ddiv(cap, np_max_k(nr, 1e-12)) : 1.0;
     double fxf = fxf0 * kf, fyf = fyf0 * kf;
     double fxr = fxr0 * kr, fyr = fyr0 * kr;
 
@@ -355,8 +368,8 @@ __device__ __forceinline__ void substep_dynamic(double* x, const Act a, double c
     double spin_r = x[SWR] + dg::ddiv(t_rear - fxr * k.wheel_radius, k.i_axle) * k.physics_dt;
     if (a.brk > 0.0 && spin_f * sf < 0.0) spin_f = 0.0;
     if (a.brk > 0.0 && spin_r * sr < 0.0) spin_r = 0.0;
-    x[SWF] = np_clip(satf ? spin_f : roll_f, -200.0, 200.0);
-    x[SWR] = np_clip(satr ? spin_r : roll_r, -200.0, 200.0);
+    x[SWF] = np_clip_k(satf ? spin_f : roll_f, -200.0, 200.0);
+    x[SWR] = np_clip_k(satr ? spin_r : roll_r, -200.0, 200.0);
     x[SVX] = vx1;
     x[SVY] = vy1;
     x[SOM] = om1;
