@@ -603,7 +603,7 @@ __device__ __forceinline__ unsigned finalize_agent(const KArgs& A, const TickOut
             const double flip = (tx * tgx + ty * tgy >= 0.0) ? 1.0 : -1.0;
             tx = tx * flip;
             ty = ty * flip;
-            double progress = np_clip((px - F.px0) * tx + (py - F.py0) * ty,
+            double progress = np_clip_k((px - F.px0) * tx + (py - F.py0) * ty,
                                       -k.progress_clamp, k.progress_clamp) * k.progress_weight;
             // cos(yaw - atan2(ty, tx)) (rewards.py:127-128) as the dot product of the
             // heading with the unit lane tangent: same value to ~1e-16, no atan2 / cos
@@ -617,9 +617,10 @@ __device__ __forceinline__ unsigned finalize_agent(const KArgs& A, const TickOut
                                        ? -k.offroad_weight : 0.0;
             const double speed = dg::dsqrt(vx * vx + vy * vy);
             const double idle = speed < k.idle_speed ? -k.idle_weight : 0.0;
-            const double ttc_v = -np_min(dg::ddiv(k.ttc_vehicle_alpha, np_max(F.ttc_min, k.ttc_floor)), k.ttc_vehicle_pmax);
-            const double tau = F.gap < INFINITY ? dg::ddiv(F.gap, np_max(vx, 0.1)) : F.gap / np_max(vx, 0.1);
-            const double ttc_e = finite(tau) ? -np_min(dg::ddiv(k.ttc_edge_alpha, np_max(tau, k.ttc_floor)), k.ttc_edge_pmax)
+            const double ttc_v = -np_min_k(dg::ddiv(k.ttc_vehicle_alpha, np_max_k(F.ttc_min, k.ttc_floor)),
+                                           k.ttc_vehicle_pmax);
+            const double tau = F.gap < INFINITY ? dg::ddiv(F.gap, np_max_k(vx, 0.1)) : F.gap / np_max_k(vx, 0.1);
+            const double ttc_e = finite(tau) ? -np_min_k(dg::ddiv(k.ttc_edge_alpha, np_max_k(tau, k.ttc_floor)), k.ttc_edge_pmax)
                                              : 0.0;
             const double total = progress + lane_t + offroad + idle + ttc_v + ttc_e;
 
