@@ -1,0 +1,65 @@
+"""Host-side pieces without a GPU: the bench's algorithmic byte / FLOP
+counts, the committed ncu traffic table, the episode log (engine.py:83-145
+semantics), the metric reduction across ranks."""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+
+import bench
+from paper_2605_08528_b200.engine import LOG_STATE_FIELDS, EpisodeLog
+from paper_2605_08528_b200.sharding import combine_metrics, metric_summary
+
+
+def test_algorithmic_bytes_and_flops():
+    # obs row + state in/out + actions + tables + flags + outputs
+    assert bench.algorithmic_bytes_per_agent(1929) == 8184
+    f = bench.policy_flops_per_agent(25.0, 15.0)
+    per_net = 25 * (5 * 96 + 96 * 96) + 15 * (7 * 96 + 96 * 96) + 11 * 64 + 64 * 64 + 256 * 128 + 128 * 64
+    assert f == 2.0 * 2 * per_net + 2.0 * 64 * 4
+
+
+def test_ncu_traffic_table_matches_profiles():
+    t = json.loads((bench.ROOT / "profiles" / "ncu_traffic.json").read_text())
+    for key in ("256x16x64", "4096x16x64"):
+        W, M, T = (int(v) for v in key.split("x"))
+        alg = bench.algorithmic_bytes_per_agent(1929) * W * M * T
+        assert 0.8 * alg < t[key]["traffic_bytes"] < 1.05 * alg, key     # no wasted re-reads
+        assert bench.ncu_traffic(W, M, T) == float(t[key]["traffic_bytes"])
+    assert bench.ncu_traffic(7, 16, 64) is None
+
+
+def _state(v):
+    return {k: np.full((2, 3), float(v)) for k in LOG_STATE_FIELDS}
+
+
+def test_episode_log_records_and_resamples(tmp_path):
+    log = EpisodeLog(control_dt=1 / 30, initial_state=_state(0.0))
+    z = np.zeros((2, 3))
+    ev = {k: np.zeros((2, 3), bool) for k in ("goal", "collision", "crash", "lane_forbidden")}
+    ev["goal"][1, 2] = True
+    for step in (1, 2):
+        log.append(step, _state(step), np.zeros((2, 3, 3)), z + step, {"total": z + step}, ev,
+                   np.zeros((2, 3), bool), np.ones((2, 3), bool), np.ones((2, 3), bool))
+    assert len(log) == 2
+    r = log.resample_60hz()
+    assert len(r) == 4 and r[0]["x"][0, 0] == 0.5 and r[1]["x"][0, 0] == 1.0 and r[2]["x"][0, 0] == 1.5
+    path = tmp_path / "log.jsonl"
+    log.to_jsonl(path)
+    rows = [json.loads(line) for line in path.read_text().splitlines()]
+    assert len(rows) == 2 * 2 * 3
+    assert rows[5]["events"] == ["goal"] and rows[5]["world"] == 1 and rows[5]["agent"] == 2
+    assert rows[0]["pose"] == [1.0, 1.0, 1.0] and rows[0]["reward"] == 1.0
+
+
+def test_combine_metrics_rank_order_and_empty():
+    valid = np.ones((2, 4), bool)
+    a = metric_summary(np.array([[0.0, 5.0, 1.0, 0.0], [0.0, 0.0, 0.0, 7.0]]), valid, 1, 2)
+    b = metric_summary(np.zeros((2, 4)), valid, 0, 0)
+    tot = combine_metrics([a, b])
+    assert tot["valid_agents"] == 16 and tot["goals"] == 1 and tot["collisions"] == 2
+    assert tot["n_drac_over"] == 2 and tot["mean_max_drac"] == 6.0
+    assert tot["sr"] == 1 / 16 and tot["cr"] == 2 / 16
+    assert combine_metrics([b])["mean_max_drac"] == 0.0
