@@ -22,6 +22,8 @@ Cases (each an .npz under tests/golden/):
   drac_wet          traj_wet's run through Engine.run_episode(record=True): per-step
                     pairwise_drac + episode_metrics (metrics.py:33-125)
   drac_events       traj_events' run, same records (collisions, DRAC > 3.4)
+  traj_sparse       3x4 on a 2-agent straight road: half the slots invalid (never alive,
+                    masked everywhere), random actions
   sysid             sysid.py: maneuver sets, 60 Hz channel rollouts of 6 candidate
                     parameter vectors on one maneuver of every kind, sysid_loss,
                     and a small five-stage run_cem (population 8, 40 trials)
@@ -315,6 +317,14 @@ def drac_events():
     _drac_record("drac_events", eng, event_actions(420, 4, 16))
 
 
+def traj_sparse():
+    scene = prepare_scene(straight_scene(agent_count=2, goal_dist=40.0))
+    eng = build_engine(cfg_of(3, 4, seed=13), scenes=[scene])
+    rec = Recorder(full_obs_steps=(1, 30, 60))
+    run_actions(eng, philox_actions(12, 60, 3, 4), rec)
+    rec.save("traj_sparse", valid=eng.valid)
+
+
 def sysid():
     import json
     from drivegrid import sysid as S
@@ -359,6 +369,6 @@ def sysid():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events", "sysid"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse"]
     for name in which:
         globals()[name]()
