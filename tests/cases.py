@@ -90,6 +90,8 @@ def case_inputs(name: str) -> Case:
         cfg = cfg_of(2, 5, assignment="fixed", seed=19)
         cfg.obs = ObsConfig(include_weather=False, k_road=20, k_vehicles=3, road_radius=12.5)
         return Case(name, C.build_inputs(cfg), philox_actions(6, 40, 2, 5), 40, tuple(range(1, 41)))
+    if name == "traj_timeout":
+        return Case(name, C.build_inputs(cfg_of(2, 16, seed=17, episode_len=25)), None, 40, (1, 25, 26, 40))
     if name == "traj_sparse":
         scene = prepare_scene(straight_scene(agent_count=2, goal_dist=40.0))
         inp = C.build_inputs(cfg_of(3, 4, seed=13), scenes=[scene])
@@ -101,7 +103,7 @@ def case_inputs(name: str) -> Case:
 
 
 TRAJ_CASES = ("traj_c1", "traj_pool", "traj_wet", "traj_bicycle", "traj_custom_obs",
-              "traj_events", "traj_events_inv", "traj_sparse")
+              "traj_events", "traj_events_inv", "traj_sparse", "traj_timeout")
 
 
 def run_case(engine, case: Case, on_step):

@@ -22,6 +22,8 @@ Cases (each an .npz under tests/golden/):
   drac_wet          traj_wet's run through Engine.run_episode(record=True): per-step
                     pairwise_drac + episode_metrics (metrics.py:33-125)
   drac_events       traj_events' run, same records (collisions, DRAC > 3.4)
+  traj_timeout      2x16 default pool, episode_len 25, 40 LaneFollower steps: every
+                    survivor times out (reason 5, not parked), then steps dead
   traj_sparse       3x4 on a 2-agent straight road: half the slots invalid (never alive,
                     masked everywhere), random actions
   sysid             sysid.py: maneuver sets, 60 Hz channel rollouts of 6 candidate
@@ -317,6 +319,19 @@ def drac_events():
     _drac_record("drac_events", eng, event_actions(420, 4, 16))
 
 
+def traj_timeout():
+    eng = build_engine(cfg_of(2, 16, seed=17, episode_len=25))
+    pol = LaneFollower(obs_config=eng.obs_config)
+    rec = Recorder(full_obs_steps=(1, 25, 26, 40))
+    obs = eng.observe()
+    for t in range(40):
+        a = pol(obs)
+        out = eng.step(a)
+        rec.add(t + 1, eng, out, a)
+        obs = out.obs
+    rec.save("traj_timeout")
+
+
 def traj_sparse():
     scene = prepare_scene(straight_scene(agent_count=2, goal_dist=40.0))
     eng = build_engine(cfg_of(3, 4, seed=13), scenes=[scene])
@@ -369,6 +384,6 @@ def sysid():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout"]
     for name in which:
         globals()[name]()
