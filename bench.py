@@ -401,7 +401,7 @@ def main():
                        "kernel_shape": eng.launch_shape(),
                        "parallelism": f"world-shard x{world_size}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(W, M, R) if world_size == 1 else None,
+                         "frac": achieved / peak, "traffic": ncu_traffic(W, M, R) if world_size == 1 and ticks_per_launch == R else None,
                          "traffic_unit": "bytes per launch (ncu dram read+write, profiles/ncu_traffic.json)",
                          "algorithmic_bytes_per_launch": per_agent * W * M * ticks_per_launch,
                          "bytes_per_agent_step": per_agent, "kernel_ms": kern_avg,
