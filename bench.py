@@ -157,6 +157,13 @@ def ncu_traffic(W, M, ticks):
     return None if rec is None else float(rec["traffic_bytes"])
 
 
+def ncu_traffic_per_launch(W, M, R, ticks_per_launch):
+    """The captured R-tick launch's dram bytes, per tick x this run's average
+    ticks per launch (the traffic is the per-tick obs / output stream)."""
+    t = ncu_traffic(W, M, R)
+    return None if t is None else t / R * ticks_per_launch
+
+
 def algorithmic_bytes_per_agent(obs_dim: int) -> int:
     """Bytes one agent-step must move to/from HBM (roofline):
     obs row write + state read/write + actions + the per-agent outputs and
@@ -401,8 +408,9 @@ def main():
                        "kernel_shape": eng.launch_shape(),
                        "parallelism": f"world-shard x{world_size}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(W, M, R) if world_size == 1 and ticks_per_launch == R else None,
-                         "traffic_unit": "bytes per launch (ncu dram read+write, profiles/ncu_traffic.json)",
+                         "frac": achieved / peak, "traffic": ncu_traffic_per_launch(W, M, R, ticks_per_launch) if world_size == 1 else None,
+                         "traffic_unit": f"bytes per launch (ncu dram read+write of a {R}-tick launch, "
+                                         "profiles/ncu_traffic.json, per tick x ticks per launch)",
                          "algorithmic_bytes_per_launch": per_agent * W * M * ticks_per_launch,
                          "bytes_per_agent_step": per_agent, "kernel_ms": kern_avg,
                          "kernel_ms_per_tick": kern_avg / ticks_per_launch,
