@@ -24,7 +24,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .params import LANE_CENTER_CODES, ROAD_EDGE_CODES
+from .params import LANE_CENTER_CODES
 
 SEGMENT_GAP = 3.0
 SEGMENT_HALF_WIDTH = 0.05
