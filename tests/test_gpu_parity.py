@@ -175,6 +175,7 @@ def test_device_lane_follower_equals_host_policy(device):
         acts_d = eng.lane_follower(obs_d)
         host = pol(obs_d.cpu().numpy())
         assert np.array_equal(acts_d.cpu().numpy(), host)
+        assert torch.equal(pol.on_device(eng, obs_d), acts_d)
         out = eng.step(acts_d)
         obs_d = out.obs
 
