@@ -15,7 +15,8 @@ from paper_2605_08528_b200 import config as C
 from paper_2605_08528_b200.friction import SURFACE_ORDER, assign_friction
 from paper_2605_08528_b200.params import ObsConfig, SimConfig
 from paper_2605_08528_b200.policies import LaneFollower
-from paper_2605_08528_b200.scenes import build_world_batch, prepare_scene, straight_scene
+from paper_2605_08528_b200.scenes import (build_world_batch, export_world_batch, import_world_batch, prepare_scene,
+                                          straight_scene)
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
@@ -96,6 +97,11 @@ def case_inputs(name: str) -> Case:
         scene = prepare_scene(straight_scene(agent_count=2, goal_dist=40.0))
         inp = C.build_inputs(cfg_of(3, 4, seed=13), scenes=[scene])
         return Case(name, inp, philox_actions(12, 60, 3, 4), 60, (1, 30, 60))
+    if name == "traj_forge":
+        inp = C.build_inputs(cfg_of(6, 16, seed=23))
+        inp.worlds = forge_roundtrip(inp.worlds)[1]
+        inp.sim = SimConfig(num_envs=6, num_agents=16, seed=23)
+        return Case(name, inp, None, 40, (1, 40))
     if name in ("traj_events", "traj_events_inv"):
         inp = C.build_inputs(cfg_of(4, 16, seed=31, invincible=name.endswith("_inv")))
         return Case(name, inp, event_actions(420, 4, 16), 420, (1, 150, 420))
@@ -103,7 +109,16 @@ def case_inputs(name: str) -> Case:
 
 
 TRAJ_CASES = ("traj_c1", "traj_pool", "traj_wet", "traj_bicycle", "traj_custom_obs",
-              "traj_events", "traj_events_inv", "traj_sparse", "traj_timeout")
+              "traj_events", "traj_events_inv", "traj_sparse", "traj_timeout", "traj_forge")
+
+
+def forge_roundtrip(worlds):
+    """(bytes of the binary world export, the batch imported back from them)."""
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        path = Path(d) / "worlds.bin"
+        export_world_batch(worlds, path)
+        return path.read_bytes(), import_world_batch(path)
 
 
 def run_case(engine, case: Case, on_step):

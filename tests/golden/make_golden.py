@@ -332,6 +332,42 @@ def traj_timeout():
     rec.save("traj_timeout")
 
 
+def traj_forge():
+    """Worlds round-tripped through the binary export (world.py:199-236): the
+    engine runs on the float32-rounded imported geometry.  The export's bytes
+    are pinned by their sha256."""
+    import hashlib
+    import tempfile
+
+    from drivegrid.config import load_scene_pool, sample_weather
+    from drivegrid.engine import Engine
+    from drivegrid.vehicle import VehicleParams
+    from drivegrid.world import build_world_batch, export_world_batch, import_world_batch
+    from drivegrid.engine import SimConfig
+    cfg = cfg_of(6, 16, seed=23)
+    pool = load_scene_pool(cfg.scene_factory)
+    built, assignment = build_world_batch(pool, 6, mode="random_fill", seed=23)
+    with tempfile.TemporaryDirectory() as d:
+        path = Path(d) / "worlds.bin"
+        export_world_batch(built, path)
+        blob = path.read_bytes()
+        worlds = import_world_batch(path)
+    frictions = [assign_friction(s, h) for s, h in sample_weather(cfg.weather, 6, 23)]
+    sim = SimConfig(num_envs=6, num_agents=16, seed=23)
+    eng = Engine(worlds, pool, assignment, frictions, sim, obs_config=cfg.obs, reward_config=cfg.reward,
+                 params=VehicleParams(), bicycle=cfg.bicycle)
+    pol = LaneFollower(obs_config=eng.obs_config)
+    rec = Recorder(full_obs_steps=(1, 40))
+    obs = eng.observe()
+    for t in range(40):
+        a = pol(obs)
+        out = eng.step(a)
+        rec.add(t + 1, eng, out, a)
+        obs = out.obs
+    rec.save("traj_forge", export_sha256=np.frombuffer(hashlib.sha256(blob).digest(), dtype=np.uint8),
+             export_nbytes=np.int64(len(blob)))
+
+
 def traj_sparse():
     scene = prepare_scene(straight_scene(agent_count=2, goal_dist=40.0))
     eng = build_engine(cfg_of(3, 4, seed=13), scenes=[scene])
@@ -384,6 +420,6 @@ def sysid():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge"]
     for name in which:
         globals()[name]()
