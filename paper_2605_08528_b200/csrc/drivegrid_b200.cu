@@ -594,7 +594,7 @@ __device__ __forceinline__ unsigned finalize_agent(const KArgs& A, const TickOut
             const int WM = A.d.W * A.d.M;
             const int64_t am = int64_t(w) * A.d.M + m;
             const double px = F.st[SX], py = F.st[SY];
-            const double vx = F.st[SVX], vy = F.st[SVY], yaw = F.st[SYAW];
+            const double vx = F.st[SVX], vy = F.st[SVY];
             const double dist = dg::dsqrt(F.lane_d2);
             const bool has_lane = finite(dist);
             const double lat = has_lane ? F.lane_lat : 0.0;

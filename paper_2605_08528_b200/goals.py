@@ -1,10 +1,14 @@
 """Goal resampling along the start lane (``eval.random_goals``).
 
-Restates drivegrid config.py:222-278: for every valid agent, the nearest lane
-polyline to its start, a target arc length drawn on Philox stream (seed, 4)
-(uniform in [goal_min_m, goal_max_m], or exactly goal_min_m when the range is
-empty), tried forward then backward along the lane; agents whose lane is too
-short keep their goal.
+Behaviour of drivegrid config.py:222-278: every valid agent gets a new goal
+on the lane polyline whose vertex lies nearest its (scene-local) start; the
+travel distance is drawn from Philox stream (seed, 4) -- uniform in
+[goal_min_m, goal_max_m], or exactly goal_min_m when the range is empty, one
+draw per valid agent in (world, agent) order -- and is walked forward along
+the lane from the nearest vertex's arc length, else backward; an agent whose
+lane is too short either way keeps its goal.  Arithmetic (cumulative arc
+lengths, the interpolation) is term for term the reference's, so the goals are
+bit-identical (tests/test_oracle_golden.py, golden ``goals_random``).
 """
 
 from __future__ import annotations
@@ -12,55 +16,61 @@ from __future__ import annotations
 import numpy as np
 
 
+def _arc_table(pts: np.ndarray):
+    """(segment vectors, their lengths, cumulative arc length at each vertex)."""
+    seg = np.diff(pts, axis=0)
+    length = np.sqrt((seg ** 2).sum(axis=1))
+    return seg, length, np.concatenate([[0.0], np.cumsum(length)])
+
+
 def polyline_arc_point(points: np.ndarray, start_arc: float, distance: float):
-    seg = np.diff(points[:, :2], axis=0)
-    seg_len = np.sqrt((seg ** 2).sum(axis=1))
-    cum = np.concatenate([[0.0], np.cumsum(seg_len)])
+    """The point ``distance`` metres of arc past ``start_arc`` (negative:
+    before it), or None off either end of the polyline."""
+    seg, length, arc = _arc_table(points[:, :2])
     target = start_arc + distance
-    if target < 0.0 or target > cum[-1]:
+    if not 0.0 <= target <= arc[-1]:
         return None
-    i = min(int(np.searchsorted(cum, target, side="right") - 1), len(seg_len) - 1)
-    frac = (target - cum[i]) / seg_len[i] if seg_len[i] > 0 else 0.0
-    return points[i, :2] + frac * seg[i]
+    k = min(int(np.searchsorted(arc, target, side="right")) - 1, len(length) - 1)
+    along = (target - arc[k]) / length[k] if length[k] > 0 else 0.0
+    return points[k, :2] + along * seg[k]
+
+
+def _nearest_lane(start_xy, lanes):
+    """(lane, arc length of its vertex nearest ``start_xy``); ties keep the
+    earlier lane and, within a lane, the earlier vertex."""
+    best_d2, pick = np.inf, None
+    for lane in lanes:
+        pts = lane.points[:, :2]
+        d2 = ((pts - start_xy) ** 2).sum(axis=1)
+        v = int(np.argmin(d2))
+        if pick is None or d2[v] < best_d2:
+            best_d2, pick = d2[v], (lane, _arc_table(pts)[2][v])
+    return pick
 
 
 def resample_goal(start_xy, scene, min_m: float, max_m: float, rng):
+    """One agent's new goal (scene-local), or None (no lanes, or the lane is
+    too short for the drawn distance in both directions)."""
     lanes = scene.lane_polylines()
     if not lanes:
         return None
-    best = None
-    for poly in lanes:
-        pts = poly.points[:, :2]
-        d2 = ((pts - start_xy) ** 2).sum(axis=1)
-        i = int(np.argmin(d2))
-        if best is None or d2[i] < best[0]:
-            seg = np.diff(pts, axis=0)
-            cum = np.concatenate([[0.0], np.cumsum(np.sqrt((seg ** 2).sum(axis=1)))])
-            best = (d2[i], poly, cum[i])
-    _, poly, start_arc = best
-    dist = min_m if min_m == max_m else rng.uniform(min_m, max_m)
-    for sign in (1.0, -1.0):
-        pt = polyline_arc_point(poly.points, start_arc, sign * dist)
-        if pt is not None:
-            return pt
-    return None
+    lane, arc0 = _nearest_lane(start_xy, lanes)
+    reach = min_m if min_m == max_m else rng.uniform(min_m, max_m)
+    ahead = polyline_arc_point(lane.points, arc0, reach)
+    return ahead if ahead is not None else polyline_arc_point(lane.points, arc0, -reach)
 
 
 def resample_goals(goal_xy, start_xy, valid, grid_offsets, pool, assignment, cfg):
-    """New goals on the nearest lane, Philox stream (seed, 4); returns a copy."""
+    """New goals for every valid slot of a (W, M) batch; returns a copy."""
     rng = np.random.Generator(np.random.Philox(np.random.SeedSequence([cfg.seed, 4])))
-    goal_xy = goal_xy.copy()
-    W, M = valid.shape
-    for w in range(W):
+    out = np.array(goal_xy, dtype=np.float64, copy=True)
+    for w, m in zip(*np.nonzero(valid)):          # row-major: (world, agent) order
         off = grid_offsets[w]
-        for m in range(M):
-            if not valid[w, m]:
-                continue
-            g = resample_goal(start_xy[w, m] - off, pool[assignment[w]], cfg.eval.goal_min_m,
-                              cfg.eval.goal_max_m, rng)
-            if g is not None:
-                goal_xy[w, m] = g + off
-    return goal_xy
+        g = resample_goal(start_xy[w, m] - off, pool[assignment[w]], cfg.eval.goal_min_m,
+                          cfg.eval.goal_max_m, rng)
+        if g is not None:
+            out[w, m] = g + off
+    return out
 
 
 def resample_engine_goals(engine, pool, assignment, cfg) -> None:

@@ -368,6 +368,26 @@ def traj_forge():
              export_nbytes=np.int64(len(blob)))
 
 
+GOAL_CASES = ((8, 29, 15.0, 60.0), (6, 31, 25.0, 25.0), (4, 37, 5000.0, 5000.0))
+
+
+def goals_random():
+    """eval.random_goals (config.py:222-278): goals before / after the
+    resampling for three (W, seed, goal_min_m, goal_max_m) cases."""
+    arrays = {}
+    for i, (W, seed, lo, hi) in enumerate(GOAL_CASES):
+        cfg = cfg_of(W, 16, seed=seed)
+        before = build_engine(cfg)
+        cfg.eval.random_goals, cfg.eval.goal_min_m, cfg.eval.goal_max_m = True, lo, hi
+        after = build_engine(cfg)
+        arrays[f"c{i}_start"] = after.start_xy
+        arrays[f"c{i}_valid"] = after.valid
+        arrays[f"c{i}_before"] = before.goal_xy
+        arrays[f"c{i}_after"] = after.goal_xy
+        print("goals_random", i, int((before.goal_xy != after.goal_xy).any(axis=-1).sum()), "goals moved")
+    np.savez_compressed(OUT / "goals_random.npz", cases=np.array(GOAL_CASES), **arrays)
+
+
 def traj_sparse():
     scene = prepare_scene(straight_scene(agent_count=2, goal_dist=40.0))
     eng = build_engine(cfg_of(3, 4, seed=13), scenes=[scene])
@@ -420,6 +440,6 @@ def sysid():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random"]
     for name in which:
         globals()[name]()

@@ -318,3 +318,27 @@ def test_state_get_set_through_the_c_abi(device):
         assert np.array_equal(oa.obs, ob.obs) and np.array_equal(oa.rewards, ob.rewards)
     for k in STATE_FIELDS:
         assert np.array_equal(a.state[k], b.state[k])
+
+
+def test_random_goals_engine_parity(device):
+    """config.build_engine with eval.random_goals: the GPU engine carries the
+    reference's resampled goals (golden goals_random) and steps like the oracle
+    driven to the same goals."""
+    g = np.load(__import__("cases").GOLDEN / "goals_random.npz")
+    W, seed, lo, hi = g["cases"][0]
+    cfg = cfg_of(int(W), 16, seed=int(seed))
+    cfg.eval.random_goals, cfg.eval.goal_min_m, cfg.eval.goal_max_m = True, float(lo), float(hi)
+    gpu = C.build_engine(cfg, device=device)
+    assert np.array_equal(gpu.goal_xy, g["c0_after"])
+    ora = OracleEngine(**C.build_inputs(cfg).as_kwargs())
+    ora.goal_xy = g["c0_after"].copy()
+    dev = Dev()
+    pol = LaneFollower(obs_config=ora.obs_config)
+    obs = ora.observe()
+    dev.f("obs0", gpu.observe(), obs, rtol=OBS_RTOL, atol=OBS_ATOL)
+    for t in range(40):
+        a = pol(obs)
+        o = ora.step(a)
+        compare(dev, t + 1, gpu.step(a), o, ora.obs_config)
+        obs = o.obs
+    assert np.array_equal(gpu.reason, ora.reason) and np.array_equal(gpu.alive, ora.alive)
