@@ -368,6 +368,30 @@ def traj_forge():
              export_nbytes=np.int64(len(blob)))
 
 
+WEATHER_CASES = ((0.5, {"AC": 0.2, "SMA": 0.3, "OGFC": 0.5}, 0.1, 0.8, "AC", 7),
+                 (1.0, {"AC": 0.0, "SMA": 2.0, "OGFC": 1.0}, 0.3, 0.3, "SMA", 11),
+                 (0.25, {"OGFC": 1.0}, 0.05, 1.5, "OGFC", 42))
+
+
+def weather_sampling():
+    """sample_weather (config.py:141-157) for three weather configs x 64 worlds,
+    and the engine's per-world mu / weather token under the first one."""
+    from drivegrid.config import WeatherConfig, sample_weather
+    out = {}
+    for i, (wet, probs, fmin, fmax, dry, seed) in enumerate(WEATHER_CASES):
+        cfg = WeatherConfig(wet_fraction=wet, surface_probs=probs, film_min_mm=fmin, film_max_mm=fmax,
+                            dry_surface=dry)
+        draws = sample_weather(cfg, 64, seed)
+        out[f"c{i}_surface"] = np.array([SURFACE_ORDER.index(s) for s, _ in draws])
+        out[f"c{i}_film"] = np.array([h for _, h in draws])
+    cfg = cfg_of(16, 4, seed=7)
+    cfg.weather.wet_fraction, cfg.weather.surface_probs = 0.5, dict(WEATHER_CASES[0][1])
+    eng = build_engine(cfg)
+    out["engine_mu_eff"], out["engine_weather"] = eng.mu_eff, eng.weather
+    np.savez_compressed(OUT / "weather_sampling.npz", **out)
+    print("weather_sampling", [int((out[f"c{i}_film"] > 0).sum()) for i in range(3)], "wet worlds")
+
+
 GOAL_CASES = ((8, 29, 15.0, 60.0), (6, 31, 25.0, 25.0), (4, 37, 5000.0, 5000.0))
 
 
@@ -440,6 +464,6 @@ def sysid():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling"]
     for name in which:
         globals()[name]()
