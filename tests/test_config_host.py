@@ -13,7 +13,7 @@ import pytest
 
 from paper_2605_08528_b200 import config as C
 from paper_2605_08528_b200.goals import polyline_arc_point, resample_goal
-from paper_2605_08528_b200.params import RewardConfig
+from paper_2605_08528_b200.params import RewardConfig, SimConfig
 from paper_2605_08528_b200.scenes import prepare_scene, straight_scene
 
 
@@ -90,3 +90,11 @@ def test_polyline_arc_point_ends_and_interpolation():
     assert np.allclose(polyline_arc_point(pts, 5.0, 3.0), [3.0, 7.0])
     assert np.allclose(polyline_arc_point(pts, 5.0, -2.5), [1.5, 2.0])
     assert polyline_arc_point(pts, 0.0, 11.5) is None and polyline_arc_point(pts, 5.0, -5.5) is None
+
+
+def test_sim_config_checks():
+    cfg = SimConfig(num_envs=2, num_agents=4)
+    assert abs(cfg.control_dt - 1 / 30) < 1e-15 and abs(cfg.episode_len * cfg.control_dt - 50.0) < 1e-9
+    for bad in (dict(num_agents=17), dict(dynamics_mode="warp")):
+        with pytest.raises(ValueError):
+            SimConfig(**bad)
