@@ -145,3 +145,7 @@ def aggregate(goal_seen, coll_seen, max_drac, valid, threshold: float = DRAC_THR
         cr=colls / n_valid if n_valid else 0.0,
         mean_max_drac=float(over.mean()) if over.size else 0.0,
         valid_agents=n_valid, goals=goals, collisions=colls, per_agent_max_drac=max_drac)
+
+
+# the CASPS harness (metrics.py:130-250 of the reference) lives in casps.py
+from .casps import BenchReport, measure_engine, run_bench, write_bench_csv  # noqa: E402,F401

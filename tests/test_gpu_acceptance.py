@@ -1,0 +1,118 @@
+"""Acceptance checks of the reference (pkg/tests/test_acceptance.py:123-296)
+that touch the stepped path, restated against the GPU engine: throughput
+shape through the CASPS harness, the reward ledger, CEM recovery of hidden
+vehicle parameters, and the dynamics-gap direction under hard rain."""
+
+from __future__ import annotations
+
+import dataclasses
+import time
+
+import numpy as np
+import pytest
+
+from paper_2605_08528_b200 import config as C
+from paper_2605_08528_b200.metrics import BenchReport, measure_engine, run_bench, write_bench_csv
+from paper_2605_08528_b200.params import PHASES, REASON_GOAL, RewardConfig, VehicleParams
+from paper_2605_08528_b200.policies import LaneFollower
+from paper_2605_08528_b200.scenes import prepare_scene, straight_scene
+from paper_2605_08528_b200.sysid import CEMConfig, allocate_trials, run_cem
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(device, W=1, M=1, mode="dynamic", wet=None, goal_dist=20.0):
+    cfg = C.RootConfig()
+    cfg.env.num_envs, cfg.env.num_agents_per_env, cfg.env.dynamics_mode = W, M, mode
+    cfg.scene_factory.assignment_mode = "fixed"
+    if wet is not None:
+        cfg.weather.wet_fraction, cfg.weather.surface_probs = 1.0, {wet[0]: 1.0}
+        cfg.weather.film_min_mm = cfg.weather.film_max_mm = wet[1]
+    scene = prepare_scene(straight_scene(agent_count=M, goal_dist=goal_dist))
+    return C.build_engine(cfg, scenes=[scene], device=device)
+
+
+def test_throughput_shape(device, tmp_path):
+    """Both paths grow from 8 to 64 worlds; the device-resident loop beats the
+    host API loop; the CPU restatement of the reference is far behind."""
+    from oracle import OracleEngine
+    reports = run_bench([(8, 16), (64, 16)], steps=20, warmup=3, repeats=2, device=device)
+    by = {(r.num_envs, r.path): r for r in reports}
+    for path in ("vectorized", "device"):
+        assert by[(64, path)].casps > by[(8, path)].casps
+    assert by[(64, "device")].casps > by[(64, "vectorized")].casps
+    for r in reports:
+        assert isinstance(r, BenchReport) and set(r.phase_ms) == set(PHASES)
+        assert all(v >= 0.0 for v in r.phase_ms.values())
+    f = tmp_path / "bench.csv"
+    write_bench_csv(reports, f)
+    assert f.read_text().splitlines()[0].startswith("W,M,backend,path,CASPS")
+    # the oracle on the same fixture, a few ticks
+    cfg = C.RootConfig()
+    cfg.env.num_envs = 64
+    scene = prepare_scene(straight_scene("bench", agent_count=16, agent_gap=8.0, lane_offsets=(0.0, 4.0, -4.0),
+                                         goal_dist=60.0))
+    ora = OracleEngine(**C.build_inputs(cfg, scenes=[scene]).as_kwargs())
+    pol = LaneFollower(obs_config=ora.obs_config)
+    obs, t0 = ora.observe(), time.perf_counter()
+    for _ in range(3):
+        obs = ora.step(pol(obs)).obs
+    cpu = 3 * 64 * 16 / (time.perf_counter() - t0)
+    assert by[(64, "vectorized")].casps >= 5.0 * cpu
+    with pytest.raises(ValueError):
+        measure_engine(_engine(device), pol, 1, 0, path="reference")
+
+
+def test_reward_ledger(device):
+    rc = RewardConfig()
+    assert (rc.goal_weight, rc.goal_radius, rc.collision_warmup_steps) == (45.0, 3.0, 24)
+    assert (rc.lane_weight, rc.lane_sigma, rc.ttc_vehicle_alpha, rc.ttc_floor) == (0.08, 1.75, 0.10, 0.5)
+    eng = _engine(device)
+    acts = np.zeros((1, 1, 3))
+    acts[..., 0] = 1.0
+    for _ in range(1500):
+        gap = float(np.hypot(*(eng.goal_xy[0, 0] - eng.pos[0, 0])))
+        out = eng.step(acts)
+        if out.dones[0, 0]:
+            break
+    assert gap > 3.0 and out.rewards[0, 0] > 45.0 - 5.0 and eng.reason[0, 0] == REASON_GOAL
+
+
+def test_sysid_recovers_hidden_torques(device):
+    cem = CEMConfig()
+    assert (cem.population, cem.elite_frac, cem.refine_window, cem.brake_window) == (24, 0.25, 0.18, 0.10)
+    assert allocate_trials(320, cem.stage_weights) == [96, 64, 48, 64, 48]
+    base = VehicleParams()
+    teacher = dataclasses.replace(base, tau_drive_max=base.tau_drive_max * 1.15,
+                                  tau_brake_front=base.tau_brake_front * 1.15,
+                                  tau_brake_rear=base.tau_brake_rear * 0.85, wheel_mass=base.wheel_mass * 1.15,
+                                  inertia_scale=base.inertia_scale * 0.85)
+    res = run_cem(teacher, cem, base=base, scale=0.07, seed=0, device=device)
+    assert res.trial_split == [96, 64, 48, 64, 48]
+    for st in res.stages:
+        h = st["history"]
+        assert all(h[i] >= h[i + 1] - 1e-15 for i in range(len(h) - 1))
+    for k in ("tau_drive_max", "tau_brake_front", "tau_brake_rear"):
+        assert abs(getattr(res.best_params, k) / getattr(teacher, k) - 1.0) <= 0.10, k
+
+
+def test_dynamics_gap_direction(device):
+    """Dry: both backends reach a 50 m goal under the LaneFollower.  Hard rain
+    (SMA, 2 mm -> the 1e-3 friction floor): only the bicycle does, and the
+    single-track model's acceleration from rest stays within mu g."""
+    def reaches(mode, wet=None):
+        eng = _engine(device, mode=mode, wet=wet, goal_dist=50.0)
+        eng.run_episode(LaneFollower(obs_config=eng.obs_config))
+        return bool(eng.event_seen["goal"].any()), eng
+
+    assert reaches("bicycle")[0] and reaches("dynamic")[0]
+    rain = ("SMA", 2.0)
+    assert reaches("bicycle", rain)[0]
+    ok, eng = reaches("dynamic", rain)
+    assert not ok and abs(eng.mu_eff[0] - 1e-3) < 1e-12
+    eng = _engine(device, wet=rain, goal_dist=50.0)
+    acts = np.zeros((1, 1, 3))
+    acts[..., 0] = 1.0
+    for _ in range(150):                                   # 5 s = 600 substeps
+        eng.step(acts)
+    assert eng.state["v_x"][0, 0] / 5.0 <= 1e-3 * 9.81 * 1.05
