@@ -61,3 +61,62 @@ def test_cem_toy_quadratic():
     x, f, hist = S.cem_minimize(lambda s: ((s - 0.3) ** 2).sum(1), np.zeros(3), lo, hi, 200,
                                 S.CEMConfig(population=20), rng)
     assert f < 1e-3 and np.all(np.diff(hist) <= 0) and np.allclose(x, 0.3, atol=0.05)
+
+
+# ---- the reference's sysid unit contract (pkg/tests/test_sysid.py:12-186), host side
+def test_desk_scale_keeps_every_tier_and_throttle_brake_coverage():
+    man = S.generate_maneuvers(0.07)
+    assert all(1 <= v <= 5 for v in S.tier_counts(man).values())
+    lon = {m.kind for m in man if m.tier == "longitudinal"}
+    assert {"throttle_step", "brake_sweep"} <= lon
+    assert [m.id for m in S.generate_maneuvers(0.2)] == [m.id for m in S.generate_maneuvers(0.2)]
+
+
+def test_schedules_stay_in_the_action_box_and_surface_thirds():
+    for m in S.generate_maneuvers(0.3):
+        for t in np.linspace(0.0, m.duration, 25):
+            a = m.action_at(float(t))
+            assert 0.0 <= a[0] <= 1.0 and -1.0 <= a[1] <= 1.0 and 0.0 <= a[2] <= 1.0
+    (surf,) = [m for m in S.generate_maneuvers(0.07) if m.tier == "surface"]
+    assert [surf.surface_at(t) for t in (0.0, surf.duration / 2, surf.duration - 0.1)] == ["dry", "wet", "gravel"]
+
+
+def test_cem_settings_validation_and_stages():
+    c = S.CEMConfig()
+    assert (c.population, c.elite_frac, c.init_std_frac, c.min_std_frac) == (24, 0.25, 0.25, 0.05)
+    assert (c.stage_weights, c.refine_window, c.brake_window) == ((0.30, 0.20, 0.15, 0.20, 0.15), 0.18, 0.10)
+    for bad in (dict(stage_weights=(0.5, 0.5, 0.1, 0.1, 0.1)), dict(population=2)):
+        with pytest.raises(ValueError):
+            S.CEMConfig(**bad)
+    assert [s.name for s in S.STAGES] == ["longitudinal", "steering", "surface", "refinement", "brake_preservation"]
+    assert S.STAGES[3].param_names == S.TUNABLE_PARAMS and S.STAGES[4].param_names == S.LONGITUDINAL_PARAMS
+
+
+def test_cem_scores_the_incumbent_first_and_ranks_nan_last():
+    seen = []
+
+    def f(x):
+        seen.append(x.copy())
+        return (x ** 2).sum(axis=1)
+
+    start = np.array([0.5, 0.5])
+    S.cem_minimize(f, start, -np.ones(2), np.ones(2), trials=8, cfg=S.CEMConfig(population=8),
+                   rng=np.random.Generator(np.random.Philox(2)))
+    assert np.array_equal(seen[0][0], start)
+
+    def g(x):
+        out = (x ** 2).sum(axis=1)
+        out[0] = np.nan
+        return out
+
+    _, loss, _ = S.cem_minimize(g, np.array([0.5]), np.array([-1.0]), np.array([1.0]), trials=8,
+                                cfg=S.CEMConfig(population=8), rng=np.random.Generator(np.random.Philox(3)))
+    assert np.isfinite(loss)
+
+
+def test_param_batch_exposes_candidate_columns():
+    base = VehicleParams()
+    vecs = np.stack([S.params_to_vector(base)] * 3)
+    vecs[1, 0] *= 1.2
+    b = S.ParamBatch(base, vecs)
+    assert b.batch_size == 3 and b.tau_drive_max.shape == (3,) and b.tau_drive_max[1] == vecs[1, 0]
