@@ -146,3 +146,50 @@ def test_metrics_off_by_default_and_reset(device):
     eng.reset_episode_metrics()
     m = eng.episode_metrics()
     assert m.goals == 0 and m.collisions == 0 and not m.per_agent_max_drac.any()
+
+
+# ---- the reference's metrics unit contract (pkg/tests/test_metrics.py:14-110)
+def _head_on_log(v_closing=8.0, gap=12.0):
+    """One logged tick: agent 1 drives straight at agent 0 from ``gap`` m."""
+    from paper_2605_08528_b200.engine import LOG_STATE_FIELDS, EpisodeLog
+    st = {k: np.zeros((1, 2)) for k in LOG_STATE_FIELDS}
+    st["x"][0, 0], st["v_x"][0, 1] = gap, v_closing
+    log = EpisodeLog(control_dt=1 / 30)
+    zero, alive = np.zeros((1, 2)), np.ones((1, 2), dtype=bool)
+    log.append(1, st, np.zeros((1, 2, 3)), zero, {"total": zero}, {k: ~alive for k in EVENT_TYPES}, ~alive, alive,
+               alive)
+    return log
+
+
+def test_hand_built_head_on_drac(device):
+    log = _head_on_log()
+    rec = log.steps[0]
+    pos = np.stack([rec["state"]["x"], rec["state"]["y"]], axis=-1)
+    vel = np.stack([rec["state"]["v_x"], rec["state"]["v_y"]], axis=-1)
+    vals = GM.pairwise_drac(pos, rec["state"]["yaw"], vel, np.full((1, 2), 1.10), np.full((1, 2), 1.12),
+                            rec["alive_pre"])
+    hull_gap = 12.0 - 2 * 1.12 - 2 * 1.10
+    assert np.allclose(vals[0], [64.0 / (2 * hull_gap)] * 2, rtol=1e-12)
+    m = GM.episode_metrics(log, np.ones((1, 2), dtype=bool))
+    assert (m.sr, m.cr, m.valid_agents) == (0.0, 0.0, 2)
+    assert abs(m.mean_max_drac - 64.0 / (2 * (12.0 - 4.44))) < 1e-9
+
+
+def test_everyone_reaching_the_goal_scores_sr_one(device):
+    from paper_2605_08528_b200.policies import LaneFollower
+    from paper_2605_08528_b200.scenes import prepare_scene, straight_scene
+    cfg = cfg_of(1, 2, assignment="fixed")
+    scene = prepare_scene(straight_scene(agent_count=2, agent_gap=12.0, goal_dist=20.0))
+    eng = C.build_engine(cfg, scenes=[scene], device=device)
+    log = eng.run_episode(LaneFollower(throttle=1.0, obs_config=eng.obs_config), record=True)
+    m = GM.episode_metrics(log, eng.valid, eng.length, eng.width)
+    assert m.sr == 1.0 and m.cr == 0.0
+
+
+def test_measure_engine_report(device):
+    from paper_2605_08528_b200.params import PHASES
+    from paper_2605_08528_b200.policies import ZeroPolicy
+    eng = Engine(**C.build_inputs(cfg_of(2, 2, assignment="fixed")).as_kwargs(), device=device)
+    rep = GM.measure_engine(eng, ZeroPolicy(), steps=6, warmup=2)
+    assert rep.casps > 0 and rep.steps == 6 and set(rep.phase_ms) == set(PHASES)
+    assert all(v >= 0 for v in rep.phase_ms.values())

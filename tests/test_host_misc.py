@@ -7,6 +7,7 @@ from __future__ import annotations
 import json
 
 import numpy as np
+import pytest
 
 import bench
 from paper_2605_08528_b200.engine import LOG_STATE_FIELDS, EpisodeLog
@@ -63,3 +64,17 @@ def test_combine_metrics_rank_order_and_empty():
     assert tot["n_drac_over"] == 2 and tot["mean_max_drac"] == 6.0
     assert tot["sr"] == 1 / 16 and tot["cr"] == 2 / 16
     assert combine_metrics([b])["mean_max_drac"] == 0.0
+
+
+def test_scalar_drac_and_bench_row():
+    """metrics.drac and BenchReport.to_row as the reference's metrics tests
+    pin them (pkg/tests/test_metrics.py:14-20, 100-110)."""
+    from paper_2605_08528_b200.metrics import BenchReport, drac
+    from paper_2605_08528_b200.params import PHASES
+    assert abs(drac(10.0, 5.0) - 10.0) < 1e-12 and drac(0.0, 5.0) == 0.0 and drac(-3.0, 5.0) == 0.0
+    with pytest.raises(ValueError):
+        drac(5.0, 0.0)
+    row = BenchReport(num_envs=8, num_agents=4, backend="dynamic", path="vectorized", casps=1234.5, steps=10,
+                      warmup_steps=2, wall_seconds=0.5, phase_ms={k: 1.0 for k in PHASES}).to_row()
+    assert (row["W"], row["M"], row["CASPS"]) == (8, 4, 1234.5)
+    assert all(f"{k}_ms" in row for k in PHASES)
