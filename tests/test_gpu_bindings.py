@@ -99,3 +99,24 @@ def test_replayed_stream_matches_engine_and_oracle(device, tmp_path):
         assert np.allclose(rew, o.rewards, rtol=1e-9, atol=1e-9)
         assert np.allclose(obs, o.obs, rtol=1e-6, atol=1e-6)
     assert obs.shape == (W, M, 1929)
+
+
+def test_cuda_actions_keep_the_step_in_hbm(device, tmp_path):
+    """A torch CUDA action batch goes straight to the kernel and every output
+    comes back as a CUDA tensor, equal to the numpy round trip of a twin
+    handle; a mis-shaped CUDA batch is rejected the same way."""
+    import torch
+    f = _cfg_file(tmp_path, W=3, M=4, seed=5)
+    host, dev = make_env(f, device=device), make_env(f, device=device)
+    host.reset()
+    dev.reset()
+    acts = np.random.Generator(np.random.Philox(8)).uniform(-1.0, 1.0, (10, 3, 4, 3))
+    for t in range(10):
+        o_h, r_h, d_h, i_h = host.step(acts[t])
+        o_d, r_d, d_d, i_d = dev.step(torch.as_tensor(acts[t], device=device))
+        assert o_d.is_cuda and r_d.is_cuda and d_d.is_cuda
+        assert np.array_equal(o_d.cpu().numpy(), o_h) and np.array_equal(r_d.cpu().numpy(), r_h)
+        assert np.array_equal(d_d.cpu().numpy(), d_h)
+        assert np.array_equal(i_d["reason"].cpu().numpy(), i_h["reason"])
+    with pytest.raises(ValueError, match="shape"):
+        dev.step(torch.zeros((3, 5, 3), device=device))
