@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 6
+#define DG_ABI_VERSION 7
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -56,7 +56,11 @@ typedef struct DgDims {
     int32_t num_scenes;
     int32_t max_scene_bytes;  /* largest per-scene geometry blob, bytes      */
     int32_t max_segments;     /* largest P over scenes                       */
-    int32_t pad_;
+    int32_t geometry_global;  /* 0: each CTA stages its scene blob in shared
+                                 memory (TMA) and translates it by the world's
+                                 grid offset; 1: blobs are per world, already
+                                 translated, read from global memory (scenes
+                                 too large for the 227 KB of shared memory)  */
 } DgDims;
 
 /* Float64 scalars, precomputed on the host with the reference's expression

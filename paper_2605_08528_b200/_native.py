@@ -24,14 +24,14 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 
 class DgDims(ct.Structure):
     _fields_ = [(n, ct.c_int32) for n in (
         "W", "M", "obs_dim", "ego_dim", "k_road", "k_vehicles", "include_weather", "dynamic",
         "decimation", "episode_len", "invincible", "collision_warmup", "num_scenes",
-        "max_scene_bytes", "max_segments", "pad_")]
+        "max_scene_bytes", "max_segments", "geometry_global")]
 
 
 CONST_FIELDS = (

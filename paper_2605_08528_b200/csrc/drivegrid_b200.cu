@@ -771,8 +771,9 @@ world_step_kernel(const KArgs A) {
     const DgConsts& k = A.k;
 
     // ---- shared memory carve-up
+    const bool geo_global = A.d.geometry_global != 0;
     uint8_t* geo = smem;
-    AgentSm* ag = reinterpret_cast<AgentSm*>(smem + align16(A.d.max_scene_bytes));
+    AgentSm* ag = reinterpret_cast<AgentSm*>(smem + (geo_global ? 0 : align16(A.d.max_scene_bytes)));
     ScanSm* sc = reinterpret_cast<ScanSm*>(ag + kMaxAgents);
     uint64_t* bar = reinterpret_cast<uint64_t*>(sc + kMaxAgents);
     uint16_t* cand_sm = reinterpret_cast<uint16_t*>(bar + 2);   // [M][take_road]
@@ -812,7 +813,7 @@ world_step_kernel(const KArgs A) {
         }
         step_now = A.step_count[w];
     }
-    if (tid == 0) {
+    if (tid == 0 && !geo_global) {
         mbar_init(bar, 1);
         bulk_load(geo, A.scene_blob + meta[0], uint32_t(meta[1]), bar);
     }
@@ -968,7 +969,11 @@ world_step_kernel(const KArgs A) {
         if (warp == 0) PHASE_MARK(2);
         __syncthreads();  // agent table + zero rows done, mbarrier init visible
         PHASE_MARK(3);
-        if (t == 0) {
+        if (t == 0 && geo_global) {
+            // per-world blob in global memory, translated on the host (same float64 adds)
+            G = scene_view(const_cast<uint8_t*>(A.scene_blob + meta[0]), A.scene_blob + meta[5], int(meta[2]),
+                           int(meta[3]), int(meta[4]));
+        } else if (t == 0) {
             mbar_wait(bar, 0);
             // the view reads the index header from the copied blob: only after the wait
             G = scene_view(geo, A.scene_blob + meta[5], int(meta[2]), int(meta[3]), int(meta[4]));
@@ -1525,6 +1530,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
     const int64_t* meta = A.scene_meta + 8 * scene;
     const uint8_t* gbase = A.scene_blob + meta[0];
     const double ox = A.grid_offset[2 * w], oy = A.grid_offset[2 * w + 1];
+    // scene-local geometry -> global (exactly mid + offset); per-world blobs
+    // (geometry_global) were translated on the host
+    const bool geo_global = A.d.geometry_global != 0;
+    auto tx = [&](double v) { return geo_global ? v : v + ox; };
+    auto ty = [&](double v) { return geo_global ? v : v + oy; };
 
     // ---- wait for the physics kernel (its writes are visible after this)
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1620,7 +1630,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
         bool hit = false;
         if (in) {
             const double2 m2 = __ldg(G.mid + q);
-            const double mx = m2.x + ox, my = m2.y + oy;
+            const double mx = tx(m2.x), my = ty(m2.y);
             const double dx = mx - px, dy = my - py;
             const double d2 = dx * dx + dy * dy;
             hit = d2 <= k.road_radius_sq;
@@ -1674,7 +1684,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
     for (int slot = lane; slot < ncand; slot += 32) {
         const int q = cand[slot];
         const double2 m2 = __ldg(G.mid + q), u2 = __ldg(G.dir + q);
-        const double dx = (m2.x + ox) - px, dy = (m2.y + oy) - py;
+        const double dx = (tx(m2.x)) - px, dy = (ty(m2.y)) - py;
         float* o = row + road0 + 5 * slot;
         o[0] = __double2float_rn(dg::ddiv(c * dx + s * dy, k.road_radius));
         o[1] = __double2float_rn(dg::ddiv(-s * dx + c * dy, k.road_radius));
@@ -1699,7 +1709,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
 #pragma unroll 2
         for (int kk = lane; kk < G.KE; kk += 32) {
             const double2 m2 = __ldg(G.edge_mid + kk);
-            const double ex = (m2.x + ox) - px, ey = (m2.y + oy) - py;
+            const double ex = (tx(m2.x)) - px, ey = (ty(m2.y)) - py;
             const double xb = c * ex + s * ey;
             if (xb > 0.0 && xb <= k.edge_range && xb < gap) gap = xb;
             if (!use_grid) {
@@ -1708,7 +1718,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
                 const double hl = __ldg(G.hl + q), hw = __ldg(G.hw + q);
                 const double reach = S.r + S.d + hl + hw + 1e-6;
                 if (ex * ex + ey * ey <= reach * reach) {
-                    const double mx = m2.x + ox, my = m2.y + oy;
+                    const double mx = tx(m2.x), my = ty(m2.y);
 #pragma unroll
                     for (int i = 0; i < 3; ++i) {
                         const double qx = S.hx[i] - mx, qy = S.hy[i] - my;
@@ -1724,7 +1734,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
         gap = warp_min(gap);
         auto lane_test = [&](int kk) {
             const double4 l4 = ldg4(G.lane_seg + kk);
-            const double ex = px - (l4.x + ox), ey = py - (l4.y + oy);
+            const double ex = px - (tx(l4.x)), ey = py - (ty(l4.y));
             const double along = ex * l4.z + ey * l4.w;
             const double lat = l4.z * ey - l4.w * ex;
             const double t = fabs(along) - __ldg(G.lane_hl + kk);
@@ -1763,7 +1773,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
         F.lane_lat = 0.0; F.lane_tx = 0.0; F.lane_ty = 0.0;
         if (best < INFINITY) {
             const double4 l4 = ldg4(G.lane_seg + best_k);
-            const double ex = px - (l4.x + ox), ey = py - (l4.y + oy);
+            const double ex = px - (tx(l4.x)), ey = py - (ty(l4.y));
             F.lane_tx = l4.z;
             F.lane_ty = l4.w;
             F.lane_lat = l4.z * ey - l4.w * ex;
@@ -1963,13 +1973,26 @@ static cudaError_t launch_world_step(const dg_engine* e, const KArgs& A, cudaStr
     return cudaErrorInvalidConfiguration;
 }
 
+// Raise a kernel's dynamic shared-memory limit to the device ceiling (opt-in
+// per-block maximum minus the kernel's static shared memory).
+template <typename K>
+static cudaError_t raise_smem_limit(K kernel) {
+    int dev = 0, optin = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, kernel);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 optin - int(fa.sharedSizeBytes));
+    return e;
+}
+
 template <bool kStep>
-static cudaError_t set_smem_attr(size_t bytes) {
+static cudaError_t set_smem_attr(size_t) {
     cudaError_t e = cudaSuccess;
 #define DG_ATTR(T, B)                                                                    \
-    if (e == cudaSuccess)                                                                \
-        e = cudaFuncSetAttribute(world_step_kernel<kStep, T, B>,                         \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e == cudaSuccess) e = raise_smem_limit(world_step_kernel<kStep, T, B>);
     DG_VARIANTS(DG_ATTR)
 #undef DG_ATTR
     return e;
@@ -1993,12 +2016,10 @@ static bool has_split_variant(int threads, int blocks) {
 }
 
 template <bool kStep>
-static cudaError_t set_split_smem_attr(size_t bytes) {
+static cudaError_t set_split_smem_attr(size_t) {
     cudaError_t e = cudaSuccess;
 #define DG_ATTR(T, B)                                                                    \
-    if (e == cudaSuccess)                                                                \
-        e = cudaFuncSetAttribute(agent_obs_kernel<kStep, T, B>,                          \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e == cudaSuccess) e = raise_smem_limit(agent_obs_kernel<kStep, T, B>);
     DG_SPLIT_VARIANTS(DG_ATTR)
 #undef DG_ATTR
     return e;
@@ -2053,7 +2074,7 @@ static size_t split_smem_bytes(int take_road, int apc) {
 }
 
 static size_t step_smem_bytes(const DgDims& d, int take_road) {
-    size_t b = size_t(align16(d.max_scene_bytes));
+    size_t b = d.geometry_global ? 0 : size_t(align16(d.max_scene_bytes));
     b += sizeof(AgentSm) * kMaxAgents + sizeof(ScanSm) * kMaxAgents;
     b += 16;  // mbarrier
     b += sizeof(uint16_t) * kMaxAgents * size_t(take_road > 0 ? take_road : 1);
@@ -2115,15 +2136,18 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
     A.take_road = d.k_road < d.max_segments ? d.k_road : d.max_segments;
     A.take_veh = d.k_vehicles < d.M ? d.k_vehicles : d.M;
     e->smem_bytes = step_smem_bytes(d, A.take_road);
-    if (e->smem_bytes > 227 * 1024) {
+    if (e->smem_bytes > 227 * 1024 - 4096) {   // headroom for the kernels' static / reserved shared memory
         delete e;
         return fail(DG_ENOSUPPORT, "dg_create: scene geometry does not fit in shared memory");
     }
     e->smem_split = split_smem_bytes(A.take_road, 8);
-    cudaError_t err = set_smem_attr<true>(e->smem_bytes);
-    if (err == cudaSuccess) err = set_smem_attr<false>(e->smem_bytes);
-    if (err == cudaSuccess) err = set_split_smem_attr<true>(e->smem_split);
-    if (err == cudaSuccess) err = set_split_smem_attr<false>(e->smem_split);
+    // The attribute belongs to the kernel, not the engine: always the device
+    // ceiling, so engines with smaller blobs never shrink another engine's limit
+    // (each launch passes its own dynamic size; occupancy follows that size).
+    cudaError_t err = set_smem_attr<true>(0);
+    if (err == cudaSuccess) err = set_smem_attr<false>(0);
+    if (err == cudaSuccess) err = set_split_smem_attr<true>(0);
+    if (err == cudaSuccess) err = set_split_smem_attr<false>(0);
     if (err != cudaSuccess) {
         delete e;
         return cuda_fail(err, "dg_create: cudaFuncSetAttribute");

@@ -123,6 +123,32 @@ def pack_scenes(scene_tables, type_norm: float, road_radius: float = 10.0,
     return blob, np.asarray(meta, dtype=np.int64), max_bytes, max_p
 
 
+def per_world_blobs(blob: np.ndarray, meta: np.ndarray, scene_of_world, grid_offsets):
+    """Scenes whose blob exceeds shared memory (DgDims.geometry_global): one
+    copy of the scene blob per world, appended after the shared per-scene
+    blobs, with the segment / lane / edge midpoints already moved by the
+    world's grid offset -- the same float64 ``mid + offset`` the kernel applies
+    when it stages a blob in shared memory.  The spatial-index lists stay
+    shared (meta[5] keeps pointing at the scene's copy)."""
+    parts, wmeta, off = [blob.tobytes()], [], len(blob)
+    for w, s in enumerate(np.asarray(scene_of_world)):
+        o, nb, P, KL, KE, aux_off, aux_len, _ = (int(v) for v in meta[s])
+        chunk = np.frombuffer(bytearray(blob[o:o + nb].tobytes()), dtype=np.uint8)
+        ox, oy = float(grid_offsets[w][0]), float(grid_offsets[w][1])
+        lane_at = 32 * P + _align16(8 * P) * 2 + _align16(4 * P)
+        edge_at = lane_at + 32 * KL + _align16(8 * KL)
+        mid = chunk[:16 * P].view(np.float64).reshape(P, 2)
+        lane = chunk[lane_at:lane_at + 32 * KL].view(np.float64).reshape(KL, 4)
+        edge = chunk[edge_at:edge_at + 16 * KE].view(np.float64).reshape(KE, 2)
+        for a in (mid, lane, edge):
+            a[:, 0] += ox
+            a[:, 1] += oy
+        parts.append(chunk.tobytes())
+        wmeta.append([off, nb, P, KL, KE, aux_off, aux_len, 0])
+        off += nb
+    return np.frombuffer(b"".join(parts), dtype=np.uint8).copy(), np.asarray(wmeta, dtype=np.int64)
+
+
 class StepOutput:
     """Result of one control tick (engine.py:70-76).  ``events`` and ``info``
     are built lazily from the packed output buffers."""
@@ -173,13 +199,21 @@ class StepBuffers:
 
 
 class Engine:
-    """Owner of the (W, M) agent state over a world batch, on one GPU."""
+    """Owner of the (W, M) agent state over a world batch, on one GPU.
+
+    Performance knobs (results are identical under every setting):
+    ``spatial_index`` (per-cell candidate lists vs full scans),
+    ``warps_per_world`` / ``launch_mode`` (kernel shape, fused vs split), and
+    ``geometry_global`` -- None stages each world's scene in shared memory and
+    falls back to per-world blobs in global memory only for scenes too large
+    for it; True / False force either path.
+    """
 
     def __init__(self, worlds, scenes, assignment, frictions, config: SimConfig,
                  obs_config: ObsConfig | None = None, reward_config: RewardConfig | None = None,
                  params: VehicleParams | None = None, bicycle: BicycleParams | None = None,
                  device=None, spatial_index: bool = True, warps_per_world: int | None = None,
-                 launch_mode: int = 0):
+                 launch_mode: int = 0, geometry_global: bool | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("drivegrid-b200 Engine needs a CUDA device (no CPU fallback)")
         self._lib = N.load_library()
@@ -252,7 +286,20 @@ class Engine:
                      "error_word", "scratch"):
             setattr(desc, name, d[name].data_ptr())
         handle = ct.c_void_p()
-        N.check(self._lib, self._lib.dg_create(ct.byref(desc), ct.byref(handle)), "dg_create")
+        status = self._lib.dg_create(ct.byref(desc), ct.byref(handle)) if not geometry_global else N.DG_ENOSUPPORT
+        too_big = status == N.DG_ENOSUPPORT and b"shared memory" in (self._lib.dg_last_error() or b"")
+        if geometry_global or (too_big and geometry_global is None):
+            # a scene too large to stage in shared memory: per-world translated
+            # blobs read from global memory instead
+            wblob, wmeta = per_world_blobs(blob, meta, t.scene_of_world, t.grid_offsets)
+            d["scene_blob"], d["scene_meta"] = up(wblob, torch.uint8), up(wmeta, torch.int64)
+            d["scene_of_world"] = up(np.arange(W), torch.int32)
+            desc.dims.num_scenes, desc.dims.geometry_global = W, 1
+            for name in ("scene_blob", "scene_meta", "scene_of_world"):
+                setattr(desc, name, d[name].data_ptr())
+            status = self._lib.dg_create(ct.byref(desc), ct.byref(handle))
+        N.check(self._lib, status, "dg_create")
+        self.geometry_global = bool(desc.dims.geometry_global)
         self._h = handle
         self._desc = desc
         if launch_mode == 1:

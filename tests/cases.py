@@ -97,6 +97,11 @@ def case_inputs(name: str) -> Case:
         scene = prepare_scene(straight_scene(agent_count=2, goal_dist=40.0))
         inp = C.build_inputs(cfg_of(3, 4, seed=13), scenes=[scene])
         return Case(name, inp, philox_actions(12, 60, 3, 4), 60, (1, 30, 60))
+    if name == "traj_dense":
+        lanes = tuple(float(x) for x in np.round(np.arange(-9.0, 9.01, 0.25), 2))
+        scene = prepare_scene(straight_scene("dense", lane_offsets=lanes, agent_count=8, agent_gap=15.0,
+                                             goal_dist=40.0))
+        return Case(name, C.build_inputs(cfg_of(2, 8, seed=3), scenes=[scene]), None, 30, (1, 30))
     if name == "traj_forge":
         inp = C.build_inputs(cfg_of(6, 16, seed=23))
         inp.worlds = forge_roundtrip(inp.worlds)[1]
@@ -109,7 +114,8 @@ def case_inputs(name: str) -> Case:
 
 
 TRAJ_CASES = ("traj_c1", "traj_pool", "traj_wet", "traj_bicycle", "traj_custom_obs",
-              "traj_events", "traj_events_inv", "traj_sparse", "traj_timeout", "traj_forge")
+              "traj_events", "traj_events_inv", "traj_sparse", "traj_timeout", "traj_forge",
+              "traj_dense")
 
 
 def forge_roundtrip(worlds):

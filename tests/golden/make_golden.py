@@ -412,6 +412,26 @@ def goals_random():
     np.savez_compressed(OUT / "goals_random.npz", cases=np.array(GOAL_CASES), **arrays)
 
 
+DENSE_LANES = tuple(float(x) for x in np.round(np.arange(-9.0, 9.01, 0.25), 2))
+
+
+def traj_dense():
+    """73 lanes 0.25 m apart: most agents see more than K_road = 350 road
+    candidates, so the first-350-by-segment-index truncation is exercised."""
+    scene = prepare_scene(straight_scene("dense", lane_offsets=DENSE_LANES, agent_count=8, agent_gap=15.0,
+                                         goal_dist=40.0))
+    eng = build_engine(cfg_of(2, 8, seed=3), scenes=[scene])
+    pol = LaneFollower(obs_config=eng.obs_config)
+    rec = Recorder(full_obs_steps=(1, 30))
+    obs = eng.observe()
+    for t in range(30):
+        a = pol(obs)
+        out = eng.step(a)
+        rec.add(t + 1, eng, out, a)
+        obs = out.obs
+    rec.save("traj_dense")
+
+
 def traj_sparse():
     scene = prepare_scene(straight_scene(agent_count=2, goal_dist=40.0))
     eng = build_engine(cfg_of(3, 4, seed=13), scenes=[scene])
@@ -464,6 +484,6 @@ def sysid():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense"]
     for name in which:
         globals()[name]()

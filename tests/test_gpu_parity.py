@@ -75,7 +75,36 @@ def compare(dev: Dev, t, g, o, oc):
 
 VARIANTS = [(n, True, None, 0) for n in TRAJ_CASES] + [(n, True, None, 1) for n in TRAJ_CASES] + [
     ("traj_events", False, 3, 0), ("traj_wet", True, 16, 0), ("traj_pool", False, 1, 0),
-    ("traj_events_inv", True, 5, 0), ("traj_events", False, 8, 1), ("traj_wet", False, 2, 1)]
+    ("traj_events_inv", True, 5, 0), ("traj_events", False, 8, 1), ("traj_wet", False, 2, 1),
+    ("traj_dense", False, 4, 0), ("traj_dense", True, 2, 1)]
+
+
+@pytest.mark.parametrize("name,mode", [("traj_events", 0), ("traj_wet", 1), ("traj_pool", 0)])
+def test_global_geometry_path_is_bit_identical(name, mode, device):
+    """Scenes read from per-world global blobs (the path of scenes too large
+    for shared memory) give exactly the outputs of the shared-memory path."""
+    case = case_inputs(name)
+    a = Engine(**case.inputs.as_kwargs(), device=device, launch_mode=mode)
+    b = Engine(**case.inputs.as_kwargs(), device=device, launch_mode=mode, geometry_global=True)
+    assert b.geometry_global and not a.geometry_global
+    pol = LaneFollower(obs_config=a.obs_config)
+    obs = a.observe()
+    assert np.array_equal(obs, b.observe())
+    for t in range(min(case.steps, 120)):
+        act = pol(obs) if case.actions is None else case.actions[t].astype(np.float64)
+        oa, ob = a.step(act), b.step(act)
+        assert np.array_equal(oa.obs, ob.obs) and np.array_equal(oa.rewards, ob.rewards)
+        assert np.array_equal(oa.dones, ob.dones) and np.array_equal(oa.info["reason"], ob.info["reason"])
+        obs = oa.obs
+    assert all(np.array_equal(a.state[k], b.state[k]) for k in STATE_FIELDS)
+
+
+def test_oversized_scene_runs_from_global_memory(device):
+    case = case_inputs("traj_dense")
+    eng = Engine(**case.inputs.as_kwargs(), device=device)
+    assert eng.geometry_global
+    with pytest.raises(Exception, match="shared memory"):
+        Engine(**case.inputs.as_kwargs(), device=device, geometry_global=False)
 
 
 @pytest.mark.parametrize("name,spatial,warps,mode", VARIANTS,
