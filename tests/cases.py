@@ -97,6 +97,11 @@ def case_inputs(name: str) -> Case:
         scene = prepare_scene(straight_scene(agent_count=2, goal_dist=40.0))
         inp = C.build_inputs(cfg_of(3, 4, seed=13), scenes=[scene])
         return Case(name, inp, philox_actions(12, 60, 3, 4), 60, (1, 30, 60))
+    if name in ("traj_obs_min", "traj_obs_one"):
+        cfg = cfg_of(3, 6, seed=29)
+        kr = kv = 0 if name == "traj_obs_min" else 1
+        cfg.obs = ObsConfig(include_weather=name == "traj_obs_min", k_road=kr, k_vehicles=kv)
+        return Case(name, C.build_inputs(cfg), philox_actions(14, 40, 3, 6), 40, (1, 20, 40))
     if name == "traj_dense":
         lanes = tuple(float(x) for x in np.round(np.arange(-9.0, 9.01, 0.25), 2))
         scene = prepare_scene(straight_scene("dense", lane_offsets=lanes, agent_count=8, agent_gap=15.0,
@@ -115,7 +120,7 @@ def case_inputs(name: str) -> Case:
 
 TRAJ_CASES = ("traj_c1", "traj_pool", "traj_wet", "traj_bicycle", "traj_custom_obs",
               "traj_events", "traj_events_inv", "traj_sparse", "traj_timeout", "traj_forge",
-              "traj_dense")
+              "traj_dense", "traj_obs_min", "traj_obs_one")
 
 
 def forge_roundtrip(worlds):

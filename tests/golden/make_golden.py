@@ -203,6 +203,18 @@ def traj_bicycle():
     rec.save("traj_bicycle")
 
 
+def traj_obs_min():
+    """Degenerate observation sizes: no road rows and no neighbour rows
+    (ego block only), with weather; then one road row and one neighbour row."""
+    for name, kr, kv, weather in (("traj_obs_min", 0, 0, True), ("traj_obs_one", 1, 1, False)):
+        cfg = cfg_of(3, 6, seed=29)
+        cfg.obs = ObsConfig(include_weather=weather, k_road=kr, k_vehicles=kv)
+        eng = build_engine(cfg)
+        rec = Recorder(full_obs_steps=(1, 20, 40))
+        run_actions(eng, philox_actions(14, 40, 3, 6), rec)
+        rec.save(name)
+
+
 def traj_custom_obs():
     cfg = cfg_of(2, 5, assignment="fixed", seed=19)
     cfg.obs = ObsConfig(include_weather=False, k_road=20, k_vehicles=3, road_radius=12.5)
@@ -484,6 +496,6 @@ def sysid():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense", "traj_obs_min"]
     for name in which:
         globals()[name]()
