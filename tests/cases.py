@@ -102,6 +102,17 @@ def case_inputs(name: str) -> Case:
         kr = kv = 0 if name == "traj_obs_min" else 1
         cfg.obs = ObsConfig(include_weather=name == "traj_obs_min", k_road=kr, k_vehicles=kv)
         return Case(name, C.build_inputs(cfg), philox_actions(14, 40, 3, 6), 40, (1, 20, 40))
+    if name == "traj_no_edges":
+        from paper_2605_08528_b200.scenes import AgentRecord, Polyline, ScenarioSpec
+        xs = np.arange(-80.0, 80.01, 2.0)
+
+        def row(y):
+            return np.stack([xs, np.full_like(xs, y), np.zeros_like(xs)], axis=1)
+
+        agents = [AgentRecord(f"a{i}", (-70.0 + 15.0 * i, 3.5 * (i % 2)), 0.0, (-20.0 + 15.0 * i, 3.5 * (i % 2)))
+                  for i in range(4)]
+        spec = ScenarioSpec("no_edges", [Polyline(1, row(0.0)), Polyline(2, row(3.5)), Polyline(6, row(7.0))], agents)
+        return Case(name, C.build_inputs(cfg_of(2, 4, seed=41), scenes=[prepare_scene(spec)]), None, 50, (1, 50))
     if name == "traj_dense":
         lanes = tuple(float(x) for x in np.round(np.arange(-9.0, 9.01, 0.25), 2))
         scene = prepare_scene(straight_scene("dense", lane_offsets=lanes, agent_count=8, agent_gap=15.0,
@@ -120,7 +131,7 @@ def case_inputs(name: str) -> Case:
 
 TRAJ_CASES = ("traj_c1", "traj_pool", "traj_wet", "traj_bicycle", "traj_custom_obs",
               "traj_events", "traj_events_inv", "traj_sparse", "traj_timeout", "traj_forge",
-              "traj_dense", "traj_obs_min", "traj_obs_one")
+              "traj_dense", "traj_obs_min", "traj_obs_one", "traj_no_edges")
 
 
 def forge_roundtrip(worlds):

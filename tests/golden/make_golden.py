@@ -215,6 +215,34 @@ def traj_obs_min():
         rec.save(name)
 
 
+def no_edge_scene(Polyline, AgentRecord, ScenarioSpec):
+    """Lane centres of both lane codes and an unrelated polyline, no road edge
+    at all (the edge subset is empty)."""
+    xs = np.arange(-80.0, 80.01, 2.0)
+
+    def row(y, z=0.0):
+        return np.stack([xs, np.full_like(xs, y), np.full_like(xs, z)], axis=1)
+
+    agents = [AgentRecord(f"a{i}", (-70.0 + 15.0 * i, 3.5 * (i % 2)), 0.0, (-20.0 + 15.0 * i, 3.5 * (i % 2)))
+              for i in range(4)]
+    return ScenarioSpec("no_edges", [Polyline(1, row(0.0)), Polyline(2, row(3.5)), Polyline(6, row(7.0))], agents)
+
+
+def traj_no_edges():
+    from drivegrid.scenario import AgentRecord, Polyline, ScenarioSpec
+    scene = prepare_scene(no_edge_scene(Polyline, AgentRecord, ScenarioSpec))
+    eng = build_engine(cfg_of(2, 4, seed=41), scenes=[scene])
+    pol = LaneFollower(obs_config=eng.obs_config)
+    rec = Recorder(full_obs_steps=(1, 50))
+    obs = eng.observe()
+    for t in range(50):
+        a = pol(obs)
+        out = eng.step(a)
+        rec.add(t + 1, eng, out, a)
+        obs = out.obs
+    rec.save("traj_no_edges")
+
+
 def traj_custom_obs():
     cfg = cfg_of(2, 5, assignment="fixed", seed=19)
     cfg.obs = ObsConfig(include_weather=False, k_road=20, k_vehicles=3, road_radius=12.5)
@@ -496,6 +524,6 @@ def sysid():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense", "traj_obs_min"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense", "traj_obs_min", "traj_no_edges"]
     for name in which:
         globals()[name]()
