@@ -56,11 +56,14 @@ typedef struct DgDims {
     int32_t num_scenes;
     int32_t max_scene_bytes;  /* largest per-scene geometry blob, bytes      */
     int32_t max_segments;     /* largest P over scenes                       */
-    int32_t geometry_global;  /* 0: each CTA stages its scene blob in shared
-                                 memory (TMA) and translates it by the world's
-                                 grid offset; 1: blobs are per world, already
-                                 translated, read from global memory (scenes
-                                 too large for the 227 KB of shared memory)  */
+    int32_t geometry_global;  /* 0: scene blobs are per scene, in scene-local
+                                 coordinates (the fused kernel stages its world's
+                                 blob in shared memory by TMA and adds the grid
+                                 offset); 1: blobs are per world, already moved
+                                 by the offset, read in place from global memory
+                                 by the split kernels (scenes too large for the
+                                 227 KB of shared memory; dg_step then takes
+                                 ticks = 1 and dg_tune only mode 1)           */
 } DgDims;
 
 /* Float64 scalars, precomputed on the host with the reference's expression

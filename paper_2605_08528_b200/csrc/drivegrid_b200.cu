@@ -771,9 +771,8 @@ world_step_kernel(const KArgs A) {
     const DgConsts& k = A.k;
 
     // ---- shared memory carve-up
-    const bool geo_global = A.d.geometry_global != 0;
     uint8_t* geo = smem;
-    AgentSm* ag = reinterpret_cast<AgentSm*>(smem + (geo_global ? 0 : align16(A.d.max_scene_bytes)));
+    AgentSm* ag = reinterpret_cast<AgentSm*>(smem + align16(A.d.max_scene_bytes));
     ScanSm* sc = reinterpret_cast<ScanSm*>(ag + kMaxAgents);
     uint64_t* bar = reinterpret_cast<uint64_t*>(sc + kMaxAgents);
     uint16_t* cand_sm = reinterpret_cast<uint16_t*>(bar + 2);   // [M][take_road]
@@ -813,7 +812,7 @@ world_step_kernel(const KArgs A) {
         }
         step_now = A.step_count[w];
     }
-    if (tid == 0 && !geo_global) {
+    if (tid == 0) {
         mbar_init(bar, 1);
         bulk_load(geo, A.scene_blob + meta[0], uint32_t(meta[1]), bar);
     }
@@ -969,11 +968,7 @@ world_step_kernel(const KArgs A) {
         if (warp == 0) PHASE_MARK(2);
         __syncthreads();  // agent table + zero rows done, mbarrier init visible
         PHASE_MARK(3);
-        if (t == 0 && geo_global) {
-            // per-world blob in global memory, translated on the host (same float64 adds)
-            G = scene_view(const_cast<uint8_t*>(A.scene_blob + meta[0]), A.scene_blob + meta[5], int(meta[2]),
-                           int(meta[3]), int(meta[4]));
-        } else if (t == 0) {
+        if (t == 0) {
             mbar_wait(bar, 0);
             // the view reads the index header from the copied blob: only after the wait
             G = scene_view(geo, A.scene_blob + meta[5], int(meta[2]), int(meta[3]), int(meta[4]));
@@ -2074,7 +2069,7 @@ static size_t split_smem_bytes(int take_road, int apc) {
 }
 
 static size_t step_smem_bytes(const DgDims& d, int take_road) {
-    size_t b = d.geometry_global ? 0 : size_t(align16(d.max_scene_bytes));
+    size_t b = size_t(align16(d.max_scene_bytes));
     b += sizeof(AgentSm) * kMaxAgents + sizeof(ScanSm) * kMaxAgents;
     b += 16;  // mbarrier
     b += sizeof(uint16_t) * kMaxAgents * size_t(take_road > 0 ? take_road : 1);
@@ -2136,7 +2131,8 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
     A.take_road = d.k_road < d.max_segments ? d.k_road : d.max_segments;
     A.take_veh = d.k_vehicles < d.M ? d.k_vehicles : d.M;
     e->smem_bytes = step_smem_bytes(d, A.take_road);
-    if (e->smem_bytes > 227 * 1024 - 4096) {   // headroom for the kernels' static / reserved shared memory
+    // headroom for the kernels' static / reserved shared memory
+    if (!d.geometry_global && e->smem_bytes > 227 * 1024 - 4096) {
         delete e;
         return fail(DG_ENOSUPPORT, "dg_create: scene geometry does not fit in shared memory");
     }
@@ -2156,6 +2152,17 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
     e->warps_per_world = d.M;
     e->min_blocks = 1;
     e->mode = 0;
+    if (d.geometry_global) {
+        // per-world blobs stay in global memory: the split kernels, which read
+        // the geometry in place (the fused kernel stages it in shared memory)
+        if (!A.scratch) {
+            delete e;
+            return fail(DG_EINVAL, "dg_create: geometry_global needs the scratch buffer");
+        }
+        e->mode = 1;
+        e->warps_per_world = 4;
+        e->min_blocks = 4;
+    }
     *out = e;
     return DG_OK;
 }
@@ -2347,6 +2354,8 @@ int dg_tune(dg_engine* eng, int32_t mode, int32_t warps_per_world, int32_t ctas_
         return DG_OK;
     }
     if (mode != 0) return fail(DG_EINVAL, "dg_tune: mode must be 0 (fused) or 1 (split)");
+    if (eng->base.d.geometry_global)
+        return fail(DG_ENOSUPPORT, "dg_tune: geometry_global engines run the split kernels (mode 1)");
     if (warps_per_world < 1 || warps_per_world > kMaxAgents)
         return fail(DG_EINVAL, "dg_tune: warps_per_world must lie in [1, 16]");
     const int nw = warps_per_world < eng->base.d.M ? warps_per_world : eng->base.d.M;

@@ -204,9 +204,10 @@ class Engine:
     Performance knobs (results are identical under every setting):
     ``spatial_index`` (per-cell candidate lists vs full scans),
     ``warps_per_world`` / ``launch_mode`` (kernel shape, fused vs split), and
-    ``geometry_global`` -- None stages each world's scene in shared memory and
-    falls back to per-world blobs in global memory only for scenes too large
-    for it; True / False force either path.
+    ``geometry_global`` -- None stages each world's scene in shared memory
+    (fused kernel) and falls back to per-world blobs read from global memory
+    by the split kernels only for scenes too large for it; True / False force
+    either path.
     """
 
     def __init__(self, worlds, scenes, assignment, frictions, config: SimConfig,
@@ -302,7 +303,10 @@ class Engine:
         self.geometry_global = bool(desc.dims.geometry_global)
         self._h = handle
         self._desc = desc
-        if launch_mode == 1:
+        if self.geometry_global:
+            # global-memory geometry: the split kernels (dg_create already chose them)
+            self.tune(warps_per_world if warps_per_world in (2, 4, 8) else 4, 0, mode=1)
+        elif launch_mode == 1:
             self.tune(warps_per_world or 4, 0, mode=1)
         elif warps_per_world:
             self.tune(warps_per_world)
@@ -572,6 +576,21 @@ class Engine:
         ``drac_max`` (float64 [W][M]) / ``metric_seen`` (uint8 [W][M]) are the
         in-kernel episode-metric accumulators (default: the engine's own when
         ``track_episode_metrics`` is on)."""
+        if self._shape["mode"] == "split" and (ticks > 1 or bufs.obs.dim() == 4):
+            # the split kernels take one tick per launch and write one output
+            # set: tick t goes to ring slot (ring_start + t) % S through views
+            slots = bufs.obs.shape[0] if bufs.obs.dim() == 4 else 1
+            for t in range(int(ticks)):
+                if next_actions is not None:
+                    a_t = actions if t == 0 else next_actions
+                else:
+                    a_t = actions[t] if ticks > 1 or actions.dim() == 4 else actions
+                slot = (ring_start + t) % slots
+                one = bufs if bufs.obs.dim() == 3 else StepBuffers(
+                    bufs.obs[slot], bufs.aux, {k: v[slot] for k, v in bufs.views.items()})
+                self.launch_step(a_t, one, autoreset, snapshot, terms, next_actions, steer_gain, throttle,
+                                 event_counts, 1, 0, drac_max, metric_seen)
+            return
         io = self._step_io(actions, bufs, autoreset, snapshot, terms, next_actions, steer_gain, throttle,
                            event_counts, ticks, ring_start, drac_max, metric_seen)
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), self._stream()), "dg_step")

@@ -79,13 +79,14 @@ VARIANTS = [(n, True, None, 0) for n in TRAJ_CASES] + [(n, True, None, 1) for n 
     ("traj_dense", False, 4, 0), ("traj_dense", True, 2, 1)]
 
 
-@pytest.mark.parametrize("name,mode", [("traj_events", 0), ("traj_wet", 1), ("traj_pool", 0)])
-def test_global_geometry_path_is_bit_identical(name, mode, device):
-    """Scenes read from per-world global blobs (the path of scenes too large
-    for shared memory) give exactly the outputs of the shared-memory path."""
+@pytest.mark.parametrize("name", ["traj_events", "traj_wet", "traj_pool"])
+def test_global_geometry_path_is_bit_identical(name, device):
+    """Per-world blobs translated on the host (the path of scenes too large for
+    shared memory) give exactly the outputs of the split kernels adding the
+    grid offset on the fly, and match the oracle like every other path."""
     case = case_inputs(name)
-    a = Engine(**case.inputs.as_kwargs(), device=device, launch_mode=mode)
-    b = Engine(**case.inputs.as_kwargs(), device=device, launch_mode=mode, geometry_global=True)
+    a = Engine(**case.inputs.as_kwargs(), device=device, launch_mode=1)
+    b = Engine(**case.inputs.as_kwargs(), device=device, geometry_global=True)
     assert b.geometry_global and not a.geometry_global
     pol = LaneFollower(obs_config=a.obs_config)
     obs = a.observe()
@@ -97,6 +98,19 @@ def test_global_geometry_path_is_bit_identical(name, mode, device):
         assert np.array_equal(oa.dones, ob.dones) and np.array_equal(oa.info["reason"], ob.info["reason"])
         obs = oa.obs
     assert all(np.array_equal(a.state[k], b.state[k]) for k in STATE_FIELDS)
+
+
+def test_global_geometry_rollout_loops_ticks(device):
+    """A multi-tick rollout on a global-geometry engine (one split launch per
+    tick) equals the same rollout on the fused engine."""
+    case = case_inputs("traj_pool")
+    a = Engine(**case.inputs.as_kwargs(), device=device)
+    b = Engine(**case.inputs.as_kwargs(), device=device, geometry_global=True)
+    a0 = a.lane_follower(a.observe_device())
+    ra = a.rollout(a0.clone(), ticks=24, policy="lane_follower", autoreset=True)
+    rb = b.rollout(a0.clone(), ticks=24, policy="lane_follower", autoreset=True)
+    for k in ("obs", "rewards", "dones"):
+        assert torch.allclose(getattr(ra, k).double(), getattr(rb, k).double(), rtol=1e-9, atol=1e-9), k
 
 
 def test_oversized_scene_runs_from_global_memory(device):

@@ -50,7 +50,7 @@ def assert_slot_equals_step(rb, slot, sb):
 
 
 @pytest.mark.parametrize("autoreset", [False, True])
-@pytest.mark.parametrize("shape", [None, (4, 4), (16, 1)])
+@pytest.mark.parametrize("shape", [None, (4, 4), (16, 1), (4, 0, 1)])
 def test_replayed_rollout_equals_steps(autoreset, shape, device):
     W, M, T = 8, 16, 48
     inp = C.build_inputs(cfg_of(W, M, seed=31))
