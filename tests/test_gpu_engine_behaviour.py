@@ -210,3 +210,36 @@ def test_episode_log_jsonl_and_60hz(device, tmp_path):
     assert len(rows) == 5 * 2 and rows[0]["step"] == 1 and "reward" in rows[0] and "pose" in rows[0]
     assert rows[2]["pose"][0] == log.steps[1]["state"]["x"][0, 0]       # float64 survives JSON
     assert len(log.resample_60hz()) == 2 * len(log)
+
+
+@pytest.mark.parametrize("quarter", [1, 2, 3])
+def test_observations_are_rotation_equivariant(quarter, device):
+    """The observation contract's equivariance (test_acceptance.py:140-186):
+    the crossroads scene turned by a quarter / half / three-quarter turn
+    (exact in float64, and the square scene box is invariant) yields the same
+    body-frame observations, rewards and events under the same actions."""
+    from paper_2605_08528_b200.scenes import AgentRecord, Polyline, ScenarioSpec, crossroads_scene
+    c, s = {1: (0.0, 1.0), 2: (-1.0, 0.0), 3: (0.0, -1.0)}[quarter]
+
+    def rot(x, y):
+        return c * x - s * y, s * x + c * y
+
+    base = crossroads_scene(agent_count=8)
+    turned = ScenarioSpec(
+        "turned",
+        [Polyline(p.type_code, np.stack([*rot(p.points[:, 0], p.points[:, 1]), p.points[:, 2]], axis=1))
+         for p in base.polylines],
+        [AgentRecord(a.id, rot(*a.start), a.start_heading + quarter * np.pi / 2, rot(*a.goal), a.length, a.width)
+         for a in base.agents])
+    ea = small_engine(device, 1, 8, scenes=[prepare_scene(base)])
+    eb = small_engine(device, 1, 8, scenes=[prepare_scene(turned)])
+    pol = LaneFollower(obs_config=ea.obs_config)
+    oa, ob = ea.observe(), eb.observe()
+    assert np.allclose(oa, ob, rtol=1e-6, atol=1e-6)
+    for _ in range(40):
+        act = pol(oa)
+        sa, sb = ea.step(act), eb.step(act)
+        assert np.allclose(sa.obs, sb.obs, rtol=1e-6, atol=1e-6)
+        assert np.allclose(sa.rewards, sb.rewards, rtol=1e-9, atol=1e-9)
+        assert np.array_equal(sa.dones, sb.dones) and np.array_equal(sa.info["reason"], sb.info["reason"])
+        oa = sa.obs
