@@ -42,6 +42,7 @@ import numpy as np
 REF = Path(os.environ.get("DRIVEGRID_REF", "/root/reference/pkg"))
 sys.dont_write_bytecode = True
 sys.path[:0] = [str(REF / "src"), str(REF / "bindings" / "src")]
+sys.path.insert(0, str(Path(__file__).resolve().parent))
 
 from drivegrid import vehicle as vh  # noqa: E402
 from drivegrid.config import RootConfig, build_engine, prepare_scene  # noqa: E402
@@ -241,6 +242,35 @@ def traj_no_edges():
         rec.add(t + 1, eng, out, a)
         obs = out.obs
     rec.save("traj_no_edges")
+
+
+def scene_verdicts():
+    """reject_degenerate_scene / prepare_scene / filter_agents over the
+    synthetic specs of scene_cases.py (scenario.py:169-260, config.py:162-168)."""
+    import json
+    import types
+
+    from drivegrid import scenario as sc
+    from drivegrid import synth
+    from scene_cases import scene_specs
+    mod = types.SimpleNamespace(Polyline=sc.Polyline, AgentRecord=sc.AgentRecord, ScenarioSpec=sc.ScenarioSpec,
+                                straight_scene=synth.straight_scene, crossroads_scene=synth.crossroads_scene,
+                                two_level_scene=synth.two_level_scene, shift_scenario=sc.shift_scenario)
+    out, arrays = [], {}
+    for i, spec in enumerate(scene_specs(mod)):
+        v = sc.reject_degenerate_scene(spec)
+        rec = {"id": spec.scenario_id, "accepted": bool(v.accepted), "reason": v.reason}
+        p = prepare_scene(spec)
+        if p is not None:
+            kept = sc.filter_agents(p)
+            rec["kept"] = len(kept)
+            arrays[f"s{i}_points"] = np.concatenate([q.points for q in p.polylines])
+            arrays[f"s{i}_agents"] = np.array([[*a.start, a.start_heading, *a.goal, a.length, a.width]
+                                                for a in p.agents])
+        out.append(rec)
+    np.savez_compressed(OUT / "scene_verdicts.npz", meta_json=np.frombuffer(json.dumps(out).encode(), np.uint8),
+                        **arrays)
+    print("scene_verdicts", [(r["id"], r["accepted"]) for r in out])
 
 
 def traj_custom_obs():
@@ -524,6 +554,6 @@ def sysid():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense", "traj_obs_min", "traj_no_edges"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense", "traj_obs_min", "traj_no_edges", "scene_verdicts"]
     for name in which:
         globals()[name]()
