@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import math
 from dataclasses import dataclass, fields
+from pathlib import Path
 
 GRAVITY = 9.81
 PHYSICS_DT = 1.0 / 120.0
@@ -179,16 +180,11 @@ class BicycleParams:
 
 
 def load_params(path) -> VehicleParams:
-    """``name = value`` file (vehicle.py:112-121)."""
-    kv = {}
-    with open(path, encoding="utf-8") as fh:
-        for line in fh:
-            line = line.strip()
-            if not line or line.startswith("#"):
-                continue
-            key, _, value = line.partition("=")
-            kv[key.strip()] = float(value)
-    return VehicleParams(**kv)
+    """``name = value`` lines; blank lines and ``#`` comments skipped, later
+    keys win (vehicle.py:112-121)."""
+    lines = (ln.strip() for ln in Path(path).read_text(encoding="utf-8").splitlines())
+    pairs = (ln.partition("=") for ln in lines if ln and not ln.startswith("#"))
+    return VehicleParams(**{key.strip(): float(value) for key, _, value in pairs})
 
 
 def save_params(p: VehicleParams, path) -> None:

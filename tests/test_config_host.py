@@ -98,3 +98,18 @@ def test_sim_config_checks():
     for bad in (dict(num_agents=17), dict(dynamics_mode="warp")):
         with pytest.raises(ValueError):
             SimConfig(**bad)
+
+
+def test_vehicle_params_file_round_trip_and_config_path(tmp_path):
+    """save_params / load_params (vehicle.py:105-121) and
+    ``vehicle_params_path`` in the YAML config."""
+    from paper_2605_08528_b200.params import VehicleParams, load_params, save_params
+    p = dataclasses.replace(VehicleParams(), tau_drive_max=1234.5, com_offset=-0.125)
+    f = tmp_path / "veh.txt"
+    save_params(p, f)
+    assert load_params(f) == p
+    f.write_text("# tuned\n\ntau_drive_max = 999.0\nkp_steer=10\n")
+    q = load_params(f)
+    assert q.tau_drive_max == 999.0 and q.kp_steer == 10.0 and q.wheel_mass == VehicleParams().wheel_mass
+    cfg = C.config_from_dict({"vehicle_params_path": str(f), "env": {"num_envs": 2, "num_agents_per_env": 2}})
+    assert C.build_inputs(cfg).params == q
