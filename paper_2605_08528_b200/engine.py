@@ -270,7 +270,8 @@ class Engine:
             "goal_xy": up(t.goal_xy, torch.float64),
             "start_yaw": up(t.start_yaw, torch.float64),
             "error_word": torch.full((1,), N.DG_NO_ERROR, dtype=torch.int32, device=dev),
-            "scratch": torch.empty(int(self._lib.dg_scratch_bytes(W, M)), dtype=torch.uint8, device=dev),
+            # zeroed once: the split kernels copy whole AgentRec records, padding included
+            "scratch": torch.zeros(int(self._lib.dg_scratch_bytes(W, M)), dtype=torch.uint8, device=dev),
         }
         oc = self.obs_config
         dims = N.DgDims(W=W, M=M, obs_dim=oc.obs_dim, ego_dim=oc.ego_dim, k_road=oc.k_road,
