@@ -385,3 +385,34 @@ def test_random_goals_engine_parity(device):
         compare(dev, t + 1, gpu.step(a), o, ora.obs_config)
         obs = o.obs
     assert np.array_equal(gpu.reason, ora.reason) and np.array_equal(gpu.alive, ora.alive)
+
+
+@pytest.mark.parametrize("scene_id", ["crowd", "shifted", "hilly", "ramp"])
+def test_scene_intake_cases_step_like_the_oracle(scene_id, device):
+    """The synthetic intake specs (tests/golden/scene_cases.py: more agents
+    than slots, an off-centre scene, an elevated one, a low ramp) stepped on
+    the GPU against the oracle under the LaneFollower."""
+    import sys
+    import types
+
+    from cases import GOLDEN
+    from paper_2605_08528_b200 import scenes as S
+    sys.path.insert(0, str(GOLDEN))
+    from scene_cases import scene_specs
+    mod = types.SimpleNamespace(Polyline=S.Polyline, AgentRecord=S.AgentRecord, ScenarioSpec=S.ScenarioSpec,
+                                straight_scene=S.straight_scene, crossroads_scene=S.crossroads_scene,
+                                two_level_scene=S.two_level_scene, shift_scenario=S.shift_scenario)
+    spec = next(s for s in scene_specs(mod) if s.scenario_id == scene_id)
+    inp = C.build_inputs(cfg_of(2, 16, seed=5), scenes=[S.prepare_scene(spec)])
+    gpu = Engine(**inp.as_kwargs(), device=device)
+    ora = OracleEngine(**inp.as_kwargs())
+    dev = Dev()
+    pol = LaneFollower(obs_config=ora.obs_config)
+    obs = ora.observe()
+    dev.f("obs0", gpu.observe(), obs, rtol=OBS_RTOL, atol=OBS_ATOL)
+    for t in range(60):
+        a = pol(obs)
+        o = ora.step(a)
+        compare(dev, t + 1, gpu.step(a), o, ora.obs_config)
+        obs = o.obs
+    assert np.array_equal(gpu.reason, ora.reason) and np.array_equal(gpu.alive, ora.alive)
