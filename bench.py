@@ -77,6 +77,21 @@ def root_config(total_worlds, M=16):
     return cfg
 
 
+def ring_slots(W, M, D):
+    """Rollout-ring slots so the ring is > 2x L2 (obs never re-read from L2)."""
+    return max(2, math.ceil(2 * L2_BYTES / (W * M * D * 4)))
+
+
+def bench_config(W, M, D=1929):
+    """The workload description, identical in both arms' lines."""
+    ring = ring_slots(W, M, D)
+    return {"workload": f"{W}x{M} default procedural pool (seed 42), dry, dynamic, LaneFollower policy, "
+                        "finished agents teleported back to their start (autoreset)",
+            "worlds": W, "agents": M, "obs_dim": D, "seed": 42, "policy": "LaneFollower", "autoreset": True,
+            "l2": f"GPU arm: obs rotate through a {ring}-slot rollout ring "
+                  f"({ring * W * M * D * 4 / 2**20:.0f} MiB > L2)"}
+
+
 def shard_inputs(cfg, rank, world_size):
     """Global host tables, sliced to this rank's contiguous world range."""
     from paper_2605_08528_b200 import config as C
@@ -148,20 +163,14 @@ def measured_peaks():
 
 
 def ncu_traffic(W, M, ticks):
-    """dram read+write bytes of one launch of this shape from the committed
-    ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    """dram read+write bytes of one launch of exactly this shape and tick
+    count from a committed ncu --set full capture (profiles/ncu_traffic.json,
+    key "WxMxticks"), or None -- never extrapolated from another tick count."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if not p.exists():
         return None
     rec = json.loads(p.read_text()).get(f"{W}x{M}x{ticks}")
-    return None if rec is None else float(rec["traffic_bytes"])
-
-
-def ncu_traffic_per_launch(W, M, R, ticks_per_launch):
-    """The captured R-tick launch's dram bytes, per tick x this run's average
-    ticks per launch (the traffic is the per-tick obs / output stream)."""
-    t = ncu_traffic(W, M, R)
-    return None if t is None else t / R * ticks_per_launch
+    return None if rec is None else (float(rec["traffic_bytes"]), rec.get("source", ""))
 
 
 def algorithmic_bytes_per_agent(obs_dim: int) -> int:
@@ -176,6 +185,39 @@ def algorithmic_bytes_per_agent(obs_dim: int) -> int:
     spawn = 4                              # spawn_step (read)
     outputs = 8 + 8 + 7 * 8 + 12 * 8 + 4 + 1 + 1 + 1 + 1  # reward, ttc_min, terms, snapshot, events, done, reason, alive, alive_pre
     return obs + state + actions + tables + flags + spawn + outputs
+
+
+def unmodified_reference(W, M, steps, warmup, cores):
+    """The reference package itself (installed unmodified in baseline/_ref by
+    pip), through its own harness: metrics.measure_engine
+    (metrics.py:158-184) on build_engine(cfg) with the LaneFollower -- the
+    vectorized path on every host thread (engine.py:258-270) over the same
+    W x M batch, and the scalar reference_step path (engine.py:423-595) on a
+    16-world sample.  measure_engine counts alive agents before each step
+    and does not reset finished agents."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "drivegrid").is_dir():
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref /root/reference)"}
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    from drivegrid.config import RootConfig as RefRoot
+    from drivegrid.config import build_engine as ref_build
+    from drivegrid.metrics import measure_engine
+    from drivegrid.policies import LaneFollower as RefLF
+
+    out = {}
+    for path, Wp, n, wu in (("vectorized", W, steps, warmup), ("scalar", min(W, 16), max(2, steps // 8), 1)):
+        cfg = RefRoot()
+        cfg.env.num_envs, cfg.env.num_agents_per_env = Wp, M
+        cfg.env.num_workers = cores if path == "vectorized" else 0
+        eng = ref_build(cfg)
+        rep = measure_engine(eng, RefLF(obs_config=eng.obs_config), n, wu, reference=path == "scalar")
+        out[path] = {"value": rep.casps, "unit": "agent-steps/s", "cores": rep.workers, "kind": "reference",
+                     "sample": f"{Wp}x{M} default pool, {n} steps after {wu} warmup ({rep.wall_seconds:.1f} s), "
+                               f"drivegrid.metrics.measure_engine(path={path!r}), unmodified reference "
+                               f"(baseline/_ref), numpy {np.__version__}",
+                     "phase_ms": {k: round(v, 3) for k, v in rep.phase_ms.items()}}
+    return out
 
 
 def run_reference(args, rank, world_size):
@@ -218,13 +260,15 @@ def run_reference(args, rank, world_size):
         "n_gpus": world_size, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
         "scaling": "weak" if world_size == 1 else "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"{W}x16 default procedural pool, LaneFollower, autoreset",
-                                        "worlds": W, "agents": 16},
+        "data": "synthetic", "config": bench_config(W, 16),
         "cpu_baseline": {"value": v, "unit": "agent-steps/s", "cores": cores, "kind": "port",
                          "sample": f"{Ws} of the {W} worlds x16 (contiguous range 0..{Ws - 1}), {args.steps} steps "
                                    f"after {args.warmup} warmup, oracle/ numpy port, numpy {np.__version__}"},
         "e2e": {"value": v, "unit": "agent-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_cpu:
+        line["reference_package"] = unmodified_reference(W if world_size == 1 else HEADLINE[0], 16,
+                                                         min(args.steps, 20), min(args.warmup, 3), cores)
     print(json.dumps(line), flush=True)
 
 
@@ -286,7 +330,7 @@ def main():
         eng.tune(nw, cps)
     W, M, D = eng.W, eng.M, eng.obs_config.obs_dim
     obs_bytes = W * M * D * 4
-    ring = max(2, math.ceil(2 * L2_BYTES / obs_bytes))
+    ring = ring_slots(W_total, M, D) if world_size == 1 else ring_slots(W, M, D)
     # every tick writes its own ring slot (obs + the per-tick aux outputs)
     rbufs = eng.new_rollout_buffers(ring)
     R = args.ticks_per_launch or DEFAULT_TICKS_PER_LAUNCH
@@ -302,6 +346,7 @@ def main():
     # events and alive agent-ticks (the CASPS numerator, counted before each tick)
     counters = torch.zeros((W, 5), dtype=torch.int32, device=dev)
     tick = [0]
+    tick_log = []          # ticks of every launch issued, in order
 
     def run_ticks(n, count=True):
         """n control ticks in ceil(n / R) launches of up to R ticks each."""
@@ -310,6 +355,7 @@ def main():
             r = min(R, n - done)
             eng.launch_step(acts, rbufs, autoreset=True, next_actions=acts, ticks=r,
                             ring_start=tick[0] % ring, event_counts=counters if count else None)
+            tick_log.append(r)
             tick[0] += r
             done += r
 
@@ -326,10 +372,14 @@ def main():
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = eng.launches
     graph = None
+    graph_ticks = []
     if not args.no_graph:
         graph = torch.cuda.CUDAGraph()
+        n0 = len(tick_log)
         with torch.cuda.graph(graph):
             run_ticks(args.steps)
+        graph_ticks = tick_log[n0:]
+        launches0 = eng.launches - len(graph_ticks)   # the captured launches run at replay
     if world_size > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -342,12 +392,14 @@ def main():
         stop.record(stream)
         torch.cuda.synchronize()
     launches = eng.launches - launches0
+    launch_ticks = list(tick_log[len(tick_log) - launches:]) if graph is None else list(graph_ticks)
     total_ms = start.elapsed_time(stop)
     if world_size > 1:
         t = torch.tensor([total_ms], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    n_launch = math.ceil(args.steps / R)
+    n_launch = len(launch_ticks)
+    assert sum(launch_ticks) == args.steps, (launch_ticks, args.steps)
     if graph is not None:
         g_step = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_step):
@@ -372,7 +424,7 @@ def main():
 
     # e2e through the numpy API on every rank at once; whole-job value =
     # all ranks' agent-ticks / the slowest rank's wall time
-    e2e_steps = args.e2e_steps or max(10, min(args.steps, 50))
+    e2e_steps = args.e2e_steps or 200
     if world_size > 1:
         dist.barrier()
     e2e = e2e_numpy(eng, e2e_steps)
@@ -393,24 +445,21 @@ def main():
         peak, peak_src = measured_peaks()
         per_agent = algorithmic_bytes_per_agent(D)
         achieved = per_agent * W * M * ticks_per_launch / (kern_avg / 1e3) / 1e9
+        uniform = len(set(launch_ticks)) == 1
+        traffic = ncu_traffic(W, M, launch_ticks[0]) if (world_size == 1 and uniform) else None
         line = {
             "metric": "CASPS", "value": value, "unit": "agent-steps/s", "n_gpus": world_size,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak" if world_size == 1 else "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{W_total}x16 default procedural pool (seed 42), dry, dynamic, "
-                                   f"LaneFollower + autoreset fused into the step",
-                       "worlds": W_total, "agents": M, "obs_dim": D,
-                       "l2": f"obs rotate through a {ring}-slot rollout ring ({ring * obs_bytes / 2**20:.0f} MiB > L2)",
-                       "launch": (f"{n_launch} persistent launches of {R} ticks"
-                                  + (", one CUDA graph" if graph is not None else ", eager")),
-                       "ticks_per_launch": R,
-                       "kernel_shape": eng.launch_shape(),
+            "config": bench_config(W_total, M, D),
+            "launch": {"launches": n_launch, "ticks_per_launch": launch_ticks[0] if uniform else launch_ticks,
+                       "max_ticks_per_launch": R, "cuda_graph": graph is not None,
+                       "ring_slots": ring, "kernel_shape": eng.launch_shape(),
                        "parallelism": f"world-shard x{world_size}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic_per_launch(W, M, R, ticks_per_launch) if world_size == 1 else None,
-                         "traffic_unit": f"bytes per launch (ncu dram read+write of a {R}-tick launch, "
-                                         "profiles/ncu_traffic.json, per tick x ticks per launch)",
+                         "frac": achieved / peak, "traffic": None if traffic is None else traffic[0],
+                         "traffic_source": None if traffic is None else traffic[1],
                          "algorithmic_bytes_per_launch": per_agent * W * M * ticks_per_launch,
                          "bytes_per_agent_step": per_agent, "kernel_ms": kern_avg,
                          "kernel_ms_per_tick": kern_avg / ticks_per_launch,
@@ -426,6 +475,7 @@ def main():
             line["c4_single_gpu"] = bench_c4(dev, steps=max(64, args.steps), R=R)
         if not args.no_cpu and world_size == 1:
             line["cpu_baseline"] = cpu_baseline(args.cpu_steps or 40)
+            line["reference_package"] = unmodified_reference(W_total, M, 20, 3, len(os.sched_getaffinity(0)))
         print(json.dumps(line), flush=True)
     if world_size > 1:
         dist.destroy_process_group()
@@ -584,15 +634,16 @@ def e2e_numpy(eng, steps):
     ticks = 0
     t0 = time.perf_counter()
     for _ in range(steps):
-        ticks += int(eng.valid.sum())
         out = eng.step(pol(obs), autoreset=True)
+        ticks += int(out.info["alive_pre"].sum())     # alive before the step (measure_engine)
         obs = out.obs
     wall = time.perf_counter() - t0
     W, M, D = eng.W, eng.M, eng.obs_config.obs_dim
-    _, aux_bytes = eng._aux_layout()
     return {"value": ticks / wall, "unit": "agent-steps/s", "h2d_bytes_per_step": W * M * 3 * 8,
-            "d2h_bytes_per_step": W * M * D * 4 + aux_bytes, "steps": steps, "ticks": ticks, "wall_s": wall,
-            "api": "Engine.step(numpy) with fused autoreset + host numpy LaneFollower"}
+            "d2h_bytes_per_step": int(eng._host_blob.numel()), "steps": steps, "ticks": ticks, "wall_s": wall,
+            "ms_per_step": 1e3 * wall / steps, "pinned_slabs": eng._host_pool.pinned_slabs,
+            "api": "Engine.step(numpy actions) -> numpy StepOutput, autoreset, host numpy LaneFollower; "
+                   "alive agents counted before each step (metrics.py:168-170)"}
 
 
 if __name__ == "__main__":

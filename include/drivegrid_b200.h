@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 7
+#define DG_ABI_VERSION 8
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -63,7 +63,8 @@ typedef struct DgDims {
                                  by the offset, read in place from global memory
                                  by the split kernels (scenes too large for the
                                  227 KB of shared memory; dg_step then takes
-                                 ticks = 1 and dg_tune only mode 1)           */
+                                 ticks = 1, written to ring slot ring_start,
+                                 and dg_tune only mode 1)                      */
 } DgDims;
 
 /* Float64 scalars, precomputed on the host with the reference's expression
@@ -164,6 +165,19 @@ typedef struct DgStepIO {
                                    (metrics.py:33-62, 101-108), or NULL        */
     uint8_t* metric_seen;       /* [W][M]      |= bit 0 goal event, bit 1 collision
                                    event of this tick (metrics.py:100-101), or NULL */
+    int32_t* index_out;         /* [W][M][dg_index_stride()] per tick slot, or NULL:
+                                   the integer decisions behind the float outputs,
+                                   for exact comparison with the reference --
+                                   [0] nearest-lane index into the world's lane
+                                       subset (rewards.py:94 argmin; -1: no lane or
+                                       agent not alive before the tick),
+                                   [1] road candidates kept n_r (observation.py:94-99),
+                                   [2] valid neighbours n_v (observation.py:242-249),
+                                   [3 .. 3+take_veh)  neighbour agent index by rank
+                                       (stable argsort, observation.py:246), first n_v,
+                                   [3+take_veh ..)    road slot -> segment index
+                                       (stable argsort of ~cand), first n_r;
+                                   entries past n_v / n_r are left untouched    */
 } DgStepIO;
 
 typedef struct dg_engine dg_engine;
@@ -250,6 +264,10 @@ int dg_tune(dg_engine* eng, int32_t mode, int32_t warps_per_world, int32_t ctas_
 
 /* Device scratch the split mode needs (per-agent records between its kernels). */
 size_t dg_scratch_bytes(int32_t W, int32_t M);
+
+/* int32 entries per agent of DgStepIO.index_out: 3 + min(k_vehicles, M) +
+ * min(k_road, max_segments). */
+int32_t dg_index_stride(dg_engine* eng);
 
 /* ------------------------------------------------------------------------
  * Policy MLP (BASELINE configs[4]: the rollout's batched policy forward,

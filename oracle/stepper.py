@@ -329,6 +329,58 @@ def one_shot(rsn, rc: P.RewardConfig):
     return np.where(rsn == P.REASON_LANE_FORBIDDEN, -rc.lane_forbidden_weight, out)
 
 
+# --------------------------------------------------------------------------- integer decisions
+
+def road_order(px, py, mid, mask, oc: P.ObsConfig):
+    """Road slot -> segment index: the stable argsort of ~cand, first
+    min(K_r, P) entries (observation.py:92-99); n = candidates kept."""
+    dx = mid[..., 0] - px[..., None]
+    dy = mid[..., 1] - py[..., None]
+    cand = (dx * dx + dy * dy <= oc.road_radius ** 2) & mask
+    take = min(oc.k_road, mid.shape[-2])
+    order = np.argsort(~cand, axis=-1, kind="stable")[..., :take]
+    return order, np.minimum(cand.sum(axis=-1), take)
+
+
+def neighbour_order(px, py, alive, oc: P.ObsConfig):
+    """Neighbour rank -> agent index: stable argsort of the distances with
+    dead agents and self at inf, first min(K_v, M) (observation.py:239-249);
+    n = finite entries."""
+    M = px.shape[1]
+    dx = px[:, None, :] - px[:, :, None]
+    dy = py[:, None, :] - py[:, :, None]
+    dist = np.sqrt(dx * dx + dy * dy)
+    dist = np.where(alive[:, None, :], dist, np.inf)
+    dist = np.where(np.eye(M, dtype=bool)[None], np.inf, dist)
+    take = min(oc.k_vehicles, M)
+    sel = np.argsort(dist, axis=-1, kind="stable")[..., :take]
+    return sel, np.isfinite(np.take_along_axis(dist, sel, axis=-1)).sum(axis=-1)
+
+
+def lane_index(px, py, lane):
+    """np.argmin (first index on ties) of the point-to-segment d2 over the
+    compacted lane subset (rewards.py:87-94); -1 where no lane exists."""
+    ex = px[..., None] - lane["mid"][..., 0]
+    ey = py[..., None] - lane["mid"][..., 1]
+    along = ex * lane["dir"][..., 0] + ey * lane["dir"][..., 1]
+    lat = lane["dir"][..., 0] * ey - lane["dir"][..., 1] * ex
+    over = np.maximum(np.abs(along) - lane["half_len"], 0.0)
+    d2 = np.where(lane["mask"], over * over + lat * lat, np.inf)
+    k = np.argmin(d2, axis=-1) if d2.shape[-1] else np.zeros(px.shape, dtype=np.int64)
+    best = np.take_along_axis(d2, k[..., None], axis=-1)[..., 0] if d2.shape[-1] else np.full(px.shape, np.inf)
+    return np.where(np.isfinite(best), k, -1)
+
+
+@dataclass
+class IndexRecord:
+    """The integer decisions of one step, in the kernel's index_out terms."""
+    lane: np.ndarray        # (W, M) nearest-lane index, -1: none / not alive before the step
+    road: np.ndarray        # (W, M, take_road) slot -> segment
+    road_n: np.ndarray      # (W, M)
+    veh: np.ndarray         # (W, M, take_veh) rank -> agent
+    veh_n: np.ndarray       # (W, M)
+
+
 # --------------------------------------------------------------------------- engine
 
 @dataclass
@@ -368,6 +420,7 @@ class OracleEngine:
         self.spawn_step = np.zeros((self.W, self.M), dtype=np.int64)
         self.event_seen = {k: np.zeros((self.W, self.M), dtype=bool) for k in P.EVENT_TYPES}
         self.step_count = 0
+        self.record_indices = False   # step() adds info["indices"] (IndexRecord)
         workers = config.effective_workers if num_workers is None else max(1, num_workers)
         self._pool = ThreadPoolExecutor(workers) if workers > 1 else None
 
@@ -449,6 +502,7 @@ class OracleEngine:
         obs, tmin = self._observe()
         alive_pre = self.alive.copy()
         snapshot = {k: v.copy() for k, v in st.items()}
+        indices = self.index_record(st, alive_pre) if self.record_indices else None
 
         # rewards and events against the pre-step alive mask
         W, M = self.W, self.M
@@ -511,7 +565,30 @@ class OracleEngine:
         info = {"alive": self.alive.copy(), "alive_pre": alive_pre, "state": snapshot,
                 "reason": self.reason.copy(), "reward_terms": terms, "ttc_min": tmin,
                 "step": self.step_count}
+        if indices is not None:
+            info["indices"] = indices
         return OracleStep(obs, rewards, finished, events, info)
+
+    def index_record(self, st, alive) -> IndexRecord:
+        """Integer decisions on the post-physics state ``st`` with the alive
+        mask the step used (world chunks like the float work)."""
+        oc = self.obs_config
+        W, M = self.W, self.M
+        take_r = min(oc.k_road, self.seg["mid"].shape[-2])
+        take_v = min(oc.k_vehicles, M)
+        rec = IndexRecord(np.full((W, M), -1, np.int64), np.zeros((W, M, take_r), np.int64),
+                          np.zeros((W, M), np.int64), np.zeros((W, M, take_v), np.int64),
+                          np.zeros((W, M), np.int64))
+
+        def work(ch):
+            px, py = st["x"][ch], st["y"][ch]
+            rec.road[ch], rec.road_n[ch] = road_order(px, py, self.seg["mid"][ch], self.seg["mask"][ch], oc)
+            rec.veh[ch], rec.veh_n[ch] = neighbour_order(px, py, alive[ch], oc)
+            lk = lane_index(px, py, {k: v[ch] for k, v in self.lane.items()})
+            rec.lane[ch] = np.where(alive[ch], lk, -1)
+
+        self._map(work)
+        return rec
 
     # ----------------------------------------------------------------- reset
     def teleport_reset(self, mask, new_starts=None, new_goals=None, new_headings=None):

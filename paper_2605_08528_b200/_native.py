@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 
 class DgDims(ct.Structure):
@@ -85,7 +85,7 @@ class DgStepIO(ct.Structure):
                                               ("event_counts", _P),
                                               ("ticks", ct.c_int32), ("ring_slots", ct.c_int32),
                                               ("ring_start", ct.c_int32), ("pad_", ct.c_int32),
-                                              ("drac_max", _P), ("metric_seen", _P)]
+                                              ("drac_max", _P), ("metric_seen", _P), ("index_out", _P)]
 
 
 # exported symbol -> (restype, argtypes)
@@ -106,6 +106,7 @@ SIGNATURES = {
     "dg_launch_count": (ct.c_int, [_P]),
     "dg_tune": (ct.c_int, [_P, ct.c_int32, ct.c_int32, ct.c_int32]),
     "dg_scratch_bytes": (ct.c_size_t, [ct.c_int32, ct.c_int32]),
+    "dg_index_stride": (ct.c_int32, [_P]),
     "dg_sysid_rollout": (ct.c_int, [_P] * 6 + [ct.c_int32, ct.c_int32, _P, _P]),
     "dg_policy_forward": (ct.c_int, [ct.POINTER(DgPolicyDesc), _P]),
     "dg_policy_scratch_bytes": (ct.c_size_t, [ct.c_int32, ct.c_int32]),

@@ -95,6 +95,8 @@ struct KArgs {
     uint8_t* scratch;    // split mode: AgentRec[W*M], int32 world_ok[W], int32 world_step[W]
     double* drac_max;    // [W][M] running max of the per-step pairwise DRAC (NULL = off)
     uint8_t* metric_seen; // [W][M] |= goal (bit 0) / collision (bit 1) events (NULL = off)
+    int32_t* index_out;   // [slot][W][M][index_stride] integer decisions (NULL = off)
+    int32_t index_stride; // 3 + take_veh + take_road
 };
 
 // ----------------------------------------------------------------- numpy-semantics helpers
@@ -845,6 +847,8 @@ world_step_kernel(const KArgs A) {
     for (int t = 0; t < T; ++t) {
         const int slot = A.ring_slots > 0 ? (A.ring_start + t) % A.ring_slots : t;
         float* obs_w = A.obs + (int64_t(slot) * WM + int64_t(w) * M) * D;
+        int32_t* ix_w = A.index_out ? A.index_out + (int64_t(slot) * WM + int64_t(w) * M) * A.index_stride
+                                    : nullptr;
         const TickOut O = tick_out(A, slot);
         if (kStep && t > 0) {
             // every tick gets the same rejection as a separate step call (s_bad was
@@ -1046,10 +1050,13 @@ world_step_kernel(const KArgs A) {
                 double ttc = k.ttc_max;
                 bool touch = false;
                 double dr = 0.0;
+                int n_valid = 0;
 #pragma unroll
                 for (int u = 0; u < kOPL; ++u) {
                     const int j = jl + kPL * u;
                     const bool nvalid = ego_ok && j < M && finite(key[u]) && rank[u] < A.take_veh;
+                    n_valid += nvalid;
+                    if (nvalid && ix_w) ix_w[int64_t(ii) * A.index_stride + 3 + rank[u]] = j;
                     if (nvalid) {
                         const AgentSm& N = ag[j];
                         const double tj = swept_ttc(ndx[u], ndy[u], N.vwx - S.vwx, N.vwy - S.vwy, c, s, S.d, N.c,
@@ -1090,6 +1097,10 @@ world_step_kernel(const KArgs A) {
                 }
                 ttc = warp_min(ttc, kPL);
                 touch = (__ballot_sync(kFull, touch) & gmask) != 0;
+                if (ix_w) {
+                    for (int o = kPL / 2; o > 0; o >>= 1) n_valid += __shfl_xor_sync(kFull, n_valid, o, kPL);
+                    if (ego_ok && jl == 0) ix_w[int64_t(ii) * A.index_stride + 2] = n_valid;
+                }
                 if (kStep && A.drac_max) {
                     dr = warp_max_nn(dr, kPL);
                     if (ego_ok && jl == 0) {
@@ -1201,9 +1212,12 @@ world_step_kernel(const KArgs A) {
             }
             const int ncand = count < A.take_road ? count : A.take_road;
             __syncwarp();
+            int32_t* ix_m = ix_w ? ix_w + int64_t(act ? m : kAPW * pr) * A.index_stride : nullptr;
             if (act) {
+                if (ix_m && hl == 0) ix_m[1] = ncand;
                 for (int slot = hl; slot < ncand; slot += kGL) {
                     const int q = cand[slot];
+                    if (ix_m) ix_m[3 + A.take_veh + slot] = q;
                     const double2 m2 = G.mid[q], u2 = G.dir[q];
                     const double dx = m2.x - px, dy = m2.y - py;
                     const double ux = u2.x, uy = u2.y;
@@ -1217,6 +1231,7 @@ world_step_kernel(const KArgs A) {
             }
             // both agents dead (or absent): no rewards / events -> skip the rest
             if (!__any_sync(kFull, rewards_needed)) {
+                if (ix_m && act && hl == 0) ix_m[0] = -1;
                 if (kStep && act && hl == 0) {
                     ScanSm& R = sc[m];
                     R.lane_d2 = INFINITY;
@@ -1281,6 +1296,7 @@ world_step_kernel(const KArgs A) {
                 const int ok = __shfl_xor_sync(kFull, best_k, o, kGL);
                 if (ob < best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
             }
+            if (ix_m && act && hl == 0) ix_m[0] = rewards_needed && best < INFINITY ? best_k : -1;
             if (kStep && act && hl == 0) {
                 ScanSm& R = sc[m];
                 if (rewards_needed) {
@@ -1498,8 +1514,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
     float4* zero_sm = reinterpret_cast<float4*>(
         smem + align16(reinterpret_cast<uint8_t*>(cand_sm + apc * A.take_road) - smem));
 
-    // ---- prologue, independent of K1: clear this CTA's obs rows (TMA bulk stores)
-    float* rows = A.obs + (int64_t(w) * M + m0) * D;
+    // ---- prologue, independent of K1: clear this CTA's obs rows (TMA bulk stores);
+    //      one tick per launch, written to ring slot ring_start (header contract)
+    const int slot = A.ring_start;
+    float* rows = A.obs + (int64_t(slot) * WM + int64_t(w) * M + m0) * D;
     for (int i = tid; i < kZeroChunk / 16; i += blockDim.x) zero_sm[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
@@ -1550,6 +1568,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
     const int road0 = A.d.ego_dim;
     const int veh0 = A.d.ego_dim + 5 * A.d.k_road;
     const bool rewards_needed = kStep && S.alive;
+    int32_t* ix_m = A.index_out ? A.index_out + (int64_t(slot) * WM + am) * A.index_stride : nullptr;
 
     // (1) neighbours: lane j <-> agent j (16 lanes), stable distance rank,
     //     swept TTC, neighbour row, hull contact
@@ -1571,6 +1590,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
             rank += (kt < key) || (kt == key && t < j);
         }
         const bool nvalid = j < M && finite(key) && rank < A.take_veh;
+        if (ix_m) {
+            if (nvalid) ix_m[3 + rank] = j;
+            const int nv = __popc(__ballot_sync(kFull, nvalid));
+            if (lane == 0) ix_m[2] = nv;
+        }
         double ttc = k.ttc_max;
         if (nvalid) {
             const AgentRec& N = ag[j];
@@ -1676,8 +1700,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
     }
     const int ncand = count < A.take_road ? count : A.take_road;
     __syncwarp();
+    if (ix_m && lane == 0) ix_m[1] = ncand;
     for (int slot = lane; slot < ncand; slot += 32) {
         const int q = cand[slot];
+        if (ix_m) ix_m[3 + A.take_veh + slot] = q;
         const double2 m2 = __ldg(G.mid + q), u2 = __ldg(G.dir + q);
         const double dx = (tx(m2.x)) - px, dy = (ty(m2.y)) - py;
         float* o = row + road0 + 5 * slot;
@@ -1751,6 +1777,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
         }
     }
     edge_hit = __any_sync(kFull, edge_hit);
+    if (ix_m && lane == 0) ix_m[0] = rewards_needed && best < INFINITY ? best_k : -1;
 
     // (5) the agent's reward / event / termination tail
     if (lane == 0) {
@@ -1781,7 +1808,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
         F.store_global = true;
         F.st_out = nullptr;
         F.flags_out = nullptr;
-        const unsigned bits = finalize_agent(A, tick_out(A, 0), w, m, F, step_now, ox, oy);
+        const unsigned bits = finalize_agent(A, tick_out(A, slot), w, m, F, step_now, ox, oy);
         count_events(A, w, bits, 1u, true, true);
     }
 }
@@ -2130,6 +2157,7 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
     A.scratch = desc->scratch;
     A.take_road = d.k_road < d.max_segments ? d.k_road : d.max_segments;
     A.take_veh = d.k_vehicles < d.M ? d.k_vehicles : d.M;
+    A.index_stride = 3 + A.take_veh + A.take_road;
     e->smem_bytes = step_smem_bytes(d, A.take_road);
     // headroom for the kernels' static / reserved shared memory
     if (!d.geometry_global && e->smem_bytes > 227 * 1024 - 4096) {
@@ -2196,6 +2224,7 @@ int dg_step(dg_engine* eng, const DgStepIO* io, void* stream) {
     A.pol_throttle = io->policy_throttle;
     A.drac_max = io->drac_max;
     A.metric_seen = io->metric_seen;
+    A.index_out = io->index_out;
     A.ticks = io->ticks > 0 ? io->ticks : 1;
     A.ring_slots = io->ring_slots > 0 ? io->ring_slots : A.ticks;
     A.ring_start = io->ring_start;
@@ -2369,5 +2398,7 @@ int dg_tune(dg_engine* eng, int32_t mode, int32_t warps_per_world, int32_t ctas_
 }
 
 size_t dg_scratch_bytes(int32_t W, int32_t M) { return split_scratch_bytes(W, M); }
+
+int32_t dg_index_stride(dg_engine* eng) { return eng ? eng->base.index_stride : 0; }
 
 }  // extern "C"

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as ct
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -147,6 +148,46 @@ def per_world_blobs(blob: np.ndarray, meta: np.ndarray, scene_of_world, grid_off
         wmeta.append([off, nb, P, KL, KE, aux_off, aux_len, 0])
         off += nb
     return np.frombuffer(b"".join(parts), dtype=np.uint8).copy(), np.asarray(wmeta, dtype=np.int64)
+
+
+class _Lease:
+    """numpy base object of one host slab hand-out: every array returned by a
+    host step is a view of it, so it dies when the caller drops the last one."""
+    __slots__ = ("__array_interface__", "__weakref__")
+
+
+class HostSlabPool:
+    """Pinned host slabs for the numpy step path, recycled once the caller has
+    dropped every array of the step that filled them (weakref on the numpy
+    base).  The reference returns fresh arrays each step (engine.py:307,
+    397-406); a freed slab is exactly that without a cudaHostAlloc per step.
+    Past ``max_pinned`` live slabs (a caller keeping every step's outputs)
+    further slabs are pageable."""
+
+    def __init__(self, nbytes: int, max_pinned: int = 16):
+        self.nbytes = int(nbytes)
+        self.max_pinned = int(max_pinned)
+        self._slabs = []          # [pinned tensor, weakref to its current lease or None]
+
+    def acquire(self):
+        """(torch uint8 host tensor to copy into, numpy uint8 view of it)."""
+        slot = next((s for s in self._slabs if s[1] is None or s[1]() is None), None)
+        if slot is None:
+            pinned = len(self._slabs) < self.max_pinned
+            t = torch.empty(self.nbytes, dtype=torch.uint8, pin_memory=pinned)
+            if not pinned:
+                return t, t.numpy()
+            slot = [t, None]
+            self._slabs.append(slot)
+        lease = _Lease()
+        lease.__array_interface__ = {"data": (slot[0].data_ptr(), False), "shape": (self.nbytes,),
+                                     "typestr": "|u1", "version": 3}
+        slot[1] = weakref.ref(lease)
+        return slot[0], np.asarray(lease)
+
+    @property
+    def pinned_slabs(self) -> int:
+        return len(self._slabs)
 
 
 class StepOutput:
@@ -330,6 +371,7 @@ class Engine:
         self._obs_dev = self._host_blob[:obs_bytes].view(torch.float32).view(W, M, oc.obs_dim)
         aux_dev = self._host_blob[self._host_obs_bytes:]
         self._host_bufs = StepBuffers(self._obs_dev, aux_dev, self._views(aux_dev))
+        self._host_pool = HostSlabPool(self._host_blob.numel())
         self.launches = 0
         self._metrics_on = False
         self._host_lay = None
@@ -404,6 +446,16 @@ class Engine:
 
     def launch_shape(self) -> dict:
         return dict(self._shape)
+
+    @property
+    def index_stride(self) -> int:
+        """int32 entries per agent of the ``index_out`` debug record."""
+        return int(self._lib.dg_index_stride(self._h))
+
+    def new_index_buffer(self, slots: int = 1) -> torch.Tensor:
+        """[slots][W][M][index_stride] int32, filled with -1."""
+        return torch.full((int(slots), self.W, self.M, self.index_stride), -1, dtype=torch.int32,
+                          device=self.device)
 
     def tune(self, warps_per_world: int, ctas_per_sm: int = 0, mode: int = 0) -> None:
         """Launch shape knob; results are unaffected.  mode 0: fused world
@@ -534,6 +586,9 @@ class Engine:
         N.check(self._lib, self._lib.dg_read_error(self._h, ct.byref(flat), self._stream()),
                 "dg_read_error")
         if flat.value >= 0:
+            # a rejected tick stops its world where it was (a multi-tick launch
+            # may have advanced the others): the host counter follows the device
+            self._step_count = int(self._d["step_count"].min().item())
             self._raise_nonfinite(flat.value)
 
     # ------------------------------------------------------------------ observe
@@ -559,7 +614,8 @@ class Engine:
                     snapshot: bool = True, terms: bool = True, next_actions: torch.Tensor | None = None,
                     steer_gain: float = 2.0, throttle: float = 0.5,
                     event_counts: torch.Tensor | None = None, ticks: int = 1, ring_start: int = 0,
-                    drac_max: torch.Tensor | None = None, metric_seen: torch.Tensor | None = None) -> None:
+                    drac_max: torch.Tensor | None = None, metric_seen: torch.Tensor | None = None,
+                    index_out: torch.Tensor | None = None) -> None:
         """Enqueue one fused launch on the current stream; no sync, no checks
         beyond the device-side non-finite guard.  Used by the fast paths.
         ``next_actions`` (float64 [W][M][3], may alias ``actions``) receives
@@ -576,7 +632,10 @@ class Engine:
 
         ``drac_max`` (float64 [W][M]) / ``metric_seen`` (uint8 [W][M]) are the
         in-kernel episode-metric accumulators (default: the engine's own when
-        ``track_episode_metrics`` is on)."""
+        ``track_episode_metrics`` is on).  ``index_out`` (int32 [S][W][M][
+        ``index_stride``], S = ring slots) receives the integer decisions of
+        every tick: nearest-lane index, road slot -> segment map, neighbour
+        order (layout: ``DgStepIO.index_out`` in the C header)."""
         if self._shape["mode"] == "split" and (ticks > 1 or bufs.obs.dim() == 4):
             # the split kernels take one tick per launch and write one output
             # set: tick t goes to ring slot (ring_start + t) % S through views
@@ -590,17 +649,18 @@ class Engine:
                 one = bufs if bufs.obs.dim() == 3 else StepBuffers(
                     bufs.obs[slot], bufs.aux, {k: v[slot] for k, v in bufs.views.items()})
                 self.launch_step(a_t, one, autoreset, snapshot, terms, next_actions, steer_gain, throttle,
-                                 event_counts, 1, 0, drac_max, metric_seen)
+                                 event_counts, 1, 0, drac_max, metric_seen,
+                                 None if index_out is None else index_out.view(-1, *index_out.shape[-3:])[slot])
             return
         io = self._step_io(actions, bufs, autoreset, snapshot, terms, next_actions, steer_gain, throttle,
-                           event_counts, ticks, ring_start, drac_max, metric_seen)
+                           event_counts, ticks, ring_start, drac_max, metric_seen, index_out)
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), self._stream()), "dg_step")
         self._step_count += int(ticks)
         self.launches += 1
 
     def _step_io(self, actions, bufs, autoreset=False, snapshot=True, terms=True, next_actions=None,
                  steer_gain=2.0, throttle=0.5, event_counts=None, ticks=1, ring_start=0, drac_max=None,
-                 metric_seen=None):
+                 metric_seen=None, index_out=None):
         if self._metrics_on:
             drac_max = self._drac_max if drac_max is None else drac_max
             metric_seen = self._metric_seen if metric_seen is None else metric_seen
@@ -618,7 +678,12 @@ class Engine:
                         policy_gain=float(steer_gain), policy_throttle=float(throttle),
                         event_counts=event_counts.data_ptr() if event_counts is not None else None,
                         ticks=int(ticks), ring_slots=int(slots), ring_start=int(ring_start),
-                        drac_max=_ptr(drac_max), metric_seen=_ptr(metric_seen))
+                        drac_max=_ptr(drac_max), metric_seen=_ptr(metric_seen), index_out=_ptr(index_out))
+        if index_out is not None:
+            want = (slots, self.W, self.M, self.index_stride)
+            if (index_out.dtype != torch.int32 or not index_out.is_cuda or not index_out.is_contiguous()
+                    or index_out.numel() != int(np.prod(want))):
+                raise ValueError(f"index_out must be a contiguous int32 CUDA tensor of {want} elements")
         return io
 
     def rollout(self, actions, ticks: int | None = None, autoreset: bool = False, policy=None,
@@ -788,11 +853,10 @@ class Engine:
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), ct.c_void_p(stream.cuda_stream)), "dg_step")
         self._step_count += 1
         self.launches += 1
-        host = torch.empty(self._host_blob.shape, dtype=torch.uint8, pin_memory=True)
+        host, hb = self._host_pool.acquire()
         host.copy_(self._host_blob, non_blocking=True)          # obs + every per-tick output, one copy
         stream.synchronize()
         t2 = time.perf_counter()
-        hb = host.numpy()
         obs = hb[:self.W * self.M * self.obs_config.obs_dim * 4].view(np.float32).reshape(bufs.obs.shape)
         hv = self._host_views(hb[self._host_obs_bytes:])
         src = dict(hv)

@@ -213,9 +213,9 @@ class PolicyMLP:
         if self._blob is None:
             self._pack()
         n = obs.numel() // oc.obs_dim
-        nets = 2 if self.critic else 1
+        n_nets = 2 if self.critic else 1
         lib = N.load_library()
-        need = int(lib.dg_policy_scratch_bytes(n, nets))
+        need = int(lib.dg_policy_scratch_bytes(n, n_nets))
         if self._emb is None or self._emb.numel() * 2 < need:
             self._emb = torch.empty(need // 2, dtype=torch.int16, device=self.device)
         d = N.DgPolicyDesc(n_agents=n, obs_dim=oc.obs_dim, ego_dim=oc.ego_dim, k_road=oc.k_road,

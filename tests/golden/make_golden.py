@@ -510,6 +510,87 @@ def traj_sparse():
     rec.save("traj_sparse", valid=eng.valid)
 
 
+class _NumpySpy:
+    """Stands in for ``np`` inside drivegrid.observation / drivegrid.rewards and
+    records the reference's own integer decisions: the stable argsorts of
+    road_context (observation.py:96) and neighbor_features_batch
+    (observation.py:246), and nearest_lane's argmin (rewards.py:94)."""
+
+    def __init__(self):
+        self.calls = []
+
+    def __getattr__(self, name):
+        return getattr(np, name)
+
+    def argsort(self, a, *args, **kw):
+        r = np.argsort(a, *args, **kw)
+        self.calls.append((sys._getframe(1).f_code.co_name, "argsort", np.array(a), r))
+        return r
+
+    def argmin(self, a, *args, **kw):
+        r = np.argmin(a, *args, **kw)
+        self.calls.append((sys._getframe(1).f_code.co_name, "argmin", np.array(a), r))
+        return r
+
+
+def _index_record(spy, take_road, take_veh):
+    """The step's calls -> (lane, road, road_n, veh, veh_n) like the kernel's
+    index_out record (-1 for no lane)."""
+    by = {name: (a, r) for name, _, a, r in spy.calls}
+    not_cand, order = by["road_context"]
+    road_n = np.minimum((~not_cand).sum(axis=-1), take_road)
+    dist, sel = by["neighbor_features_batch"]
+    sel = sel[..., :take_veh]
+    veh_n = np.isfinite(np.take_along_axis(dist, sel, axis=-1)).sum(axis=-1)
+    d2, k = by["nearest_lane"]
+    best = np.take_along_axis(d2, k[..., None], axis=-1)[..., 0]
+    lane = np.where(np.isfinite(best), k, -1)
+    return lane, order[..., :take_road], road_n, sel, veh_n
+
+
+def index_pins():
+    """Integer decisions of the reference step (nearest-lane index, road slot
+    -> segment map, neighbour order) captured from the reference's own
+    argsort / argmin calls, serial engine (one world chunk per call)."""
+    import drivegrid.observation as obs_mod
+    import drivegrid.rewards as rw_mod
+    spy = _NumpySpy()
+    saved = obs_mod.np, rw_mod.np
+    obs_mod.np, rw_mod.np = spy, spy
+    try:
+        for name, steps in (("traj_events", 160), ("traj_pool", 60)):
+            if name == "traj_events":
+                cfg = cfg_of(4, 16, seed=31)
+                acts = event_actions(steps, 4, 16)
+            else:
+                cfg = cfg_of(4, 16)
+                acts = None
+            cfg.env.num_workers = 1
+            eng = build_engine(cfg)
+            take_road = min(eng.obs_config.k_road, eng.seg_mid.shape[-2])
+            take_veh = min(eng.obs_config.k_vehicles, 16)
+            pol = LaneFollower(obs_config=eng.obs_config)
+            obs = eng.observe()
+            rows = {k: [] for k in ("lane", "road", "road_n", "veh", "veh_n", "actions")}
+            for t in range(steps):
+                a = pol(obs) if acts is None else acts[t].astype(np.float64)
+                alive_pre = eng.alive.copy()
+                spy.calls.clear()
+                out = eng.step(a)
+                lane, road, road_n, veh, veh_n = _index_record(spy, take_road, take_veh)
+                rows["lane"].append(np.where(alive_pre, lane, -1))
+                rows["road"].append(road.astype(np.int16))
+                rows["road_n"].append(road_n)
+                rows["veh"].append(veh.astype(np.int8))
+                rows["veh_n"].append(veh_n)
+                rows["actions"].append(a)
+                obs = out.obs
+            np.savez_compressed(OUT / f"{name}_indices.npz", **{k: np.stack(v) for k, v in rows.items()})
+            print(f"{name}_indices", steps, "steps")
+    finally:
+        obs_mod.np, rw_mod.np = saved
+
+
 def sysid():
     import json
     from drivegrid import sysid as S
@@ -554,6 +635,6 @@ def sysid():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense", "traj_obs_min", "traj_no_edges", "scene_verdicts"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense", "traj_obs_min", "traj_no_edges", "scene_verdicts", "index_pins"]
     for name in which:
         globals()[name]()
