@@ -28,7 +28,7 @@ def test_ncu_traffic_table_matches_profiles():
         W, M, T = (int(v) for v in key.split("x"))
         alg = bench.algorithmic_bytes_per_agent(1929) * W * M * T
         assert 0.8 * alg < t[key]["traffic_bytes"] < 1.05 * alg, key     # no wasted re-reads
-        assert bench.ncu_traffic(W, M, T) == float(t[key]["traffic_bytes"])
+        assert bench.ncu_traffic(W, M, T)[0] == float(t[key]["traffic_bytes"])
     assert bench.ncu_traffic(7, 16, 64) is None
 
 
