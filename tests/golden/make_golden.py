@@ -146,6 +146,18 @@ def friction():
     print("friction")
 
 
+def friction_table():
+    """mu_effective of the reference over a dense film sweep (the vectorised
+    host table, friction.mu_table, must reproduce it)."""
+    g = np.random.Generator(np.random.Philox(21))
+    films = np.concatenate([[0.0, 1e-9, 0.3, 0.86, 1.0, 2.0, 5.0], g.uniform(0.0, 3.0, 993)])
+    slips = np.array([0.15, 0.8, 0.5, 1.0, 0.0])
+    mu = np.array([[[mu_effective(s, float(h), slip=float(sl)) for h in films] for sl in slips]
+                   for s in SURFACE_ORDER])
+    np.savez_compressed(OUT / "friction_table.npz", films=films, slips=slips, mu=mu)
+    print("friction_table")
+
+
 def traj_c1():
     scene = prepare_scene(straight_scene(agent_count=1, goal_dist=50.0))
     eng = build_engine(cfg_of(1, 1, invincible=True, episode_len=2000), scenes=[scene])
@@ -633,7 +645,7 @@ def sysid():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["init_default", "friction", "traj_c1", "traj_pool", "traj_wet",
+    which = sys.argv[1:] or ["init_default", "friction", "friction_table", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
                              "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense", "traj_obs_min", "traj_no_edges", "scene_verdicts", "index_pins"]
     for name in which:

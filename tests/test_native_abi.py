@@ -70,3 +70,20 @@ def test_create_rejects_bad_descriptions_without_a_gpu():
     d.dims.W, d.dims.M = 1, 17
     assert lib.dg_create(ct.byref(d), ct.byref(h)) == N.DG_EINVAL
     assert b"M <= 16" in lib.dg_last_error()
+
+
+def test_integration_stub_matches_the_binding():
+    """The ctypes stub INTEGRATION.md hands a drivegrid maintainer declares
+    the same struct fields (names, types, offsets) as this package's binding."""
+    import re
+    text = (N.ROOT / "INTEGRATION.md").read_text()
+    block = next(b for b in re.findall(r"```python\n(.*?)```", text, re.S) if "class DgDims" in b)
+    block = block.replace('ct.CDLL("libdrivegrid_b200.so")', f'ct.CDLL({str(N.LIB_PATH)!r})')
+    ns = {"CONST_FIELDS": N.CONST_FIELDS}
+    exec(compile(block, "INTEGRATION.md", "exec"), ns)
+    for name in ("DgDims", "DgConsts", "DgEngineDesc", "DgStepIO"):
+        stub, ours = ns[name], getattr(N, name)
+        assert [f[0] for f in stub._fields_] == [f[0] for f in ours._fields_], name
+        assert ct.sizeof(stub) == ct.sizeof(ours), name
+        for f, _ in ours._fields_:
+            assert getattr(stub, f).offset == getattr(ours, f).offset, (name, f)
