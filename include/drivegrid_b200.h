@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 8
+#define DG_ABI_VERSION 9
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -250,6 +250,23 @@ int dg_sysid_rollout(const void* consts, const double* mu, const int32_t* tick_s
                      const uint8_t* surface, const int64_t* out_offset, int32_t B, int32_t n_maneuvers,
                      double* out, void* stream);
 
+/* Host delivery of one step's outputs (the numpy path of Engine.step /
+ * observe, engine.py:297-335, env.py:48-65).  dg_host_alloc returns zeroed,
+ * mapped, portable pinned host memory (cudaHostAlloc); dg_host_free releases it.
+ * dg_to_host writes the engine's device observation `obs` [W][M][D] into
+ * such a slab `host_obs` (same layout) so that the slab equals it bit for
+ * bit, moving only the non-zero prefix of every row's road and vehicle blocks
+ * over PCIe; `prev_len` (device int32 [W*M][2], zero for a fresh slab) holds
+ * the prefix lengths the slab currently carries and is updated.  Then
+ * `aux_bytes` of the packed per-tick outputs `aux` (device) are copied to
+ * `host_aux` (pinned).  `bytes` (device u64, optional) accumulates the
+ * observation bytes written to the host.  Async on `stream`; the slab is valid
+ * after the stream synchronises. */
+int dg_host_alloc(size_t bytes, void** host_ptr);
+int dg_host_free(void* host_ptr);
+int dg_to_host(dg_engine* eng, const float* obs, float* host_obs, int32_t* prev_len, const void* aux,
+               void* host_aux, size_t aux_bytes, unsigned long long* bytes, void* stream);
+
 /* Kernel launches issued by the last dg_step/dg_observe/dg_reset call. */
 int dg_launch_count(dg_engine* eng);
 
@@ -259,6 +276,9 @@ int dg_launch_count(dg_engine* eng);
  *   mode 1 (split): a physics kernel (one warp per world) chained by
  *                   programmatic dependent launch to a per-agent kernel with
  *                   warps_per_world (2, 4 or 8) agents per CTA; needs scratch
+ *   mode 2 (fused, physics warp): mode 0 with warps_per_world (<= 8) scan
+ *                   warps plus one warp that runs tick t + 1's physics while
+ *                   the others build tick t's observation (multi-tick launches)
  * ctas_per_sm selects the register budget of the kernel variant (0 = default). */
 int dg_tune(dg_engine* eng, int32_t mode, int32_t warps_per_world, int32_t ctas_per_sm);
 

@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 
 class DgDims(ct.Structure):
@@ -113,6 +113,9 @@ SIGNATURES = {
     "dg_policy_last_error": (ct.c_char_p, []),
     "dg_gae": (ct.c_int, [_P, _P, _P, ct.c_int32, ct.c_int64, ct.c_double, ct.c_double, _P, _P, _P]),
     "dg_pairwise_drac": (ct.c_int, [_P] * 8 + [ct.c_int32, ct.c_int32, ct.c_int32, _P, ct.c_int32, ct.c_int32, _P]),
+    "dg_host_alloc": (ct.c_int, [ct.c_size_t, ct.POINTER(_P)]),
+    "dg_host_free": (ct.c_int, [_P]),
+    "dg_to_host": (ct.c_int, [_P, _P, _P, _P, _P, _P, ct.c_size_t, _P, _P]),
 }
 
 

@@ -40,6 +40,7 @@ namespace {
 constexpr int kMaxAgents = 16;
 constexpr int kZeroChunk = 4096;   // bytes of zeros in shared memory, source of the TMA row clears
 constexpr unsigned kFull = 0xffffffffu;
+constexpr unsigned kBitFinished = 32u;   // finalize_agent: done or timed out this tick
 
 enum StateField {
     SX = 0, SY, SYAW, SVX, SVY, SOM, SANG, SRATE, SWF, SWR, SBF, SBR
@@ -717,7 +718,7 @@ __device__ __forceinline__ unsigned finalize_agent(const KArgs& A, const TickOut
                 F.flags_out[3] = spawn;
             }
             return (rnow == 0 ? 0u : 1u << (rnow == 1 ? 0 : rnow == 2 ? 1 : rnow == 3 ? 2 : 3)) |
-                   (alive ? 16u : 0u);
+                   (alive ? 16u : 0u) | (finished ? kBitFinished : 0u);
         }
 
 // Episode counters [W][5] (goal, collision, crash, lane_forbidden, alive
@@ -757,8 +758,171 @@ __device__ __forceinline__ long long gtimer() { long long t; asm volatile("mov.u
 #define WARP_MARK(i) do { } while (0)
 #endif
 
+// Built with -DDG_TICK_TIMERS: per-CTA clock64 sums over every tick of a
+// (multi-tick) launch -- slots 0..4 the phases of thread 0's tick (action
+// check, phase 1, phase 2 incl. its barrier, tail, closing barrier), 8 + w the
+// scan time of warp w, 30 / 31 the physics warp's ego block / physics.
+#ifdef DG_TICK_TIMERS
+__device__ long long g_tick_acc[65536][40];
+#define TT_DECL long long tt_last = clock64(), tt_w = 0; (void)tt_w
+#define TT_ACC(i) do { if (threadIdx.x == 0) { const long long n_ = clock64(); g_tick_acc[blockIdx.x][i] += n_ - tt_last; tt_last = n_; } } while (0)
+#define TT_WSTART() do { if ((threadIdx.x & 31) == 0) tt_w = clock64(); } while (0)
+#define TT_WACC(i) do { if ((threadIdx.x & 31) == 0) { const long long n_ = clock64(); g_tick_acc[blockIdx.x][i] += n_ - tt_w; tt_w = n_; } } while (0)
+#else
+#define TT_DECL do { } while (0)
+#define TT_ACC(i) do { } while (0)
+#define TT_WSTART() do { } while (0)
+#define TT_WACC(i) do { } while (0)
+#endif
+
+// The raw (unclipped) actions of tick t for agent am: the fused policy's
+// shared-memory record when `fed` is given, else the caller's [T][W][M][3] array.
+__device__ __forceinline__ void load_actions(const KArgs& A, int t, int64_t am, const double* fed, double* raw) {
+    if (fed) {
+        raw[0] = fed[0]; raw[1] = fed[1]; raw[2] = fed[2];
+        return;
+    }
+    const int64_t ab = int64_t(t) * A.d.W * A.d.M * 3 + am * 3;
+    if (A.actions_f64) {
+        const double* a = reinterpret_cast<const double*>(A.actions);
+        raw[0] = a[ab]; raw[1] = a[ab + 1]; raw[2] = a[ab + 2];
+    } else {
+        const float* a = reinterpret_cast<const float*>(A.actions);
+        raw[0] = a[ab]; raw[1] = a[ab + 1]; raw[2] = a[ab + 2];
+    }
+}
+
+// Physics of one agent for one control tick (decode + decimation substeps,
+// engine.py:410-421 with the alive mask) from state x0, and the derived
+// per-tick record the scans read (heading cos/sin, world velocity, hull
+// centres, speed feature).  run = false leaves the state as it is.
+__device__ __forceinline__ void agent_physics(const KArgs& A, int w, AgentSm& S, const double* x0, int alive,
+                                              const double* raw, bool run) {
+    const DgConsts& k = A.k;
+    double x[DG_NUM_STATE];
+#pragma unroll
+    for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = x0[f];
+    S.px0 = x[SX];
+    S.py0 = x[SY];
+    if (alive && x[SX] != -12345.678) LANE0_MARK(25);  // after the state loads landed
+    if (run) {
+        Act act;
+        act.thr = np_clip(raw[0], 0.0, 1.0);
+        act.steer = np_clip(raw[1], -1.0, 1.0);
+        act.brk = np_clip(raw[2], 0.0, 1.0);
+        if (A.d.dynamic) {
+            const double cap = A.mu_eff[w] * k.f_z;
+            for (int i = 0; i < A.d.decimation; ++i) {
+                substep_dynamic(x, act, cap, k);
+#ifdef DG_PHASE_TIMERS
+                if (i < 4 && x[SX] != -12345.678) LANE0_MARK(28 + i);
+#endif
+            }
+        } else {
+            step_bicycle(x, act, k);
+        }
+    }
+    if (x[SX] != -12345.678) LANE0_MARK(26);          // after the substeps
+#pragma unroll
+    for (int f = 0; f < DG_NUM_STATE; ++f) S.st[f] = x[f];
+    double s_, c_;
+    sincos(x[SYAW], &s_, &c_);
+    S.c = c_;
+    S.s = s_;
+    S.vwx = x[SVX] * c_ - x[SVY] * s_;
+    S.vwy = x[SVX] * s_ + x[SVY] * c_;
+    S.f_spd = __double2float_rn(dg::ddiv(dg::dsqrt(x[SVX] * x[SVX] + x[SVY] * x[SVY]), k.speed_norm));
+    const double offs[3] = {-1.0, 0.0, 1.0};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double o = offs[i] * S.d;
+        S.hx[i] = x[SX] + o * c_;
+        S.hy[i] = x[SY] + o * s_;
+    }
+    S.alive = alive;
+    LANE0_MARK(27);
+}
+
+// Zero n floats at p with a group of gsz (>= 4) lanes, li = lane in the group:
+// scalar head up to 16-byte alignment, float4 body, scalar tail.
+__device__ __forceinline__ void zero_span(float* p, int n, int li, int gsz) {
+    if (n <= 0) return;
+    int head = int((16u - unsigned(reinterpret_cast<uintptr_t>(p) & 15u)) & 15u) >> 2;
+    head = head < n ? head : n;
+    if (li < head) p[li] = 0.0f;
+    float4* q = reinterpret_cast<float4*>(p + head);
+    const int n4 = (n - head) >> 2;
+    for (int i = li; i < n4; i += gsz) q[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int done = head + 4 * n4;
+    if (li < n - done) p[done + li] = 0.0f;
+}
+
+// Zero n floats of observation rows at base (one warp): TMA bulk stores from
+// the zeroed shared buffer for the 16-byte-aligned body (the lanes issue them
+// and, with wait, wait for their completion; else every lane of the warp must
+// call bulk_commit_and_wait later), plain stores for the unaligned head / tail.
+__device__ __forceinline__ void zero_obs_block(float* base, int64_t n, const float4* zero_sm, int lane,
+                                               bool wait = true) {
+    const uintptr_t b0 = reinterpret_cast<uintptr_t>(base);
+    const uintptr_t b1 = b0 + uintptr_t(n) * 4;
+    const uintptr_t a0 = (b0 + 15) & ~uintptr_t(15), a1 = b1 & ~uintptr_t(15);
+    if (a0 < a1) {
+        for (uintptr_t p = b0 + 4 * lane; p < a0; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
+        for (uintptr_t p = a1 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
+        // every lane issues its share of the chunks (one bulk group per lane)
+        asm volatile("fence.proxy.async.global;" ::: "memory");   // after earlier generic writes
+        for (uintptr_t p = a0 + uintptr_t(lane) * kZeroChunk; p < a1; p += 32 * uintptr_t(kZeroChunk)) {
+            const uintptr_t nb = a1 - p < uintptr_t(kZeroChunk) ? a1 - p : uintptr_t(kZeroChunk);
+            bulk_store(reinterpret_cast<void*>(p), zero_sm, uint32_t(nb));
+        }
+        if (wait) bulk_commit_and_wait();
+        else asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    } else {
+        for (uintptr_t p = b0 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
+    }
+}
+
+// Which phase-2 work units a scan warp takes: 2a units = ego pairs (egos 2u,
+// 2u + 1), 2b units = groups of `apw` agents.  Default: both kinds strided over
+// the warps (every warp one of each at 8 warps).  kSpec (7 scan warps beside
+// the physics warp): the 2b units go two per warp to the first warps, the 2a
+// units are split evenly over the rest -- measured costs ~7k / ~5k cycles per
+// unit, so 16 agents on 7 warps finish in max(2 x 7k, 3 x 5k) instead of the
+// 19k a strided 7-warp split would take.
+struct ScanSchedule {
+    int a_lo, a_hi, a_step;   // 2a units
+    int b_lo, b_hi, b_step;   // 2b units
+};
+
+template <bool kSpec>
+__device__ __forceinline__ ScanSchedule scan_schedule(int M, int apw, int warp, int nwarps) {
+    ScanSchedule r;
+    const int PA = (M + 1) / 2, PB = (M + apw - 1) / apw;
+    if (!kSpec) {
+        r.a_lo = warp; r.a_hi = PA; r.a_step = nwarps;
+        r.b_lo = warp; r.b_hi = PB; r.b_step = nwarps;
+        return r;
+    }
+    r.a_step = r.b_step = 1;
+    int nb = (PB + 1) / 2;
+    nb = nb < nwarps ? nb : nwarps;
+    const int na = nwarps - nb;
+    const int pb = (PB + nb - 1) / nb;
+    r.b_lo = warp < nb ? warp * pb : 0;
+    r.b_hi = warp < nb ? min(PB, r.b_lo + pb) : 0;
+    if (na > 0) {
+        const int pa = (PA + na - 1) / na;
+        r.a_lo = warp >= nb ? (warp - nb) * pa : 0;
+        r.a_hi = warp >= nb ? min(PA, r.a_lo + pa) : 0;
+    } else {
+        r.a_lo = 0;
+        r.a_hi = warp == 0 ? PA : 0;
+    }
+    return r;
+}
+
 // ----------------------------------------------------------------- the fused step kernel
-template <bool kStep, int kThreads, int kMinBlocks>
+template <bool kStep, int kThreads, int kMinBlocks, bool kSpec>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 world_step_kernel(const KArgs A) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -766,16 +930,24 @@ world_step_kernel(const KArgs A) {
     const int tid = threadIdx.x;
     const int lane = tid & 31;
     const int warp = tid >> 5;
-    const int nwarps = blockDim.x >> 5;
+    // kSpec: the last warp is the physics warp (pw); the scans run on the others
+    const int nwarps = (blockDim.x >> 5) - (kSpec ? 1 : 0);
+    const int pw = nwarps;
     const int M = A.d.M;
     const int WM = A.d.W * M;
     const int D = A.d.obs_dim;
     const DgConsts& k = A.k;
+    TT_DECL;
 
-    // ---- shared memory carve-up
+    // ---- shared memory carve-up: three agent tables (kSpec: tick t is read from
+    //      table t & 1 while the physics warp writes tick t + 1 into the other, and
+    //      table 2 takes tick t + 1 of agents teleported back to their start); the
+    //      rollout carry (st_next, flags_next, act) lives in table 0
     uint8_t* geo = smem;
-    AgentSm* ag = reinterpret_cast<AgentSm*>(smem + align16(A.d.max_scene_bytes));
-    ScanSm* sc = reinterpret_cast<ScanSm*>(ag + kMaxAgents);
+    AgentSm* const ag_home = reinterpret_cast<AgentSm*>(smem + align16(A.d.max_scene_bytes));
+    AgentSm* const ag_rst = ag_home + 2 * kMaxAgents;
+    AgentSm* ag = ag_home;
+    ScanSm* sc = reinterpret_cast<ScanSm*>(ag_home + 3 * kMaxAgents);
     uint64_t* bar = reinterpret_cast<uint64_t*>(sc + kMaxAgents);
     uint16_t* cand_sm = reinterpret_cast<uint16_t*>(bar + 2);   // [M][take_road]
     float4* zero_sm = reinterpret_cast<float4*>(
@@ -842,9 +1014,21 @@ world_step_kernel(const KArgs A) {
         S.sy = A.start_xy[2 * am + 1];
         S.start_yaw = A.start_yaw[am];
         S.valid = A.valid[am];
+        if constexpr (kSpec) {
+            for (int tb = 1; tb < 3; ++tb) {
+                AgentSm& S1 = ag_home[tb * kMaxAgents + m];
+                S1.r = S.r; S1.d = S.d; S1.len = S.len; S1.wid = S.wid; S1.f_len = S.f_len; S1.f_wid = S.f_wid;
+                S1.gx = S.gx; S1.gy = S.gy; S1.sx = S.sx; S1.sy = S.sy; S1.start_yaw = S.start_yaw;
+                S1.valid = S.valid;
+            }
+        }
     }
     SceneView G;
+    bool zero_early = false;   // kSpec physics warp: the next slot's clear is in flight
     for (int t = 0; t < T; ++t) {
+        if constexpr (kSpec) ag = ag_home + (t & 1) * kMaxAgents;
+        AgentSm* const agn = ag_home + ((t + 1) & 1) * kMaxAgents;   // kSpec: tick t + 1
+        (void)agn;
         const int slot = A.ring_slots > 0 ? (A.ring_start + t) % A.ring_slots : t;
         float* obs_w = A.obs + (int64_t(slot) * WM + int64_t(w) * M) * D;
         int32_t* ix_w = A.index_out ? A.index_out + (int64_t(slot) * WM + int64_t(w) * M) * A.index_stride
@@ -852,20 +1036,22 @@ world_step_kernel(const KArgs A) {
         const TickOut O = tick_out(A, slot);
         if (kStep && t > 0) {
             // every tick gets the same rejection as a separate step call (s_bad was
-            // reset at the end of the previous tick, before its closing barrier)
-            if (tid < 3 * M) {
+            // reset at the end of the previous tick, before its closing barrier;
+            // kSpec: the physics warp checked this tick's actions during the
+            // previous tick's scans, two barriers ago)
+            if (!kSpec && tid < 3 * M) {
                 const int64_t flat = t * act_tick + int64_t(w) * M * 3 + tid;
-                const double v = feedback ? ag[tid / 3].act[tid % 3]
+                const double v = feedback ? ag_home[tid / 3].act[tid % 3]
                                : A.actions_f64 ? reinterpret_cast<const double*>(A.actions)[flat]
                                                : double(reinterpret_cast<const float*>(A.actions)[flat]);
                 if (!finite(v)) atomicMin(&s_bad, int(flat));
             }
-            __syncthreads();
+            if (!kSpec) __syncthreads();
             if (s_bad != DG_NO_ERROR) {
                 // ticks 0..t-1 stand (as t separate step calls would leave them)
                 if (warp == 0 && lane < M) {
                     const int64_t am = int64_t(w) * M + lane;
-                    const AgentSm& S = ag[lane];
+                    const AgentSm& S = ag_home[lane];
 #pragma unroll
                     for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = S.st_next[f];
                     A.alive[am] = uint8_t(S.flags_next[0]);
@@ -880,94 +1066,27 @@ world_step_kernel(const KArgs A) {
                 return;
             }
         }
+        TT_ACC(0);
 
         PHASE_MARK(1);
-        // ---- phase 1: warp 0, lane m: agent m physics (SIMT across agents)
-        if (warp == 0 && lane < M) {
+        // ---- phase 1: warp 0, lane m: agent m physics (SIMT across agents).  kSpec:
+        //      only tick 0 -- later ticks were computed ahead by the physics warp
+        if ((!kSpec || t == 0) && warp == 0 && lane < M) {
             const int m = lane;
             const int64_t am = int64_t(w) * M + m;
             AgentSm& S = ag[m];
-            double x[DG_NUM_STATE];
-#pragma unroll
-            for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = S.st_next[f];
-            const int alive = S.flags_next[0];
-            S.reason = S.flags_next[1];
-            S.seen = S.flags_next[2];
-            S.spawn = S.flags_next[3];
-            S.px0 = x[SX];
-            S.py0 = x[SY];
-            if (alive && x[SX] != -12345.678) LANE0_MARK(25);  // after the state loads landed
-            if (kStep && alive) {
-                double raw0, raw1, raw2;
-                if (t > 0 && feedback) {
-                    raw0 = S.act[0]; raw1 = S.act[1]; raw2 = S.act[2];
-                } else {
-                    const int64_t ab = t * act_tick + am * 3;
-                    if (A.actions_f64) {
-                        const double* a = reinterpret_cast<const double*>(A.actions);
-                        raw0 = a[ab]; raw1 = a[ab + 1]; raw2 = a[ab + 2];
-                    } else {
-                        const float* a = reinterpret_cast<const float*>(A.actions);
-                        raw0 = a[ab]; raw1 = a[ab + 1]; raw2 = a[ab + 2];
-                    }
-                }
-                Act act;
-                act.thr = np_clip(raw0, 0.0, 1.0);
-                act.steer = np_clip(raw1, -1.0, 1.0);
-                act.brk = np_clip(raw2, 0.0, 1.0);
-                if (A.d.dynamic) {
-                    const double cap = A.mu_eff[w] * k.f_z;
-                    for (int i = 0; i < A.d.decimation; ++i) {
-                        substep_dynamic(x, act, cap, k);
-#ifdef DG_PHASE_TIMERS
-                        if (i < 4 && x[SX] != -12345.678) LANE0_MARK(28 + i);
-#endif
-                    }
-                } else {
-                    step_bicycle(x, act, k);
-                }
-            }
-            if (x[SX] != -12345.678) LANE0_MARK(26);          // after the substeps
-#pragma unroll
-            for (int f = 0; f < DG_NUM_STATE; ++f) S.st[f] = x[f];
-            double s_, c_;
-            sincos(x[SYAW], &s_, &c_);
-            S.c = c_;
-            S.s = s_;
-            S.vwx = x[SVX] * c_ - x[SVY] * s_;
-            S.vwy = x[SVX] * s_ + x[SVY] * c_;
-            S.f_spd = __double2float_rn(dg::ddiv(dg::dsqrt(x[SVX] * x[SVX] + x[SVY] * x[SVY]), k.speed_norm));
-            const double offs[3] = {-1.0, 0.0, 1.0};
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const double o = offs[i] * S.d;
-                S.hx[i] = x[SX] + o * c_;
-                S.hy[i] = x[SY] + o * s_;
-            }
-            S.alive = alive;
-            LANE0_MARK(27);
+            const AgentSm& H = ag_home[m];
+            S.reason = H.flags_next[1];
+            S.seen = H.flags_next[2];
+            S.spawn = H.flags_next[3];
+            double raw[3] = {0.0, 0.0, 0.0};
+            if (kStep && H.flags_next[0]) load_actions(A, t, am, t > 0 && feedback ? H.act : nullptr, raw);
+            agent_physics(A, w, S, H.st_next, H.flags_next[0], raw, kStep && H.flags_next[0]);
         }
         // the zero background of the world's obs block: TMA bulk stores from a
         // zeroed shared buffer, issued by one thread of a warp that is idle
         // during the physics; unaligned head/tail floats by plain stores
-        if (warp == (nwarps > 1 ? 1 : 0)) {
-            const uintptr_t b0 = reinterpret_cast<uintptr_t>(obs_w);
-            const uintptr_t b1 = b0 + uintptr_t(M) * D * 4;
-            const uintptr_t a0 = (b0 + 15) & ~uintptr_t(15), a1 = b1 & ~uintptr_t(15);
-            if (a0 < a1) {
-                for (uintptr_t p = b0 + 4 * lane; p < a0; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
-                for (uintptr_t p = a1 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
-                if (lane == 0) {
-                    for (uintptr_t p = a0; p < a1; p += kZeroChunk) {
-                        const uintptr_t n = a1 - p < uintptr_t(kZeroChunk) ? a1 - p : uintptr_t(kZeroChunk);
-                        bulk_store(reinterpret_cast<void*>(p), zero_sm, uint32_t(n));
-                    }
-                    bulk_commit_and_wait();
-                }
-            } else {
-                for (uintptr_t p = b0 + 4 * lane; p < b1; p += 128) *reinterpret_cast<float*>(p) = 0.0f;
-            }
-        }
+        if ((!kSpec || t == 0) && warp == (nwarps > 1 ? 1 : 0)) zero_obs_block(obs_w, int64_t(M) * D, zero_sm, lane);
 
         if (warp == 0) PHASE_MARK(2);
         __syncthreads();  // agent table + zero rows done, mbarrier init visible
@@ -999,19 +1118,71 @@ world_step_kernel(const KArgs A) {
         }
 
         PHASE_MARK(4);
+        TT_ACC(1);
+        TT_WSTART();
+        if (kSpec && warp == pw) {
+            // ---- the physics warp, concurrently with the scans of tick t: lanes m < 16
+            //      write the ego block of tick t (+ the fused policy's action for t + 1),
+            //      check tick t + 1's actions and run its physics from this tick's
+            //      post-physics state, assuming the tail leaves the agent alone (true
+            //      unless it finishes); lanes 16 + m run the same physics from agent m's
+            //      spawn state, the tick-(t + 1) state if the tail teleports it back
+            //      (autoreset).  finalize takes that, or re-derives a parked agent.
+            // the next tick's zero background: TMA bulk stores issued now, completed
+            // before the tick's closing barrier -- they stream out under the scans
+            // and the tail (a slot shared by consecutive ticks is cleared in the tail)
+            const int slot1 = A.ring_slots > 0 ? (A.ring_start + t + 1) % A.ring_slots : t + 1;
+            zero_early = t + 1 < T && slot1 != slot;
+            if (zero_early)
+                zero_obs_block(A.obs + (int64_t(slot1) * WM + int64_t(w) * M) * D, int64_t(M) * D, zero_sm, lane,
+                               false);
+            const int m = lane & 15;
+            const bool rst = lane >= 16;
+            AgentSm& S = ag[m < M ? m : 0];
+            AgentSm& H = ag_home[m < M ? m : 0];
+            const int64_t am = int64_t(w) * M + m;
+            if (!rst && m < M)
+                write_ego(obs_w + int64_t(m) * D, k, A, w, am, S.st[SX], S.st[SY], S.c, S.s, S.st[SVX], S.st[SVY],
+                          S.gx, S.gy, feedback ? H.act : nullptr);
+            TT_WACC(30);
+            __syncwarp();
+            if (kStep && t + 1 < T && m < M) {
+                double raw[3];
+                load_actions(A, t + 1, am, feedback ? H.act : nullptr, raw);
+                if (!rst) {
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        if (!finite(raw[j])) atomicMin(&s_bad, int((t + 1) * act_tick + am * 3 + j));
+                }
+                const bool go = !rst || (A.autoreset && S.valid);
+                double x0[DG_NUM_STATE];
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) x0[f] = rst ? ((f == SBF || f == SBR) ? 1.0 : 0.0) : S.st[f];
+                if (rst) {
+                    x0[SX] = S.sx;
+                    x0[SY] = S.sy;
+                    x0[SYAW] = S.start_yaw;
+                }
+                const int alive = rst ? 1 : S.alive;
+                if (go) agent_physics(A, w, rst ? ag_rst[m] : agn[m], x0, alive, raw, alive != 0);
+            }
+            TT_WACC(31);
+        } else {
         // ---- phase 2a: agent pairs.  kPL lanes per ego agent, each lane owns the other
         //      agents j = jl + kPL * u (u < 16 / kPL): 16 lanes x 1 at 8 warps per world,
         //      8 lanes x 2 at 4 warps (four egos per warp in one pass).  Stable distance
         //      rank, swept-circle TTC, neighbour rows, hull contact, optional DRAC.
         const int road0 = A.d.ego_dim;
         const int veh0 = A.d.ego_dim + 5 * A.d.k_road;
+        const ScanSchedule sched = scan_schedule<kSpec>(M, kThreads <= 128 ? 4 : 2, warp, nwarps);
         {
             constexpr int kPL = 16;                           // lanes per ego (8 measured slower at 4 warps)
             constexpr int kOPL = kMaxAgents / kPL;            // other agents per lane
             constexpr int kEPW = 32 / kPL;                    // egos per warp
             const int grp = lane / kPL, jl = lane % kPL;
             const unsigned gmask = ((1u << kPL) - 1u) << (kPL * grp);
-            for (int i = kEPW * warp + grp; i - grp < M; i += kEPW * nwarps) {
+            for (int u = sched.a_lo; u < sched.a_hi; u += sched.a_step) {
+                const int i = kEPW * u + grp;
                 const bool ego_ok = i < M;
                 const int ii = ego_ok ? i : 0;
                 const AgentSm& S = ag[ii];
@@ -1101,6 +1272,7 @@ world_step_kernel(const KArgs A) {
                     for (int o = kPL / 2; o > 0; o >>= 1) n_valid += __shfl_xor_sync(kFull, n_valid, o, kPL);
                     if (ego_ok && jl == 0) ix_w[int64_t(ii) * A.index_stride + 2] = n_valid;
                 }
+
                 if (kStep && A.drac_max) {
                     dr = warp_max_nn(dr, kPL);
                     if (ego_ok && jl == 0) {
@@ -1118,6 +1290,7 @@ world_step_kernel(const KArgs A) {
         }
 
         W1_MARK(34);
+        TT_WACC(20 + warp);
         // ---- phase 2b: each lane group scans the scene for one agent -- a warp takes
         //      kAPW consecutive agents (16 lanes x 2 at 8 warps per world, 8 lanes x 4 at
         //      4 warps), so the agents' dependent load / reduction chains overlap in one
@@ -1127,7 +1300,7 @@ world_step_kernel(const KArgs A) {
         constexpr int kGL = kThreads <= 128 ? 8 : 16;       // lanes per agent
         constexpr int kAPW = 32 / kGL;                      // agents per warp
         constexpr unsigned kGMask = (1u << kGL) - 1u;
-        for (int pr = warp; kAPW * pr < M; pr += nwarps) {
+        for (int pr = sched.b_lo; pr < sched.b_hi; pr += sched.b_step) {
             const int half = lane / kGL, hl = lane % kGL;
             const unsigned hshift = unsigned(kGL) * unsigned(half);
             const int m = kAPW * pr + half;
@@ -1312,15 +1485,18 @@ world_step_kernel(const KArgs A) {
                 }
             }
         }
+        TT_WACC(8 + warp);
+        }   // phase 2 (kSpec: the scan warps)
         WARP_MARK(0);
         __syncthreads();
         PHASE_MARK(5);
+        TT_ACC(2);
 
         // ---- phase 3: one lane per agent (SIMT across the world's agents):
         //      warp 0 -> rewards, events, termination, state for the next tick;
         //      warp 1 (or warp 0 afterwards) -> the ego block (+ fused policy)
         const int ego_warp = nwarps > 1 ? 1 : 0;
-        if (warp == ego_warp && lane < M) {
+        if (!kSpec && warp == ego_warp && lane < M) {
             AgentSm& S = ag[lane];
             write_ego(obs_w + int64_t(lane) * D, k, A, w, int64_t(w) * M + lane, S.st[SX], S.st[SY], S.c, S.s,
                       S.st[SVX], S.st[SVY], S.gx, S.gy, feedback ? S.act : nullptr);
@@ -1346,20 +1522,55 @@ world_step_kernel(const KArgs A) {
                 }
                 F.ttc_min = R.ttc_min; F.gap = R.gap;
                 F.edge_hit = R.edge_hit; F.touch = R.touch;
-                F.alive = S.alive; F.valid = S.valid; F.reason = S.reason; F.seen = S.seen; F.spawn = S.spawn;
+                AgentSm& H = ag_home[m];
+                F.alive = S.alive; F.valid = S.valid;
+                F.reason = kSpec ? H.flags_next[1] : S.reason;
+                F.seen = kSpec ? H.flags_next[2] : S.seen;
+                F.spawn = kSpec ? H.flags_next[3] : S.spawn;
                 F.start_yaw = S.start_yaw;
                 F.store_global = t + 1 == T;
-                F.st_out = S.st_next;
-                F.flags_out = S.flags_next;
+                F.st_out = H.st_next;
+                F.flags_out = H.flags_next;
                 const unsigned bits = finalize_agent(A, O, w, m, F, step_now + t, ox, oy);
                 count_events(A, w, bits, __activemask(), lane == 0, false);
+                if (kSpec && t + 1 < T && (bits & kBitFinished)) {
+                    // the tail moved the agent: teleported back to its start -> the
+                    // physics warp's spawn-state branch; parked / timed out -> dead,
+                    // no physics, the record re-derived from the post-tail state
+                    AgentSm& N1 = agn[m];
+                    if (H.flags_next[0]) {
+                        const AgentSm& R1 = ag_rst[m];
+#pragma unroll
+                        for (int f = 0; f < DG_NUM_STATE; ++f) N1.st[f] = R1.st[f];
+                        N1.px0 = R1.px0; N1.py0 = R1.py0; N1.c = R1.c; N1.s = R1.s;
+                        N1.vwx = R1.vwx; N1.vwy = R1.vwy; N1.f_spd = R1.f_spd;
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) { N1.hx[i] = R1.hx[i]; N1.hy[i] = R1.hy[i]; }
+                        N1.alive = 1;
+                    } else {
+                        const double none[3] = {0.0, 0.0, 0.0};
+                        agent_physics(A, w, N1, H.st_next, 0, none, false);
+                    }
+                }
+            }
+
+            if (kSpec && warp == pw && t + 1 < T) {
+                if (zero_early) {
+                    bulk_commit_and_wait();
+                } else {   // consecutive ticks share the slot: clear it after this tick's writes
+                    const int slot1 = A.ring_slots > 0 ? (A.ring_start + t + 1) % A.ring_slots : t + 1;
+                    zero_obs_block(A.obs + (int64_t(slot1) * WM + int64_t(w) * M) * D, int64_t(M) * D, zero_sm,
+                                   lane);
+                }
             }
             if (tid == 0) A.step_count[w] = step_now + t + 1;
             PHASE_MARK(6);
             GT_MARK(33);
+            TT_ACC(3);
         }
-        if (kStep && tid == 0) s_bad = DG_NO_ERROR;   // for the next tick's action check
+        if (!kSpec && kStep && tid == 0) s_bad = DG_NO_ERROR;   // for the next tick's action check
         if (t + 1 < T) __syncthreads();   // next tick reads st_next / act written above
+        TT_ACC(4);
     }
 }
 
@@ -1962,6 +2173,62 @@ __global__ void lane_follower_kernel(const float* obs, double* actions, int64_t 
 
 }  // namespace
 
+
+// ----------------------------------------------------------------- host delivery of observations
+// The numpy step path (engine.py:297-335 returns host arrays) moves the
+// observation to a mapped pinned host slab without carrying its zero tails
+// over PCIe: every row is [ego | road 5*k_road | vehicles 7*k_veh] and the
+// kernel writes road / vehicle slots prefix-compacted over a zero background,
+// so per block only the prefix up to the last non-zero float (bitwise: -0.0
+// and NaN count as non-zero) has to cross the link.  The slab keeps, per row,
+// the prefix lengths it currently holds (prev, device memory); a row whose
+// new prefix is shorter gets zeros over the difference, so the slab equals the
+// device rows bit for bit after every call.  One warp per row; stores to the
+// host are 32 consecutive floats per instruction.
+__device__ __forceinline__ int last_nonzero_prefix(const float* p, int n, int lane) {
+    int last = 0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        const bool nz = i < n && __float_as_uint(__ldg(p + i)) != 0u;
+        const unsigned b = __ballot_sync(kFull, nz);
+        if (b) last = i0 + 32 - __clz(b);
+    }
+    return last;
+}
+
+__device__ __forceinline__ void copy_to_host(const float* src, float* dst, int n, int lane) {
+    for (int i = lane; i < n; i += 32) dst[i] = __ldg(src + i);
+}
+
+__device__ __forceinline__ void zero_host(float* dst, int n, int lane) {
+    for (int i = lane; i < n; i += 32) dst[i] = 0.0f;
+}
+
+__global__ void __launch_bounds__(256) obs_to_host_kernel(const float* obs, float* host, int32_t* prev, int64_t rows,
+                                                          int D, int ego, int road_n, int veh_n,
+                                                          unsigned long long* bytes) {
+    const int lane = threadIdx.x & 31;
+    const int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const float* src = obs + r * D;
+    float* dst = host + r * D;
+    const int lr = last_nonzero_prefix(src + ego, road_n, lane);
+    const int lv = last_nonzero_prefix(src + ego + road_n, veh_n, lane);
+    const int pr = prev[2 * r], pv = prev[2 * r + 1];
+    copy_to_host(src, dst, ego + lr, lane);
+    if (pr > lr) zero_host(dst + ego + lr, pr - lr, lane);
+    copy_to_host(src + ego + road_n, dst + ego + road_n, lv, lane);
+    if (pv > lv) zero_host(dst + ego + road_n + lv, pv - lv, lane);
+    if (lane == 0) {
+        prev[2 * r] = lr;
+        prev[2 * r + 1] = lv;
+        if (bytes) {
+            const int n = ego + lr + (pr > lr ? pr - lr : 0) + lv + (pv > lv ? pv - lv : 0);
+            atomicAdd(bytes, 4ull * unsigned(n));
+        }
+    }
+}
+
 // =========================================================================== C ABI
 
 struct dg_engine {
@@ -1971,23 +2238,29 @@ struct dg_engine {
     int launches;
     int warps_per_world;   // fused: CTA = warps_per_world warps; split: agents (warps) per CTA
     int min_blocks;        // register budget: resident CTAs per SM the variant is built for
-    int mode;              // 0 = fused world kernel, 1 = split physics + per-agent kernels (PDL)
+    int mode;              // 0 = fused world kernel, 1 = split physics + per-agent kernels (PDL),
+                           // 2 = fused with a physics warp running one tick ahead (kSpec)
     size_t smem_split;     // dynamic smem of the per-agent kernel
 };
 
 #define DG_VARIANTS(X)                                                                 \
-    X(512, 1) X(512, 2) X(256, 2) X(256, 3) X(256, 4) X(128, 4) X(128, 6) X(128, 8)
+    X(512, 1, false) X(512, 2, false) X(256, 2, false) X(256, 3, false) X(256, 4, false)  \
+    X(128, 4, false) X(128, 6, false) X(128, 8, false) X(256, 2, true)
 
 // Kernel variants: (threads per CTA, min resident CTAs per SM) bounds trade
-// registers for occupancy; dg_tune picks one.
+// registers for occupancy; dg_tune picks one.  The kSpec variant is up to 7
+// scan warps plus the physics warp (256 threads: 128 registers at 2 CTAs/SM).
+static int variant_threads(int nw, bool spec) { return spec ? 256 : (nw > 8 ? 512 : (nw > 4 ? 256 : 128)); }
+
 template <bool kStep>
 static cudaError_t launch_world_step(const dg_engine* e, const KArgs& A, cudaStream_t st) {
     const int nw = e->warps_per_world;
-    const int threads = nw > 8 ? 512 : (nw > 4 ? 256 : 128);
+    const bool spec = e->mode == 2;
+    const int threads = variant_threads(nw, spec);
     const dim3 grid(A.d.W);
-#define DG_LAUNCH(T, B)                                                                  \
-    if (threads == T && e->min_blocks == B) {                                            \
-        world_step_kernel<kStep, T, B><<<grid, 32 * nw, e->smem_bytes, st>>>(A);         \
+#define DG_LAUNCH(T, B, S)                                                               \
+    if (threads == T && e->min_blocks == B && spec == S) {                               \
+        world_step_kernel<kStep, T, B, S><<<grid, 32 * (nw + (S ? 1 : 0)), e->smem_bytes, st>>>(A); \
         return cudaGetLastError();                                                       \
     }
     DG_VARIANTS(DG_LAUNCH)
@@ -2013,15 +2286,15 @@ static cudaError_t raise_smem_limit(K kernel) {
 template <bool kStep>
 static cudaError_t set_smem_attr(size_t) {
     cudaError_t e = cudaSuccess;
-#define DG_ATTR(T, B)                                                                    \
-    if (e == cudaSuccess) e = raise_smem_limit(world_step_kernel<kStep, T, B>);
+#define DG_ATTR(T, B, S)                                                                 \
+    if (e == cudaSuccess) e = raise_smem_limit(world_step_kernel<kStep, T, B, S>);
     DG_VARIANTS(DG_ATTR)
 #undef DG_ATTR
     return e;
 }
 
-static bool has_variant(int threads, int blocks) {
-#define DG_HAS(T, B) if (threads == T && blocks == B) return true;
+static bool has_variant(int threads, int blocks, bool spec) {
+#define DG_HAS(T, B, S) if (threads == T && blocks == B && spec == S) return true;
     DG_VARIANTS(DG_HAS)
 #undef DG_HAS
     return false;
@@ -2074,7 +2347,7 @@ static cudaError_t launch_split(const dg_engine* e, const KArgs& A, cudaStream_t
 
 template <bool kStep>
 static cudaError_t launch_step_any(const dg_engine* e, const KArgs& A, cudaStream_t st) {
-    return e->mode == 1 ? launch_split<kStep>(e, A, st) : launch_world_step<kStep>(e, A, st);
+    return e->mode == 1 ? launch_split<kStep>(e, A, st) : launch_world_step<kStep>(e, A, st);   // 0, 2: fused
 }
 
 static thread_local char g_err[512] = "";
@@ -2097,7 +2370,7 @@ static size_t split_smem_bytes(int take_road, int apc) {
 
 static size_t step_smem_bytes(const DgDims& d, int take_road) {
     size_t b = size_t(align16(d.max_scene_bytes));
-    b += sizeof(AgentSm) * kMaxAgents + sizeof(ScanSm) * kMaxAgents;
+    b += sizeof(AgentSm) * 3 * kMaxAgents + sizeof(ScanSm) * kMaxAgents;   // three agent tables
     b += 16;  // mbarrier
     b += sizeof(uint16_t) * kMaxAgents * size_t(take_road > 0 ? take_road : 1);
     b = size_t(align16(int64_t(b))) + kZeroChunk;
@@ -2359,7 +2632,64 @@ int dg_set_state(dg_engine* eng, const double* src, void* stream) {
     return e == cudaSuccess ? DG_OK : cuda_fail(e, "dg_set_state");
 }
 
+
+int dg_host_alloc(size_t bytes, void** host_ptr) {
+    if (!host_ptr) return fail(DG_EINVAL, "dg_host_alloc: null output pointer");
+    void* p = nullptr;
+    cudaError_t e = cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) return cuda_fail(e, "dg_host_alloc");
+    std::memset(p, 0, bytes);
+    *host_ptr = p;
+    return DG_OK;
+}
+
+int dg_host_free(void* host_ptr) {
+    if (!host_ptr) return DG_OK;
+    const cudaError_t e = cudaFreeHost(host_ptr);
+    return e == cudaSuccess ? DG_OK : cuda_fail(e, "dg_host_free");
+}
+
+int dg_to_host(dg_engine* eng, const float* obs, float* host_obs, int32_t* prev_len, const void* aux,
+               void* host_aux, size_t aux_bytes, unsigned long long* bytes, void* stream) {
+    if (!eng || !obs || !host_obs || !prev_len) return fail(DG_EINVAL, "dg_to_host: null argument");
+    if (aux_bytes && (!aux || !host_aux)) return fail(DG_EINVAL, "dg_to_host: null aux buffer");
+    const DgDims& d = eng->base.d;
+    void* dptr = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&dptr, host_obs, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "dg_to_host: host slab is not mapped pinned memory");
+    const int64_t rows = int64_t(d.W) * d.M;
+    const int per_cta = 8;
+    const int64_t grid = (rows + per_cta - 1) / per_cta;
+    if (grid > 0)
+        obs_to_host_kernel<<<unsigned(grid), 32 * per_cta, 0, static_cast<cudaStream_t>(stream)>>>(
+            obs, static_cast<float*>(dptr), prev_len, rows, d.obs_dim, d.ego_dim, 5 * d.k_road, 7 * d.k_vehicles,
+            bytes);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "dg_to_host");
+    if (aux_bytes) {
+        e = cudaMemcpyAsync(host_aux, aux, aux_bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream));
+        if (e != cudaSuccess) return cuda_fail(e, "dg_to_host: aux copy");
+    }
+    return DG_OK;
+}
+
 int dg_launch_count(dg_engine* eng) { return eng ? eng->launches : 0; }
+
+#ifdef DG_TICK_TIMERS
+int dg_debug_tick_clocks(long long* host_out, int n_blocks, int reset) {
+    const int n = n_blocks < 65536 ? n_blocks : 65536;
+    cudaError_t e;
+    if (reset) {
+        static long long zeros[65536 * 40 / 64];
+        e = cudaSuccess;
+        for (int i = 0; i < 64 && e == cudaSuccess; ++i)
+            e = cudaMemcpyToSymbol(g_tick_acc, zeros, sizeof(zeros), sizeof(zeros) * i);
+    } else {
+        e = cudaMemcpyFromSymbol(host_out, g_tick_acc, sizeof(long long) * 40 * n);
+    }
+    return e == cudaSuccess ? DG_OK : cuda_fail(e, "dg_debug_tick_clocks");
+}
+#endif
 
 #ifdef DG_PHASE_TIMERS
 int dg_debug_phase_clocks(long long* host_out, int n_blocks) {
@@ -2382,18 +2712,21 @@ int dg_tune(dg_engine* eng, int32_t mode, int32_t warps_per_world, int32_t ctas_
         eng->min_blocks = blocks;
         return DG_OK;
     }
-    if (mode != 0) return fail(DG_EINVAL, "dg_tune: mode must be 0 (fused) or 1 (split)");
+    if (mode != 0 && mode != 2)
+        return fail(DG_EINVAL, "dg_tune: mode must be 0 (fused), 1 (split) or 2 (fused, physics warp)");
     if (eng->base.d.geometry_global)
         return fail(DG_ENOSUPPORT, "dg_tune: geometry_global engines run the split kernels (mode 1)");
     if (warps_per_world < 1 || warps_per_world > kMaxAgents)
         return fail(DG_EINVAL, "dg_tune: warps_per_world must lie in [1, 16]");
     const int nw = warps_per_world < eng->base.d.M ? warps_per_world : eng->base.d.M;
-    const int threads = nw > 8 ? 512 : (nw > 4 ? 256 : 128);
-    int blocks = ctas_per_sm > 0 ? ctas_per_sm : (threads == 512 ? 1 : threads == 256 ? 2 : 4);
-    if (!has_variant(threads, blocks)) return fail(DG_EINVAL, "dg_tune: no kernel variant for this shape");
+    const bool spec = mode == 2;
+    if (spec && nw > 7) return fail(DG_EINVAL, "dg_tune: mode 2 takes at most 7 scan warps");
+    const int threads = variant_threads(nw, spec);
+    int blocks = ctas_per_sm > 0 ? ctas_per_sm : (threads == 512 ? 1 : threads >= 256 ? 2 : 4);
+    if (!has_variant(threads, blocks, spec)) return fail(DG_EINVAL, "dg_tune: no kernel variant for this shape");
     eng->warps_per_world = nw;
     eng->min_blocks = blocks;
-    eng->mode = 0;
+    eng->mode = mode;
     return DG_OK;
 }
 

@@ -190,6 +190,57 @@ class HostSlabPool:
         return len(self._slabs)
 
 
+class MappedSlabPool:
+    """Mapped pinned host slabs (dg_host_alloc) the numpy step path hands out:
+    the device writes the observation rows straight into the slab, only the
+    non-zero prefix of each row's road / vehicle blocks crossing PCIe
+    (dg_to_host), then DMAs the packed per-tick outputs behind them.  Each
+    slab carries the per-row prefix lengths it holds (device int32 [rows][2])
+    so a later step zeroes exactly what went stale.  Recycled like
+    HostSlabPool; past ``max_slabs`` live slabs ``acquire`` returns None and
+    the caller falls back to a full copy."""
+
+    def __init__(self, lib, nbytes: int, rows: int, device, max_slabs: int = 8):
+        self._lib = lib
+        self.nbytes = int(nbytes)
+        self.rows = int(rows)
+        self.device = device
+        self.max_slabs = int(max_slabs)
+        self._slabs = []          # [host pointer, prev_len tensor, weakref to the current lease or None]
+
+    def acquire(self):
+        """(host pointer, prev_len device tensor, numpy uint8 view) or None."""
+        slot = next((s for s in self._slabs if s[2] is None or s[2]() is None), None)
+        if slot is None:
+            if len(self._slabs) >= self.max_slabs:
+                return None
+            p = ct.c_void_p()
+            N.check(self._lib, self._lib.dg_host_alloc(self.nbytes, ct.byref(p)), "dg_host_alloc")
+            slot = [p.value, torch.zeros((self.rows, 2), dtype=torch.int32, device=self.device), None]
+            self._slabs.append(slot)
+        lease = _Lease()
+        lease.__array_interface__ = {"data": (slot[0], False), "shape": (self.nbytes,), "typestr": "|u1",
+                                     "version": 3}
+        slot[2] = weakref.ref(lease)
+        return slot[0], slot[1], np.asarray(lease)
+
+    @property
+    def slabs(self) -> int:
+        return len(self._slabs)
+
+    def release_all(self):
+        """Free every slab (outstanding arrays of them become invalid)."""
+        for ptr, _, _ in self._slabs:
+            self._lib.dg_host_free(ct.c_void_p(ptr))
+        self._slabs = []
+
+    def __del__(self):
+        try:
+            self.release_all()
+        except Exception:  # interpreter teardown
+            pass
+
+
 class StepOutput:
     """Result of one control tick (engine.py:70-76).  ``events`` and ``info``
     are built lazily from the packed output buffers."""
@@ -255,7 +306,7 @@ class Engine:
                  obs_config: ObsConfig | None = None, reward_config: RewardConfig | None = None,
                  params: VehicleParams | None = None, bicycle: BicycleParams | None = None,
                  device=None, spatial_index: bool = True, warps_per_world: int | None = None,
-                 launch_mode: int = 0, geometry_global: bool | None = None):
+                 launch_mode: int | None = None, geometry_global: bool | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("drivegrid-b200 Engine needs a CUDA device (no CPU fallback)")
         self._lib = N.load_library()
@@ -351,14 +402,16 @@ class Engine:
         elif launch_mode == 1:
             self.tune(warps_per_world or 4, 0, mode=1)
         elif warps_per_world:
-            self.tune(warps_per_world)
+            self.tune(warps_per_world, 0, mode=launch_mode or 0)
         elif W > 2 * torch.cuda.get_device_properties(self.device).multi_processor_count:
             # more worlds than 8-warp CTAs fit at once (2 per SM): 4 warps/world,
             # 4 CTAs/SM (measured on B200: 512 worlds 270 -> 307 M CASPS, 1024: 280 -> 317)
             self.tune(min(M, 4), 4 if M > 4 else 0)
         else:
-            # every world resident as an 8-warp CTA (2 per SM): latency-bound regime
-            self.tune(min(M, 8))
+            # every world resident as an 8-warp CTA (2 per SM): latency-bound regime;
+            # mode 2: 7 scan warps + a warp running the next tick's physics meanwhile
+            mode = 2 if launch_mode is None else launch_mode
+            self.tune(min(M, 7 if mode == 2 else 8), 0, mode=mode)
         self._step_count = 0
         self.phase_seconds = {k: 0.0 for k in PHASES}
         self._act_dev = torch.empty((W, M, 3), dtype=torch.float64, device=dev)
@@ -372,6 +425,8 @@ class Engine:
         aux_dev = self._host_blob[self._host_obs_bytes:]
         self._host_bufs = StepBuffers(self._obs_dev, aux_dev, self._views(aux_dev))
         self._host_pool = HostSlabPool(self._host_blob.numel())
+        self._mapped_pool = MappedSlabPool(self._lib, self._host_blob.numel(), W * M, dev)
+        self.d2h_bytes = torch.zeros(1, dtype=torch.int64, device=dev)   # obs bytes written by dg_to_host
         self.launches = 0
         self._metrics_on = False
         self._host_lay = None
@@ -460,11 +515,12 @@ class Engine:
     def tune(self, warps_per_world: int, ctas_per_sm: int = 0, mode: int = 0) -> None:
         """Launch shape knob; results are unaffected.  mode 0: fused world
         kernel with ``warps_per_world`` warps; mode 1: split physics + per-agent
-        kernels with ``warps_per_world`` agents per CTA.  ``ctas_per_sm`` picks
+        kernels with ``warps_per_world`` agents per CTA; mode 2: fused with one
+        more warp that computes tick t + 1's physics while the others scan tick t.  ``ctas_per_sm`` picks
         the register budget of the kernel variant (0 = default)."""
         N.check(self._lib, self._lib.dg_tune(self._h, int(mode), int(warps_per_world), int(ctas_per_sm)),
                 "dg_tune")
-        self._shape = {"mode": "split" if mode else "fused", "warps": int(warps_per_world),
+        self._shape = {"mode": ("fused", "split", "fused+physics-warp")[int(mode)], "warps": int(warps_per_world),
                        "ctas_per_sm": int(ctas_per_sm)}
 
     # ------------------------------------------------------------------ device state views
@@ -853,8 +909,20 @@ class Engine:
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), ct.c_void_p(stream.cuda_stream)), "dg_step")
         self._step_count += 1
         self.launches += 1
-        host, hb = self._host_pool.acquire()
-        host.copy_(self._host_blob, non_blocking=True)          # obs + every per-tick output, one copy
+        slab = self._mapped_pool.acquire()
+        if slab is not None:
+            # obs rows written into the mapped slab by the device (non-zero prefixes
+            # only), the packed per-tick outputs DMA'd behind them
+            ptr, prev, hb = slab
+            ob = self._host_obs_bytes
+            N.check(self._lib, self._lib.dg_to_host(
+                self._h, _ptr(self._obs_dev), ct.c_void_p(ptr), _ptr(prev), _ptr(self._host_bufs.aux),
+                ct.c_void_p(ptr + ob), self._host_blob.numel() - ob, _ptr(self.d2h_bytes),
+                ct.c_void_p(stream.cuda_stream)), "dg_to_host")
+            self.launches += 1
+        else:
+            host, hb = self._host_pool.acquire()
+            host.copy_(self._host_blob, non_blocking=True)          # obs + every per-tick output, one copy
         stream.synchronize()
         t2 = time.perf_counter()
         obs = hb[:self.W * self.M * self.obs_config.obs_dim * 4].view(np.float32).reshape(bufs.obs.shape)

@@ -78,9 +78,9 @@ def compare_tick(dev: Dev, t, views: dict, slot: int, obs: np.ndarray, ix: np.nd
     dev.f("obs", obs, o.obs, rtol=OBS_RTOL, atol=OBS_ATOL)
 
 
-def run_philox(device, W, M, ticks, shape=None):
+def run_philox(device, W, M, ticks, shape=None, launch_mode=None):
     inp = headline_inputs(W, M)
-    gpu = Engine(**inp.as_kwargs(), device=device)
+    gpu = Engine(**inp.as_kwargs(), device=device, launch_mode=launch_mode)
     if shape is not None:
         assert gpu.launch_shape() == shape
     ora = OracleEngine(**inp.as_kwargs(), num_workers=16)
@@ -102,12 +102,14 @@ def run_philox(device, W, M, ticks, shape=None):
     return dev, ora
 
 
-def run_bench_path(device, W, M, launches, R=64, ring=None, shape=None):
+def run_bench_path(device, W, M, launches, R=64, ring=None, shape=None, launch_mode=None, inp=None,
+                   autoreset=True):
     """bench.py's timed loop (persistent R-tick launches, fused LaneFollower +
     autoreset, ring_start = tick % ring) against the oracle driven the same
     way on its own observations."""
-    inp = headline_inputs(W, M)
-    gpu = Engine(**inp.as_kwargs(), device=device)
+    inp = inp if inp is not None else headline_inputs(W, M)
+    W, M = inp.sim.num_envs, inp.sim.num_agents
+    gpu = Engine(**inp.as_kwargs(), device=device, launch_mode=launch_mode)
     if shape is not None:
         assert gpu.launch_shape() == shape
     ora = OracleEngine(**inp.as_kwargs(), num_workers=16)
@@ -124,13 +126,14 @@ def run_bench_path(device, W, M, launches, R=64, ring=None, shape=None):
     dev, tick, resets, act_mismatch = Dev(), 0, 0, 0
     for _ in range(launches):
         start = tick % ring
-        gpu.launch_step(acts, rb, autoreset=True, next_actions=acts, ticks=R, ring_start=start, index_out=ix)
+        gpu.launch_step(acts, rb, autoreset=autoreset, next_actions=acts, ticks=R, ring_start=start, index_out=ix)
         torch.cuda.synchronize()
         obs_ring = rb.obs  # [ring][W][M][D]
         for t in range(R):
             a = pol(obs)
             o = ora.step(a)
-            ora.teleport_reset(o.dones)
+            if autoreset:
+                ora.teleport_reset(o.dones)
             resets += int(o.dones.sum())
             slot = (start + t) % ring
             compare_tick(dev, tick + t + 1, rb.views, slot, obs_ring[slot].cpu().numpy(),
@@ -150,16 +153,35 @@ def run_bench_path(device, W, M, launches, R=64, ring=None, shape=None):
     return dev, resets
 
 
-def test_headline_philox_stream_200_ticks(device):
-    dev, ora = run_philox(device, 256, 16, 200, shape={"mode": "fused", "warps": 8, "ctas_per_sm": 0})
+HEADLINE_SHAPES = {2: {"mode": "fused+physics-warp", "warps": 7, "ctas_per_sm": 0},
+                   0: {"mode": "fused", "warps": 8, "ctas_per_sm": 0}}
+
+
+@pytest.mark.parametrize("mode", [2, 0])
+def test_headline_philox_stream_200_ticks(mode, device):
+    dev, ora = run_philox(device, 256, 16, 200, shape=HEADLINE_SHAPES[mode], launch_mode=mode)
     print("\n[256x16 philox, 200 ticks] max |gpu - oracle|:", {k: f"{v:.2e}" for k, v in sorted(dev.max.items())})
 
 
-def test_headline_bench_path_256_ticks(device):
-    dev, resets = run_bench_path(device, 256, 16, launches=4, shape={"mode": "fused", "warps": 8, "ctas_per_sm": 0})
+@pytest.mark.parametrize("mode", [2, 0])
+def test_headline_bench_path_256_ticks(mode, device):
+    dev, resets = run_bench_path(device, 256, 16, launches=4, shape=HEADLINE_SHAPES[mode], launch_mode=mode)
     assert resets > 0                        # the autoreset path ran
     print(f"\n[256x16 bench path, 4 x 64 ticks, {resets} resets] max |gpu - oracle|:",
           {k: f"{v:.2e}" for k, v in sorted(dev.max.items())})
+
+
+@pytest.mark.parametrize("mode", [2, 0])
+def test_timeout_and_park_in_persistent_launch(mode, device):
+    """No autoreset, episode_len 25 (the traj_timeout fixture's config): in
+    one 40-tick launch agents collide / leave the lane and are parked, the
+    survivors time out at tick 25 and stay dead -- the physics warp's
+    next-tick guess is wrong for every one of them and must be redone."""
+    from cases import case_inputs
+    inp = case_inputs("traj_timeout").inputs
+    dev, finished = run_bench_path(device, 0, 0, launches=1, R=40, ring=40, launch_mode=mode, inp=inp,
+                                   autoreset=False)
+    assert finished > 0
 
 
 def test_c4_variant_philox_64_ticks(device):

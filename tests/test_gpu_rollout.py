@@ -50,7 +50,7 @@ def assert_slot_equals_step(rb, slot, sb):
 
 
 @pytest.mark.parametrize("autoreset", [False, True])
-@pytest.mark.parametrize("shape", [None, (4, 4), (16, 1), (4, 0, 1)])
+@pytest.mark.parametrize("shape", [None, (4, 4), (16, 1), (4, 0, 1), (8, 0, 0), (7, 0, 2), (3, 0, 2), (1, 0, 2)])
 def test_replayed_rollout_equals_steps(autoreset, shape, device):
     W, M, T = 8, 16, 48
     inp = C.build_inputs(cfg_of(W, M, seed=31))
@@ -116,7 +116,8 @@ def test_ring_slots_wrap(device):
     assert_same_engine(a, b)
 
 
-@pytest.mark.parametrize("name", ["traj_c1", "traj_events", "traj_wet", "traj_bicycle"])
+@pytest.mark.parametrize("name", ["traj_c1", "traj_events", "traj_wet", "traj_bicycle", "traj_sparse",
+                                  "traj_events_inv"])
 def test_rollout_matches_oracle(name, device):
     case = case_inputs(name)
     gpu = Engine(**case.inputs.as_kwargs(), device=device)
