@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 9
+#define DG_ABI_VERSION 10
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -178,6 +178,11 @@ typedef struct DgStepIO {
                                    [3+take_veh ..)    road slot -> segment index
                                        (stable argsort of ~cand), first n_r;
                                    entries past n_v / n_r are left untouched    */
+    int16_t* prefix_out;        /* [W][M][2] per tick slot, or NULL: the length in
+                                   floats of the part of each agent's road block
+                                   (5 n_r) and vehicle block (7 n_v) that can be
+                                   non-zero -- the rest of the row is zero
+                                   (dg_to_host moves only these prefixes)      */
 } DgStepIO;
 
 typedef struct dg_engine dg_engine;
@@ -256,7 +261,9 @@ int dg_sysid_rollout(const void* consts, const double* mu, const int32_t* tick_s
  * dg_to_host writes the engine's device observation `obs` [W][M][D] into
  * such a slab `host_obs` (same layout) so that the slab equals it bit for
  * bit, moving only the non-zero prefix of every row's road and vehicle blocks
- * over PCIe; `prev_len` (device int32 [W*M][2], zero for a fresh slab) holds
+ * over PCIe -- the lengths come from `prefix` (the step's DgStepIO.prefix_out)
+ * or, when it is NULL, from a scan for the last non-zero float (bitwise);
+ * `prev_len` (device int32 [W*M][2], zero for a fresh slab) holds
  * the prefix lengths the slab currently carries and is updated.  Then
  * `aux_bytes` of the packed per-tick outputs `aux` (device) are copied to
  * `host_aux` (pinned).  `bytes` (device u64, optional) accumulates the
@@ -264,8 +271,8 @@ int dg_sysid_rollout(const void* consts, const double* mu, const int32_t* tick_s
  * after the stream synchronises. */
 int dg_host_alloc(size_t bytes, void** host_ptr);
 int dg_host_free(void* host_ptr);
-int dg_to_host(dg_engine* eng, const float* obs, float* host_obs, int32_t* prev_len, const void* aux,
-               void* host_aux, size_t aux_bytes, unsigned long long* bytes, void* stream);
+int dg_to_host(dg_engine* eng, const float* obs, const int16_t* prefix, float* host_obs, int32_t* prev_len,
+               const void* aux, void* host_aux, size_t aux_bytes, unsigned long long* bytes, void* stream);
 
 /* Kernel launches issued by the last dg_step/dg_observe/dg_reset call. */
 int dg_launch_count(dg_engine* eng);

@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 
 class DgDims(ct.Structure):
@@ -85,7 +85,8 @@ class DgStepIO(ct.Structure):
                                               ("event_counts", _P),
                                               ("ticks", ct.c_int32), ("ring_slots", ct.c_int32),
                                               ("ring_start", ct.c_int32), ("pad_", ct.c_int32),
-                                              ("drac_max", _P), ("metric_seen", _P), ("index_out", _P)]
+                                              ("drac_max", _P), ("metric_seen", _P), ("index_out", _P),
+                                              ("prefix_out", _P)]
 
 
 # exported symbol -> (restype, argtypes)
@@ -115,7 +116,7 @@ SIGNATURES = {
     "dg_pairwise_drac": (ct.c_int, [_P] * 8 + [ct.c_int32, ct.c_int32, ct.c_int32, _P, ct.c_int32, ct.c_int32, _P]),
     "dg_host_alloc": (ct.c_int, [ct.c_size_t, ct.POINTER(_P)]),
     "dg_host_free": (ct.c_int, [_P]),
-    "dg_to_host": (ct.c_int, [_P, _P, _P, _P, _P, _P, ct.c_size_t, _P, _P]),
+    "dg_to_host": (ct.c_int, [_P, _P, _P, _P, _P, _P, _P, ct.c_size_t, _P, _P]),
 }
 
 

@@ -98,6 +98,7 @@ struct KArgs {
     uint8_t* metric_seen; // [W][M] |= goal (bit 0) / collision (bit 1) events (NULL = off)
     int32_t* index_out;   // [slot][W][M][index_stride] integer decisions (NULL = off)
     int32_t index_stride; // 3 + take_veh + take_road
+    int16_t* prefix_out;  // [slot][W][M][2] non-zero obs prefix: 5 n_r, 7 n_v floats (NULL = off)
 };
 
 // ----------------------------------------------------------------- numpy-semantics helpers
@@ -1133,9 +1134,13 @@ world_step_kernel(const KArgs A) {
             // and the tail (a slot shared by consecutive ticks is cleared in the tail)
             const int slot1 = A.ring_slots > 0 ? (A.ring_start + t + 1) % A.ring_slots : t + 1;
             zero_early = t + 1 < T && slot1 != slot;
+#ifdef DG_EXP_NOZERO
+            zero_early = false;
+#endif
             if (zero_early)
                 zero_obs_block(A.obs + (int64_t(slot1) * WM + int64_t(w) * M) * D, int64_t(M) * D, zero_sm, lane,
                                false);
+            TT_WACC(29);
             const int m = lane & 15;
             const bool rst = lane >= 16;
             AgentSm& S = ag[m < M ? m : 0];
@@ -1268,9 +1273,11 @@ world_step_kernel(const KArgs A) {
                 }
                 ttc = warp_min(ttc, kPL);
                 touch = (__ballot_sync(kFull, touch) & gmask) != 0;
-                if (ix_w) {
+                if (ix_w || A.prefix_out) {
                     for (int o = kPL / 2; o > 0; o >>= 1) n_valid += __shfl_xor_sync(kFull, n_valid, o, kPL);
-                    if (ego_ok && jl == 0) ix_w[int64_t(ii) * A.index_stride + 2] = n_valid;
+                    if (ix_w && ego_ok && jl == 0) ix_w[int64_t(ii) * A.index_stride + 2] = n_valid;
+                    if (A.prefix_out && ego_ok && jl == 0)
+                        A.prefix_out[(int64_t(slot) * WM + int64_t(w) * M + ii) * 2 + 1] = int16_t(7 * n_valid);
                 }
 
                 if (kStep && A.drac_max) {
@@ -1388,6 +1395,8 @@ world_step_kernel(const KArgs A) {
             int32_t* ix_m = ix_w ? ix_w + int64_t(act ? m : kAPW * pr) * A.index_stride : nullptr;
             if (act) {
                 if (ix_m && hl == 0) ix_m[1] = ncand;
+                if (A.prefix_out && hl == 0)
+                    A.prefix_out[(int64_t(slot) * WM + int64_t(w) * M + m) * 2] = int16_t(5 * ncand);
                 for (int slot = hl; slot < ncand; slot += kGL) {
                     const int q = cand[slot];
                     if (ix_m) ix_m[3 + A.take_veh + slot] = q;
@@ -1531,9 +1540,16 @@ world_step_kernel(const KArgs A) {
                 F.store_global = t + 1 == T;
                 F.st_out = H.st_next;
                 F.flags_out = H.flags_next;
+                TT_ACC(5);
                 const unsigned bits = finalize_agent(A, O, w, m, F, step_now + t, ox, oy);
+                TT_ACC(6);
                 count_events(A, w, bits, __activemask(), lane == 0, false);
+                TT_ACC(7);
+#ifdef DG_EXP_NOFIX
+                if (false) {
+#else
                 if (kSpec && t + 1 < T && (bits & kBitFinished)) {
+#endif
                     // the tail moved the agent: teleported back to its start -> the
                     // physics warp's spawn-state branch; parked / timed out -> dead,
                     // no physics, the record re-derived from the post-tail state
@@ -1558,9 +1574,11 @@ world_step_kernel(const KArgs A) {
                 if (zero_early) {
                     bulk_commit_and_wait();
                 } else {   // consecutive ticks share the slot: clear it after this tick's writes
+#ifndef DG_EXP_NOZERO
                     const int slot1 = A.ring_slots > 0 ? (A.ring_start + t + 1) % A.ring_slots : t + 1;
                     zero_obs_block(A.obs + (int64_t(slot1) * WM + int64_t(w) * M) * D, int64_t(M) * D, zero_sm,
                                    lane);
+#endif
                 }
             }
             if (tid == 0) A.step_count[w] = step_now + t + 1;
@@ -1780,6 +1798,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
     const int veh0 = A.d.ego_dim + 5 * A.d.k_road;
     const bool rewards_needed = kStep && S.alive;
     int32_t* ix_m = A.index_out ? A.index_out + (int64_t(slot) * WM + am) * A.index_stride : nullptr;
+    int16_t* px_m = A.prefix_out ? A.prefix_out + (int64_t(slot) * WM + am) * 2 : nullptr;
 
     // (1) neighbours: lane j <-> agent j (16 lanes), stable distance rank,
     //     swept TTC, neighbour row, hull contact
@@ -1801,10 +1820,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
             rank += (kt < key) || (kt == key && t < j);
         }
         const bool nvalid = j < M && finite(key) && rank < A.take_veh;
-        if (ix_m) {
-            if (nvalid) ix_m[3 + rank] = j;
+        if (ix_m || px_m) {
+            if (ix_m && nvalid) ix_m[3 + rank] = j;
             const int nv = __popc(__ballot_sync(kFull, nvalid));
-            if (lane == 0) ix_m[2] = nv;
+            if (ix_m && lane == 0) ix_m[2] = nv;
+            if (px_m && lane == 0) px_m[1] = int16_t(7 * nv);
         }
         double ttc = k.ttc_max;
         if (nvalid) {
@@ -1912,6 +1932,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) agent_obs_kernel(const K
     const int ncand = count < A.take_road ? count : A.take_road;
     __syncwarp();
     if (ix_m && lane == 0) ix_m[1] = ncand;
+    if (px_m && lane == 0) px_m[0] = int16_t(5 * ncand);
     for (int slot = lane; slot < ncand; slot += 32) {
         const int q = cand[slot];
         if (ix_m) ix_m[3 + A.take_veh + slot] = q;
@@ -2196,24 +2217,33 @@ __device__ __forceinline__ int last_nonzero_prefix(const float* p, int n, int la
     return last;
 }
 
+// src and dst share their alignment modulo 16 bytes (row offsets are equal and
+// both bases are 16-byte aligned): scalar head, 16-byte body, scalar tail.
 __device__ __forceinline__ void copy_to_host(const float* src, float* dst, int n, int lane) {
-    for (int i = lane; i < n; i += 32) dst[i] = __ldg(src + i);
+    if (n <= 0) return;
+    int head = int((16u - unsigned(reinterpret_cast<uintptr_t>(dst) & 15u)) & 15u) >> 2;
+    head = head < n ? head : n;
+    if (lane < head) dst[lane] = __ldg(src + lane);
+    const float4* s4 = reinterpret_cast<const float4*>(src + head);
+    float4* d4 = reinterpret_cast<float4*>(dst + head);
+    const int n4 = (n - head) >> 2;
+    for (int i = lane; i < n4; i += 32) d4[i] = __ldg(s4 + i);
+    const int done = head + 4 * n4;
+    if (lane < n - done) dst[done + lane] = __ldg(src + done + lane);
 }
 
-__device__ __forceinline__ void zero_host(float* dst, int n, int lane) {
-    for (int i = lane; i < n; i += 32) dst[i] = 0.0f;
-}
+__device__ __forceinline__ void zero_host(float* dst, int n, int lane) { zero_span(dst, n, lane, 32); }
 
-__global__ void __launch_bounds__(256) obs_to_host_kernel(const float* obs, float* host, int32_t* prev, int64_t rows,
-                                                          int D, int ego, int road_n, int veh_n,
-                                                          unsigned long long* bytes) {
+__global__ void __launch_bounds__(256) obs_to_host_kernel(const float* obs, const int16_t* prefix, float* host,
+                                                          int32_t* prev, int64_t rows, int D, int ego, int road_n,
+                                                          int veh_n, unsigned long long* bytes) {
     const int lane = threadIdx.x & 31;
     const int64_t r = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (r >= rows) return;
     const float* src = obs + r * D;
     float* dst = host + r * D;
-    const int lr = last_nonzero_prefix(src + ego, road_n, lane);
-    const int lv = last_nonzero_prefix(src + ego + road_n, veh_n, lane);
+    const int lr = prefix ? min(int(prefix[2 * r]), road_n) : last_nonzero_prefix(src + ego, road_n, lane);
+    const int lv = prefix ? min(int(prefix[2 * r + 1]), veh_n) : last_nonzero_prefix(src + ego + road_n, veh_n, lane);
     const int pr = prev[2 * r], pv = prev[2 * r + 1];
     copy_to_host(src, dst, ego + lr, lane);
     if (pr > lr) zero_host(dst + ego + lr, pr - lr, lane);
@@ -2498,6 +2528,7 @@ int dg_step(dg_engine* eng, const DgStepIO* io, void* stream) {
     A.drac_max = io->drac_max;
     A.metric_seen = io->metric_seen;
     A.index_out = io->index_out;
+    A.prefix_out = io->prefix_out;
     A.ticks = io->ticks > 0 ? io->ticks : 1;
     A.ring_slots = io->ring_slots > 0 ? io->ring_slots : A.ticks;
     A.ring_start = io->ring_start;
@@ -2649,8 +2680,8 @@ int dg_host_free(void* host_ptr) {
     return e == cudaSuccess ? DG_OK : cuda_fail(e, "dg_host_free");
 }
 
-int dg_to_host(dg_engine* eng, const float* obs, float* host_obs, int32_t* prev_len, const void* aux,
-               void* host_aux, size_t aux_bytes, unsigned long long* bytes, void* stream) {
+int dg_to_host(dg_engine* eng, const float* obs, const int16_t* prefix, float* host_obs, int32_t* prev_len,
+               const void* aux, void* host_aux, size_t aux_bytes, unsigned long long* bytes, void* stream) {
     if (!eng || !obs || !host_obs || !prev_len) return fail(DG_EINVAL, "dg_to_host: null argument");
     if (aux_bytes && (!aux || !host_aux)) return fail(DG_EINVAL, "dg_to_host: null aux buffer");
     const DgDims& d = eng->base.d;
@@ -2662,8 +2693,8 @@ int dg_to_host(dg_engine* eng, const float* obs, float* host_obs, int32_t* prev_
     const int64_t grid = (rows + per_cta - 1) / per_cta;
     if (grid > 0)
         obs_to_host_kernel<<<unsigned(grid), 32 * per_cta, 0, static_cast<cudaStream_t>(stream)>>>(
-            obs, static_cast<float*>(dptr), prev_len, rows, d.obs_dim, d.ego_dim, 5 * d.k_road, 7 * d.k_vehicles,
-            bytes);
+            obs, prefix, static_cast<float*>(dptr), prev_len, rows, d.obs_dim, d.ego_dim, 5 * d.k_road,
+            7 * d.k_vehicles, bytes);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "dg_to_host");
     if (aux_bytes) {

@@ -427,6 +427,7 @@ class Engine:
         self._host_pool = HostSlabPool(self._host_blob.numel())
         self._mapped_pool = MappedSlabPool(self._lib, self._host_blob.numel(), W * M, dev)
         self.d2h_bytes = torch.zeros(1, dtype=torch.int64, device=dev)   # obs bytes written by dg_to_host
+        self._prefix_dev = torch.zeros((W, M, 2), dtype=torch.int16, device=dev)   # non-zero obs prefixes
         self.launches = 0
         self._metrics_on = False
         self._host_lay = None
@@ -671,7 +672,7 @@ class Engine:
                     steer_gain: float = 2.0, throttle: float = 0.5,
                     event_counts: torch.Tensor | None = None, ticks: int = 1, ring_start: int = 0,
                     drac_max: torch.Tensor | None = None, metric_seen: torch.Tensor | None = None,
-                    index_out: torch.Tensor | None = None) -> None:
+                    index_out: torch.Tensor | None = None, prefix_out: torch.Tensor | None = None) -> None:
         """Enqueue one fused launch on the current stream; no sync, no checks
         beyond the device-side non-finite guard.  Used by the fast paths.
         ``next_actions`` (float64 [W][M][3], may alias ``actions``) receives
@@ -691,7 +692,9 @@ class Engine:
         ``track_episode_metrics`` is on).  ``index_out`` (int32 [S][W][M][
         ``index_stride``], S = ring slots) receives the integer decisions of
         every tick: nearest-lane index, road slot -> segment map, neighbour
-        order (layout: ``DgStepIO.index_out`` in the C header)."""
+        order (layout: ``DgStepIO.index_out`` in the C header).  ``prefix_out``
+        (int16 [S][W][M][2]) receives per agent the length of the road / vehicle
+        block prefix that can be non-zero (``DgStepIO.prefix_out``)."""
         if self._shape["mode"] == "split" and (ticks > 1 or bufs.obs.dim() == 4):
             # the split kernels take one tick per launch and write one output
             # set: tick t goes to ring slot (ring_start + t) % S through views
@@ -706,17 +709,21 @@ class Engine:
                     bufs.obs[slot], bufs.aux, {k: v[slot] for k, v in bufs.views.items()})
                 self.launch_step(a_t, one, autoreset, snapshot, terms, next_actions, steer_gain, throttle,
                                  event_counts, 1, 0, drac_max, metric_seen,
-                                 None if index_out is None else index_out.view(-1, *index_out.shape[-3:])[slot])
+                                 None if index_out is None else index_out.view(-1, *index_out.shape[-3:])[slot],
+                                 None if prefix_out is None else prefix_out.view(-1, self.W, self.M, 2)[slot])
             return
+        if prefix_out is not None and (prefix_out.dtype != torch.int16 or not prefix_out.is_contiguous()
+                                       or prefix_out.numel() % (self.W * self.M * 2)):
+            raise ValueError("prefix_out must be a contiguous int16 CUDA tensor of [S][W][M][2]")
         io = self._step_io(actions, bufs, autoreset, snapshot, terms, next_actions, steer_gain, throttle,
-                           event_counts, ticks, ring_start, drac_max, metric_seen, index_out)
+                           event_counts, ticks, ring_start, drac_max, metric_seen, index_out, prefix_out)
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), self._stream()), "dg_step")
         self._step_count += int(ticks)
         self.launches += 1
 
     def _step_io(self, actions, bufs, autoreset=False, snapshot=True, terms=True, next_actions=None,
                  steer_gain=2.0, throttle=0.5, event_counts=None, ticks=1, ring_start=0, drac_max=None,
-                 metric_seen=None, index_out=None):
+                 metric_seen=None, index_out=None, prefix_out=None):
         if self._metrics_on:
             drac_max = self._drac_max if drac_max is None else drac_max
             metric_seen = self._metric_seen if metric_seen is None else metric_seen
@@ -734,7 +741,8 @@ class Engine:
                         policy_gain=float(steer_gain), policy_throttle=float(throttle),
                         event_counts=event_counts.data_ptr() if event_counts is not None else None,
                         ticks=int(ticks), ring_slots=int(slots), ring_start=int(ring_start),
-                        drac_max=_ptr(drac_max), metric_seen=_ptr(metric_seen), index_out=_ptr(index_out))
+                        drac_max=_ptr(drac_max), metric_seen=_ptr(metric_seen), index_out=_ptr(index_out),
+                        prefix_out=_ptr(prefix_out))
         if index_out is not None:
             want = (slots, self.W, self.M, self.index_stride)
             if (index_out.dtype != torch.int32 or not index_out.is_cuda or not index_out.is_contiguous()
@@ -904,7 +912,8 @@ class Engine:
         io = self._host_io.get(key)
         if io is None:
             # the host path always uses the same device buffers: build its DgStepIO once
-            io = self._host_io[key] = self._step_io(self._act_dev, bufs, autoreset=autoreset)
+            io = self._host_io[key] = self._step_io(self._act_dev, bufs, autoreset=autoreset,
+                                                    prefix_out=self._prefix_dev)
         stream = torch.cuda.current_stream(self.device)
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), ct.c_void_p(stream.cuda_stream)), "dg_step")
         self._step_count += 1
@@ -916,7 +925,8 @@ class Engine:
             ptr, prev, hb = slab
             ob = self._host_obs_bytes
             N.check(self._lib, self._lib.dg_to_host(
-                self._h, _ptr(self._obs_dev), ct.c_void_p(ptr), _ptr(prev), _ptr(self._host_bufs.aux),
+                self._h, _ptr(self._obs_dev), _ptr(self._prefix_dev), ct.c_void_p(ptr), _ptr(prev),
+                _ptr(self._host_bufs.aux),
                 ct.c_void_p(ptr + ob), self._host_blob.numel() - ob, _ptr(self.d2h_bytes),
                 ct.c_void_p(stream.cuda_stream)), "dg_to_host")
             self.launches += 1

@@ -80,3 +80,26 @@ def test_shrinking_prefixes_are_zeroed(device):
     assert a._mapped_pool.slabs == 1                   # the same slab served both ticks
     assert np.array_equal(bits(o2.obs), bits(want))
     assert (o2.obs[..., 11:1761] != 0).sum() == 0
+
+
+@pytest.mark.parametrize("mode", [2, 0, 1])
+def test_prefix_record_bounds_the_nonzero_obs(mode, device):
+    """DgStepIO.prefix_out (5 n_r, 7 n_v floats) equals the kernel's own
+    candidate / neighbour counts and nothing past it is non-zero -- the
+    property dg_to_host relies on -- in every launch mode."""
+    W, M = 16, 16
+    inp = C.build_inputs(cfg_of(W, M, seed=8))
+    eng = Engine(**inp.as_kwargs(), device=device, launch_mode=mode)
+    oc = eng.obs_config
+    road0, veh0 = oc.ego_dim, oc.ego_dim + 5 * oc.k_road
+    bufs = eng.new_step_buffers()
+    ix = eng.new_index_buffer(1)
+    px = torch.full((W, M, 2), -1, dtype=torch.int16, device=device)
+    acts = philox_actions(9, 12, W, M).astype(np.float64)
+    for t in range(12):
+        eng.launch_step(torch.from_numpy(acts[t]).to(device), bufs, index_out=ix, prefix_out=px)
+        p, i, o = px.cpu().numpy(), ix[0].cpu().numpy(), bufs.obs.cpu().numpy()
+        assert np.array_equal(p[..., 0], 5 * i[..., 1]) and np.array_equal(p[..., 1], 7 * i[..., 2])
+        cols = np.arange(o.shape[-1])
+        past = ((cols >= road0) & (cols < veh0) & (cols >= road0 + p[..., :1])) | (cols >= veh0 + p[..., 1:])
+        assert not np.any(o.view(np.uint32)[past]), f"tick {t}: non-zero obs past the prefix"

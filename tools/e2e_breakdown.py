@@ -51,13 +51,15 @@ for _ in range(steps):
     t3 = time.perf_counter()
     key = (True, eng._metrics_on)
     io = eng._host_io.get(key) or eng._host_io.setdefault(key, eng._step_io(eng._act_dev, eng._host_bufs,
-                                                                              autoreset=True))
+                                                                              autoreset=True,
+                                                                              prefix_out=eng._prefix_dev))
     N.check(lib, lib.dg_step(eng._h, ct.byref(io), ct.c_void_p(stream.cuda_stream)), "dg_step")
     ev[2].record(stream)
     t4 = time.perf_counter()
     ptr, prev, hb = eng._mapped_pool.acquire()
     ob = eng._host_obs_bytes
-    N.check(lib, lib.dg_to_host(eng._h, _ptr(eng._obs_dev), ct.c_void_p(ptr), _ptr(prev), _ptr(eng._host_bufs.aux),
+    N.check(lib, lib.dg_to_host(eng._h, _ptr(eng._obs_dev), _ptr(eng._prefix_dev), ct.c_void_p(ptr), _ptr(prev),
+                                _ptr(eng._host_bufs.aux),
                                 ct.c_void_p(ptr + ob), eng._host_blob.numel() - ob, _ptr(eng.d2h_bytes),
                                 ct.c_void_p(stream.cuda_stream)), "dg_to_host")
     ev[4].record(stream)

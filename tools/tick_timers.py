@@ -13,7 +13,9 @@ import numpy as np  # noqa: E402
 from paper_2605_08528_b200 import _native as N  # noqa: E402
 
 dbg = ROOT / "paper_2605_08528_b200" / "libdrivegrid_b200_ticktimers.so"
-subprocess.run(["/usr/local/cuda/bin/nvcc", *N.NVCC_FLAGS, "-DDG_TICK_TIMERS", "-I", str(ROOT / "include"),
+import os  # noqa: E402
+extra = os.environ.get("DG_EXTRA_FLAGS", "").split()
+subprocess.run(["/usr/local/cuda/bin/nvcc", *N.NVCC_FLAGS, "-DDG_TICK_TIMERS", *extra, "-I", str(ROOT / "include"),
                 "-o", str(dbg), *map(str, N.SOURCES)], check=True)
 N.LIB_PATH = dbg
 import torch  # noqa: E402
@@ -47,13 +49,16 @@ for sh in shapes:
     out = np.zeros((W, 40), dtype=np.int64)
     assert lib.dg_debug_tick_clocks(out.ctypes.data, W, 0) == 0
     per = out / T
-    names = ["check", "phase1", "phase2+bar", "tail", "end-bar"]
-    print(f"W={W} T={T} warps={nw} mode={mode} ({eng.launch_shape()}): {s0.elapsed_time(s1) / T * 1e3:.2f} us/tick "
+    names = ["check", "phase1", "phase2+bar", "tail-rest", "end-bar"]
+    print(f"[{' '.join(extra)}] W={W} T={T} warps={nw} mode={mode} ({eng.launch_shape()}): {s0.elapsed_time(s1) / T * 1e3:.2f} us/tick "
           f"(timer build)")
     for i, nme in enumerate(names):
         print(f"  {nme:12s} median {np.median(per[:, i]):8.0f}  p90 {np.percentile(per[:, i], 90):8.0f}")
-    print(f"  sum          median {np.median(per[:, :5].sum(1)):8.0f}")
+    print(f"  sum          median {np.median(per[:, :8].sum(1)):8.0f}")
+    print(f"  tail split: to-finalize {np.median(per[:, 5]):.0f}  finalize {np.median(per[:, 6]):.0f}  "
+          f"count_events {np.median(per[:, 7]):.0f}  rest {np.median(per[:, 3]):.0f}")
     print("  pairs (2a) per warp (median over CTAs):", np.median(per[:, 20:20 + nw], axis=0).astype(int))
     print("  scans (2b) per warp (median over CTAs):", np.median(per[:, 8:8 + nw], axis=0).astype(int))
     if mode == 2:
-        print(f"  physics warp: ego {np.median(per[:, 30]):.0f}  physics {np.median(per[:, 31]):.0f}")
+        print(f"  physics warp: zero-issue {np.median(per[:, 29]):.0f}  ego {np.median(per[:, 30]):.0f}  "
+              f"physics {np.median(per[:, 31]):.0f}")
