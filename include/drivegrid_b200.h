@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 10
+#define DG_ABI_VERSION 11
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -361,6 +361,126 @@ size_t dg_policy_scratch_bytes(int32_t n_agents, int32_t nets);
 int dg_gae(const double* rewards, const uint8_t* dones, const float* values, int32_t T, int64_t N,
            double gamma, double lambda, float* advantages, float* returns, void* stream);
 const char* dg_policy_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * On-device world construction.  Replaces the reference's
+ * O(W) Python init: build_world_batch (world.py:82-194 -- segmentize,
+ * scene_segments, grid_offsets, assign_scenes, the padded (W, P_max)
+ * arrays), the Engine spawn table (engine.py:192-227 with filter_agents,
+ * scenario.py:169-192), Engine._compact_subset (engine.py:234-253) and
+ * eval.random_goals (resample_goal / polyline_arc_point,
+ * config.py:222-278).  The host keeps scene intake (JSON, recentre, z-flatten,
+ * degeneracy verdicts, config.py:162-189), the Philox draws (the scene-order
+ * permutation of assign_scenes, the goal distances) and weather / friction.
+ * Every output is bit-identical to the reference. */
+
+/* The prepared scene pool, flattened (device arrays). */
+typedef struct DgScenePool {
+    int32_t num_scenes, num_polylines, num_points, num_agents;
+    const double* points;        /* [num_points][2] polyline vertices x, y (scene-local,
+                                    recentred), polyline after polyline, scene after scene */
+    const int32_t* poly_start;   /* [num_polylines + 1] first vertex of each polyline       */
+    const int32_t* poly_type;    /* [num_polylines] type code                               */
+    const int32_t* scene_poly;   /* [num_scenes + 1] first polyline of each scene           */
+    const double* agents;        /* [num_agents][7] start x, start y, start heading, goal x,
+                                    goal y, length, width -- file order within a scene      */
+    const int32_t* scene_agent;  /* [num_scenes + 1] first agent record of each scene       */
+} DgScenePool;
+
+typedef struct DgSceneBuild {
+    double gap;                  /* segment_gap (SEGMENT_GAP 3.0)                           */
+    double bbox_half;            /* scene_factory.bbox_half                                 */
+    double half_width;           /* SEGMENT_HALF_WIDTH (0.05)                               */
+    double goal_radius;          /* filter_agents' start-goal threshold                     */
+    int32_t cap;                 /* agents kept per scene (num_agents_per_env)              */
+    int32_t pad_;
+} DgSceneBuild;
+
+/* Per-scene tables (device, caller-allocated).  Scene s owns the rows from
+ * base(s) = poly_start[scene_poly[s]] - scene_poly[s] (its first candidate pair)
+ * on: segments [base, base + seg_count[s]) in scene_segments order, lane / edge
+ * index lists (scene-local segment indices, ascending) at lane_index + base /
+ * edge_index + base.  Arrays marked [pairs] hold num_points - num_polylines rows. */
+typedef struct DgSceneSegments {
+    double* mid;                 /* [pairs][2] 0.5 * (a + b)                                */
+    double* dir;                 /* [pairs][2] (b - a) / |b - a|                            */
+    int32_t* type;               /* [pairs]                                                  */
+    double* half_len;            /* [pairs] 0.5 * |b - a|                                   */
+    double* half_wid;            /* [pairs] half_width                                      */
+    int32_t* lane_index;         /* [pairs]                                                  */
+    int32_t* edge_index;         /* [pairs]                                                  */
+    double* arc;                 /* [num_points] cumulative arc length at each vertex of
+                                    its polyline (np.cumsum order)                          */
+    int32_t* seg_count;          /* [num_scenes]                                             */
+    int32_t* lane_count;         /* [num_scenes]                                             */
+    int32_t* edge_count;         /* [num_scenes]                                             */
+    int32_t* lane_polys;         /* [num_scenes] lane polylines of the scene                */
+    int32_t* kept_count;         /* [num_scenes] filter_agents(scene, cap) length           */
+    int32_t* kept_agent;         /* [num_agents] scene s: kept_agent[scene_agent[s] + k] =
+                                    pool index of its k-th kept agent                       */
+} DgSceneSegments;
+
+/* Scene tables for a pool: one CTA per scene (3 passes: ordered segment
+ * compaction, arc tables, spawn filter).  Asynchronous on stream. */
+int dg_build_scenes(const DgScenePool* pool, const DgSceneBuild* build, DgSceneSegments* out, void* stream);
+
+/* World w of this build is world world_base + w of the batch (a rank's shard
+ * builds only its own worlds): scene scene_order[(world_base + w) % num_scenes]
+ * (assign_scenes: the Philox permutation for random_fill, the identity for
+ * fixed), grid offset ((g % grid_cols) * pitch, (g / grid_cols) * pitch) with
+ * g = world_base + w and grid_cols = ceil(sqrt(total worlds)). */
+typedef struct DgWorldBuild {
+    int32_t W, M, num_scenes, grid_cols;
+    int64_t world_base;
+    double pitch, offstage_x, wheelbase;
+    const int32_t* scene_order;  /* [num_scenes]                                           */
+    /* engine tables (required) */
+    int32_t* assignment;         /* [W]                                                     */
+    double* grid_offset;         /* [W][2]                                                  */
+    uint8_t* valid;              /* [W][M]                                                  */
+    uint8_t* alive;              /* [W][M] = valid, or NULL                                 */
+    double* start_xy;            /* [W][M][2] global                                        */
+    double* goal_xy;             /* [W][M][2] global                                        */
+    double* start_yaw;           /* [W][M]                                                  */
+    double* length;              /* [W][M] (4.0 in empty slots)                             */
+    double* width;               /* [W][M] (2.0 in empty slots)                             */
+    double* r_hull;              /* [W][M] circle_layout (observation.py:44-48)             */
+    double* d_hull;              /* [W][M]                                                  */
+    double* state;               /* [12][W][M] initial state (parked empty slots)           */
+    /* eval.random_goals: goal_min == goal_max walks exactly goal_min; else
+       goal_draws [draws] holds rng.uniform(goal_min, goal_max) of Philox stream
+       (seed, 4), one per valid agent of a scene with lanes, in (world, agent)
+       order over the whole batch (world 0 first, also for a shard) */
+    int32_t random_goals, pad_;
+    double goal_min, goal_max;
+    const double* goal_draws;
+    /* padded WorldBatch (p_max > 0; world.py:148-194) [W][p_max](..) */
+    int32_t p_max, k_lane, k_edge, pad2_;
+    double* wb_mid;              /* [W][p_max][2] scene-local                               */
+    double* wb_dir;
+    int32_t* wb_type;
+    double* wb_half_len;
+    double* wb_half_wid;
+    uint8_t* wb_mask;
+    /* _compact_subset (k_lane / k_edge > 0): [W][K](..), midpoints global */
+    double* lane_mid;
+    double* lane_dir;
+    double* lane_half_len;
+    double* lane_half_wid;
+    uint8_t* lane_mask;
+    double* edge_mid;
+    double* edge_dir;
+    double* edge_half_len;
+    double* edge_half_wid;
+    uint8_t* edge_mask;
+} DgWorldBuild;
+
+/* Per-world tables of a batch from dg_build_scenes' output: one thread per
+ * (world, agent) slot (spawn table + initial state, then the goal walk) and
+ * per (world, segment) / (world, k) for the optional padded and subset
+ * arrays.  Asynchronous on stream. */
+int dg_build_worlds(const DgScenePool* pool, const DgSceneSegments* scenes, const DgWorldBuild* build,
+                    void* stream);
 
 const char* dg_last_error(void);
 int dg_abi_version(void);

@@ -16,7 +16,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB_PATH = PKG / "libdrivegrid_b200.so"
-SOURCES = [PKG / "csrc" / "drivegrid_b200.cu", PKG / "csrc" / "dg_policy.cu"]
+SOURCES = [PKG / "csrc" / "drivegrid_b200.cu", PKG / "csrc" / "dg_policy.cu", PKG / "csrc" / "dg_worlds.cu"]
 DEPS = [PKG / "csrc" / "dg_fastmath.cuh", PKG / "csrc" / "dg_umma.cuh"]
 HEADER = ROOT / "include" / "drivegrid_b200.h"
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 
 class DgDims(ct.Structure):
@@ -89,6 +89,41 @@ class DgStepIO(ct.Structure):
                                               ("prefix_out", _P)]
 
 
+class DgScenePool(ct.Structure):
+    _fields_ = [(n, ct.c_int32) for n in ("num_scenes", "num_polylines", "num_points", "num_agents")] + [
+        (n, _P) for n in ("points", "poly_start", "poly_type", "scene_poly", "agents", "scene_agent")]
+
+
+class DgSceneBuild(ct.Structure):
+    _fields_ = [(n, ct.c_double) for n in ("gap", "bbox_half", "half_width", "goal_radius")] + [
+        ("cap", ct.c_int32), ("pad_", ct.c_int32)]
+
+
+SCENE_SEG_FIELDS = ("mid", "dir", "type", "half_len", "half_wid", "lane_index", "edge_index", "arc",
+                    "seg_count", "lane_count", "edge_count", "lane_polys", "kept_count", "kept_agent")
+
+
+class DgSceneSegments(ct.Structure):
+    _fields_ = [(n, _P) for n in SCENE_SEG_FIELDS]
+
+
+WORLD_OUT_FIELDS = ("assignment", "grid_offset", "valid", "alive", "start_xy", "goal_xy", "start_yaw",
+                    "length", "width", "r_hull", "d_hull", "state")
+WORLD_OPT_FIELDS = ("wb_mid", "wb_dir", "wb_type", "wb_half_len", "wb_half_wid", "wb_mask",
+                    "lane_mid", "lane_dir", "lane_half_len", "lane_half_wid", "lane_mask",
+                    "edge_mid", "edge_dir", "edge_half_len", "edge_half_wid", "edge_mask")
+
+
+class DgWorldBuild(ct.Structure):
+    _fields_ = ([(n, ct.c_int32) for n in ("W", "M", "num_scenes", "grid_cols")] + [("world_base", ct.c_int64)]
+                + [(n, ct.c_double) for n in ("pitch", "offstage_x", "wheelbase")] + [("scene_order", _P)]
+                + [(n, _P) for n in WORLD_OUT_FIELDS]
+                + [("random_goals", ct.c_int32), ("pad_", ct.c_int32), ("goal_min", ct.c_double),
+                   ("goal_max", ct.c_double), ("goal_draws", _P)]
+                + [(n, ct.c_int32) for n in ("p_max", "k_lane", "k_edge", "pad2_")]
+                + [(n, _P) for n in WORLD_OPT_FIELDS])
+
+
 # exported symbol -> (restype, argtypes)
 SIGNATURES = {
     "dg_abi_version": (ct.c_int, []),
@@ -117,6 +152,10 @@ SIGNATURES = {
     "dg_host_alloc": (ct.c_int, [ct.c_size_t, ct.POINTER(_P)]),
     "dg_host_free": (ct.c_int, [_P]),
     "dg_to_host": (ct.c_int, [_P, _P, _P, _P, _P, _P, _P, ct.c_size_t, _P, _P]),
+    "dg_build_scenes": (ct.c_int, [ct.POINTER(DgScenePool), ct.POINTER(DgSceneBuild), ct.POINTER(DgSceneSegments),
+                                   _P]),
+    "dg_build_worlds": (ct.c_int, [ct.POINTER(DgScenePool), ct.POINTER(DgSceneSegments), ct.POINTER(DgWorldBuild),
+                                   _P]),
 }
 
 

@@ -2392,6 +2392,10 @@ static int cuda_fail(cudaError_t e, const char* where) {
     return DG_ECUDA;
 }
 
+// error reporting for the library's other translation units (dg_worlds.cu)
+int dg_internal_fail(int code, const char* msg) { return fail(code, msg); }
+int dg_internal_cuda_fail(cudaError_t e, const char* where) { return cuda_fail(e, where); }
+
 static size_t split_smem_bytes(int take_road, int apc) {
     size_t b = sizeof(AgentRec) * kMaxAgents;
     b += sizeof(uint16_t) * size_t(apc) * size_t(take_road > 0 ? take_road : 1);

@@ -32,6 +32,8 @@ from .params import (CRASH_SPEED_LIMIT, DENSE_TERMS, EVENT_TYPES, GRAVITY, OFFST
                      STATE_FIELDS, BicycleParams, ObsConfig, RewardConfig, SimConfig, VehicleParams)
 from .spatial import build_scene_index
 from .tables import build_tables, compact_subset, edge_mask_of, lane_mask_of
+from .worldgen import DeviceWorldBatch
+from .worldgen import engine_tables as device_engine_tables
 
 TERM_NAMES = (*DENSE_TERMS, "total")
 
@@ -320,8 +322,14 @@ class Engine:
         self.bicycle = bicycle or BicycleParams()
         self.worlds = worlds
         self.frictions = frictions
-        t = build_tables(worlds, scenes, assignment, frictions, config, self.params)
+        if isinstance(worlds, DeviceWorldBatch):
+            # on-device world construction: the spawn table and initial state are
+            # written by the GPU into the arrays the engine binds (worldgen.py)
+            t = device_engine_tables(worlds, frictions, config, self.params)
+        else:
+            t = build_tables(worlds, scenes, assignment, frictions, config, self.params)
         self.tables = t
+        built = getattr(t, "dev", None)
         W, M = t.W, t.M
         self.W, self.M = W, M
         self.valid = t.valid.copy()
@@ -333,7 +341,9 @@ class Engine:
 
         dev = self.device
 
-        def up(a, dtype):
+        def up(a, dtype, key=None):
+            if built is not None and key in built:
+                return built[key]
             return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype).to(dev)
 
         reach = float((t.r_hull + t.d_hull).max())
@@ -343,24 +353,25 @@ class Engine:
         self._d = d = {
             "scene_blob": up(blob, torch.uint8),
             "scene_meta": up(meta, torch.int64),
-            "scene_of_world": up(t.scene_of_world, torch.int32),
-            "grid_offset": up(t.grid_offsets, torch.float64),
+            "scene_of_world": up(t.scene_of_world, torch.int32, "assignment"),
+            "grid_offset": up(t.grid_offsets, torch.float64, "grid_offset"),
             "mu_eff": up(t.mu_eff, torch.float64),
             "weather": up(t.weather, torch.float64),
-            "valid": up(t.valid, torch.uint8),
-            "length": up(t.length, torch.float64),
-            "width": up(t.width, torch.float64),
-            "r_hull": up(t.r_hull, torch.float64),
-            "d_hull": up(t.d_hull, torch.float64),
-            "state": up(np.stack([t.state0[k] for k in STATE_FIELDS]), torch.float64),
-            "alive": up(t.valid, torch.uint8),
+            "valid": up(t.valid, torch.uint8, "valid"),
+            "length": up(t.length, torch.float64, "length"),
+            "width": up(t.width, torch.float64, "width"),
+            "r_hull": up(t.r_hull, torch.float64, "r_hull"),
+            "d_hull": up(t.d_hull, torch.float64, "d_hull"),
+            "state": up(None if built is not None else np.stack([t.state0[k] for k in STATE_FIELDS]),
+                        torch.float64, "state"),
+            "alive": up(t.valid, torch.uint8, "alive"),
             "reason": torch.zeros((W, M), dtype=torch.int8, device=dev),
             "event_seen": torch.zeros((W, M), dtype=torch.uint8, device=dev),
             "spawn_step": torch.zeros((W, M), dtype=torch.int32, device=dev),
             "step_count": torch.zeros((W,), dtype=torch.int32, device=dev),
-            "start_xy": up(t.start_xy, torch.float64),
-            "goal_xy": up(t.goal_xy, torch.float64),
-            "start_yaw": up(t.start_yaw, torch.float64),
+            "start_xy": up(None if built is not None else t.start_xy, torch.float64, "start_xy"),
+            "goal_xy": up(None if built is not None else t.goal_xy, torch.float64, "goal_xy"),
+            "start_yaw": up(None if built is not None else t.start_yaw, torch.float64, "start_yaw"),
             "error_word": torch.full((1,), N.DG_NO_ERROR, dtype=torch.int32, device=dev),
             # zeroed once: the split kernels copy whole AgentRec records, padding included
             "scratch": torch.zeros(int(self._lib.dg_scratch_bytes(W, M)), dtype=torch.uint8, device=dev),
@@ -614,13 +625,15 @@ class Engine:
     @property
     def lane(self) -> dict:
         if self._lane is None:
-            self._lane = compact_subset(self.worlds, lane_mask_of(self.worlds.type_codes, self.worlds.mask))
+            self._lane = (self.worlds.compact_subset("lane") if isinstance(self.worlds, DeviceWorldBatch) else
+                          compact_subset(self.worlds, lane_mask_of(self.worlds.type_codes, self.worlds.mask)))
         return self._lane
 
     @property
     def edge(self) -> dict:
         if self._edge is None:
-            self._edge = compact_subset(self.worlds, edge_mask_of(self.worlds.type_codes, self.worlds.mask))
+            self._edge = (self.worlds.compact_subset("edge") if isinstance(self.worlds, DeviceWorldBatch) else
+                          compact_subset(self.worlds, edge_mask_of(self.worlds.type_codes, self.worlds.mask)))
         return self._edge
 
     def reset_phase_timers(self):

@@ -27,6 +27,8 @@ def shard_range(W: int, rank: int, world_size: int) -> tuple[int, int]:
 
 
 def shard_worlds(worlds: WorldBatch, lo: int, hi: int) -> WorldBatch:
+    if hasattr(worlds, "shard"):
+        return worlds.shard(lo, hi)       # DeviceWorldBatch: the rank builds only its worlds
     sl = slice(lo, hi)
     return WorldBatch(worlds.midpoints[sl], worlds.directions[sl], worlds.type_codes[sl],
                       worlds.half_lengths[sl], worlds.half_widths[sl], worlds.mask[sl],

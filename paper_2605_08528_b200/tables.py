@@ -109,6 +109,15 @@ def scene_tables_of(worlds: WorldBatch):
     return tables, index
 
 
+def world_friction(frictions, params: VehicleParams):
+    """Per-world mu_eff = min(mu_static, dry ground) and the weather token
+    (engine.py:188-190)."""
+    ground_mu, _ = ground_material(1.0, params.f_lon_dry, params.f_lat_dry)
+    mu_eff = np.array([min(f.mu_static, ground_mu) for f in frictions], dtype=np.float64)
+    weather = np.stack([f.weather_token for f in frictions], axis=0).astype(np.float64)
+    return mu_eff, weather
+
+
 def build_tables(worlds: WorldBatch, scenes, assignment, frictions, config: SimConfig,
                  params: VehicleParams) -> EngineTables:
     W, M = config.num_envs, config.num_agents
@@ -116,9 +125,7 @@ def build_tables(worlds: WorldBatch, scenes, assignment, frictions, config: SimC
         raise ValueError(f"world batch has {worlds.num_worlds} worlds, config wants {W}")
     if len(frictions) != W:
         raise ValueError("need one friction assignment per world")
-    ground_mu, _ = ground_material(1.0, params.f_lon_dry, params.f_lat_dry)
-    mu_eff = np.array([min(f.mu_static, ground_mu) for f in frictions], dtype=np.float64)
-    weather = np.stack([f.weather_token for f in frictions], axis=0).astype(np.float64)
+    mu_eff, weather = world_friction(frictions, params)
 
     state = {k: np.zeros((W, M)) for k in STATE_FIELDS}
     state["brake_sign_front"][:] = 1.0

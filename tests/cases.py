@@ -159,3 +159,89 @@ def run_case(engine, case: Case, on_step):
             a = case.actions[t].astype(np.float64)
             out = engine.step(a)
             on_step(t + 1, out, a)
+
+
+# ---------------------------------------------------------------- world construction
+def worlds_case_pool():
+    """The prepared scene_cases pool (make_golden.worlds_cases)."""
+    import types
+
+    import sys
+
+    from paper_2605_08528_b200 import scenes as S
+    if str(GOLDEN) not in sys.path:
+        sys.path.insert(0, str(GOLDEN))
+    from scene_cases import scene_specs
+    mod = types.SimpleNamespace(Polyline=S.Polyline, AgentRecord=S.AgentRecord, ScenarioSpec=S.ScenarioSpec,
+                                straight_scene=S.straight_scene, crossroads_scene=S.crossroads_scene,
+                                two_level_scene=S.two_level_scene, shift_scenario=S.shift_scenario)
+    return [p for p in map(prepare_scene, scene_specs(mod)) if p is not None]
+
+
+def world_cfg(W, M=16, seed=42, goals=None):
+    cfg = cfg_of(W, M, seed=seed)
+    if goals is not None:
+        cfg.eval.random_goals, cfg.eval.goal_min_m, cfg.eval.goal_max_m = True, goals[0], goals[1]
+    return cfg
+
+
+def canon(a):
+    a = np.asarray(a)
+    if a.dtype.kind == "f":
+        a = a.astype(np.float64)
+    elif a.dtype.kind in "iu":
+        a = a.astype(np.int64)
+    return np.ascontiguousarray(a)
+
+
+def host_world_arrays(cfg, scenes=None) -> dict:
+    """The init tables of the host build (scenes / tables / goals restatement),
+    keyed like make_golden._world_arrays."""
+    from paper_2605_08528_b200.goals import resample_goals
+    from paper_2605_08528_b200.params import STATE_FIELDS
+    from paper_2605_08528_b200.tables import build_tables, compact_subset, edge_mask_of, lane_mask_of
+    inp = C.build_inputs(cfg, scenes)
+    w = inp.worlds
+    t = build_tables(w, inp.scenes, inp.assignment, inp.frictions, inp.sim, inp.params)
+    goal_xy = t.goal_xy
+    if cfg.eval.random_goals:
+        goal_xy = resample_goals(t.goal_xy, t.start_xy, t.valid, w.grid_offsets, inp.scenes, inp.assignment, cfg)
+    out = {"midpoints": w.midpoints, "directions": w.directions, "type_codes": w.type_codes,
+           "half_lengths": w.half_lengths, "half_widths": w.half_widths, "mask": w.mask,
+           "grid_offsets": w.grid_offsets, "valid": t.valid, "start_xy": t.start_xy, "goal_xy": goal_xy,
+           "start_yaw": t.start_yaw, "length": t.length, "width": t.width, "r_hull": t.r_hull,
+           "d_hull": t.d_hull, "scenario_ids": np.frombuffer("\n".join(w.scenario_ids).encode(), np.uint8)}
+    for sub, fn in (("lane", lane_mask_of), ("edge", edge_mask_of)):
+        for k, v in compact_subset(w, fn(w.type_codes, w.mask)).items():
+            out[f"{sub}_{k}"] = v
+    for k in STATE_FIELDS:
+        out["state_" + k] = t.state0[k]
+    return out
+
+
+def engine_world_arrays(eng) -> dict:
+    """The same tables read back from a GPU engine (device world construction)."""
+    from paper_2605_08528_b200.params import STATE_FIELDS
+    w = eng.worlds
+    out = {"midpoints": w.midpoints, "directions": w.directions, "type_codes": w.type_codes,
+           "half_lengths": w.half_lengths, "half_widths": w.half_widths, "mask": w.mask,
+           "grid_offsets": w.grid_offsets, "valid": eng.valid, "start_xy": eng.start_xy,
+           "goal_xy": eng.goal_xy, "start_yaw": eng.start_yaw, "length": eng.length, "width": eng.width,
+           "r_hull": eng.r_hull, "d_hull": eng.d_hull,
+           "scenario_ids": np.frombuffer("\n".join(w.scenario_ids).encode(), np.uint8)}
+    for sub in ("lane", "edge"):
+        for k, v in getattr(eng, sub).items():
+            out[f"{sub}_{k}"] = v
+    st = eng.state
+    for k in STATE_FIELDS:
+        out["state_" + k] = st[k]
+    return out
+
+
+def check_world_hashes(arrays: dict, golden, tag: str) -> None:
+    import hashlib
+    for k, v in arrays.items():
+        c = canon(v)
+        want = bytes(golden[f"{tag}__{k}__sha"]).decode()
+        assert tuple(c.shape) == tuple(golden[f"{tag}__{k}__shape"]), (tag, k, c.shape)
+        assert hashlib.sha256(c.tobytes()).hexdigest() == want, f"{tag}: {k} differs from the reference"

@@ -26,6 +26,9 @@ Cases (each an .npz under tests/golden/):
                     survivor times out (reason 5, not parked), then steps dead
   traj_sparse       3x4 on a 2-agent straight road: half the slots invalid (never alive,
                     masked everywhere), random actions
+  worlds_4096       sha256 of every init table of build_engine at 4096x16 (plain and
+                    eval.random_goals) -- the on-device world construction pins
+  worlds_cases      the scene_cases pool at 29 worlds: full init tables (+ random goals)
   sysid             sysid.py: maneuver sets, 60 Hz channel rollouts of 6 candidate
                     parameter vectors on one maneuver of every kind, sysid_loss,
                     and a small five-stage run_cem (population 8, 40 trials)
@@ -494,6 +497,78 @@ def goals_random():
     np.savez_compressed(OUT / "goals_random.npz", cases=np.array(GOAL_CASES), **arrays)
 
 
+def _world_arrays(eng):
+    """Every per-world init table of a reference engine (world.py:148-194,
+    engine.py:176-253, config.py:236-278), canonical dtypes."""
+    w = eng.worlds
+    out = {"midpoints": w.midpoints, "directions": w.directions, "type_codes": w.type_codes,
+           "half_lengths": w.half_lengths, "half_widths": w.half_widths, "mask": w.mask,
+           "grid_offsets": w.grid_offsets, "valid": eng.valid, "start_xy": eng.start_xy,
+           "goal_xy": eng.goal_xy, "start_yaw": eng.start_yaw, "length": eng.length, "width": eng.width,
+           "r_hull": eng.r_hull, "d_hull": eng.d_hull,
+           "scenario_ids": np.frombuffer("\n".join(w.scenario_ids).encode(), np.uint8)}
+    for sub in ("lane", "edge"):
+        for k, v in getattr(eng, sub).items():
+            out[f"{sub}_{k}"] = v
+    for k in vh.STATE_FIELDS:
+        out["state_" + k] = eng.state[k]
+    return out
+
+
+def _canon(a):
+    a = np.asarray(a)
+    if a.dtype.kind == "f":
+        a = a.astype(np.float64)
+    elif a.dtype.kind in "iu":
+        a = a.astype(np.int64)
+    return np.ascontiguousarray(a)
+
+
+def worlds_4096():
+    """On-device world construction pins at the scale it is for:
+    sha256 of every init table of the reference's build_engine at 4096x16
+    (default pool), with and without eval.random_goals (15-60 m)."""
+    import hashlib
+    arrays = {}
+    for tag, goals in (("plain", False), ("goals", True)):
+        cfg = cfg_of(4096, 16)
+        if goals:
+            cfg.eval.random_goals, cfg.eval.goal_min_m, cfg.eval.goal_max_m = True, 15.0, 60.0
+        eng = build_engine(cfg)
+        for k, v in _world_arrays(eng).items():
+            c = _canon(v)
+            arrays[f"{tag}__{k}__sha"] = np.frombuffer(hashlib.sha256(c.tobytes()).hexdigest().encode(), np.uint8)
+            arrays[f"{tag}__{k}__shape"] = np.array(c.shape, dtype=np.int64)
+        arrays[f"{tag}__goal_xy_head"] = eng.goal_xy[:64]
+    np.savez_compressed(OUT / "worlds_4096.npz", **arrays)
+    print("worlds_4096", len(arrays))
+
+
+def worlds_cases():
+    """The scene_cases pool (crowd > cap, edge-only scene without lanes, far goals,
+    off-centre, elevated) through the reference's build_engine at 29 worlds:
+    full init tables, with random goals (10-50 m; the lane-less scene draws none)."""
+    import types
+
+    from drivegrid import scenario as sc
+    from drivegrid import synth
+    from scene_cases import scene_specs
+    mod = types.SimpleNamespace(Polyline=sc.Polyline, AgentRecord=sc.AgentRecord, ScenarioSpec=sc.ScenarioSpec,
+                                straight_scene=synth.straight_scene, crossroads_scene=synth.crossroads_scene,
+                                two_level_scene=synth.two_level_scene, shift_scenario=sc.shift_scenario)
+    pool = [p for p in map(prepare_scene, scene_specs(mod)) if p is not None]
+    arrays = {}
+    for tag, goals in (("plain", False), ("goals", True)):
+        cfg = cfg_of(29, 16, seed=7)
+        if goals:
+            cfg.eval.random_goals, cfg.eval.goal_min_m, cfg.eval.goal_max_m = True, 10.0, 50.0
+        eng = build_engine(cfg, scenes=pool)
+        for k, v in _world_arrays(eng).items():
+            arrays[f"{tag}__{k}"] = _canon(v)
+    np.savez_compressed(OUT / "worlds_cases.npz", **arrays)
+    print("worlds_cases", len(pool), "scenes")
+
+
 DENSE_LANES = tuple(float(x) for x in np.round(np.arange(-9.0, 9.01, 0.25), 2))
 
 
@@ -647,6 +722,6 @@ def sysid():
 if __name__ == "__main__":
     which = sys.argv[1:] or ["init_default", "friction", "friction_table", "traj_c1", "traj_pool", "traj_wet",
                              "traj_bicycle", "traj_custom_obs", "traj_reset", "traj_events",
-                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense", "traj_obs_min", "traj_no_edges", "scene_verdicts", "index_pins"]
+                             "traj_events_inv", "drac_wet", "drac_events", "sysid", "traj_sparse", "traj_timeout", "traj_forge", "goals_random", "weather_sampling", "traj_dense", "traj_obs_min", "traj_no_edges", "scene_verdicts", "index_pins", "worlds_4096", "worlds_cases"]
     for name in which:
         globals()[name]()

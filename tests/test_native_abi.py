@@ -46,7 +46,8 @@ def test_library_targets_sm100a():
     assert "sm_100a" in out
 
 
-@pytest.mark.parametrize("struct", ["DgDims", "DgConsts", "DgEngineDesc", "DgStepIO"])
+@pytest.mark.parametrize("struct", ["DgDims", "DgConsts", "DgEngineDesc", "DgStepIO", "DgScenePool",
+                                    "DgSceneBuild", "DgSceneSegments", "DgWorldBuild"])
 def test_struct_layout_matches_c(struct, tmp_path):
     src = tmp_path / "sz.c"
     fields = [f for f, _ in getattr(N, struct)._fields_]
@@ -87,3 +88,11 @@ def test_integration_stub_matches_the_binding():
         assert ct.sizeof(stub) == ct.sizeof(ours), name
         for f, _ in ours._fields_:
             assert getattr(stub, f).offset == getattr(ours, f).offset, (name, f)
+
+
+def test_world_build_rejects_bad_arguments_without_a_gpu():
+    lib = N.load_library()
+    assert lib.dg_build_scenes(None, None, None, None) == N.DG_EINVAL
+    pool, seg, b = N.DgScenePool(), N.DgSceneSegments(), N.DgWorldBuild()
+    assert lib.dg_build_worlds(ct.byref(pool), ct.byref(seg), ct.byref(b), None) == N.DG_EINVAL
+    assert b"bad dimensions" in lib.dg_last_error()
