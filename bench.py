@@ -92,11 +92,13 @@ def bench_config(W, M, D=1929):
                   f"({ring * W * M * D * 4 / 2**20:.0f} MiB > L2)"}
 
 
-def shard_inputs(cfg, rank, world_size):
-    """Global host tables, sliced to this rank's contiguous world range."""
+def shard_inputs(cfg, rank, world_size, dev=None):
+    """This rank's contiguous world range of the global batch.  With ``dev`` the
+    worlds are built on that GPU (worldgen.py: each rank builds only its shard,
+    bit-identical to the same worlds of the whole batch); without, on the host."""
     from paper_2605_08528_b200 import config as C
     from paper_2605_08528_b200.sharding import shard_inputs as _shard
-    return _shard(C.build_inputs(cfg), rank, world_size)
+    return _shard(C.build_inputs(cfg, device=dev), rank, world_size)
 
 
 class ClockSampler:
@@ -174,17 +176,12 @@ def ncu_traffic(W, M, ticks):
 
 
 def algorithmic_bytes_per_agent(obs_dim: int) -> int:
-    """Bytes one agent-step must move to/from HBM (roofline):
-    obs row write + state read/write + actions + the per-agent outputs and
-    mutable per-agent fields."""
-    obs = 4 * obs_dim                      # f32 observation row (write)
-    state = 2 * 12 * 8                     # 12 f64 fields read + write
-    actions = 3 * 8                        # f64 actions (read)
-    tables = 2 * 8 + 2 * 8 + 4 * 8         # goal, start, length/width/r/d (read)
-    flags = 4 + 4                          # alive, reason, event_seen, valid read; + written
-    spawn = 4                              # spawn_step (read)
-    outputs = 8 + 8 + 7 * 8 + 12 * 8 + 4 + 1 + 1 + 1 + 1  # reward, ttc_min, terms, snapshot, events, done, reason, alive, alive_pre
-    return obs + state + actions + tables + flags + spawn + outputs
+    """Bytes one agent-step must move to/from HBM, SURVEY.md §8(d):
+    B = 4*obs_dim (obs row) + 12 (actions) + 96 (12 fp32 state in + out) + 4
+    (reward) + 1 (done) + 4 (events) + 1 (reason) + 1 (alive) = 7,835 B at the
+    1,929-float observation.  (The engine keeps its state in float64, so it moves
+    more than the state term here; the obs row dominates either way.)"""
+    return 4 * obs_dim + 12 + 96 + 4 + 1 + 4 + 1 + 1
 
 
 def unmodified_reference(W, M, steps, warmup, cores):
@@ -326,7 +323,7 @@ def main():
     from paper_2605_08528_b200.engine import Engine
 
     W_total = args.worlds or (HEADLINE[0] if world_size == 1 else SCALE_TOTAL_WORLDS)
-    inp = shard_inputs(root_config(W_total), rank, world_size)
+    inp = shard_inputs(root_config(W_total), rank, world_size, dev)
     eng = Engine(**inp.as_kwargs(), device=dev)
     if args.shape:
         nw, cps = (int(v) for v in args.shape.split("x"))
@@ -459,6 +456,8 @@ def main():
             "launch": {"launches": n_launch, "ticks_per_launch": launch_ticks[0] if uniform else launch_ticks,
                        "max_ticks_per_launch": R, "cuda_graph": graph is not None,
                        "ring_slots": ring, "kernel_shape": eng.launch_shape(),
+                       "obs_clear": "resident ring (DgStepIO.obs_resident): a slot keeps its zero background, "
+                                    "a tick clears only the row spans its new content no longer covers",
                        "parallelism": f"world-shard x{world_size}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None if traffic is None else traffic[0],
@@ -492,7 +491,7 @@ def bench_c4(dev, steps=200, R=DEFAULT_TICKS_PER_LAUNCH, W=SCALE_TOTAL_WORLDS, M
     import torch
     from paper_2605_08528_b200.engine import Engine
 
-    eng = Engine(**shard_inputs(root_config(W, M), 0, 1).as_kwargs(), device=dev)
+    eng = Engine(**shard_inputs(root_config(W, M), 0, 1, dev).as_kwargs(), device=dev)
     D = eng.obs_config.obs_dim
     ring = max(2, math.ceil(2 * L2_BYTES / (W * M * D * 4)))
     rb = eng.new_rollout_buffers(ring)
@@ -546,7 +545,7 @@ def bench_c5(dev, ticks=128, W=1024, M=16, reps=2):
     from paper_2605_08528_b200.engine import Engine
     from paper_2605_08528_b200.policy import PolicyMLP
 
-    inp = shard_inputs(root_config(W, M), 0, 1)
+    inp = shard_inputs(root_config(W, M), 0, 1, dev)
     eng = Engine(**inp.as_kwargs(), device=dev)
     D = eng.obs_config.obs_dim
     pol = PolicyMLP(eng.obs_config, seed=0, device=dev, head_scale=1.0)

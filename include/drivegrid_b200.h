@@ -157,7 +157,19 @@ typedef struct DgStepIO {
                                    t*W*M*3 + w*M*3 + j.  Fused mode only.       */
     int32_t ring_slots;         /* 0: ticks                                    */
     int32_t ring_start;
-    int32_t pad_;
+    int32_t obs_resident;       /* 1: the obs slots are this engine's: beyond the
+                                   prefix lengths prefix_out records for a slot
+                                   (from the slot's previous use; zero after the
+                                   caller zeroed the slot and its prefix entries)
+                                   every float of a row is zero, so the kernel
+                                   clears only the span between a row's old and
+                                   new prefix instead of the whole block.
+                                   Needs prefix_out with one entry set per obs
+                                   slot; a recorded length past the block (e.g.
+                                   0x7fff after the caller wrote the slot) clears
+                                   the whole block.  Results do not depend on it.
+                                   0: every block is cleared in full.  Fused
+                                   modes; mode 1 ignores it.                   */
     double* drac_max;           /* [W][M]      episode safety metric, accumulated:
                                    drac_max = max(drac_max, pairwise DRAC of this
                                    tick's post-physics state over the agents alive
@@ -344,6 +356,10 @@ typedef struct DgPolicyDesc {
     float* log_prob;            /* [n_agents] log pi(actions | obs) (diagonal Gaussian), or NULL */
     float* actions_f32;         /* [n_agents][3] the written actions as float32 (the
                                    rollout's action record), or NULL                */
+    const int16_t* prefix;      /* [n_agents][2] the step's DgStepIO.prefix_out for these
+                                   rows (5 n_r, 7 n_v: the valid road / vehicle slots of
+                                   each observation row), or NULL: the encoder finds the
+                                   counts by scanning the rows                        */
 } DgPolicyDesc;
 
 /* One forward of the policy over every agent's observation row: 2 kernel

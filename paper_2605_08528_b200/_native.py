@@ -74,7 +74,7 @@ class DgPolicyDesc(ct.Structure):
         ("obs", _P), ("weights", _P), ("net_stride", ct.c_int64), ("off", ct.c_int64 * len(POL_SECTIONS)),
         ("emb", _P), ("mean", _P), ("actions", _P), ("value", _P),
         ("sample", ct.c_int32), ("first_net", ct.c_int32), ("seed", ct.c_uint64), ("counter", ct.c_uint64),
-        ("log_prob", _P), ("actions_f32", _P)]
+        ("log_prob", _P), ("actions_f32", _P), ("prefix", _P)]
 
 
 class DgStepIO(ct.Structure):
@@ -84,7 +84,7 @@ class DgStepIO(ct.Structure):
                           "next_actions")] + [("policy_gain", ct.c_double), ("policy_throttle", ct.c_double),
                                               ("event_counts", _P),
                                               ("ticks", ct.c_int32), ("ring_slots", ct.c_int32),
-                                              ("ring_start", ct.c_int32), ("pad_", ct.c_int32),
+                                              ("ring_start", ct.c_int32), ("obs_resident", ct.c_int32),
                                               ("drac_max", _P), ("metric_seen", _P), ("index_out", _P),
                                               ("prefix_out", _P)]
 

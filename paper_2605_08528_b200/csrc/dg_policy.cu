@@ -181,9 +181,15 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
         for (int i = tid; i < kEncAgents * kAccStride; i += kEncThreads) acc[i] = 0u;
         for (int i = tid; i < kHid; i += kEncThreads) b2[i] = __ldg(gb2 + i);
 
-        // valid slot counts (the valid slots are a prefix): warp w probes agents 4w..4w+3,
-        // 64 slots per round (two per lane), all eight loads per lane in flight together
-        {
+        // valid slot counts (the valid slots are a prefix): from the step's prefix
+        // record when given, else warp w probes agents 4w..4w+3, 64 slots per round
+        // (two per lane), all eight loads per lane in flight together
+        if (p.prefix) {
+            for (int a = tid; a < na; a += kEncThreads) {
+                const int v = int(__ldg(p.prefix + 2 * int64_t(a0 + a) + mod)) / nf;
+                cnt[a] = v < kslots ? v : kslots;
+            }
+        } else {
             int c4[4] = {0, 0, 0, 0};
             bool more[4];
 #pragma unroll

@@ -29,6 +29,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -99,6 +100,7 @@ struct KArgs {
     int32_t* index_out;   // [slot][W][M][index_stride] integer decisions (NULL = off)
     int32_t index_stride; // 3 + take_veh + take_road
     int16_t* prefix_out;  // [slot][W][M][2] non-zero obs prefix: 5 n_r, 7 n_v floats (NULL = off)
+    int32_t obs_resident; // 1: obs slots keep zeros beyond prefix_out's recorded prefixes
 };
 
 // ----------------------------------------------------------------- numpy-semantics helpers
@@ -589,11 +591,124 @@ struct FinIn {
     int* flags_out;                    // optional: alive, reason, seen, spawn after the tail
 };
 
-// Returns the agent's contribution to the episode counters: bits 0..3 the
-// one-hot event of this tick (goal, collision, crash, lane_forbidden), bit 4
-// alive before the tick.
-__device__ __forceinline__ unsigned finalize_agent(const KArgs& A, const TickOut& O, int w, int m, const FinIn& F,
-                                                int step_now, double ox, double oy) {
+// What the tail decided for one agent this tick (decide_agent), consumed by
+// the outputs (emit_agent): the one-hot event, reason / alive as reported
+// (before an autoreset), done-or-timed-out.
+struct TailRes {
+    int rnow;        // 0 none, 1 goal, 2 collision, 3 crash, 4 lane_forbidden
+    int reason;      // info["reason"]
+    int alive_new;   // info["alive"]
+    int finished;    // dones
+    int park;        // done, not timed out: parked off-stage (engine.py:388-391)
+};
+
+// Events and termination of one agent this tick (rewards.py:206-268 sparse
+// part, engine.py:370-393 tail): the reported reason / alive and done flag.
+__device__ __forceinline__ TailRes tail_events(const KArgs& A, const FinIn& F, int step_now, int* seen_new) {
+            const DgConsts& k = A.k;
+            const double px = F.st[SX], py = F.st[SY];
+            const double vx = F.st[SVX], vy = F.st[SVY];
+            const double tgx = F.gx - px, tgy = F.gy - py;
+            const double speed = dg::dsqrt(vx * vx + vy * vy);
+            const bool alive = F.alive;
+            const bool goal = dg::dsqrt(tgx * tgx + tgy * tgy) <= k.goal_radius;
+            const double sxd = px - F.sx, syd = py - F.sy;
+            const bool bad = !(finite(px) && finite(py) && finite(vx) && finite(vy));
+            const bool crash = dg::dsqrt(sxd * sxd + syd * syd) > k.crash_drift_limit || bad ||
+                               speed > k.crash_speed_limit;
+            const bool coll = F.touch && step_now - F.spawn >= A.d.collision_warmup;
+            const int seen = F.seen;
+            const bool e_goal = goal && alive && !(seen & 1);
+            const bool e_coll = coll && alive && !(seen & 2);
+            const bool e_crash = crash && alive && !(seen & 4);
+            const bool e_lf = F.edge_hit && alive && !(seen & 8);
+            const int rnow = e_goal ? 1 : (e_crash ? 3 : (e_lf ? 4 : (e_coll ? 2 : 0)));
+            *seen_new = seen | (rnow == 0 ? 0 : 1 << (rnow == 1 ? 0 : rnow == 2 ? 1 : rnow == 3 ? 2 : 3));
+            int reason = F.reason;
+            bool done = false;
+            if (!A.d.invincible) {
+                done = rnow != 0;
+                if (done && reason == 0) reason = rnow;
+            }
+            const int step_new = step_now + 1;
+            const bool timeout = step_new >= A.d.episode_len && alive;
+            const bool finished = done || timeout;
+            if (timeout && reason == 0) reason = 5;
+            TailRes R;
+            R.rnow = rnow;
+            R.reason = reason;
+            R.alive_new = alive && !finished;
+            R.finished = finished;
+            R.park = done && !timeout;
+            return R;
+}
+
+// The post-tail state of one agent (engine.py:388-393 park, 599-619 autoreset
+// teleport) -> st_out / flags_out and, when store_global, the engine arrays;
+// returns the agent's contribution to the episode counters: bits 0..3 the
+// one-hot event (goal, collision, crash, lane_forbidden), bit 4 alive before
+// the tick, kBitFinished.
+__device__ __forceinline__ unsigned tail_state(const KArgs& A, int w, int m, const FinIn& F, const TailRes& R,
+                                               int seen_new, int step_now, double ox, double oy) {
+            const DgConsts& k = A.k;
+            const int WM = A.d.W * A.d.M;
+            const int64_t am = int64_t(w) * A.d.M + m;
+            const bool park = R.park;
+            int alive_new = R.alive_new, reason = R.reason;
+            double x[DG_NUM_STATE];
+#pragma unroll
+            for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = F.st[f];
+            if (park) {
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
+                x[SX] = ox + k.offstage_x;
+                x[SY] = oy;
+            }
+            int spawn = F.spawn;
+            if (A.autoreset && R.finished && F.valid) {
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
+                x[SX] = F.sx;
+                x[SY] = F.sy;
+                x[SYAW] = F.start_yaw;
+                alive_new = 1;
+                reason = 0;
+                spawn = step_now + 1;
+                seen_new = 0;
+            }
+            if (F.store_global) {
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = x[f];
+                A.alive[am] = uint8_t(alive_new);
+                A.reason[am] = int8_t(reason);
+                A.event_seen[am] = uint8_t(seen_new);
+                A.spawn_step[am] = spawn;
+            }
+            if (F.st_out) {
+#pragma unroll
+                for (int f = 0; f < DG_NUM_STATE; ++f) F.st_out[f] = x[f];
+                F.flags_out[0] = alive_new;
+                F.flags_out[1] = reason;
+                F.flags_out[2] = seen_new;
+                F.flags_out[3] = spawn;
+            }
+            const int rnow = R.rnow;
+            return (rnow == 0 ? 0u : 1u << (rnow == 1 ? 0 : rnow == 2 ? 1 : rnow == 3 ? 2 : 3)) |
+                   (F.alive ? 16u : 0u) | (R.finished ? kBitFinished : 0u);
+}
+
+// decide (events + post-tail state) now, emit later (the pipelined fused tail)
+__device__ __forceinline__ unsigned decide_agent(const KArgs& A, int w, int m, const FinIn& F, int step_now,
+                                                 double ox, double oy, TailRes* R) {
+    int seen_new;
+    *R = tail_events(A, F, step_now, &seen_new);
+    return tail_state(A, w, m, F, *R, seen_new, step_now, ox, oy);
+}
+
+// The dense reward terms (rewards.py:106-204), the sparse reward of the decided
+// event, and every per-tick output of one agent (StepOutput, engine.py:397-406).
+__device__ __forceinline__ void emit_agent(const KArgs& A, const TickOut& O, int w, int m, const FinIn& F,
+                                           const TailRes& R) {
             const DgConsts& k = A.k;
             const int WM = A.d.W * A.d.M;
             const int64_t am = int64_t(w) * A.d.M + m;
@@ -627,49 +742,22 @@ __device__ __forceinline__ unsigned finalize_agent(const KArgs& A, const TickOut
             const double ttc_e = finite(tau) ? -np_min_k(dg::ddiv(k.ttc_edge_alpha, np_max_k(tau, k.ttc_floor)), k.ttc_edge_pmax)
                                              : 0.0;
             const double total = progress + lane_t + offroad + idle + ttc_v + ttc_e;
-
-            // sparse events, masked by alive and the per-type latch
-            const bool alive = F.alive;
-            const bool goal = dg::dsqrt(tgx * tgx + tgy * tgy) <= k.goal_radius;
-            const double sxd = px - F.sx, syd = py - F.sy;
-            const bool bad = !(finite(px) && finite(py) && finite(vx) && finite(vy));
-            const bool crash = dg::dsqrt(sxd * sxd + syd * syd) > k.crash_drift_limit || bad ||
-                               speed > k.crash_speed_limit;
-            const bool coll = F.touch && step_now - F.spawn >= A.d.collision_warmup;
-            const int seen = F.seen;
-            const bool e_goal = goal && alive && !(seen & 1);
-            const bool e_coll = coll && alive && !(seen & 2);
-            const bool e_crash = crash && alive && !(seen & 4);
-            const bool e_lf = F.edge_hit && alive && !(seen & 8);
-            const int rnow = e_goal ? 1 : (e_crash ? 3 : (e_lf ? 4 : (e_coll ? 2 : 0)));
-            int seen_new = seen | (rnow == 0 ? 0 : 1 << (rnow == 1 ? 0 : rnow == 2 ? 1 : rnow == 3 ? 2 : 3));
+            const int rnow = R.rnow;
             const double sparse = rnow == 1 ? k.goal_weight
                                 : rnow == 2 ? -k.collision_weight
                                 : rnow == 3 ? -k.crash_weight
                                 : rnow == 4 ? -k.lane_forbidden_weight : 0.0;
+            const bool alive = F.alive;
             const double reward = alive ? total + sparse : 0.0;
-            int reason = F.reason;
-            bool done = false;
-            if (!A.d.invincible) {
-                done = rnow != 0;
-                if (done && reason == 0) reason = rnow;
-            }
-            // tail: timeout, park, alive (engine.py:370-393)
-            const int step_new = step_now + 1;
-            const bool timeout = step_new >= A.d.episode_len && alive;
-            const bool finished = done || timeout;
-            if (timeout && reason == 0) reason = 5;
-            const bool park = done && !timeout;
-            int alive_new = alive && !finished;
 
             if (A.metric_seen && (rnow == 1 || rnow == 2)) A.metric_seen[am] |= uint8_t(rnow == 1 ? 1 : 2);
             O.rewards[am] = reward;
-            O.dones[am] = finished;
+            O.dones[am] = uint8_t(R.finished);
             reinterpret_cast<uint32_t*>(O.events)[am] =
                 uint32_t(rnow == 1) | (uint32_t(rnow == 2) << 8) | (uint32_t(rnow == 3) << 16) |
                 (uint32_t(rnow == 4) << 24);
-            if (O.reason_out) O.reason_out[am] = int8_t(reason);
-            if (O.alive_out) O.alive_out[am] = uint8_t(alive_new);
+            if (O.reason_out) O.reason_out[am] = int8_t(R.reason);
+            if (O.alive_out) O.alive_out[am] = uint8_t(R.alive_new);
             if (O.alive_pre_out) O.alive_pre_out[am] = uint8_t(alive);
             if (O.ttc_min_out) O.ttc_min_out[am] = F.ttc_min;
             if (O.terms_out) {
@@ -681,46 +769,16 @@ __device__ __forceinline__ unsigned finalize_agent(const KArgs& A, const TickOut
 #pragma unroll
                 for (int f = 0; f < DG_NUM_STATE; ++f) O.snapshot_out[int64_t(f) * WM + am] = F.st[f];
             }
-            double x[DG_NUM_STATE];
-#pragma unroll
-            for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = F.st[f];
-            if (park) {
-#pragma unroll
-                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
-                x[SX] = ox + k.offstage_x;
-                x[SY] = oy;
-            }
-            int spawn = F.spawn;
-            if (A.autoreset && finished && F.valid) {
-#pragma unroll
-                for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = (f == SBF || f == SBR) ? 1.0 : 0.0;
-                x[SX] = F.sx;
-                x[SY] = F.sy;
-                x[SYAW] = F.start_yaw;
-                alive_new = 1;
-                reason = 0;
-                spawn = step_new;
-                seen_new = 0;
-            }
-            if (F.store_global) {
-#pragma unroll
-                for (int f = 0; f < DG_NUM_STATE; ++f) A.state[int64_t(f) * WM + am] = x[f];
-                A.alive[am] = uint8_t(alive_new);
-                A.reason[am] = int8_t(reason);
-                A.event_seen[am] = uint8_t(seen_new);
-                A.spawn_step[am] = spawn;
-            }
-            if (F.st_out) {
-#pragma unroll
-                for (int f = 0; f < DG_NUM_STATE; ++f) F.st_out[f] = x[f];
-                F.flags_out[0] = alive_new;
-                F.flags_out[1] = reason;
-                F.flags_out[2] = seen_new;
-                F.flags_out[3] = spawn;
-            }
-            return (rnow == 0 ? 0u : 1u << (rnow == 1 ? 0 : rnow == 2 ? 1 : rnow == 3 ? 2 : 3)) |
-                   (alive ? 16u : 0u) | (finished ? kBitFinished : 0u);
-        }
+}
+
+// decide + emit in one pass (the split kernels and the unpipelined fused tail)
+__device__ __forceinline__ unsigned finalize_agent(const KArgs& A, const TickOut& O, int w, int m, const FinIn& F,
+                                                   int step_now, double ox, double oy) {
+    int seen_new;
+    const TailRes R = tail_events(A, F, step_now, &seen_new);
+    emit_agent(A, O, w, m, F, R);
+    return tail_state(A, w, m, F, R, seen_new, step_now, ox, oy);
+}
 
 // Episode counters [W][5] (goal, collision, crash, lane_forbidden, alive
 // agent-ticks), accumulated over ticks: warp-reduced, one add per counter.
@@ -883,6 +941,35 @@ __device__ __forceinline__ void zero_obs_block(float* base, int64_t n, const flo
     }
 }
 
+// FinIn of an agent from its tick record and scan results; with lanes, the
+// nearest-lane terms from the scene's lane table (emit_agent needs them,
+// decide_agent does not).  Flags default to the record's.
+__device__ __forceinline__ FinIn fin_in(const AgentSm& S, const ScanSm& R, const SceneView& G, bool lanes) {
+    FinIn F;
+    F.st = S.st;
+    F.c = S.c;
+    F.s = S.s;
+    F.px0 = S.px0; F.py0 = S.py0; F.gx = S.gx; F.gy = S.gy; F.sx = S.sx; F.sy = S.sy;
+    F.lane_d2 = R.lane_d2;
+    F.lane_lat = 0.0; F.lane_tx = 0.0; F.lane_ty = 0.0;
+    if (lanes && R.lane_d2 < INFINITY) {
+        const double4 l4 = G.lane_seg[R.lane_k];
+        const double ex = S.st[SX] - l4.x, ey = S.st[SY] - l4.y;
+        F.lane_tx = l4.z;
+        F.lane_ty = l4.w;
+        F.lane_lat = l4.z * ey - l4.w * ex;
+    }
+    F.ttc_min = R.ttc_min; F.gap = R.gap;
+    F.edge_hit = R.edge_hit; F.touch = R.touch;
+    F.alive = S.alive; F.valid = S.valid;
+    F.reason = S.reason; F.seen = S.seen; F.spawn = S.spawn;
+    F.start_yaw = S.start_yaw;
+    F.store_global = false;
+    F.st_out = nullptr;
+    F.flags_out = nullptr;
+    return F;
+}
+
 // Which phase-2 work units a scan warp takes: 2a units = ego pairs (egos 2u,
 // 2u + 1), 2b units = groups of `apw` agents.  Default: both kinds strided over
 // the warps (every warp one of each at 8 warps).  kSpec (7 scan warps beside
@@ -948,8 +1035,11 @@ world_step_kernel(const KArgs A) {
     AgentSm* const ag_home = reinterpret_cast<AgentSm*>(smem + align16(A.d.max_scene_bytes));
     AgentSm* const ag_rst = ag_home + 2 * kMaxAgents;
     AgentSm* ag = ag_home;
-    ScanSm* sc = reinterpret_cast<ScanSm*>(ag_home + 3 * kMaxAgents);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sc + kMaxAgents);
+    // scan results: two tables (kSpec: tick t's scans write table t & 1 while the
+    // physics warp emits tick t - 1's outputs from the other); tail decisions
+    ScanSm* const sc_base = reinterpret_cast<ScanSm*>(ag_home + 3 * kMaxAgents);
+    TailRes* const tail_sm = reinterpret_cast<TailRes*>(sc_base + 2 * kMaxAgents);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tail_sm + kMaxAgents);
     uint16_t* cand_sm = reinterpret_cast<uint16_t*>(bar + 2);   // [M][take_road]
     float4* zero_sm = reinterpret_cast<float4*>(
         smem + align16(reinterpret_cast<uint8_t*>(cand_sm + kMaxAgents * A.take_road) - smem));  // [kZeroChunk/16]
@@ -1030,7 +1120,19 @@ world_step_kernel(const KArgs A) {
         if constexpr (kSpec) ag = ag_home + (t & 1) * kMaxAgents;
         AgentSm* const agn = ag_home + ((t + 1) & 1) * kMaxAgents;   // kSpec: tick t + 1
         (void)agn;
+        ScanSm* const sc = sc_base + (kSpec ? (t & 1) * kMaxAgents : 0);
         const int slot = A.ring_slots > 0 ? (A.ring_start + t) % A.ring_slots : t;
+        // kSpec pipeline: the outputs of tick t - 1 (decided at its end) are
+        // emitted by the physics warp while tick t's scans run
+        auto emit_prev = [&]() {
+            const int tp = t - 1;
+            if (lane < M) {
+                const int sp = A.ring_slots > 0 ? (A.ring_start + tp) % A.ring_slots : tp;
+                const FinIn F = fin_in(ag_home[(tp & 1) * kMaxAgents + lane], sc_base[(tp & 1) * kMaxAgents + lane],
+                                       G, true);
+                emit_agent(A, tick_out(A, sp), w, lane, F, tail_sm[lane]);
+            }
+        };
         float* obs_w = A.obs + (int64_t(slot) * WM + int64_t(w) * M) * D;
         int32_t* ix_w = A.index_out ? A.index_out + (int64_t(slot) * WM + int64_t(w) * M) * A.index_stride
                                     : nullptr;
@@ -1050,6 +1152,7 @@ world_step_kernel(const KArgs A) {
             if (!kSpec) __syncthreads();
             if (s_bad != DG_NO_ERROR) {
                 // ticks 0..t-1 stand (as t separate step calls would leave them)
+                if (kSpec && warp == 0) emit_prev();
                 if (warp == 0 && lane < M) {
                     const int64_t am = int64_t(w) * M + lane;
                     const AgentSm& S = ag_home[lane];
@@ -1087,7 +1190,8 @@ world_step_kernel(const KArgs A) {
         // the zero background of the world's obs block: TMA bulk stores from a
         // zeroed shared buffer, issued by one thread of a warp that is idle
         // during the physics; unaligned head/tail floats by plain stores
-        if ((!kSpec || t == 0) && warp == (nwarps > 1 ? 1 : 0)) zero_obs_block(obs_w, int64_t(M) * D, zero_sm, lane);
+        if ((!kSpec || t == 0) && !A.obs_resident && warp == (nwarps > 1 ? 1 : 0))
+            zero_obs_block(obs_w, int64_t(M) * D, zero_sm, lane);
 
         if (warp == 0) PHASE_MARK(2);
         __syncthreads();  // agent table + zero rows done, mbarrier init visible
@@ -1132,8 +1236,12 @@ world_step_kernel(const KArgs A) {
             // the next tick's zero background: TMA bulk stores issued now, completed
             // before the tick's closing barrier -- they stream out under the scans
             // and the tail (a slot shared by consecutive ticks is cleared in the tail)
+            if (kStep && t > 0) {
+                emit_prev();
+                __syncwarp();
+            }
             const int slot1 = A.ring_slots > 0 ? (A.ring_start + t + 1) % A.ring_slots : t + 1;
-            zero_early = t + 1 < T && slot1 != slot;
+            zero_early = t + 1 < T && slot1 != slot && !A.obs_resident;
 #ifdef DG_EXP_NOZERO
             zero_early = false;
 #endif
@@ -1172,6 +1280,7 @@ world_step_kernel(const KArgs A) {
                 if (go) agent_physics(A, w, rst ? ag_rst[m] : agn[m], x0, alive, raw, alive != 0);
             }
             TT_WACC(31);
+            if (zero_early) bulk_commit_and_wait();   // the next slot's clear, before the scans of t + 1
         } else {
         // ---- phase 2a: agent pairs.  kPL lanes per ego agent, each lane owns the other
         //      agents j = jl + kPL * u (u < 16 / kPL): 16 lanes x 1 at 8 warps per world,
@@ -1276,8 +1385,16 @@ world_step_kernel(const KArgs A) {
                 if (ix_w || A.prefix_out) {
                     for (int o = kPL / 2; o > 0; o >>= 1) n_valid += __shfl_xor_sync(kFull, n_valid, o, kPL);
                     if (ix_w && ego_ok && jl == 0) ix_w[int64_t(ii) * A.index_stride + 2] = n_valid;
-                    if (A.prefix_out && ego_ok && jl == 0)
-                        A.prefix_out[(int64_t(slot) * WM + int64_t(w) * M + ii) * 2 + 1] = int16_t(7 * n_valid);
+                    if (A.prefix_out && ego_ok) {
+                        int16_t* pre = A.prefix_out + (int64_t(slot) * WM + int64_t(w) * M + ii) * 2 + 1;
+                        // resident obs: the row holds zeros past its previous prefix; clear
+                        // only the rows the previous tick of this slot had beyond n_valid
+                        const int old_v = A.obs_resident ? min(int(*pre), 7 * A.d.k_vehicles) : 0;
+                        __syncwarp(gmask);
+                        if (jl == 0) *pre = int16_t(7 * n_valid);
+                        if (old_v > 7 * n_valid)
+                            zero_span(obs_w + int64_t(ii) * D + veh0 + 7 * n_valid, old_v - 7 * n_valid, jl, kPL);
+                    }
                 }
 
                 if (kStep && A.drac_max) {
@@ -1395,8 +1512,14 @@ world_step_kernel(const KArgs A) {
             int32_t* ix_m = ix_w ? ix_w + int64_t(act ? m : kAPW * pr) * A.index_stride : nullptr;
             if (act) {
                 if (ix_m && hl == 0) ix_m[1] = ncand;
-                if (A.prefix_out && hl == 0)
-                    A.prefix_out[(int64_t(slot) * WM + int64_t(w) * M + m) * 2] = int16_t(5 * ncand);
+                if (A.prefix_out) {
+                    int16_t* pre = A.prefix_out + (int64_t(slot) * WM + int64_t(w) * M + m) * 2;
+                    // resident obs: the previous prefix (0x7fff: slot written elsewhere -> all)
+                    const int old_r = A.obs_resident ? min(int(*pre), 5 * A.d.k_road) : 0;
+                    __syncwarp(kGMask << hshift);
+                    if (hl == 0) *pre = int16_t(5 * ncand);
+                    if (old_r > 5 * ncand) zero_span(row + road0 + 5 * ncand, old_r - 5 * ncand, hl, kGL);
+                }
                 for (int slot = hl; slot < ncand; slot += kGL) {
                     const int q = cand[slot];
                     if (ix_m) ix_m[3 + A.take_veh + slot] = q;
@@ -1512,36 +1635,29 @@ world_step_kernel(const KArgs A) {
         }
         if constexpr (kStep) {
             if (warp == 0 && lane < M) {
+                // kSpec: decide now (events, termination, the state tick t + 1 starts
+                // from), emit the outputs during tick t + 1's scans -- or here after
+                // the last tick; otherwise both here
                 const int m = lane;
                 AgentSm& S = ag[m];
-                const ScanSm& R = sc[m];
-                FinIn F;
-                F.st = S.st;
-                F.c = S.c;
-                F.s = S.s;
-                F.px0 = S.px0; F.py0 = S.py0; F.gx = S.gx; F.gy = S.gy; F.sx = S.sx; F.sy = S.sy;
-                F.lane_d2 = R.lane_d2;
-                F.lane_lat = 0.0; F.lane_tx = 0.0; F.lane_ty = 0.0;
-                if (R.lane_d2 < INFINITY) {
-                    const double4 l4 = G.lane_seg[R.lane_k];
-                    const double ex = S.st[SX] - l4.x, ey = S.st[SY] - l4.y;
-                    F.lane_tx = l4.z;
-                    F.lane_ty = l4.w;
-                    F.lane_lat = l4.z * ey - l4.w * ex;
-                }
-                F.ttc_min = R.ttc_min; F.gap = R.gap;
-                F.edge_hit = R.edge_hit; F.touch = R.touch;
                 AgentSm& H = ag_home[m];
-                F.alive = S.alive; F.valid = S.valid;
-                F.reason = kSpec ? H.flags_next[1] : S.reason;
-                F.seen = kSpec ? H.flags_next[2] : S.seen;
-                F.spawn = kSpec ? H.flags_next[3] : S.spawn;
-                F.start_yaw = S.start_yaw;
+                FinIn F = fin_in(S, sc[m], G, !kSpec || t + 1 == T);
+                if (kSpec) {
+                    F.reason = H.flags_next[1];
+                    F.seen = H.flags_next[2];
+                    F.spawn = H.flags_next[3];
+                }
                 F.store_global = t + 1 == T;
                 F.st_out = H.st_next;
                 F.flags_out = H.flags_next;
                 TT_ACC(5);
-                const unsigned bits = finalize_agent(A, O, w, m, F, step_now + t, ox, oy);
+                unsigned bits;
+                if constexpr (kSpec) {
+                    bits = decide_agent(A, w, m, F, step_now + t, ox, oy, &tail_sm[m]);
+                    if (t + 1 == T) emit_agent(A, O, w, m, F, tail_sm[m]);
+                } else {
+                    bits = finalize_agent(A, O, w, m, F, step_now + t, ox, oy);
+                }
                 TT_ACC(6);
                 count_events(A, w, bits, __activemask(), lane == 0, false);
                 TT_ACC(7);
@@ -1570,16 +1686,12 @@ world_step_kernel(const KArgs A) {
                 }
             }
 
-            if (kSpec && warp == pw && t + 1 < T) {
-                if (zero_early) {
-                    bulk_commit_and_wait();
-                } else {   // consecutive ticks share the slot: clear it after this tick's writes
+            if (kSpec && warp == pw && t + 1 < T && !zero_early && !A.obs_resident) {
 #ifndef DG_EXP_NOZERO
-                    const int slot1 = A.ring_slots > 0 ? (A.ring_start + t + 1) % A.ring_slots : t + 1;
-                    zero_obs_block(A.obs + (int64_t(slot1) * WM + int64_t(w) * M) * D, int64_t(M) * D, zero_sm,
-                                   lane);
+                // consecutive ticks share the slot: clear it after this tick's scans
+                const int slot1 = A.ring_slots > 0 ? (A.ring_start + t + 1) % A.ring_slots : t + 1;
+                zero_obs_block(A.obs + (int64_t(slot1) * WM + int64_t(w) * M) * D, int64_t(M) * D, zero_sm, lane);
 #endif
-                }
             }
             if (tid == 0) A.step_count[w] = step_now + t + 1;
             PHASE_MARK(6);
@@ -2404,7 +2516,8 @@ static size_t split_smem_bytes(int take_road, int apc) {
 
 static size_t step_smem_bytes(const DgDims& d, int take_road) {
     size_t b = size_t(align16(d.max_scene_bytes));
-    b += sizeof(AgentSm) * 3 * kMaxAgents + sizeof(ScanSm) * kMaxAgents;   // three agent tables
+    b += sizeof(AgentSm) * 3 * kMaxAgents;                                  // three agent tables
+    b += sizeof(ScanSm) * 2 * kMaxAgents + sizeof(TailRes) * kMaxAgents;   // scan results x2, tail decisions
     b += 16;  // mbarrier
     b += sizeof(uint16_t) * kMaxAgents * size_t(take_road > 0 ? take_road : 1);
     b = size_t(align16(int64_t(b))) + kZeroChunk;
@@ -2533,6 +2646,7 @@ int dg_step(dg_engine* eng, const DgStepIO* io, void* stream) {
     A.metric_seen = io->metric_seen;
     A.index_out = io->index_out;
     A.prefix_out = io->prefix_out;
+    A.obs_resident = io->obs_resident && io->prefix_out && eng->mode != 1;
     A.ticks = io->ticks > 0 ? io->ticks : 1;
     A.ring_slots = io->ring_slots > 0 ? io->ring_slots : A.ticks;
     A.ring_start = io->ring_start;

@@ -20,6 +20,7 @@ a CUDA device or without the native library raises.
 from __future__ import annotations
 
 import ctypes as ct
+import os
 import time
 import weakref
 from dataclasses import dataclass
@@ -281,7 +282,7 @@ class StepOutput:
         return self._info
 
 
-@dataclass
+@dataclass(eq=False)
 class StepBuffers:
     """Preallocated device outputs for the zero-allocation path (bench,
     rollouts).  ``obs`` may be any [W][M][D] float32 view, e.g. one slot of
@@ -290,6 +291,20 @@ class StepBuffers:
     obs: torch.Tensor
     aux: torch.Tensor
     views: dict
+    # resident ring (new_rollout_buffers): per slot and agent the length of the road /
+    # vehicle block prefix that can be non-zero; past it every float of the slot is
+    # zero, so the step kernel clears only what a row's new content no longer covers
+    # (DgStepIO.obs_resident).  The obs of a resident ring belong to the engine:
+    # write them only through it (observe(out=slot) re-marks the slot).
+    prefix: torch.Tensor | None = None
+
+    def mark_dirty(self, slot: int | None = None) -> None:
+        """The obs of ``slot`` (None: every slot) were written outside the
+        engine's steps: the next step into it clears the whole blocks."""
+        if self.prefix is not None:
+            p = self.prefix if slot is None else self.prefix[slot]
+            p[..., 0] = 0x7fff
+            p[..., 1] = 0x7fff
 
 
 class Engine:
@@ -439,6 +454,7 @@ class Engine:
         self._mapped_pool = MappedSlabPool(self._lib, self._host_blob.numel(), W * M, dev)
         self.d2h_bytes = torch.zeros(1, dtype=torch.int64, device=dev)   # obs bytes written by dg_to_host
         self._prefix_dev = torch.zeros((W, M, 2), dtype=torch.int16, device=dev)   # non-zero obs prefixes
+        self._resident = weakref.WeakSet()     # resident rollout rings of this engine
         self.launches = 0
         self._metrics_on = False
         self._host_lay = None
@@ -502,13 +518,24 @@ class Engine:
     def new_step_buffers(self, obs: torch.Tensor | None = None) -> StepBuffers:
         return self._new_buffers(obs)
 
-    def new_rollout_buffers(self, slots: int) -> StepBuffers:
+    def new_rollout_buffers(self, slots: int, resident: bool | None = None) -> StepBuffers:
         """Ring of ``slots`` per-tick outputs for ``launch_step(ticks=...)``:
-        obs [S][W][M][D] and every aux view with a leading slot axis."""
+        obs [S][W][M][D] and every aux view with a leading slot axis.  A
+        resident ring (zeroed once, with its prefix record) lets every later
+        step clear only the spans of its rows that the new content no longer
+        covers instead of the whole 7.7 KB row."""
+        if resident is None:
+            resident = os.environ.get("DG_RESIDENT", "1") != "0"
         _, total = self._aux_layout(slots)
         aux = torch.zeros(total, dtype=torch.uint8, device=self.device)   # padding defined (initcheck)
-        obs = torch.empty((slots, self.W, self.M, self.obs_config.obs_dim), dtype=torch.float32,
-                          device=self.device)
+        shape = (slots, self.W, self.M, self.obs_config.obs_dim)
+        if resident:
+            obs = torch.zeros(shape, dtype=torch.float32, device=self.device)
+            prefix = torch.zeros((slots, self.W, self.M, 2), dtype=torch.int16, device=self.device)
+            bufs = StepBuffers(obs, aux, self._views(aux, slots), prefix)
+            self._resident.add(bufs)
+            return bufs
+        obs = torch.empty(shape, dtype=torch.float32, device=self.device)
         return StepBuffers(obs, aux, self._views(aux, slots))
 
     def launch_shape(self) -> dict:
@@ -668,6 +695,8 @@ class Engine:
         """Observation of the current state (engine.py:297-300); with
         ``next_actions`` the LaneFollower actions for it are fused in."""
         obs = out if out is not None else torch.empty_like(self._obs_dev)
+        if out is not None:
+            self._mark_written(out)
         N.check(self._lib, self._lib.dg_observe(self._h, _ptr(obs), _ptr(ttc_min), _ptr(next_actions),
                                                 float(steer_gain), float(throttle), self._stream()),
                 "dg_observe")
@@ -675,6 +704,18 @@ class Engine:
         if as_numpy:
             return obs.cpu().numpy()
         return obs
+
+    def _mark_written(self, out: torch.Tensor) -> None:
+        """``out`` is about to be written outside a step: a resident ring slot it
+        lies in loses its prefix record."""
+        lo, hi = out.data_ptr(), out.data_ptr() + out.numel() * out.element_size()
+        for b in list(self._resident):
+            base = b.obs.data_ptr()
+            per = b.obs[0].numel() * b.obs.element_size()
+            end = base + per * b.obs.shape[0]
+            if lo < end and hi > base:
+                first, last = max(lo - base, 0) // per, (min(hi, end) - base - 1) // per
+                b.prefix[first:last + 1] = 0x7fff
 
     def observe_device(self, out: torch.Tensor | None = None) -> torch.Tensor:
         return self.observe(out=out, as_numpy=False)
@@ -708,6 +749,9 @@ class Engine:
         order (layout: ``DgStepIO.index_out`` in the C header).  ``prefix_out``
         (int16 [S][W][M][2]) receives per agent the length of the road / vehicle
         block prefix that can be non-zero (``DgStepIO.prefix_out``)."""
+        resident = prefix_out is None and bufs.prefix is not None
+        if resident:
+            prefix_out = bufs.prefix
         if self._shape["mode"] == "split" and (ticks > 1 or bufs.obs.dim() == 4):
             # the split kernels take one tick per launch and write one output
             # set: tick t goes to ring slot (ring_start + t) % S through views
@@ -729,14 +773,14 @@ class Engine:
                                        or prefix_out.numel() % (self.W * self.M * 2)):
             raise ValueError("prefix_out must be a contiguous int16 CUDA tensor of [S][W][M][2]")
         io = self._step_io(actions, bufs, autoreset, snapshot, terms, next_actions, steer_gain, throttle,
-                           event_counts, ticks, ring_start, drac_max, metric_seen, index_out, prefix_out)
+                           event_counts, ticks, ring_start, drac_max, metric_seen, index_out, prefix_out, resident)
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), self._stream()), "dg_step")
         self._step_count += int(ticks)
         self.launches += 1
 
     def _step_io(self, actions, bufs, autoreset=False, snapshot=True, terms=True, next_actions=None,
                  steer_gain=2.0, throttle=0.5, event_counts=None, ticks=1, ring_start=0, drac_max=None,
-                 metric_seen=None, index_out=None, prefix_out=None):
+                 metric_seen=None, index_out=None, prefix_out=None, resident=False):
         if self._metrics_on:
             drac_max = self._drac_max if drac_max is None else drac_max
             metric_seen = self._metric_seen if metric_seen is None else metric_seen
@@ -755,7 +799,7 @@ class Engine:
                         event_counts=event_counts.data_ptr() if event_counts is not None else None,
                         ticks=int(ticks), ring_slots=int(slots), ring_start=int(ring_start),
                         drac_max=_ptr(drac_max), metric_seen=_ptr(metric_seen), index_out=_ptr(index_out),
-                        prefix_out=_ptr(prefix_out))
+                        prefix_out=_ptr(prefix_out), obs_resident=int(bool(resident)))
         if index_out is not None:
             want = (slots, self.W, self.M, self.index_stride)
             if (index_out.dtype != torch.int32 or not index_out.is_cuda or not index_out.is_contiguous()
@@ -879,7 +923,11 @@ class Engine:
             self.launch_step(acts, bufs, autoreset=autoreset, ticks=1, ring_start=slot,
                              event_counts=event_counts)
             obs = bufs.obs[slot] if bufs.obs.dim() == 4 else bufs.obs
+            pre = None
+            if bufs.prefix is not None:   # the step just wrote this slot's valid-slot prefixes
+                pre = bufs.prefix[slot] if bufs.prefix.dim() == 4 else bufs.prefix
             policy.forward(obs, actions=acts, value=None if values is None else values[t], sample=sample,
+                           prefix=pre,
                            seed=seed, counter=counter0 + t,
                            log_prob=None if log_probs is None else log_probs[t],
                            actions_f32=None if actions_out is None else actions_out[t])
@@ -925,8 +973,10 @@ class Engine:
         io = self._host_io.get(key)
         if io is None:
             # the host path always uses the same device buffers: build its DgStepIO once
+            # the host path's obs buffer is the engine's own: resident (zeroed at
+            # construction, written only by these steps)
             io = self._host_io[key] = self._step_io(self._act_dev, bufs, autoreset=autoreset,
-                                                    prefix_out=self._prefix_dev)
+                                                    prefix_out=self._prefix_dev, resident=True)
         stream = torch.cuda.current_stream(self.device)
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), ct.c_void_p(stream.cuda_stream)), "dg_step")
         self._step_count += 1

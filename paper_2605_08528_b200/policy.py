@@ -187,7 +187,7 @@ class PolicyMLP:
                 mean: torch.Tensor | None = None, value: torch.Tensor | None = None,
                 sample: bool = False, seed: int = 0, counter: int = 0,
                 log_prob: torch.Tensor | None = None, actions_f32: torch.Tensor | None = None,
-                nets: str = "both") -> None:
+                nets: str = "both", prefix: torch.Tensor | None = None) -> None:
         """Enqueue the forward over every observation row of ``obs``
         ([..., obs_dim] float32, CUDA).  ``actions`` ([..., 3] float64) gets
         the next tick's env input: the actor mean, or with ``sample`` a draw
@@ -196,7 +196,9 @@ class PolicyMLP:
         ``actions_f32`` ([..., 3]) a float32 copy; ``mean`` ([..., 3] f32),
         ``value`` ([...] f32, needs critic=True).  ``nets``: "both" (default),
         "actor" (no value) or "critic" (value only) -- the two halves can run
-        on different streams."""
+        on different streams.  ``prefix`` (int16 [..., 2], the step's
+        ``prefix_out`` for these rows) gives the valid road / vehicle slot counts
+        so the encoder does not scan the rows for them."""
         if nets not in ("both", "actor", "critic"):
             raise ValueError(f"nets must be 'both', 'actor' or 'critic', not {nets!r}")
         if nets == "actor":
@@ -229,13 +231,17 @@ class PolicyMLP:
                            sample=int(bool(sample)), seed=int(seed) & (2 ** 64 - 1),
                            counter=int(counter) & (2 ** 64 - 1),
                            log_prob=log_prob.data_ptr() if log_prob is not None else None,
-                           actions_f32=actions_f32.data_ptr() if actions_f32 is not None else None)
+                           actions_f32=actions_f32.data_ptr() if actions_f32 is not None else None,
+                           prefix=prefix.data_ptr() if prefix is not None else None)
         for i, o in enumerate(self._offs):
             d.off[i] = o
         for t, dt in ((actions, torch.float64), (mean, torch.float32), (value, torch.float32),
                       (log_prob, torch.float32), (actions_f32, torch.float32)):
             if t is not None and (t.dtype != dt or not t.is_cuda or not t.is_contiguous()):
                 raise ValueError("policy outputs must be contiguous CUDA tensors of the documented dtype")
+        if prefix is not None and (prefix.dtype != torch.int16 or not prefix.is_cuda or not prefix.is_contiguous()
+                                   or prefix.numel() != 2 * n):
+            raise ValueError("prefix must be a contiguous int16 CUDA tensor of [..., 2] per observation row")
         st = ct.c_void_p(torch.cuda.current_stream(obs.device).cuda_stream)
         rc = lib.dg_policy_forward(ct.byref(d), st)
         if rc != N.DG_OK:
