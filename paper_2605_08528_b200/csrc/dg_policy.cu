@@ -62,6 +62,18 @@ __device__ __forceinline__ float elu_log2(float y) {
     return y > 0.0f ? y : fmaf(e, kLog2e, -kLog2e);
 }
 
+#ifdef DG_EXP_ELU2
+__device__ __forceinline__ uint32_t elu_log2_bf16x2(float lo, float hi) {
+    const uint32_t y = umma::pack_bf16(lo, hi);
+    uint32_t m, e, r, o;
+    asm("min.bf16x2 %0, %1, %2;" : "=r"(m) : "r"(y), "r"(0u));
+    asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(e) : "r"(m));
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(e), "r"(0x3FB93FB9u), "r"(0xBFB9BFB9u));
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(o) : "r"(y), "r"(r));
+    return o;
+}
+#endif
+
 // float <-> order-preserving unsigned (0 = "no value yet")
 __device__ __forceinline__ uint32_t f2o(float x) {
     const uint32_t b = __float_as_uint(x);
@@ -297,10 +309,22 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
 #pragma unroll
                 for (int cc = 0; cc < 3; ++cc) {
                     umma::tmem_wait16(raw + 16 * cc);
+#ifdef DG_EXP_ELU2
+                    uint32_t h[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        h[i] = elu_log2_bf16x2(__uint_as_float(raw[16 * cc + 2 * i]),
+                                               __uint_as_float(raw[16 * cc + 2 * i + 1]));
+                    const int c = c0 + 16 * cc;
+                    *reinterpret_cast<uint4*>(A1 + umma::kmajor_offset(r, c, kHid)) = make_uint4(h[0], h[1], h[2], h[3]);
+                    *reinterpret_cast<uint4*>(A1 + umma::kmajor_offset(r, c + 8, kHid)) =
+                        make_uint4(h[4], h[5], h[6], h[7]);
+#else
                     float v[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) v[i] = elu_log2(__uint_as_float(raw[16 * cc + i]));
                     store_row16(A1, r, c0 + 16 * cc, kHid, v);
+#endif
                 }
             }
             umma::fence_async_smem();

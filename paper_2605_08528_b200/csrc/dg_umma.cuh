@@ -84,7 +84,11 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "UMMA_WAIT_%=:\n\t"
+#ifdef DG_EXP_SUSPEND
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+#else
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+#endif
         "@!p bra UMMA_WAIT_%=;\n}"
         ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }

@@ -822,12 +822,19 @@ __device__ __forceinline__ long long gtimer() { long long t; asm volatile("mov.u
 // check, phase 1, phase 2 incl. its barrier, tail, closing barrier), 8 + w the
 // scan time of warp w, 30 / 31 the physics warp's ego block / physics.
 #ifdef DG_TICK_TIMERS
+// per-CTA cycle sums in shared memory (one writer per slot), copied out once at
+// the end of the launch: no global read-modify-write inside the timed ticks
 __device__ long long g_tick_acc[65536][40];
-#define TT_DECL long long tt_last = clock64(), tt_w = 0; (void)tt_w
-#define TT_ACC(i) do { if (threadIdx.x == 0) { const long long n_ = clock64(); g_tick_acc[blockIdx.x][i] += n_ - tt_last; tt_last = n_; } } while (0)
+#define TT_DECL __shared__ long long s_tt[40]; \
+    if (threadIdx.x < 40) s_tt[threadIdx.x] = 0; \
+    __syncthreads(); \
+    long long tt_last = clock64(), tt_w = 0; (void)tt_w
+#define TT_ACC(i) do { if (threadIdx.x == 0) { const long long n_ = clock64(); s_tt[i] += n_ - tt_last; tt_last = n_; } } while (0)
 #define TT_WSTART() do { if ((threadIdx.x & 31) == 0) tt_w = clock64(); } while (0)
-#define TT_WACC(i) do { if ((threadIdx.x & 31) == 0) { const long long n_ = clock64(); g_tick_acc[blockIdx.x][i] += n_ - tt_w; tt_w = n_; } } while (0)
+#define TT_WACC(i) do { if ((threadIdx.x & 31) == 0) { const long long n_ = clock64(); s_tt[i] += n_ - tt_w; tt_w = n_; } } while (0)
+#define TT_FLUSH() do { __syncthreads(); if (threadIdx.x < 40) g_tick_acc[blockIdx.x][threadIdx.x] = s_tt[threadIdx.x]; } while (0)
 #else
+#define TT_FLUSH() do { } while (0)
 #define TT_DECL do { } while (0)
 #define TT_ACC(i) do { } while (0)
 #define TT_WSTART() do { } while (0)
@@ -1702,6 +1709,7 @@ world_step_kernel(const KArgs A) {
         if (t + 1 < T) __syncthreads();   // next tick reads st_next / act written above
         TT_ACC(4);
     }
+    TT_FLUSH();
 }
 
 // ----------------------------------------------------------------- split launch mode

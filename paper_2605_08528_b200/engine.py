@@ -910,28 +910,59 @@ class Engine:
                       autoreset: bool = False, values: torch.Tensor | None = None,
                       event_counts: torch.Tensor | None = None, sample: bool = False, seed: int = 0,
                       counter0: int = 0, log_probs: torch.Tensor | None = None,
-                      actions_out: torch.Tensor | None = None) -> None:
+                      actions_out: torch.Tensor | None = None, overlap_critic: bool = True) -> None:
         """Enqueue ``ticks`` x (step launch -> policy forward): tick t reads
         ``acts`` ([W][M][3] float64) and the policy overwrites it with the next
         tick's actions (the mean, or a Philox draw with ``sample``, counter
         ``counter0 + t``); per tick t: ``values[t]``, ``log_probs[t]``,
         ``actions_out[t]`` (the action chosen on tick t's observation).  No
-        sync, no checks (the fast path of ``rollout`` and the bench)."""
+        sync, no checks (the fast path of ``rollout`` and the bench).
+
+        With ``overlap_critic`` the value head -- which no later tick depends on
+        -- runs on a side stream, so only step -> actor forward is on the
+        rollout's critical path; the side stream joins the current one before
+        this returns (also under CUDA-graph capture), and a ring slot is not
+        overwritten before the critic has read it."""
         slots = bufs.obs.shape[0] if bufs.obs.dim() == 4 else 1
+        side = None
+        if values is not None and overlap_critic:
+            side = self._side_stream()
+            main = torch.cuda.current_stream(self.device)
+            side.wait_stream(main)
+            done = [None] * int(ticks)          # critic of tick t has read its slot
         for t in range(int(ticks)):
             slot = (ring_start + t) % slots
+            if side is not None and t >= slots and done[t - slots] is not None:
+                main.wait_event(done[t - slots])   # the step below overwrites the slot of tick t - slots
             self.launch_step(acts, bufs, autoreset=autoreset, ticks=1, ring_start=slot,
                              event_counts=event_counts)
             obs = bufs.obs[slot] if bufs.obs.dim() == 4 else bufs.obs
             pre = None
             if bufs.prefix is not None:   # the step just wrote this slot's valid-slot prefixes
                 pre = bufs.prefix[slot] if bufs.prefix.dim() == 4 else bufs.prefix
-            policy.forward(obs, actions=acts, value=None if values is None else values[t], sample=sample,
-                           prefix=pre,
-                           seed=seed, counter=counter0 + t,
+            if side is not None:
+                ready = torch.cuda.Event()
+                ready.record(main)
+            policy.forward(obs, actions=acts, value=None if values is None or side is not None else values[t],
+                           sample=sample, prefix=pre, seed=seed, counter=counter0 + t,
                            log_prob=None if log_probs is None else log_probs[t],
-                           actions_f32=None if actions_out is None else actions_out[t])
+                           actions_f32=None if actions_out is None else actions_out[t],
+                           nets="actor" if side is not None else "both")
             self.launches += policy.launches()
+            if side is not None:
+                side.wait_event(ready)
+                with torch.cuda.stream(side):
+                    policy.forward(obs, value=values[t], prefix=pre, nets="critic")
+                    done[t] = torch.cuda.Event()
+                    done[t].record(side)
+                self.launches += policy.launches()
+        if side is not None:
+            torch.cuda.current_stream(self.device).wait_stream(side)
+
+    def _side_stream(self) -> torch.cuda.Stream:
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(self.device)
+        return self._side
 
     def step(self, actions, autoreset: bool = False) -> StepOutput:
         """One 30 Hz control tick (engine.py:334-406)."""

@@ -17,7 +17,7 @@ for r in rows:
     if r and r[0] == "File Path":
         fname = r[1]
         continue
-    if not (fname.endswith("drivegrid_b200.cu") or fname.endswith(sys.argv[-1] if sys.argv[-1].endswith(".cu") else "drivegrid_b200.cu")):
+    if not ((fname.endswith("drivegrid_b200.cu") or fname.endswith("dg_policy.cu") or fname.endswith("dg_umma.cuh")) or fname.endswith(sys.argv[-1] if sys.argv[-1].endswith(".cu") else "drivegrid_b200.cu")):
         continue
     if r and r[0] == "Line No":
         hdr = r

@@ -5,7 +5,15 @@ import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import os  # noqa: E402
+
 import torch  # noqa: E402
+
+from paper_2605_08528_b200 import _native as N  # noqa: E402
+
+if os.environ.get("DG_LIB_PATH"):          # a variant build (tools/policy_variants.py)
+    N.LIB_PATH = Path(os.environ["DG_LIB_PATH"])
+    N.load_library(build_if_missing=False)
 
 from paper_2605_08528_b200 import config as C  # noqa: E402
 from paper_2605_08528_b200.engine import Engine  # noqa: E402
