@@ -61,10 +61,11 @@ typedef struct DgDims {
                                  blob in shared memory by TMA and adds the grid
                                  offset); 1: blobs are per world, already moved
                                  by the offset, read in place from global memory
-                                 by the split kernels (scenes too large for the
-                                 227 KB of shared memory; dg_step then takes
-                                 ticks = 1, written to ring slot ring_start,
-                                 and dg_tune only mode 1)                      */
+                                 by the fused kernel's global-geometry variants
+                                 (modes 0 and 2, multi-tick) or the split
+                                 kernels (mode 1: ticks = 1, written to ring
+                                 slot ring_start) -- scenes too large for the
+                                 227 KB of shared memory                       */
 } DgDims;
 
 /* Float64 scalars, precomputed on the host with the reference's expression

@@ -1017,7 +1017,11 @@ __device__ __forceinline__ ScanSchedule scan_schedule(int M, int apw, int warp, 
 }
 
 // ----------------------------------------------------------------- the fused step kernel
-template <bool kStep, int kThreads, int kMinBlocks, bool kSpec>
+// kGeoGlobal: the world's geometry is a per-world blob already moved by the grid
+// offset, read in place from global memory (L1 / L2) -- scenes too large for
+// shared memory (DgDims.geometry_global); otherwise the scene blob is staged in
+// shared memory by TMA and offset there.
+template <bool kStep, int kThreads, int kMinBlocks, bool kSpec, bool kGeoGlobal>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 world_step_kernel(const KArgs A) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -1039,7 +1043,7 @@ world_step_kernel(const KArgs A) {
     //      table 2 takes tick t + 1 of agents teleported back to their start); the
     //      rollout carry (st_next, flags_next, act) lives in table 0
     uint8_t* geo = smem;
-    AgentSm* const ag_home = reinterpret_cast<AgentSm*>(smem + align16(A.d.max_scene_bytes));
+    AgentSm* const ag_home = reinterpret_cast<AgentSm*>(smem + (kGeoGlobal ? 0 : align16(A.d.max_scene_bytes)));
     AgentSm* const ag_rst = ag_home + 2 * kMaxAgents;
     AgentSm* ag = ag_home;
     // scan results: two tables (kSpec: tick t's scans write table t & 1 while the
@@ -1084,7 +1088,7 @@ world_step_kernel(const KArgs A) {
         }
         step_now = A.step_count[w];
     }
-    if (tid == 0) {
+    if (!kGeoGlobal && tid == 0) {
         mbar_init(bar, 1);
         bulk_load(geo, A.scene_blob + meta[0], uint32_t(meta[1]), bar);
     }
@@ -1203,7 +1207,10 @@ world_step_kernel(const KArgs A) {
         if (warp == 0) PHASE_MARK(2);
         __syncthreads();  // agent table + zero rows done, mbarrier init visible
         PHASE_MARK(3);
-        if (t == 0) {
+        if (kGeoGlobal && t == 0) {
+            G = scene_view(const_cast<uint8_t*>(A.scene_blob + meta[0]), A.scene_blob + meta[5], int(meta[2]),
+                           int(meta[3]), int(meta[4]));
+        } else if (t == 0) {
             mbar_wait(bar, 0);
             // the view reads the index header from the copied blob: only after the wait
             G = scene_view(geo, A.scene_blob + meta[5], int(meta[2]), int(meta[3]), int(meta[4]));
@@ -2394,8 +2401,9 @@ struct dg_engine {
 };
 
 #define DG_VARIANTS(X)                                                                 \
-    X(512, 1, false) X(512, 2, false) X(256, 2, false) X(256, 3, false) X(256, 4, false)  \
-    X(128, 4, false) X(128, 6, false) X(128, 8, false) X(256, 2, true)
+    X(512, 1, false, false) X(512, 2, false, false) X(256, 2, false, false) X(256, 3, false, false) \
+    X(256, 4, false, false) X(128, 4, false, false) X(128, 6, false, false) X(128, 8, false, false) \
+    X(256, 2, true, false) X(256, 2, false, true) X(128, 4, false, true) X(256, 2, true, true)
 
 // Kernel variants: (threads per CTA, min resident CTAs per SM) bounds trade
 // registers for occupancy; dg_tune picks one.  The kSpec variant is up to 7
@@ -2406,11 +2414,12 @@ template <bool kStep>
 static cudaError_t launch_world_step(const dg_engine* e, const KArgs& A, cudaStream_t st) {
     const int nw = e->warps_per_world;
     const bool spec = e->mode == 2;
+    const bool geo = A.d.geometry_global != 0;
     const int threads = variant_threads(nw, spec);
     const dim3 grid(A.d.W);
-#define DG_LAUNCH(T, B, S)                                                               \
-    if (threads == T && e->min_blocks == B && spec == S) {                               \
-        world_step_kernel<kStep, T, B, S><<<grid, 32 * (nw + (S ? 1 : 0)), e->smem_bytes, st>>>(A); \
+#define DG_LAUNCH(T, B, S, G)                                                            \
+    if (threads == T && e->min_blocks == B && spec == S && geo == G) {                   \
+        world_step_kernel<kStep, T, B, S, G><<<grid, 32 * (nw + (S ? 1 : 0)), e->smem_bytes, st>>>(A); \
         return cudaGetLastError();                                                       \
     }
     DG_VARIANTS(DG_LAUNCH)
@@ -2436,15 +2445,15 @@ static cudaError_t raise_smem_limit(K kernel) {
 template <bool kStep>
 static cudaError_t set_smem_attr(size_t) {
     cudaError_t e = cudaSuccess;
-#define DG_ATTR(T, B, S)                                                                 \
-    if (e == cudaSuccess) e = raise_smem_limit(world_step_kernel<kStep, T, B, S>);
+#define DG_ATTR(T, B, S, G)                                                              \
+    if (e == cudaSuccess) e = raise_smem_limit(world_step_kernel<kStep, T, B, S, G>);
     DG_VARIANTS(DG_ATTR)
 #undef DG_ATTR
     return e;
 }
 
-static bool has_variant(int threads, int blocks, bool spec) {
-#define DG_HAS(T, B, S) if (threads == T && blocks == B && spec == S) return true;
+static bool has_variant(int threads, int blocks, bool spec, bool geo) {
+#define DG_HAS(T, B, S, G) if (threads == T && blocks == B && spec == S && geo == G) return true;
     DG_VARIANTS(DG_HAS)
 #undef DG_HAS
     return false;
@@ -2523,7 +2532,7 @@ static size_t split_smem_bytes(int take_road, int apc) {
 }
 
 static size_t step_smem_bytes(const DgDims& d, int take_road) {
-    size_t b = size_t(align16(d.max_scene_bytes));
+    size_t b = d.geometry_global ? 0 : size_t(align16(d.max_scene_bytes));   // global: read in place
     b += sizeof(AgentSm) * 3 * kMaxAgents;                                  // three agent tables
     b += sizeof(ScanSm) * 2 * kMaxAgents + sizeof(TailRes) * kMaxAgents;   // scan results x2, tail decisions
     b += 16;  // mbarrier
@@ -2609,14 +2618,13 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
     e->min_blocks = 1;
     e->mode = 0;
     if (d.geometry_global) {
-        // per-world blobs stay in global memory: the split kernels, which read
-        // the geometry in place (the fused kernel stages it in shared memory)
-        if (!A.scratch) {
-            delete e;
-            return fail(DG_EINVAL, "dg_create: geometry_global needs the scratch buffer");
-        }
-        e->mode = 1;
-        e->warps_per_world = 4;
+        // per-world blobs stay in global memory, read in place: by the split
+        // kernels when the scratch buffer is there (measured 2x faster than the
+        // fused kernel's kGeoGlobal variants on the dense 6,000-segment scene:
+        // a warp per agent beats a 16-lane group on 350-row road blocks), else
+        // by the fused kernel (dg_tune picks either later)
+        e->mode = A.scratch ? 1 : 0;
+        e->warps_per_world = 4 < d.M ? 4 : d.M;
         e->min_blocks = 4;
     }
     *out = e;
@@ -2871,8 +2879,6 @@ int dg_tune(dg_engine* eng, int32_t mode, int32_t warps_per_world, int32_t ctas_
     }
     if (mode != 0 && mode != 2)
         return fail(DG_EINVAL, "dg_tune: mode must be 0 (fused), 1 (split) or 2 (fused, physics warp)");
-    if (eng->base.d.geometry_global)
-        return fail(DG_ENOSUPPORT, "dg_tune: geometry_global engines run the split kernels (mode 1)");
     if (warps_per_world < 1 || warps_per_world > kMaxAgents)
         return fail(DG_EINVAL, "dg_tune: warps_per_world must lie in [1, 16]");
     const int nw = warps_per_world < eng->base.d.M ? warps_per_world : eng->base.d.M;
@@ -2880,7 +2886,8 @@ int dg_tune(dg_engine* eng, int32_t mode, int32_t warps_per_world, int32_t ctas_
     if (spec && nw > 7) return fail(DG_EINVAL, "dg_tune: mode 2 takes at most 7 scan warps");
     const int threads = variant_threads(nw, spec);
     int blocks = ctas_per_sm > 0 ? ctas_per_sm : (threads == 512 ? 1 : threads >= 256 ? 2 : 4);
-    if (!has_variant(threads, blocks, spec)) return fail(DG_EINVAL, "dg_tune: no kernel variant for this shape");
+    if (!has_variant(threads, blocks, spec, eng->base.d.geometry_global != 0))
+        return fail(DG_EINVAL, "dg_tune: no kernel variant for this shape");
     eng->warps_per_world = nw;
     eng->min_blocks = blocks;
     eng->mode = mode;

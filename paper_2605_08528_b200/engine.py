@@ -422,8 +422,16 @@ class Engine:
         self.geometry_global = bool(desc.dims.geometry_global)
         self._h = handle
         self._desc = desc
-        if self.geometry_global:
-            # global-memory geometry: the split kernels (dg_create already chose them)
+        if self.geometry_global and launch_mode in (0, 2):
+            # global-memory geometry on the fused kernel's kGeoGlobal variants
+            # (multi-tick launches): 4 warps x 4 CTAs/SM, or mode 2
+            if launch_mode == 2:
+                self.tune(min(M, 7), 0, mode=2)
+            else:
+                self.tune(warps_per_world or min(M, 4), 4 if M > 4 else 0)
+        elif self.geometry_global:
+            # global-memory geometry: the split kernels, one warp per agent (2x the
+            # fused variant on the dense 6,000-segment scene, tools/dense_scene_timing.py)
             self.tune(warps_per_world if warps_per_world in (2, 4, 8) else 4, 0, mode=1)
         elif launch_mode == 1:
             self.tune(warps_per_world or 4, 0, mode=1)

@@ -113,6 +113,30 @@ def test_global_geometry_rollout_loops_ticks(device):
         assert torch.allclose(getattr(ra, k).double(), getattr(rb, k).double(), rtol=1e-9, atol=1e-9), k
 
 
+@pytest.mark.parametrize("mode", [0, 2])
+def test_global_geometry_fused_variants(mode, device):
+    """The fused kernel's global-geometry variants (kGeoGlobal: geometry read in
+    place, multi-tick launches) on the dense scene give exactly the split
+    kernels' outputs, tick by tick and over a 12-tick rollout launch."""
+    case = case_inputs("traj_dense")
+    a = Engine(**case.inputs.as_kwargs(), device=device)                       # split
+    b = Engine(**case.inputs.as_kwargs(), device=device, launch_mode=mode)     # fused, global geometry
+    assert a.geometry_global and b.geometry_global and b.launch_shape()["mode"] != "split"
+    pol = LaneFollower(obs_config=a.obs_config)
+    obs = a.observe()
+    assert np.array_equal(obs, b.observe())
+    for t in range(6):
+        oa, ob = a.step(pol(obs)), b.step(pol(obs))
+        assert np.array_equal(oa.obs, ob.obs) and np.array_equal(oa.rewards, ob.rewards)
+        assert np.array_equal(oa.dones, ob.dones)
+        obs = oa.obs
+    a0 = a.lane_follower(a.observe_device())
+    ra = a.rollout(a0.clone(), ticks=12, policy="lane_follower", autoreset=True)
+    rb = b.rollout(a0.clone(), ticks=12, policy="lane_follower", autoreset=True)
+    assert torch.equal(ra.obs, rb.obs) and torch.equal(ra.rewards, rb.rewards)
+    assert all(np.array_equal(a.state[k], b.state[k]) for k in STATE_FIELDS)
+
+
 def test_oversized_scene_runs_from_global_memory(device):
     case = case_inputs("traj_dense")
     eng = Engine(**case.inputs.as_kwargs(), device=device)

@@ -11,6 +11,11 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch  # noqa: E402
 
+from paper_2605_08528_b200 import _native as N  # noqa: E402
+
+if os.environ.get("DG_LIB_PATH"):          # a variant build (tools/step_variants.py)
+    N.LIB_PATH = Path(os.environ["DG_LIB_PATH"])
+    N.load_library(build_if_missing=False)
 from paper_2605_08528_b200 import config as C  # noqa: E402
 from paper_2605_08528_b200.engine import Engine  # noqa: E402
 
@@ -27,6 +32,9 @@ for st in settings:
         os.environ[k] = v
     for W, R, n in ((256, 20, 10), (256, 64, 4), (4096, 64, 2)):
         eng = Engine(**inputs[W].as_kwargs(), device=dev)
+        if W <= 296 and os.environ.get("SWEEP_SHAPE"):          # "warps:mode", e.g. 8:2
+            nw, md = (int(v) for v in os.environ["SWEEP_SHAPE"].split(":"))
+            eng.tune(nw, 0, mode=md)
         M, D = eng.M, eng.obs_config.obs_dim
         ring = max(2, -(-(300 << 20) // (W * M * D * 4)))
         rb = eng.new_rollout_buffers(ring)
