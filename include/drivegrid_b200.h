@@ -361,6 +361,14 @@ typedef struct DgPolicyDesc {
                                    rows (5 n_r, 7 n_v: the valid road / vehicle slots of
                                    each observation row), or NULL: the encoder finds the
                                    counts by scanning the rows                        */
+    int32_t* work_counter;      /* [2] zero-initialised int32 (device), or NULL: the
+                                   encoder's work queue -- persistent CTAs take (net,
+                                   agent group, modality) items by one atomic each;
+                                   entry first_net is used and reset to 0 by the
+                                   forward's second kernel, so one buffer serves every
+                                   forward on a stream (an actor-only and a
+                                   critic-only forward may run concurrently).  NULL:
+                                   one CTA per (agent group, net)                   */
 } DgPolicyDesc;
 
 /* One forward of the policy over every agent's observation row: 2 kernel

@@ -74,7 +74,7 @@ class DgPolicyDesc(ct.Structure):
         ("obs", _P), ("weights", _P), ("net_stride", ct.c_int64), ("off", ct.c_int64 * len(POL_SECTIONS)),
         ("emb", _P), ("mean", _P), ("actions", _P), ("value", _P),
         ("sample", ct.c_int32), ("first_net", ct.c_int32), ("seed", ct.c_uint64), ("counter", ct.c_uint64),
-        ("log_prob", _P), ("actions_f32", _P), ("prefix", _P)]
+        ("log_prob", _P), ("actions_f32", _P), ("prefix", _P), ("work_counter", _P)]
 
 
 class DgStepIO(ct.Structure):

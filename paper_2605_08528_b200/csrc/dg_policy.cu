@@ -142,9 +142,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const DgPolicyDesc p) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int net = blockIdx.y + p.first_net;
-    const int a0 = blockIdx.x * kEncAgents;
-    const int na = min(kEncAgents, p.n_agents - a0);
+    __shared__ int s_item;
     uint8_t* A0 = sm + EncSmem::kA0;
     uint8_t* A1 = sm + EncSmem::kA1;
     uint8_t* W1 = sm + EncSmem::kW1;
@@ -174,9 +172,37 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
     const uint32_t lane_base = uint32_t(32 * q) << 16;
     const int c0 = 48 * hf;
     uint32_t phase = 0;
-    const uint8_t* wb = net_base(p, net);
+    uint32_t wphase = 0;           // parity of the weights barrier (one TMA load per item)
+    const int nets = p.first_net == 1 ? 1 : (p.critic ? 2 : 1);
+    const int n_groups = (p.n_agents + kEncAgents - 1) / kEncAgents;
+    const int n_items = 2 * nets * n_groups;
+    int step = 0;
 
-    for (int mod = 0; mod < 2; ++mod) {
+    // Work items (net, agent group, modality).  With the work queue (persistent
+    // CTAs, about three per SM): the road items (twice the tiles) first, then the
+    // vehicle items, handed out by one atomic per item -- no tail of idle SMs
+    // behind the last wave.  Without: this CTA's group of its net, both modalities.
+    for (;;) {
+        int net, g, mod;
+        if (p.work_counter) {
+            if (tid == 0) s_item = atomicAdd(p.work_counter + p.first_net, 1);
+            __syncthreads();
+            const int item = s_item;
+            if (item >= n_items) break;
+            mod = item / (nets * n_groups);
+            const int rem = item - mod * nets * n_groups;
+            net = p.first_net + rem / n_groups;
+            g = rem - (rem / n_groups) * n_groups;
+        } else {
+            if (step == 2) break;
+            mod = step;
+            net = blockIdx.y + p.first_net;
+            g = blockIdx.x;
+        }
+        ++step;
+        const int a0 = g * kEncAgents;
+        const int na = min(kEncAgents, p.n_agents - a0);
+        const uint8_t* wb = net_base(p, net);
         const int nf = mod == 0 ? 5 : 7;
         const int kslots = mod == 0 ? p.k_road : p.k_vehicles;
         const int fbase = mod == 0 ? p.ego_dim : p.ego_dim + 5 * p.k_road;
@@ -291,7 +317,7 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
             umma::fence_before();
             __syncthreads();
             if (tid == 0) {
-                if (t0 == 0) umma::bar_wait(bar + 1, uint32_t(mod));   // weights landed
+                if (t0 == 0) umma::bar_wait(bar + 1, wphase);        // weights landed
                 umma::fence_after();
                 umma::gemm_128xN(tmem, A0, W1, kHid, 16);
                 umma::commit(bar);
@@ -398,6 +424,8 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
             const float v1 = u1 ? elu(o2f(u1) + b2[c + 1]) : 0.0f;
             *reinterpret_cast<uint32_t*>(out + int64_t(a) * kEmb + c) = umma::pack_bf16(v0, v1);
         }
+        if (S == 0 && tid == 0) umma::bar_wait(bar + 1, wphase);   // no tile waited: retire the weight load
+        wphase ^= 1u;
         __syncthreads();
     }
     umma::fence_before();
@@ -483,6 +511,8 @@ __global__ void __launch_bounds__(kTrunkThreads, 1) policy_trunk_kernel(const Dg
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + TrunkSmem::kBar + 32);
 
     const uint8_t* wb = net_base(p, net);
+    // the encoder's work queue is drained (stream order): re-arm it for the next forward
+    if (p.work_counter && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) p.work_counter[p.first_net] = 0;
     if (warp == 0) umma::tmem_alloc(tmem_slot, 256);
     if (tid == 32) {
         // weights by TMA bulk copies, one mbarrier each, so the ego layers start
@@ -708,7 +738,16 @@ int dg_policy_forward(const DgPolicyDesc* desc, void* stream) {
         if (dev >= 0 && dev < 64) attr_set[dev] = true;
     }
     if (enc > 200 * 1024) return pol_fail(DG_ENOSUPPORT, "dg_policy_forward: encoder shared memory too large");
-    dim3 g1((p.n_agents + kEncAgents - 1) / kEncAgents, nets);
+    const int groups = (p.n_agents + kEncAgents - 1) / kEncAgents;
+    dim3 g1(groups, nets);
+    if (p.work_counter) {
+        // persistent: as many CTAs as are resident at once (3 per SM), never more than items
+        static int n_sm[64] = {};
+        if (dev >= 0 && dev < 64 && n_sm[dev] == 0) cudaDeviceGetAttribute(&n_sm[dev], cudaDevAttrMultiProcessorCount, dev);
+        const int sms = dev >= 0 && dev < 64 && n_sm[dev] > 0 ? n_sm[dev] : 148;
+        const int items = 2 * nets * groups;
+        g1 = dim3(items < 3 * sms ? items : 3 * sms, 1);
+    }
     policy_encoder_kernel<<<g1, kEncThreads, enc, st>>>(p);
     dim3 g2((p.n_agents + kTrunkAgents - 1) / kTrunkAgents, nets);
     policy_trunk_kernel<<<g2, kTrunkThreads, TrunkSmem::kTotal, st>>>(p);

@@ -104,6 +104,7 @@ class PolicyMLP:
         self.log_std = torch.zeros(3)
         self._blob = None
         self._emb = None
+        self._work = torch.zeros(2, dtype=torch.int32, device=self.device)   # encoder work queues (actor, critic)
 
     @staticmethod
     def _linear(fin, fout, g):
@@ -232,7 +233,8 @@ class PolicyMLP:
                            counter=int(counter) & (2 ** 64 - 1),
                            log_prob=log_prob.data_ptr() if log_prob is not None else None,
                            actions_f32=actions_f32.data_ptr() if actions_f32 is not None else None,
-                           prefix=prefix.data_ptr() if prefix is not None else None)
+                           prefix=prefix.data_ptr() if prefix is not None else None,
+                           work_counter=self._work.data_ptr())
         for i, o in enumerate(self._offs):
             d.off[i] = o
         for t, dt in ((actions, torch.float64), (mean, torch.float32), (value, torch.float32),
