@@ -13,8 +13,17 @@ from paper_2605_08528_b200 import _native as N  # noqa: E402
 
 variants = [a.split("=", 1) for a in sys.argv[1:]]
 for name, flags in variants:
-    subprocess.run(["/usr/local/cuda/bin/nvcc", *N.NVCC_FLAGS, *flags.split(), "-I", str(ROOT / "include"),
-                    "-o", f"/tmp/libdg_{name}.so", *map(str, N.SOURCES)], check=True, capture_output=True)
+    # "--src=PATH" swaps the step-kernel source (e.g. a committed revision, git show REV:path > PATH)
+    srcs = [str(x) for x in N.SOURCES]
+    fl = []
+    for f in flags.split():
+        if f.startswith("--src="):
+            srcs[0] = f[len("--src="):]
+        else:
+            fl.append(f)
+    subprocess.run(["/usr/local/cuda/bin/nvcc", *N.NVCC_FLAGS, *fl, "-I", str(ROOT / "include"),
+                    "-I", str(ROOT / "paper_2605_08528_b200" / "csrc"), "-o", f"/tmp/libdg_{name}.so", *srcs],
+                   check=True, capture_output=True)
 for rnd in range(2):
     for name, flags in variants:
         env = dict(os.environ, DG_LIB_PATH=f"/tmp/libdg_{name}.so", SWEEP_COUNT="1")

@@ -46,7 +46,7 @@ for sh in shapes:
     eng.launch_step(acts, rb, autoreset=True, next_actions=acts, ticks=T)
     s1.record()
     torch.cuda.synchronize()
-    out = np.zeros((W, 40), dtype=np.int64)
+    out = np.zeros((W, 48), dtype=np.int64)
     assert lib.dg_debug_tick_clocks(out.ctypes.data, W, 0) == 0
     per = out / T
     names = ["check", "phase1", "phase2+bar", "tail-rest", "end-bar"]
@@ -59,6 +59,11 @@ for sh in shapes:
           f"count_events {np.median(per[:, 7]):.0f}  rest {np.median(per[:, 3]):.0f}")
     print("  pairs (2a) per warp (median over CTAs):", np.median(per[:, 20:20 + nw], axis=0).astype(int))
     print("  scans (2b) per warp (median over CTAs):", np.median(per[:, 8:8 + nw], axis=0).astype(int))
+    sub = per[:, 32:41]
+    if sub.any():
+        print("  2a sub-phases per 2a warp slot (key+rank | ttc+rows+contact | reduce+store):",
+              np.median(sub[:, 0:3], axis=0).astype(int), np.median(sub[:, 3:6], axis=0).astype(int),
+              np.median(sub[:, 6:9], axis=0).astype(int))
     if mode == 2:
         print(f"  physics warp: zero-issue {np.median(per[:, 29]):.0f}  ego {np.median(per[:, 30]):.0f}  "
               f"physics {np.median(per[:, 31]):.0f}")
