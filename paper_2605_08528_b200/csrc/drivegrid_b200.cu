@@ -824,15 +824,15 @@ __device__ __forceinline__ long long gtimer() { long long t; asm volatile("mov.u
 #ifdef DG_TICK_TIMERS
 // per-CTA cycle sums in shared memory (one writer per slot), copied out once at
 // the end of the launch: no global read-modify-write inside the timed ticks
-__device__ long long g_tick_acc[65536][40];
-#define TT_DECL __shared__ long long s_tt[40]; \
-    if (threadIdx.x < 40) s_tt[threadIdx.x] = 0; \
+__device__ long long g_tick_acc[65536][48];
+#define TT_DECL __shared__ long long s_tt[48]; \
+    if (threadIdx.x < 48) s_tt[threadIdx.x] = 0; \
     __syncthreads(); \
     long long tt_last = clock64(), tt_w = 0; (void)tt_w
 #define TT_ACC(i) do { if (threadIdx.x == 0) { const long long n_ = clock64(); s_tt[i] += n_ - tt_last; tt_last = n_; } } while (0)
 #define TT_WSTART() do { if ((threadIdx.x & 31) == 0) tt_w = clock64(); } while (0)
 #define TT_WACC(i) do { if ((threadIdx.x & 31) == 0) { const long long n_ = clock64(); s_tt[i] += n_ - tt_w; tt_w = n_; } } while (0)
-#define TT_FLUSH() do { __syncthreads(); if (threadIdx.x < 40) g_tick_acc[blockIdx.x][threadIdx.x] = s_tt[threadIdx.x]; } while (0)
+#define TT_FLUSH() do { __syncthreads(); if (threadIdx.x < 48) g_tick_acc[blockIdx.x][threadIdx.x] = s_tt[threadIdx.x]; } while (0)
 #else
 #define TT_FLUSH() do { } while (0)
 #define TT_DECL do { } while (0)
@@ -1346,6 +1346,7 @@ world_step_kernel(const KArgs A) {
                             }
                         }
                     }
+                TT_WACC(32 + (warp & 7) % 3);     // 2a sub-timers: key + rank
                 double ttc = k.ttc_max;
                 bool touch = false;
                 double dr = 0.0;
@@ -1394,6 +1395,7 @@ world_step_kernel(const KArgs A) {
                         dr = d1 > dr ? d1 : dr;
                     }
                 }
+                TT_WACC(35 + (warp & 7) % 3);     // TTC, rows, contact
                 ttc = warp_min(ttc, kPL);
                 touch = (__ballot_sync(kFull, touch) & gmask) != 0;
                 if (ix_w || A.prefix_out) {
@@ -1424,6 +1426,7 @@ world_step_kernel(const KArgs A) {
                     sc[ii].touch = touch;
                     if (!kStep && A.ttc_min_out) A.ttc_min_out[int64_t(w) * M + ii] = ttc;
                 }
+                TT_WACC(38 + (warp & 7) % 3);     // reductions, prefix, sc
             }
         }
 
@@ -2845,12 +2848,12 @@ int dg_debug_tick_clocks(long long* host_out, int n_blocks, int reset) {
     const int n = n_blocks < 65536 ? n_blocks : 65536;
     cudaError_t e;
     if (reset) {
-        static long long zeros[65536 * 40 / 64];
+        static long long zeros[65536 * 48 / 64];
         e = cudaSuccess;
         for (int i = 0; i < 64 && e == cudaSuccess; ++i)
             e = cudaMemcpyToSymbol(g_tick_acc, zeros, sizeof(zeros), sizeof(zeros) * i);
     } else {
-        e = cudaMemcpyFromSymbol(host_out, g_tick_acc, sizeof(long long) * 40 * n);
+        e = cudaMemcpyFromSymbol(host_out, g_tick_acc, sizeof(long long) * 48 * n);
     }
     return e == cudaSuccess ? DG_OK : cuda_fail(e, "dg_debug_tick_clocks");
 }
