@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 11
+#define DG_ABI_VERSION 12
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -196,6 +196,15 @@ typedef struct DgStepIO {
                                    (5 n_r) and vehicle block (7 n_v) that can be
                                    non-zero -- the rest of the row is zero
                                    (dg_to_host moves only these prefixes)      */
+    uint64_t* phase_cycles;     /* [5] or NULL: device cycles spent per phase of
+                                   the reference's phase_seconds (engine.py:33,
+                                   342-395) -- action, physics, observation,
+                                   reward_termination, reset -- summed over the
+                                   warps that run them (lane 0 of each warp times
+                                   its own segments), added to the 5 counters.
+                                   Phases run concurrently on different warps,
+                                   so they measure where the device work goes,
+                                   not a wall-clock split.  Fused modes only.  */
 } DgStepIO;
 
 typedef struct dg_engine dg_engine;

@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 11
+ABI_VERSION = 12
 
 
 class DgDims(ct.Structure):
@@ -86,7 +86,7 @@ class DgStepIO(ct.Structure):
                                               ("ticks", ct.c_int32), ("ring_slots", ct.c_int32),
                                               ("ring_start", ct.c_int32), ("obs_resident", ct.c_int32),
                                               ("drac_max", _P), ("metric_seen", _P), ("index_out", _P),
-                                              ("prefix_out", _P)]
+                                              ("prefix_out", _P), ("phase_cycles", _P)]
 
 
 class DgScenePool(ct.Structure):

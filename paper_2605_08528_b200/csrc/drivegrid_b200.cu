@@ -101,6 +101,7 @@ struct KArgs {
     int32_t index_stride; // 3 + take_veh + take_road
     int16_t* prefix_out;  // [slot][W][M][2] non-zero obs prefix: 5 n_r, 7 n_v floats (NULL = off)
     int32_t obs_resident; // 1: obs slots keep zeros beyond prefix_out's recorded prefixes
+    unsigned long long* phase_cycles; // [5] device cycles per phase, summed (NULL = off)
 };
 
 // ----------------------------------------------------------------- numpy-semantics helpers
@@ -841,6 +842,16 @@ __device__ long long g_tick_acc[65536][48];
 #define TT_WACC(i) do { } while (0)
 #endif
 
+// ---- per-phase device cycles (DgStepIO.phase_cycles, the reference's
+// phase_seconds: action, physics, observation, reward_termination, reset).
+// Lane 0 of every warp adds the cycles it spends in each phase to a shared
+// counter; one global add per phase at the end of the launch.  Off (one
+// predicated branch per mark) when the pointer is NULL.
+enum { PH_ACTION = 0, PH_PHYSICS, PH_OBSERVATION, PH_REWARD, PH_RESET };
+#define PH_START() do { if (ph_on && (threadIdx.x & 31) == 0) ph_t = clock64(); } while (0)
+#define PH_ADD(i) do { if (ph_on && (threadIdx.x & 31) == 0) { const long long n_ = clock64(); \
+    atomicAdd(&s_ph[i], (unsigned long long)(n_ - ph_t)); ph_t = n_; } } while (0)
+
 // The raw (unclipped) actions of tick t for agent am: the fused policy's
 // shared-memory record when `fed` is given, else the caller's [T][W][M][3] array.
 __device__ __forceinline__ void load_actions(const KArgs& A, int t, int64_t am, const double* fed, double* raw) {
@@ -1021,7 +1032,10 @@ __device__ __forceinline__ ScanSchedule scan_schedule(int M, int apw, int warp, 
 // offset, read in place from global memory (L1 / L2) -- scenes too large for
 // shared memory (DgDims.geometry_global); otherwise the scene blob is staged in
 // shared memory by TMA and offset there.
-template <bool kStep, int kThreads, int kMinBlocks, bool kSpec, bool kGeoGlobal>
+// kPhase: the per-phase cycle counters are compiled in (DgStepIO.phase_cycles;
+// instantiated for the engine's default shapes, launched only when requested --
+// they cost the plain variants 2-3 % in registers even when off)
+template <bool kStep, int kThreads, int kMinBlocks, bool kSpec, bool kGeoGlobal, bool kPhase = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
 world_step_kernel(const KArgs A) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -1037,6 +1051,10 @@ world_step_kernel(const KArgs A) {
     const int D = A.d.obs_dim;
     const DgConsts& k = A.k;
     TT_DECL;
+    __shared__ unsigned long long s_ph[5];
+    const bool ph_on = kPhase && A.phase_cycles != nullptr;
+    long long ph_t = 0;
+    if (ph_on && tid < 5) s_ph[tid] = 0;
 
     // ---- shared memory carve-up: three agent tables (kSpec: tick t is read from
     //      table t & 1 while the physics warp writes tick t + 1 into the other, and
@@ -1072,6 +1090,7 @@ world_step_kernel(const KArgs A) {
     GT_MARK(32);
     PHASE_MARK(0);
     int step_now = 0;
+    PH_START();
     if constexpr (kStep) {
         if (tid == 0) s_bad = DG_NO_ERROR;
         __syncthreads();
@@ -1087,6 +1106,7 @@ world_step_kernel(const KArgs A) {
             return;
         }
         step_now = A.step_count[w];
+        PH_ADD(PH_ACTION);
     }
     if (!kGeoGlobal && tid == 0) {
         mbar_init(bar, 1);
@@ -1195,14 +1215,19 @@ world_step_kernel(const KArgs A) {
             S.seen = H.flags_next[2];
             S.spawn = H.flags_next[3];
             double raw[3] = {0.0, 0.0, 0.0};
+            PH_START();
             if (kStep && H.flags_next[0]) load_actions(A, t, am, t > 0 && feedback ? H.act : nullptr, raw);
             agent_physics(A, w, S, H.st_next, H.flags_next[0], raw, kStep && H.flags_next[0]);
+            PH_ADD(PH_PHYSICS);
         }
         // the zero background of the world's obs block: TMA bulk stores from a
         // zeroed shared buffer, issued by one thread of a warp that is idle
         // during the physics; unaligned head/tail floats by plain stores
-        if ((!kSpec || t == 0) && !A.obs_resident && warp == (nwarps > 1 ? 1 : 0))
+        if ((!kSpec || t == 0) && !A.obs_resident && warp == (nwarps > 1 ? 1 : 0)) {
+            PH_START();
             zero_obs_block(obs_w, int64_t(M) * D, zero_sm, lane);
+            PH_ADD(PH_OBSERVATION);
+        }
 
         if (warp == 0) PHASE_MARK(2);
         __syncthreads();  // agent table + zero rows done, mbarrier init visible
@@ -1250,9 +1275,11 @@ world_step_kernel(const KArgs A) {
             // the next tick's zero background: TMA bulk stores issued now, completed
             // before the tick's closing barrier -- they stream out under the scans
             // and the tail (a slot shared by consecutive ticks is cleared in the tail)
+            PH_START();
             if (kStep && t > 0) {
                 emit_prev();
                 __syncwarp();
+                PH_ADD(PH_REWARD);
             }
             const int slot1 = A.ring_slots > 0 ? (A.ring_start + t + 1) % A.ring_slots : t + 1;
             zero_early = t + 1 < T && slot1 != slot && !A.obs_resident;
@@ -1271,6 +1298,7 @@ world_step_kernel(const KArgs A) {
             if (!rst && m < M)
                 write_ego(obs_w + int64_t(m) * D, k, A, w, am, S.st[SX], S.st[SY], S.c, S.s, S.st[SVX], S.st[SVY],
                           S.gx, S.gy, feedback ? H.act : nullptr);
+            PH_ADD(PH_OBSERVATION);
             TT_WACC(30);
             __syncwarp();
             if (kStep && t + 1 < T && m < M) {
@@ -1281,6 +1309,7 @@ world_step_kernel(const KArgs A) {
                     for (int j = 0; j < 3; ++j)
                         if (!finite(raw[j])) atomicMin(&s_bad, int((t + 1) * act_tick + am * 3 + j));
                 }
+                PH_ADD(PH_ACTION);
                 const bool go = !rst || (A.autoreset && S.valid);
                 double x0[DG_NUM_STATE];
 #pragma unroll
@@ -1292,6 +1321,7 @@ world_step_kernel(const KArgs A) {
                 }
                 const int alive = rst ? 1 : S.alive;
                 if (go) agent_physics(A, w, rst ? ag_rst[m] : agn[m], x0, alive, raw, alive != 0);
+                PH_ADD(PH_PHYSICS);
             }
             TT_WACC(31);
             if (zero_early) bulk_commit_and_wait();   // the next slot's clear, before the scans of t + 1
@@ -1300,6 +1330,7 @@ world_step_kernel(const KArgs A) {
         //      agents j = jl + kPL * u (u < 16 / kPL): 16 lanes x 1 at 8 warps per world,
         //      8 lanes x 2 at 4 warps (four egos per warp in one pass).  Stable distance
         //      rank, swept-circle TTC, neighbour rows, hull contact, optional DRAC.
+        PH_START();
         const int road0 = A.d.ego_dim;
         const int veh0 = A.d.ego_dim + 5 * A.d.k_road;
         const ScanSchedule sched = scan_schedule<kSpec>(M, kThreads <= 128 ? 4 : 2, warp, nwarps);
@@ -1432,6 +1463,7 @@ world_step_kernel(const KArgs A) {
 
         W1_MARK(34);
         TT_WACC(20 + warp);
+        PH_ADD(PH_OBSERVATION);
         // ---- phase 2b: each lane group scans the scene for one agent -- a warp takes
         //      kAPW consecutive agents (16 lanes x 2 at 8 warps per world, 8 lanes x 4 at
         //      4 warps), so the agents' dependent load / reduction chains overlap in one
@@ -1635,6 +1667,7 @@ world_step_kernel(const KArgs A) {
             }
         }
         TT_WACC(8 + warp);
+        PH_ADD(PH_OBSERVATION);
         }   // phase 2 (kSpec: the scan warps)
         WARP_MARK(0);
         __syncthreads();
@@ -1647,8 +1680,10 @@ world_step_kernel(const KArgs A) {
         const int ego_warp = nwarps > 1 ? 1 : 0;
         if (!kSpec && warp == ego_warp && lane < M) {
             AgentSm& S = ag[lane];
+            PH_START();
             write_ego(obs_w + int64_t(lane) * D, k, A, w, int64_t(w) * M + lane, S.st[SX], S.st[SY], S.c, S.s,
                       S.st[SVX], S.st[SVY], S.gx, S.gy, feedback ? S.act : nullptr);
+            PH_ADD(PH_OBSERVATION);
         }
         if constexpr (kStep) {
             if (warp == 0 && lane < M) {
@@ -1667,6 +1702,7 @@ world_step_kernel(const KArgs A) {
                 F.store_global = t + 1 == T;
                 F.st_out = H.st_next;
                 F.flags_out = H.flags_next;
+                PH_START();
                 TT_ACC(5);
                 unsigned bits;
                 if constexpr (kSpec) {
@@ -1678,6 +1714,7 @@ world_step_kernel(const KArgs A) {
                 TT_ACC(6);
                 count_events(A, w, bits, __activemask(), lane == 0, false);
                 TT_ACC(7);
+                PH_ADD(PH_REWARD);
 #ifdef DG_EXP_NOFIX
                 if (false) {
 #else
@@ -1701,6 +1738,7 @@ world_step_kernel(const KArgs A) {
                         agent_physics(A, w, N1, H.st_next, 0, none, false);
                     }
                 }
+                PH_ADD(PH_RESET);
             }
 
             if (kSpec && warp == pw && t + 1 < T && !zero_early && !A.obs_resident) {
@@ -1720,6 +1758,10 @@ world_step_kernel(const KArgs A) {
         TT_ACC(4);
     }
     TT_FLUSH();
+    if (ph_on) {
+        __syncthreads();
+        if (tid < 5 && s_ph[tid]) atomicAdd(A.phase_cycles + tid, s_ph[tid]);
+    }
 }
 
 // ----------------------------------------------------------------- split launch mode
@@ -2403,6 +2445,9 @@ struct dg_engine {
     size_t smem_split;     // dynamic smem of the per-agent kernel
 };
 
+// the shapes the engine picks by default also come with the phase counters
+#define DG_PHASE_VARIANTS(X) X(256, 2, true, false) X(256, 2, false, false) X(128, 4, false, false)
+
 #define DG_VARIANTS(X)                                                                 \
     X(512, 1, false, false) X(512, 2, false, false) X(256, 2, false, false) X(256, 3, false, false) \
     X(256, 4, false, false) X(128, 4, false, false) X(128, 6, false, false) X(128, 8, false, false) \
@@ -2420,6 +2465,15 @@ static cudaError_t launch_world_step(const dg_engine* e, const KArgs& A, cudaStr
     const bool geo = A.d.geometry_global != 0;
     const int threads = variant_threads(nw, spec);
     const dim3 grid(A.d.W);
+    if (A.phase_cycles) {
+#define DG_LAUNCH_PH(T, B, S, G)                                                         \
+        if (threads == T && e->min_blocks == B && spec == S && geo == G) {               \
+            world_step_kernel<kStep, T, B, S, G, true><<<grid, 32 * (nw + (S ? 1 : 0)), e->smem_bytes, st>>>(A); \
+            return cudaGetLastError();                                                   \
+        }
+        DG_PHASE_VARIANTS(DG_LAUNCH_PH)
+#undef DG_LAUNCH_PH
+    }
 #define DG_LAUNCH(T, B, S, G)                                                            \
     if (threads == T && e->min_blocks == B && spec == S && geo == G) {                   \
         world_step_kernel<kStep, T, B, S, G><<<grid, 32 * (nw + (S ? 1 : 0)), e->smem_bytes, st>>>(A); \
@@ -2451,6 +2505,10 @@ static cudaError_t set_smem_attr(size_t) {
 #define DG_ATTR(T, B, S, G)                                                              \
     if (e == cudaSuccess) e = raise_smem_limit(world_step_kernel<kStep, T, B, S, G>);
     DG_VARIANTS(DG_ATTR)
+#undef DG_ATTR
+#define DG_ATTR(T, B, S, G)                                                              \
+    if (e == cudaSuccess) e = raise_smem_limit(world_step_kernel<kStep, T, B, S, G, true>);
+    DG_PHASE_VARIANTS(DG_ATTR)
 #undef DG_ATTR
     return e;
 }
@@ -2666,6 +2724,7 @@ int dg_step(dg_engine* eng, const DgStepIO* io, void* stream) {
     A.index_out = io->index_out;
     A.prefix_out = io->prefix_out;
     A.obs_resident = io->obs_resident && io->prefix_out && eng->mode != 1;
+    A.phase_cycles = reinterpret_cast<unsigned long long*>(io->phase_cycles);
     A.ticks = io->ticks > 0 ? io->ticks : 1;
     A.ring_slots = io->ring_slots > 0 ? io->ring_slots : A.ticks;
     A.ring_start = io->ring_start;

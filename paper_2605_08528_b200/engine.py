@@ -454,15 +454,22 @@ class Engine:
         obs_bytes = W * M * oc.obs_dim * 4
         self._host_obs_bytes = _align16(obs_bytes)
         _, aux_total = self._aux_layout()
-        self._host_blob = torch.zeros(self._host_obs_bytes + aux_total, dtype=torch.uint8, device=dev)
+        # [obs | aux | 5 x int64 phase cycles]: the phase counters ride in the same
+        # D2H as the per-tick outputs
+        self._phase_off = self._host_obs_bytes + aux_total
+        self._host_blob = torch.zeros(self._phase_off + 48, dtype=torch.uint8, device=dev)
         self._obs_dev = self._host_blob[:obs_bytes].view(torch.float32).view(W, M, oc.obs_dim)
-        aux_dev = self._host_blob[self._host_obs_bytes:]
+        aux_dev = self._host_blob[self._host_obs_bytes:self._phase_off]
         self._host_bufs = StepBuffers(self._obs_dev, aux_dev, self._views(aux_dev))
         self._host_pool = HostSlabPool(self._host_blob.numel())
         self._mapped_pool = MappedSlabPool(self._lib, self._host_blob.numel(), W * M, dev)
         self.d2h_bytes = torch.zeros(1, dtype=torch.int64, device=dev)   # obs bytes written by dg_to_host
         self._prefix_dev = torch.zeros((W, M, 2), dtype=torch.int16, device=dev)   # non-zero obs prefixes
         self._resident = weakref.WeakSet()     # resident rollout rings of this engine
+        # per-phase device cycles of the host-path steps (DgStepIO.phase_cycles)
+        self._phase_dev = self._host_blob[self._phase_off:self._phase_off + 40].view(torch.int64)
+        self._phase_host = None          # int64 [5] view of the last host slab
+        self._phase_prev = np.zeros(5, dtype=np.int64)
         self.launches = 0
         self._metrics_on = False
         self._host_lay = None
@@ -788,7 +795,7 @@ class Engine:
 
     def _step_io(self, actions, bufs, autoreset=False, snapshot=True, terms=True, next_actions=None,
                  steer_gain=2.0, throttle=0.5, event_counts=None, ticks=1, ring_start=0, drac_max=None,
-                 metric_seen=None, index_out=None, prefix_out=None, resident=False):
+                 metric_seen=None, index_out=None, prefix_out=None, resident=False, phase_cycles=None):
         if self._metrics_on:
             drac_max = self._drac_max if drac_max is None else drac_max
             metric_seen = self._metric_seen if metric_seen is None else metric_seen
@@ -807,7 +814,8 @@ class Engine:
                         event_counts=event_counts.data_ptr() if event_counts is not None else None,
                         ticks=int(ticks), ring_slots=int(slots), ring_start=int(ring_start),
                         drac_max=_ptr(drac_max), metric_seen=_ptr(metric_seen), index_out=_ptr(index_out),
-                        prefix_out=_ptr(prefix_out), obs_resident=int(bool(resident)))
+                        prefix_out=_ptr(prefix_out), obs_resident=int(bool(resident)),
+                        phase_cycles=_ptr(phase_cycles))
         if index_out is not None:
             want = (slots, self.W, self.M, self.index_stride)
             if (index_out.dtype != torch.int32 or not index_out.is_cuda or not index_out.is_contiguous()
@@ -994,6 +1002,21 @@ class Engine:
         src["step"] = self._step_count
         return StepOutput(bufs.obs, v["rewards"], v["dones"].bool(), v["events"], src, to_host=False)
 
+    def _book_phases(self, wall: float) -> None:
+        """Split a step's device + delivery wall time over the reference's
+        PHASES (engine.py:33, 342-395) in proportion to the device cycles the
+        fused kernel spent in each (DgStepIO.phase_cycles); the split kernels do
+        not record them -- their time goes to "physics"."""
+        cyc = np.array(self._phase_host, dtype=np.int64)
+        d = cyc - self._phase_prev
+        self._phase_prev = cyc
+        tot = float(d.sum())
+        if tot <= 0.0:
+            self.phase_seconds["physics"] += wall
+            return
+        for i, k in enumerate(PHASES):
+            self.phase_seconds[k] += wall * float(d[i]) / tot
+
     def _step_host(self, actions, autoreset: bool) -> StepOutput:
         t0 = time.perf_counter()
         a = np.asarray(actions, dtype=np.float64)
@@ -1015,7 +1038,8 @@ class Engine:
             # the host path's obs buffer is the engine's own: resident (zeroed at
             # construction, written only by these steps)
             io = self._host_io[key] = self._step_io(self._act_dev, bufs, autoreset=autoreset,
-                                                    prefix_out=self._prefix_dev, resident=True)
+                                                    prefix_out=self._prefix_dev, resident=True,
+                                                    phase_cycles=self._phase_dev)
         stream = torch.cuda.current_stream(self.device)
         N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), ct.c_void_p(stream.cuda_stream)), "dg_step")
         self._step_count += 1
@@ -1042,7 +1066,8 @@ class Engine:
         src = dict(hv)
         src["step"] = self._step_count
         self.phase_seconds["action"] += t1 - t0
-        self.phase_seconds["physics"] += t2 - t1  # the fused kernel covers every phase
+        self._phase_host = hb[self._phase_off:self._phase_off + 40].view(np.int64).copy()   # no view: the slab recycles
+        self._book_phases(t2 - t1)
         return StepOutput(obs, hv["rewards"], hv["dones"].astype(bool), hv["events"], src, to_host=True)
 
     # ------------------------------------------------------------------ resets

@@ -243,3 +243,33 @@ def test_observations_are_rotation_equivariant(quarter, device):
         assert np.allclose(sa.rewards, sb.rewards, rtol=1e-9, atol=1e-9)
         assert np.array_equal(sa.dones, sb.dones) and np.array_equal(sa.info["reason"], sb.info["reason"])
         oa = sa.obs
+
+
+def test_phase_seconds_split_by_device_phase_cycles(device):
+    """Engine.phase_seconds (engine.py:33, 342-395) on the GPU: the fused kernel
+    counts device cycles per phase (DgStepIO.phase_cycles), the host books each
+    step's wall time over the phases in that proportion -- every phase the step
+    runs gets time, and the phases sum to the measured step time."""
+    import time
+
+    from paper_2605_08528_b200.params import PHASES
+    from paper_2605_08528_b200.policies import LaneFollower
+    eng = C.build_engine(C.RootConfig(), device=device)
+    pol = LaneFollower(obs_config=eng.obs_config)
+    obs = eng.observe()
+    for _ in range(3):
+        obs = eng.step(pol(obs), autoreset=True).obs
+    eng.reset_phase_timers()
+    t0 = time.perf_counter()
+    acts = [pol(obs)]
+    for _ in range(20):
+        obs = eng.step(acts[-1], autoreset=True).obs
+        acts.append(pol(obs))
+    wall = time.perf_counter() - t0
+    ph = eng.phase_seconds
+    assert set(ph) == set(PHASES)
+    for k in ("action", "physics", "observation", "reward_termination"):
+        assert ph[k] > 0.0, k
+    assert 0.3 * wall < sum(ph.values()) <= wall
+    cyc = np.array(eng._phase_host)
+    assert cyc[2] > cyc[1] > 0 and cyc[3] > 0          # observation > physics > 0 on the device
