@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <new>
 
 #include "dg_fastmath.cuh"
@@ -47,9 +48,36 @@ enum StateField {
     SX = 0, SY, SYAW, SVX, SVY, SOM, SANG, SRATE, SWF, SWR, SBF, SBR
 };
 
+// Refined reciprocals (dg::drcp_refined) of the constant divisors, computed once
+// on the device at engine creation: a division by a constant becomes
+// dg::ddiv_y(a, b, rc.b) -- the same value ddiv(a, b) computes, without the
+// reciprocal's five dependent FMAs on every use (kernel-parameter constants).
+struct Rcp {
+    double steer_inertia, wheel_radius, chassis_mass, yaw_inertia, i_axle, wheelbase;
+    double bbox_half, speed_norm, pi, ttc_max, road_radius, lane_sigma;
+};
+
+__device__ __forceinline__ Rcp make_rcp(const DgConsts& k) {
+    Rcp r;
+    r.steer_inertia = dg::drcp_refined(k.steer_inertia);
+    r.wheel_radius = dg::drcp_refined(k.wheel_radius);
+    r.chassis_mass = dg::drcp_refined(k.chassis_mass);
+    r.yaw_inertia = dg::drcp_refined(k.yaw_inertia);
+    r.i_axle = dg::drcp_refined(k.i_axle);
+    r.wheelbase = dg::drcp_refined(k.wheelbase);
+    r.bbox_half = dg::drcp_refined(k.bbox_half);
+    r.speed_norm = dg::drcp_refined(k.speed_norm);
+    r.pi = dg::drcp_refined(3.141592653589793);
+    r.ttc_max = dg::drcp_refined(k.ttc_max);
+    r.road_radius = dg::drcp_refined(k.road_radius);
+    r.lane_sigma = dg::drcp_refined(k.lane_sigma);
+    return r;
+}
+
 struct KArgs {
     DgDims d;
     DgConsts k;
+    Rcp rc;
     // engine tables
     const uint8_t* scene_blob;
     const int64_t* scene_meta;
@@ -321,10 +349,11 @@ __device__ __forceinline__ void sincos_steer(double x, double* s, double* c) {
 
 // One 120 Hz substep of the single-track model (vehicle.py:237-336), with the
 // reference's expression order; x[] is the 12-field state.
-__device__ __forceinline__ void substep_dynamic(double* x, const Act a, double cap, const DgConsts& k) {
+__device__ __forceinline__ void substep_dynamic(double* x, const Act a, double cap, const DgConsts& k,
+                                                const Rcp& rc) {
     double tau_s = np_clip_k(k.kp_steer * (k.theta_max * a.steer - x[SANG]) - k.kd_steer * x[SRATE],
                            -k.tau_steer_max, k.tau_steer_max);
-    double rate = x[SRATE] + dg::ddiv(tau_s, k.steer_inertia) * k.physics_dt;
+    double rate = x[SRATE] + dg::ddiv_y(tau_s, k.steer_inertia, rc.steer_inertia) * k.physics_dt;
     double ang = x[SANG] + rate * k.physics_dt;
     double ang_c = np_clip_k(ang, -k.steer_limit, k.steer_limit);
     rate = (ang_c == ang) ? rate : 0.0;
@@ -338,11 +367,12 @@ __device__ __forceinline__ void substep_dynamic(double* x, const Act a, double c
     double tbr = -sr * a.brk * k.tau_brake_rear;
     double t_front = 2.0 * (k.tau_drive_max * a.thr + tbf);
     double t_rear = 2.0 * tbr;
-    double fxf0 = dg::ddiv(t_front, k.wheel_radius);
-    double fxr0 = dg::ddiv(t_rear, k.wheel_radius);
+    double fxf0 = dg::ddiv_y(t_front, k.wheel_radius, rc.wheel_radius);
+    double fxr0 = dg::ddiv_y(t_rear, k.wheel_radius, rc.wheel_radius);
     double den = np_max_k(vx, 0.5);
-    double fyf0 = k.cornering_stiffness * (ang - dg::ddiv(vy + k.a_f * om, den));
-    double fyr0 = k.cornering_stiffness * dg::ddiv(-(vy - k.b_r * om), den);
+    const double rden = dg::drcp_refined(den);          // one reciprocal for both divisions
+    double fyf0 = k.cornering_stiffness * (ang - dg::ddiv_y(vy + k.a_f * om, den, rden));
+    double fyr0 = k.cornering_stiffness * dg::ddiv_y(-(vy - k.b_r * om), den, rden);
 
     double nf = dg::dsqrt(fxf0 * fxf0 + fyf0 * fyf0);
     double nr = dg::dsqrt(fxr0 * fxr0 + fyr0 * fyr0);
@@ -355,9 +385,10 @@ __device__ __forceinline__ void substep_dynamic(double* x, const Act a, double c
     double sd, cd;
     sincos_steer(ang, &sd, &cd);
     const double m = k.chassis_mass;
-    double ax = dg::ddiv(fxf * cd - fyf * sd + fxr, m) + vy * om;
-    double ay = dg::ddiv(fyf * cd + fxf * sd + fyr - k.lambda_lat * vy, m) - vx * om;
-    double omd = dg::ddiv(k.a_f * (fyf * cd + fxf * sd) - k.b_r * fyr - k.lambda_yaw * om, k.yaw_inertia);
+    double ax = dg::ddiv_y(fxf * cd - fyf * sd + fxr, m, rc.chassis_mass) + vy * om;
+    double ay = dg::ddiv_y(fyf * cd + fxf * sd + fyr - k.lambda_lat * vy, m, rc.chassis_mass) - vx * om;
+    double omd = dg::ddiv_y(k.a_f * (fyf * cd + fxf * sd) - k.b_r * fyr - k.lambda_yaw * om, k.yaw_inertia,
+                            rc.yaw_inertia);
     double vx1 = vx + ax * k.physics_dt;
     double vy1 = vy + ay * k.physics_dt;
     double om1 = om + omd * k.physics_dt;
@@ -369,10 +400,10 @@ __device__ __forceinline__ void substep_dynamic(double* x, const Act a, double c
     x[SY] = x[SY] + (vx1 * sy + vy1 * cy) * k.physics_dt;
     x[SYAW] = x[SYAW] + om1 * k.physics_dt;
 
-    double roll_f = dg::ddiv((vy1 + k.a_f * om1) * sd + vx1 * cd, k.wheel_radius);
-    double roll_r = dg::ddiv(vx1, k.wheel_radius);
-    double spin_f = x[SWF] + dg::ddiv(t_front - fxf * k.wheel_radius, k.i_axle) * k.physics_dt;
-    double spin_r = x[SWR] + dg::ddiv(t_rear - fxr * k.wheel_radius, k.i_axle) * k.physics_dt;
+    double roll_f = dg::ddiv_y((vy1 + k.a_f * om1) * sd + vx1 * cd, k.wheel_radius, rc.wheel_radius);
+    double roll_r = dg::ddiv_y(vx1, k.wheel_radius, rc.wheel_radius);
+    double spin_f = x[SWF] + dg::ddiv_y(t_front - fxf * k.wheel_radius, k.i_axle, rc.i_axle) * k.physics_dt;
+    double spin_r = x[SWR] + dg::ddiv_y(t_rear - fxr * k.wheel_radius, k.i_axle, rc.i_axle) * k.physics_dt;
     if (a.brk > 0.0 && spin_f * sf < 0.0) spin_f = 0.0;
     if (a.brk > 0.0 && spin_r * sr < 0.0) spin_r = 0.0;
     x[SWF] = np_clip_k(satf ? spin_f : roll_f, -200.0, 200.0);
@@ -387,12 +418,12 @@ __device__ __forceinline__ void substep_dynamic(double* x, const Act a, double c
 }
 
 // One 30 Hz kinematic bicycle tick (vehicle.py:208-232).
-__device__ __forceinline__ void step_bicycle(double* x, const Act a, const DgConsts& k) {
+__device__ __forceinline__ void step_bicycle(double* x, const Act a, const DgConsts& k, const Rcp& rc) {
     double delta = a.steer * k.bic_steer_max;
     double v = x[SVX];
     double v1 = np_max(v + (a.thr * k.bic_a_max - a.brk * k.bic_b_max - np_sign(v) * k.bic_c_roll) * k.control_dt, 0.0);
     double yaw = x[SYAW];
-    double rate = dg::ddiv(v1 * tan(delta), k.wheelbase);
+    double rate = dg::ddiv_y(v1 * tan(delta), k.wheelbase, rc.wheelbase);
     double sy, cy;
     sincos(yaw, &sy, &cy);
     x[SX] = x[SX] + v1 * cy * k.control_dt;
@@ -403,8 +434,8 @@ __device__ __forceinline__ void step_bicycle(double* x, const Act a, const DgCon
     x[SOM] = rate;
     x[SANG] = delta;
     x[SRATE] = 0.0;
-    x[SWF] = dg::ddiv(v1, k.wheel_radius);
-    x[SWR] = dg::ddiv(v1, k.wheel_radius);
+    x[SWF] = dg::ddiv_y(v1, k.wheel_radius, rc.wheel_radius);
+    x[SWR] = dg::ddiv_y(v1, k.wheel_radius, rc.wheel_radius);
 }
 
 // ----------------------------------------------------------------- swept-circle TTC
@@ -519,9 +550,9 @@ __device__ __forceinline__ void write_ego(float* row, const DgConsts& k, const K
     double sh, ch;
     sincos_of_bearing(yb, xb, dist, &sh, &ch);
     const float f2 = __double2float_rn(sh), f3 = __double2float_rn(ch);
-    const float f4 = __double2float_rn(dg::ddiv(dist, k.bbox_half));
-    row[0] = __double2float_rn(dg::ddiv(xb, k.bbox_half));
-    row[1] = __double2float_rn(dg::ddiv(yb, k.bbox_half));
+    const float f4 = __double2float_rn(dg::ddiv_y(dist, k.bbox_half, A.rc.bbox_half));
+    row[0] = __double2float_rn(dg::ddiv_y(xb, k.bbox_half, A.rc.bbox_half));
+    row[1] = __double2float_rn(dg::ddiv_y(yb, k.bbox_half, A.rc.bbox_half));
     row[2] = f2;
     row[3] = f3;
     row[4] = f4;
@@ -543,8 +574,8 @@ __device__ __forceinline__ void write_ego(float* row, const DgConsts& k, const K
             act_sm[2] = 0.0;
         }
     }
-    row[5] = __double2float_rn(dg::ddiv(vx, k.speed_norm));
-    row[6] = __double2float_rn(dg::ddiv(vy, k.speed_norm));
+    row[5] = __double2float_rn(dg::ddiv_y(vx, k.speed_norm, A.rc.speed_norm));
+    row[6] = __double2float_rn(dg::ddiv_y(vy, k.speed_norm, A.rc.speed_norm));
     if (A.d.include_weather) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) row[7 + i] = __double2float_rn(A.weather[4 * w + i]);
@@ -729,7 +760,7 @@ __device__ __forceinline__ void emit_agent(const KArgs& A, const TickOut& O, int
             // heading with the unit lane tangent: same value to ~1e-16, no atan2 / cos
             // on the tail's critical path (yaw NaN -> NaN, as numpy)
             const double align = np_max(0.0, F.c * tx + F.s * ty);
-            const double ls = dg::ddiv(lat, k.lane_sigma);
+            const double ls = dg::ddiv_y(lat, k.lane_sigma, A.rc.lane_sigma);
             const double quality = exp(-(ls * ls)) * (k.lane_heading_base + k.lane_heading_weight * align);
             const double lane_t = has_lane ? k.lane_weight * quality : 0.0;
             progress = has_lane ? progress : 0.0;
@@ -890,13 +921,13 @@ __device__ __forceinline__ void agent_physics(const KArgs& A, int w, AgentSm& S,
         if (A.d.dynamic) {
             const double cap = A.mu_eff[w] * k.f_z;
             for (int i = 0; i < A.d.decimation; ++i) {
-                substep_dynamic(x, act, cap, k);
+                substep_dynamic(x, act, cap, k, A.rc);
 #ifdef DG_PHASE_TIMERS
                 if (i < 4 && x[SX] != -12345.678) LANE0_MARK(28 + i);
 #endif
             }
         } else {
-            step_bicycle(x, act, k);
+            step_bicycle(x, act, k, A.rc);
         }
     }
     if (x[SX] != -12345.678) LANE0_MARK(26);          // after the substeps
@@ -908,7 +939,7 @@ __device__ __forceinline__ void agent_physics(const KArgs& A, int w, AgentSm& S,
     S.s = s_;
     S.vwx = x[SVX] * c_ - x[SVY] * s_;
     S.vwy = x[SVX] * s_ + x[SVY] * c_;
-    S.f_spd = __double2float_rn(dg::ddiv(dg::dsqrt(x[SVX] * x[SVX] + x[SVY] * x[SVY]), k.speed_norm));
+    S.f_spd = __double2float_rn(dg::ddiv_y(dg::dsqrt(x[SVX] * x[SVX] + x[SVY] * x[SVY]), k.speed_norm, A.rc.speed_norm));
     const double offs[3] = {-1.0, 0.0, 1.0};
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
@@ -1395,13 +1426,13 @@ world_step_kernel(const KArgs A) {
                         ttc = sel_min(ttc, tj);
                         const double wrap = wrap_angle(N.st[SYAW] - S.st[SYAW]);
                         float* o = obs_w + int64_t(ii) * D + veh0 + 7 * rank[u];
-                        o[0] = __double2float_rn(dg::ddiv(c * ndx[u] + s * ndy[u], k.bbox_half));
-                        o[1] = __double2float_rn(dg::ddiv(-s * ndx[u] + c * ndy[u], k.bbox_half));
+                        o[0] = __double2float_rn(dg::ddiv_y(c * ndx[u] + s * ndy[u], k.bbox_half, A.rc.bbox_half));
+                        o[1] = __double2float_rn(dg::ddiv_y(-s * ndx[u] + c * ndy[u], k.bbox_half, A.rc.bbox_half));
                         o[2] = N.f_len;
                         o[3] = N.f_wid;
-                        o[4] = __double2float_rn(dg::ddiv(wrap, 3.141592653589793));
+                        o[4] = __double2float_rn(dg::ddiv_y(wrap, 3.141592653589793, A.rc.pi));
                         o[5] = N.f_spd;
-                        o[6] = __double2float_rn(dg::ddiv(tj, k.ttc_max));
+                        o[6] = __double2float_rn(dg::ddiv_y(tj, k.ttc_max, A.rc.ttc_max));
                     }
                     // hull contact; centres sit within d of the position, so a pair
                     // farther apart than r_a + r_b + d_a + d_b (+1e-4 m) cannot touch
@@ -1576,8 +1607,8 @@ world_step_kernel(const KArgs A) {
                     const double dx = m2.x - px, dy = m2.y - py;
                     const double ux = u2.x, uy = u2.y;
                     float* o = row + road0 + 5 * slot;
-                    o[0] = __double2float_rn(dg::ddiv(c * dx + s * dy, k.road_radius));
-                    o[1] = __double2float_rn(dg::ddiv(-s * dx + c * dy, k.road_radius));
+                    o[0] = __double2float_rn(dg::ddiv_y(c * dx + s * dy, k.road_radius, A.rc.road_radius));
+                    o[1] = __double2float_rn(dg::ddiv_y(-s * dx + c * dy, k.road_radius, A.rc.road_radius));
                     o[2] = G.type_feat[q];
                     o[3] = __double2float_rn(c * ux + s * uy);
                     o[4] = __double2float_rn(-s * ux + c * uy);
@@ -1858,9 +1889,9 @@ __global__ void __launch_bounds__(32) world_physics_kernel(const KArgs A) {
         act.brk = np_clip(raw2, 0.0, 1.0);
         if (A.d.dynamic) {
             const double cap = A.mu_eff[w] * k.f_z;
-            for (int i = 0; i < A.d.decimation; ++i) substep_dynamic(x, act, cap, k);
+            for (int i = 0; i < A.d.decimation; ++i) substep_dynamic(x, act, cap, k, A.rc);
         } else {
-            step_bicycle(x, act, k);
+            step_bicycle(x, act, k, A.rc);
         }
         // the post-physics state (the info snapshot; the tail parks from here)
 #pragma unroll
@@ -2318,6 +2349,7 @@ __global__ void __launch_bounds__(64) sysid_rollout_kernel(const DgConsts* const
     const int m = blockIdx.y;
     if (b >= B) return;
     const DgConsts k = consts[b];
+    const Rcp rc = make_rcp(k);           // this candidate's constants
     double x[DG_NUM_STATE];
 #pragma unroll
     for (int f = 0; f < DG_NUM_STATE; ++f) x[f] = 0.0;
@@ -2334,7 +2366,7 @@ __global__ void __launch_bounds__(64) sysid_rollout_kernel(const DgConsts* const
         a.brk = actions[3 * t + 2];
         const double cap = mu[3 * b + surface[t]] * k.f_z;
         for (int sub = 0; sub < 4; ++sub) {
-            substep_dynamic(x, a, cap, k);
+            substep_dynamic(x, a, cap, k, rc);
             if (sub & 1) {
                 double* r = o + rec * B + b;
                 r[0 * T60 * B] = x[SX];
@@ -2570,6 +2602,10 @@ static cudaError_t launch_step_any(const dg_engine* e, const KArgs& A, cudaStrea
     return e->mode == 1 ? launch_split<kStep>(e, A, st) : launch_world_step<kStep>(e, A, st);   // 0, 2: fused
 }
 
+// engine creation: the refined reciprocals of the constant divisors (Rcp)
+__device__ Rcp g_rcp_out;
+__global__ void rcp_kernel(const DgConsts k) { g_rcp_out = make_rcp(k); }
+
 static thread_local char g_err[512] = "";
 
 static int fail(int code, const char* msg) {
@@ -2631,6 +2667,18 @@ int dg_create(const DgEngineDesc* desc, dg_engine** out) {
     std::memset(&A, 0, sizeof(A));
     A.d = d;
     A.k = desc->k;
+    {
+        // the constant divisors' refined reciprocals, as the GPU computes them
+        static std::mutex rcp_mu;
+        std::lock_guard<std::mutex> lock(rcp_mu);
+        rcp_kernel<<<1, 1>>>(desc->k);
+        cudaError_t rerr = cudaGetLastError();
+        if (rerr == cudaSuccess) rerr = cudaMemcpyFromSymbol(&A.rc, g_rcp_out, sizeof(Rcp));
+        if (rerr != cudaSuccess) {
+            delete e;
+            return cuda_fail(rerr, "dg_create: reciprocal constants");
+        }
+    }
     A.scene_blob = desc->scene_blob;
     A.scene_meta = desc->scene_meta;
     A.scene_of_world = desc->scene_of_world;
