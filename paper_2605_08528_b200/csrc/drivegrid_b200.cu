@@ -41,6 +41,7 @@ namespace {
 
 constexpr int kMaxAgents = 16;
 constexpr int kZeroChunk = 4096;   // bytes of zeros in shared memory, source of the TMA row clears
+constexpr int kPfxSlots = 16;      // resident rings up to this many slots keep the world's prefix record in smem
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned kBitFinished = 32u;   // finalize_agent: done or timed out this tick
 
@@ -1104,6 +1105,16 @@ world_step_kernel(const KArgs A) {
     float4* zero_sm = reinterpret_cast<float4*>(
         smem + align16(reinterpret_cast<uint8_t*>(cand_sm + kMaxAgents * A.take_road) - smem));  // [kZeroChunk/16]
     for (int i = tid; i < kZeroChunk / 16; i += blockDim.x) zero_sm[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // resident ring: this world's prefix record of every slot, cached for the launch
+    // (the global record is still written every tick)
+    int16_t* const pfx_sm = reinterpret_cast<int16_t*>(zero_sm + kZeroChunk / 16);   // [kPfxSlots][16][2]
+    const bool pfx_cached = kStep && A.obs_resident && A.ring_slots <= kPfxSlots;
+    if (pfx_cached)
+        for (int i = tid; i < A.ring_slots * M * 2; i += blockDim.x) {
+            const int sl = i / (2 * M), r = i % (2 * M);
+            pfx_sm[(sl * kMaxAgents + r / 2) * 2 + (r & 1)] =
+                A.prefix_out[(int64_t(sl) * A.d.W * M + int64_t(w) * M + r / 2) * 2 + (r & 1)];
+        }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     __shared__ int s_bad;
@@ -1467,9 +1478,14 @@ world_step_kernel(const KArgs A) {
                         int16_t* pre = A.prefix_out + (int64_t(slot) * WM + int64_t(w) * M + ii) * 2 + 1;
                         // resident obs: the row holds zeros past its previous prefix; clear
                         // only the rows the previous tick of this slot had beyond n_valid
-                        const int old_v = A.obs_resident ? min(int(*pre), 7 * A.d.k_vehicles) : 0;
+                        int16_t* const pc = pfx_sm + (slot * kMaxAgents + ii) * 2 + 1;
+                        const int old_v = !A.obs_resident ? 0
+                                          : min(int(pfx_cached ? *pc : *pre), 7 * A.d.k_vehicles);
                         __syncwarp(gmask);
-                        if (jl == 0) *pre = int16_t(7 * n_valid);
+                        if (jl == 0) {
+                            *pre = int16_t(7 * n_valid);
+                            if (pfx_cached) *pc = int16_t(7 * n_valid);
+                        }
                         if (old_v > 7 * n_valid)
                             zero_span(obs_w + int64_t(ii) * D + veh0 + 7 * n_valid, old_v - 7 * n_valid, jl, kPL);
                     }
@@ -1595,9 +1611,13 @@ world_step_kernel(const KArgs A) {
                 if (A.prefix_out) {
                     int16_t* pre = A.prefix_out + (int64_t(slot) * WM + int64_t(w) * M + m) * 2;
                     // resident obs: the previous prefix (0x7fff: slot written elsewhere -> all)
-                    const int old_r = A.obs_resident ? min(int(*pre), 5 * A.d.k_road) : 0;
+                    int16_t* const pc = pfx_sm + (slot * kMaxAgents + m) * 2;
+                    const int old_r = !A.obs_resident ? 0 : min(int(pfx_cached ? *pc : *pre), 5 * A.d.k_road);
                     __syncwarp(kGMask << hshift);
-                    if (hl == 0) *pre = int16_t(5 * ncand);
+                    if (hl == 0) {
+                        *pre = int16_t(5 * ncand);
+                        if (pfx_cached) *pc = int16_t(5 * ncand);
+                    }
                     if (old_r > 5 * ncand) zero_span(row + road0 + 5 * ncand, old_r - 5 * ncand, hl, kGL);
                 }
                 for (int slot = hl; slot < ncand; slot += kGL) {
@@ -2635,6 +2655,7 @@ static size_t step_smem_bytes(const DgDims& d, int take_road) {
     b += 16;  // mbarrier
     b += sizeof(uint16_t) * kMaxAgents * size_t(take_road > 0 ? take_road : 1);
     b = size_t(align16(int64_t(b))) + kZeroChunk;
+    b += sizeof(int16_t) * kPfxSlots * kMaxAgents * 2;   // resident-ring prefix cache
     return b;
 }
 
