@@ -1115,6 +1115,12 @@ world_step_kernel(const KArgs A) {
             pfx_sm[(sl * kMaxAgents + r / 2) * 2 + (r & 1)] =
                 A.prefix_out[(int64_t(sl) * A.d.W * M + int64_t(w) * M + r / 2) * 2 + (r & 1)];
         }
+    // pairs phase: each ego's neighbour order of the previous tick (rank of agent
+    // j, agent at rank r) and whether it is set
+    __shared__ int8_t s_rank[kMaxAgents][kMaxAgents];
+    __shared__ int8_t s_ord[kMaxAgents][kMaxAgents];
+    __shared__ int8_t s_rok[kMaxAgents];
+    if (tid < kMaxAgents) s_rok[tid] = 0;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     __shared__ int s_bad;
@@ -1406,6 +1412,24 @@ world_step_kernel(const KArgs A) {
                 int rank[kOPL];
 #pragma unroll
                 for (int u = 0; u < kOPL; ++u) rank[u] = 0;
+                // The previous tick's order is reused when it still sorts this tick's
+                // keys: every agent's key against its predecessor's in that order (one
+                // shuffle) -- a sorted permutation is unique, so the ranks are the stable
+                // argsort's.  Otherwise (or at a launch's first tick) the full count.
+                bool full = true;
+                if constexpr (kOPL == 1) {
+                    const bool have = ego_ok && jl < M && s_rok[ii];
+                    const int r0 = have ? int(s_rank[ii][jl]) : 0;
+                    const int pj = have && r0 > 0 ? int(s_ord[ii][r0 - 1]) : jl;
+                    const double kp = __shfl_sync(kFull, key[0], pj, kPL);
+                    const bool ok = !ego_ok || jl >= M || (have && (r0 == 0 || kp < key[0] ||
+                                                                    (kp == key[0] && pj < jl)));
+                    full = !__all_sync(kFull, ok);
+                    rank[0] = r0;
+                }
+                if (full) {
+#pragma unroll
+                for (int u = 0; u < kOPL; ++u) rank[u] = 0;
 #pragma unroll
                 for (int v = 0; v < kOPL; ++v)
                     for (int sl = 0; sl < kPL; ++sl) {
@@ -1419,6 +1443,15 @@ world_step_kernel(const KArgs A) {
                             }
                         }
                     }
+                    if constexpr (kOPL == 1) {
+                        if (ego_ok && jl < M) {
+                            s_rank[ii][jl] = int8_t(rank[0]);
+                            s_ord[ii][rank[0]] = int8_t(jl);
+                        }
+                        __syncwarp();
+                        if (ego_ok && jl == 0) s_rok[ii] = 1;
+                    }
+                }
                 TT_WACC(32 + (warp & 7) % 3);     // 2a sub-timers: key + rank
                 double ttc = k.ttc_max;
                 bool touch = false;
