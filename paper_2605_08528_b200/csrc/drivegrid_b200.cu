@@ -1505,7 +1505,11 @@ world_step_kernel(const KArgs A) {
                 ttc = warp_min(ttc, kPL);
                 touch = (__ballot_sync(kFull, touch) & gmask) != 0;
                 if (ix_w || A.prefix_out) {
-                    for (int o = kPL / 2; o > 0; o >>= 1) n_valid += __shfl_xor_sync(kFull, n_valid, o, kPL);
+                    if constexpr (kOPL == 1) {
+                        n_valid = __popc(__ballot_sync(kFull, n_valid != 0) & gmask);   // one vote, no chain
+                    } else {
+                        for (int o = kPL / 2; o > 0; o >>= 1) n_valid += __shfl_xor_sync(kFull, n_valid, o, kPL);
+                    }
                     if (ix_w && ego_ok && jl == 0) ix_w[int64_t(ii) * A.index_stride + 2] = n_valid;
                     if (A.prefix_out && ego_ok) {
                         int16_t* pre = A.prefix_out + (int64_t(slot) * WM + int64_t(w) * M + ii) * 2 + 1;
