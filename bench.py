@@ -373,11 +373,19 @@ def main():
     launches0 = eng.launches
     graph = None
     graph_ticks = []
+    # device-side bracket of the K ticks: event-record nodes captured inside the
+    # graph (cudaEventRecordExternal) fire when the device reaches them, so the
+    # host's graph-submission latency before the first launch is not booked as
+    # step time; the host-bracketed time is reported beside it (ms_incl_submit)
+    g_start = torch.cuda.Event(enable_timing=True, external=True)
+    g_stop = torch.cuda.Event(enable_timing=True, external=True)
     if not args.no_graph:
         graph = torch.cuda.CUDAGraph()
         n0 = len(tick_log)
         with torch.cuda.graph(graph):
+            g_start.record()
             run_ticks(args.steps)
+            g_stop.record()
         graph_ticks = tick_log[n0:]
         launches0 = eng.launches - len(graph_ticks)   # the captured launches run at replay
     if world_size > 1:
@@ -394,6 +402,9 @@ def main():
     launches = eng.launches - launches0
     launch_ticks = list(tick_log[len(tick_log) - launches:]) if graph is None else list(graph_ticks)
     total_ms = start.elapsed_time(stop)
+    ms_incl_submit = total_ms
+    if graph is not None:
+        total_ms = g_start.elapsed_time(g_stop)
     if world_size > 1:
         t = torch.tensor([total_ms], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -402,13 +413,14 @@ def main():
     assert sum(launch_ticks) == args.steps, (launch_ticks, args.steps)
     if graph is not None:
         g_step = torch.cuda.CUDAGraph()
+        k0 = torch.cuda.Event(enable_timing=True, external=True)
+        k1 = torch.cuda.Event(enable_timing=True, external=True)
         with torch.cuda.graph(g_step):
+            k0.record()
             run_ticks(args.steps, count=False)
+            k1.record()
         torch.cuda.synchronize()
-        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k0.record(stream)
         g_step.replay()
-        k1.record(stream)
         torch.cuda.synchronize()
         kern_total = k0.elapsed_time(k1)
     else:
@@ -455,6 +467,11 @@ def main():
             "config": bench_config(W_total, M, D),
             "launch": {"launches": n_launch, "ticks_per_launch": launch_ticks[0] if uniform else launch_ticks,
                        "max_ticks_per_launch": R, "cuda_graph": graph is not None,
+                       "timing": ("CUDA events captured inside the graph (cudaEventRecordExternal): device time "
+                                  "from the first launch of the K ticks to the end of the last; barrier + "
+                                  "synchronize around the replay" if graph is not None else
+                                  "CUDA events around the launches on the launching stream"),
+                       "ms_incl_submit": ms_incl_submit,
                        "ring_slots": ring, "kernel_shape": eng.launch_shape(),
                        "obs_clear": "resident ring (DgStepIO.obs_resident): a slot keeps its zero background, "
                                     "a tick clears only the row spans its new content no longer covers",

@@ -43,6 +43,12 @@ namespace {
 #ifndef DG_ENC_AGENTS
 #define DG_ENC_AGENTS 32
 #endif
+#ifndef DG_L2_NOSEL
+#define DG_L2_NOSEL 1
+#endif
+#ifndef DG_ENC_CTAS_PER_SM
+#define DG_ENC_CTAS_PER_SM 3
+#endif
 constexpr int kEncAgents = DG_ENC_AGENTS;   // agents per encoder CTA (<= 32: one per lane in the scan)
 constexpr int kTrunkAgents = 128;  // agents per trunk CTA (one TMEM lane each)
 constexpr int kHid = 96;           // road / vehicle encoder width
@@ -378,8 +384,13 @@ __global__ void __launch_bounds__(kEncThreads, 3) policy_encoder_kernel(const Dg
                 for (int cc = 0; cc < 3; ++cc) umma::tmem_wait16(raw + 16 * cc);
 #pragma unroll
                 for (int i = 0; i < 24; ++i)
+#if DG_L2_NOSEL
+                    // rows past the last segment fill whole segments that are never stored
+                    pk[i] = umma::pack_bf16(__uint_as_float(raw[2 * i]), __uint_as_float(raw[2 * i + 1]));
+#else
                     pk[i] = valid ? umma::pack_bf16(__uint_as_float(raw[2 * i]), __uint_as_float(raw[2 * i + 1]))
                                   : 0xff80ff80u;
+#endif
             }
             const bool bA = (lane >> 2) & 1, bB = (lane >> 1) & 1, bC = lane & 1;
             uint32_t qa[12];
@@ -482,6 +493,36 @@ struct TrunkSmem {
     static constexpr int kBar = kHead + 128 * 4 * 4;
     static constexpr int kTotal = kBar + 64;
 };
+
+#ifndef DG_TRUNK_BATCH
+#define DG_TRUNK_BATCH 1
+#endif
+// NC 16-column TMEM chunks of this thread's row: with DG_TRUNK_BATCH all loads are in
+// flight together (one ~70-cycle wait instead of NC), then fn(chunk, v[16]) per chunk
+template <int NC, class Fn>
+__device__ __forceinline__ void tmem_chunks(uint32_t taddr, Fn&& fn) {
+#if DG_TRUNK_BATCH
+    uint32_t raw[16 * NC];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) umma::tmem_ld16_issue(taddr + 16 * cc, raw + 16 * cc);
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) umma::tmem_wait16(raw + 16 * cc);
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(raw[16 * cc + i]);
+        fn(cc, v);
+    }
+#else
+#pragma unroll 1
+    for (int cc = 0; cc < NC; ++cc) {
+        float v[16];
+        umma::tmem_ld16(taddr + 16 * cc, v);
+        fn(cc, v);
+    }
+#endif
+}
 
 __global__ void __launch_bounds__(kTrunkThreads, 1) policy_trunk_kernel(const DgPolicyDesc p) {
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -586,44 +627,36 @@ __global__ void __launch_bounds__(kTrunkThreads, 1) policy_trunk_kernel(const Dg
 
     // ego L1 -> Ae1 (32 columns per thread)
     run(0, Ae0, We1, kEgo, 16, 1);
-#pragma unroll 1
-    for (int c = 32 * hf; c < 32 * hf + 32; c += 16) {
-        float v[16];
-        umma::tmem_ld16(tmem + lane_base + c, v);
+tmem_chunks<2>(tmem + lane_base + 32 * hf, [&](int cc, float* v) {
+        const int c = 32 * hf + 16 * cc;
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = elu(v[i] + be1[c + i]);
         store_row16(Ae1, r, c, kEgo, v);
-    }
+    });
     sync_for_mma();
     // ego L2 -> At[:, 0:64]
     run(64, Ae1, We2, kEgo, kEgo, 1);
-#pragma unroll 1
-    for (int c = 32 * hf; c < 32 * hf + 32; c += 16) {
-        float v[16];
-        umma::tmem_ld16(tmem + lane_base + 64 + c, v);
+tmem_chunks<2>(tmem + lane_base + 64 + 32 * hf, [&](int cc, float* v) {
+        const int c = 32 * hf + 16 * cc;
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = elu(v[i] + be2[c + i]);
         store_row16(At, r, c, 256, v);
-    }
+    });
     sync_for_mma();
     // trunk L1 -> At2 (64 columns per thread)
     run(128, At, Wt1, kT1, 256, 2);
-#pragma unroll 1
-    for (int c = 64 * hf; c < 64 * hf + 64; c += 16) {
-        float v[16];
-        umma::tmem_ld16(tmem + lane_base + 128 + c, v);
+tmem_chunks<4>(tmem + lane_base + 128 + 64 * hf, [&](int cc, float* v) {
+        const int c = 64 * hf + 16 * cc;
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = elu(v[i] + bt1[c + i]);
         store_row16(At2, r, c, kT1, v);
-    }
+    });
     sync_for_mma();
     // trunk L2 -> registers -> head partial sums over this thread's 32 columns
     run(0, At2, Wt2, kT2, kT1, 3);
     float y[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
-    for (int c = 32 * hf; c < 32 * hf + 32; c += 16) {
-        float v[16];
-        umma::tmem_ld16(tmem + lane_base + c, v);
+tmem_chunks<2>(tmem + lane_base + 32 * hf, [&](int cc, float* v) {
+        const int c = 32 * hf + 16 * cc;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             const float h = elu(v[i] + bt2[c + i]);
@@ -631,7 +664,7 @@ __global__ void __launch_bounds__(kTrunkThreads, 1) policy_trunk_kernel(const Dg
             for (int j = 0; j < 4; ++j)
                 if (j < nout) y[j] = fmaf(h, wh[j * 64 + c + i], y[j]);
         }
-    }
+    });
     if (hf == 1) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) part[4 * r + j] = y[j];
@@ -746,7 +779,7 @@ int dg_policy_forward(const DgPolicyDesc* desc, void* stream) {
         if (dev >= 0 && dev < 64 && n_sm[dev] == 0) cudaDeviceGetAttribute(&n_sm[dev], cudaDevAttrMultiProcessorCount, dev);
         const int sms = dev >= 0 && dev < 64 && n_sm[dev] > 0 ? n_sm[dev] : 148;
         const int items = 2 * nets * groups;
-        g1 = dim3(items < 3 * sms ? items : 3 * sms, 1);
+        g1 = dim3(items < DG_ENC_CTAS_PER_SM * sms ? items : DG_ENC_CTAS_PER_SM * sms, 1);
     }
     policy_encoder_kernel<<<g1, kEncThreads, enc, st>>>(p);
     dim3 g2((p.n_agents + kTrunkAgents - 1) / kTrunkAgents, nets);
