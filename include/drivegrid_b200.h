@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define DG_ABI_VERSION 12
+#define DG_ABI_VERSION 13
 #define DG_NUM_STATE 12
 #define DG_NUM_TERMS 7
 #define DG_NO_ERROR 0x7fffffff
@@ -295,6 +295,27 @@ int dg_host_alloc(size_t bytes, void** host_ptr);
 int dg_host_free(void* host_ptr);
 int dg_to_host(dg_engine* eng, const float* obs, const int16_t* prefix, float* host_obs, int32_t* prev_len,
                const void* aux, void* host_aux, size_t aux_bytes, unsigned long long* bytes, void* stream);
+
+/* The numpy step path in one host call (replaces the four calls of
+ * Engine._step_host: the host finiteness check engine.py:291-294, the action
+ * H2D copy, dg_step, dg_to_host; engine.py:334-406 behind env.py:48-65).
+ * host_actions: the caller's float64 [W][M][3] (any host memory); checked for
+ * finiteness while copied into pinned_actions (pinned, same size) -- a
+ * non-finite value returns DG_ENONFINITE with *bad_index = its flat index,
+ * before anything is queued or mutated; else *bad_index = -1.  Then, on
+ * `stream`: pinned_actions -> io->actions (device, io->actions_f64 = 1), the
+ * step of `io`, and -- when host_obs is non-NULL -- dg_to_host(io->obs,
+ * io->prefix_out, host_obs, prev_len, aux, host_aux, aux_bytes, bytes). */
+int dg_step_host(dg_engine* eng, const DgStepIO* io, const double* host_actions, double* pinned_actions,
+                 float* host_obs, int32_t* prev_len, const void* aux, void* host_aux, size_t aux_bytes,
+                 unsigned long long* bytes, int64_t* bad_index, void* stream);
+
+/* Host LaneFollower (policies.py:21-43) over float32 observation rows
+ * obs [rows][obs_dim] (host memory) -> out [rows][3] float64 (throttle, steer,
+ * brake): bit-identical to the numpy policy (NaN and -0.0 included).  Host
+ * code, no device work. */
+int dg_lane_follower_rows(const float* obs, int64_t rows, int32_t obs_dim, double steer_gain, double throttle,
+                          double bbox_half, double* out);
 
 /* Kernel launches issued by the last dg_step/dg_observe/dg_reset call. */
 int dg_launch_count(dg_engine* eng);

@@ -24,7 +24,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 DG_OK, DG_EINVAL, DG_ENONFINITE, DG_ECUDA, DG_ENOSUPPORT = 0, 1, 2, 3, 4
 DG_NO_ERROR = 0x7FFFFFFF
-ABI_VERSION = 12
+ABI_VERSION = 13
 
 
 class DgDims(ct.Structure):
@@ -152,6 +152,9 @@ SIGNATURES = {
     "dg_host_alloc": (ct.c_int, [ct.c_size_t, ct.POINTER(_P)]),
     "dg_host_free": (ct.c_int, [_P]),
     "dg_to_host": (ct.c_int, [_P, _P, _P, _P, _P, _P, _P, ct.c_size_t, _P, _P]),
+    "dg_step_host": (ct.c_int, [_P, ct.POINTER(DgStepIO), _P, _P, _P, _P, _P, _P, ct.c_size_t, _P,
+                                ct.POINTER(ct.c_int64), _P]),
+    "dg_lane_follower_rows": (ct.c_int, [_P, ct.c_int64, ct.c_int32, ct.c_double, ct.c_double, ct.c_double, _P]),
     "dg_build_scenes": (ct.c_int, [ct.POINTER(DgScenePool), ct.POINTER(DgSceneBuild), ct.POINTER(DgSceneSegments),
                                    _P]),
     "dg_build_worlds": (ct.c_int, [ct.POINTER(DgScenePool), ct.POINTER(DgSceneSegments), ct.POINTER(DgWorldBuild),

@@ -3006,6 +3006,67 @@ int dg_to_host(dg_engine* eng, const float* obs, const int16_t* prefix, float* h
     return DG_OK;
 }
 
+// The numpy step path in one call (Engine._step_host; engine.py:334-406 behind
+// env.py:48-65): the caller's float64 actions are checked for finiteness while
+// they are copied into the pinned staging buffer (engine.py:291-294: a
+// non-finite value returns DG_ENONFINITE with its flat index before anything is
+// launched or mutated), then the H2D copy, the step and the host delivery are
+// queued on one stream -- one host call instead of four.
+int dg_step_host(dg_engine* eng, const DgStepIO* io, const double* host_actions, double* pinned_actions,
+                 float* host_obs, int32_t* prev_len, const void* aux, void* host_aux, size_t aux_bytes,
+                 unsigned long long* bytes, int64_t* bad_index, void* stream) {
+    if (!eng || !io || !host_actions || !pinned_actions || !bad_index)
+        return fail(DG_EINVAL, "dg_step_host: null argument");
+    if (!io->actions_f64 || !io->actions) return fail(DG_EINVAL, "dg_step_host: io must carry float64 device actions");
+    const DgDims& d = eng->base.d;
+    const int64_t n = int64_t(d.W) * d.M * 3;
+    *bad_index = -1;
+    bool ok = true;
+    for (int64_t i = 0; i < n; ++i) {
+        const double a = host_actions[i];
+        pinned_actions[i] = a;
+        ok &= std::isfinite(a);
+    }
+    if (!ok) {
+        for (int64_t i = 0; i < n; ++i)
+            if (!std::isfinite(host_actions[i])) { *bad_index = i; break; }
+        return fail(DG_ENONFINITE, "dg_step_host: non-finite action");
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(const_cast<void*>(io->actions), pinned_actions, size_t(n) * sizeof(double),
+                                    cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "dg_step_host: action copy");
+    int rc = dg_step(eng, io, stream);
+    if (rc != DG_OK || !host_obs) return rc;
+    const int launches = eng->launches;
+    rc = dg_to_host(eng, io->obs, io->prefix_out, host_obs, prev_len, aux, host_aux, aux_bytes, bytes, stream);
+    eng->launches = launches + 1;
+    return rc;
+}
+
+// Host LaneFollower (policies.py:21-43) over float32 observation rows [rows][D]:
+// float64 arithmetic as the numpy expression -- np.clip(gain * sin, -1, 1) as
+// minimum(maximum(x, -1), 1), the goal-behind override, the distance-dependent
+// throttle -- NaN and -0.0 included; one pass, each row's ego features read once.
+int dg_lane_follower_rows(const float* obs, int64_t rows, int32_t obs_dim, double steer_gain, double throttle,
+                          double bbox_half, double* out) {
+    if (!obs || !out || rows < 0 || obs_dim < 5) return fail(DG_EINVAL, "dg_lane_follower_rows: bad argument");
+    const double half = throttle * 0.5;
+    for (int64_t r = 0; r < rows; ++r) {
+        if (r + 16 < rows) __builtin_prefetch(obs + (r + 16) * obs_dim + 2);
+        const float* g = obs + r * obs_dim + 2;
+        const double sn = double(g[0]), cs = double(g[1]), dist = double(g[2]) * bbox_half;
+        double steer = steer_gain * sn;
+        steer = steer < -1.0 ? -1.0 : steer;      // np.maximum(x, -1): NaN and -0.0 pass through
+        steer = steer > 1.0 ? 1.0 : steer;        // np.minimum(x, 1)
+        if (cs < 0.0) steer = sn >= 0.0 ? 1.0 : -1.0;
+        out[3 * r] = dist > 5.0 ? throttle : half;
+        out[3 * r + 1] = steer;
+        out[3 * r + 2] = 0.0;
+    }
+    return DG_OK;
+}
+
 int dg_launch_count(dg_engine* eng) { return eng ? eng->launches : 0; }
 
 #ifdef DG_TICK_TIMERS

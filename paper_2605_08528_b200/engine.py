@@ -1019,17 +1019,10 @@ class Engine:
 
     def _step_host(self, actions, autoreset: bool) -> StepOutput:
         t0 = time.perf_counter()
-        a = np.asarray(actions, dtype=np.float64)
+        a = np.ascontiguousarray(actions, dtype=np.float64)
         want = (self.W, self.M, 3)
         if a.shape != want:
             raise ValueError(f"actions shape {a.shape}, expected {want}")
-        bad = ~np.isfinite(a)
-        if bad.any():
-            w, m, _ = np.argwhere(bad)[0]
-            raise ValueError(f"non-finite action for world {w} agent {m}")
-        self._act_host.numpy()[...] = a
-        self._act_dev.copy_(self._act_host, non_blocking=True)
-        t1 = time.perf_counter()
         bufs = self._host_bufs
         key = (bool(autoreset), self._metrics_on)
         io = self._host_io.get(key)
@@ -1041,22 +1034,31 @@ class Engine:
                                                     prefix_out=self._prefix_dev, resident=True,
                                                     phase_cycles=self._phase_dev)
         stream = torch.cuda.current_stream(self.device)
-        N.check(self._lib, self._lib.dg_step(self._h, ct.byref(io), ct.c_void_p(stream.cuda_stream)), "dg_step")
-        self._step_count += 1
-        self.launches += 1
         slab = self._mapped_pool.acquire()
+        t1 = time.perf_counter()
+        # one host call: finiteness check while staging the actions in pinned memory
+        # (raises before anything is queued, engine.py:291-294), H2D, the step and --
+        # with a mapped slab -- the delivery: obs rows written into the slab by the
+        # device (non-zero prefixes only), the packed per-tick outputs DMA'd behind them
+        bad = ct.c_int64(-1)
         if slab is not None:
-            # obs rows written into the mapped slab by the device (non-zero prefixes
-            # only), the packed per-tick outputs DMA'd behind them
             ptr, prev, hb = slab
             ob = self._host_obs_bytes
-            N.check(self._lib, self._lib.dg_to_host(
-                self._h, _ptr(self._obs_dev), _ptr(self._prefix_dev), ct.c_void_p(ptr), _ptr(prev),
-                _ptr(self._host_bufs.aux),
-                ct.c_void_p(ptr + ob), self._host_blob.numel() - ob, _ptr(self.d2h_bytes),
-                ct.c_void_p(stream.cuda_stream)), "dg_to_host")
-            self.launches += 1
+            rc = self._lib.dg_step_host(self._h, ct.byref(io), a.ctypes.data, self._act_host.data_ptr(),
+                                        ct.c_void_p(ptr), _ptr(prev), _ptr(self._host_bufs.aux),
+                                        ct.c_void_p(ptr + ob), self._host_blob.numel() - ob, _ptr(self.d2h_bytes),
+                                        ct.byref(bad), ct.c_void_p(stream.cuda_stream))
         else:
+            rc = self._lib.dg_step_host(self._h, ct.byref(io), a.ctypes.data, self._act_host.data_ptr(),
+                                        None, None, None, None, 0, None, ct.byref(bad),
+                                        ct.c_void_p(stream.cuda_stream))
+        if rc == N.DG_ENONFINITE and bad.value >= 0:
+            w, m = divmod(bad.value // 3, self.M)
+            raise ValueError(f"non-finite action for world {w} agent {m}")
+        N.check(self._lib, rc, "dg_step_host")
+        self._step_count += 1
+        self.launches += 2 if slab is not None else 1
+        if slab is None:
             host, hb = self._host_pool.acquire()
             host.copy_(self._host_blob, non_blocking=True)          # obs + every per-tick output, one copy
         stream.synchronize()

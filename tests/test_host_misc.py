@@ -83,3 +83,31 @@ def test_scalar_drac_and_bench_row():
                       warmup_steps=2, wall_seconds=0.5, phase_ms={k: 1.0 for k in PHASES}).to_row()
     assert (row["W"], row["M"], row["CASPS"]) == (8, 4, 1234.5)
     assert all(f"{k}_ms" in row for k in PHASES)
+
+
+def test_native_lane_follower_rows_match_the_numpy_policy():
+    """dg_lane_follower_rows (host code in the native library) gives the numpy
+    LaneFollower's bits (policies.py:21-43), NaN / -0.0 / clip edges included,
+    for [W][M][D] and [rows][D] batches and other gains."""
+    from paper_2605_08528_b200.params import ObsConfig
+    from paper_2605_08528_b200.policies import LaneFollower, _host_lib
+    if _host_lib() is None:
+        pytest.skip("native library not built")
+    rng = np.random.default_rng(7)
+    obs = np.zeros((8, 16, 1929), np.float32)
+    obs[..., :11] = (rng.standard_normal((8, 16, 11)) * 3).astype(np.float32)
+    special = [np.nan, -0.0, 0.0, 0.5, -0.5, 0.25, -0.25, np.inf, -np.inf, 1e-30, -1e-30]
+    for i, v in enumerate(special):
+        obs[0, i % 16, 2 + i % 3] = v
+        obs[1, i % 16, 2 + (i + 1) % 3] = v
+        obs[2, i % 16, 2:5] = v
+    obs[3, :, 4] = np.float32(5.0 / ObsConfig().bbox_half)        # the throttle threshold
+    for gain, thr in ((2.0, 0.5), (1.0, 0.3), (3, 1)):
+        lf = LaneFollower(steer_gain=gain, throttle=thr, obs_config=ObsConfig())
+        for o in (obs, obs.reshape(-1, 1929), obs[:, :, :11].copy()):
+            a, b = lf(o), lf.numpy(o)
+            assert a.shape == b.shape
+            assert np.array_equal(a.view(np.int64), b.view(np.int64))
+    # non-contiguous / float64 observations take the numpy expression
+    lf = LaneFollower(obs_config=ObsConfig())
+    assert np.array_equal(lf(obs[:, ::2]).view(np.int64), lf.numpy(obs[:, ::2]).view(np.int64))
