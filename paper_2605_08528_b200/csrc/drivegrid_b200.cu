@@ -2532,6 +2532,15 @@ struct dg_engine {
     int mode;              // 0 = fused world kernel, 1 = split physics + per-agent kernels (PDL),
                            // 2 = fused with a physics warp running one tick ahead (kSpec)
     size_t smem_split;     // dynamic smem of the per-agent kernel
+    // dg_to_host: the packed per-tick outputs go down on a side stream while the
+    // obs rows are written into the slab (the SM stores leave PCIe headroom)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_aux = nullptr;
+    ~dg_engine() {
+        if (ev_ready) cudaEventDestroy(ev_ready);
+        if (ev_aux) cudaEventDestroy(ev_aux);
+        if (side) cudaStreamDestroy(side);
+    }
 };
 
 // the shapes the engine picks by default also come with the phase counters
@@ -2991,17 +3000,32 @@ int dg_to_host(dg_engine* eng, const float* obs, const int16_t* prefix, float* h
     cudaError_t e = cudaHostGetDevicePointer(&dptr, host_obs, 0);
     if (e != cudaSuccess) return cuda_fail(e, "dg_to_host: host slab is not mapped pinned memory");
     const int64_t rows = int64_t(d.W) * d.M;
-    const int per_cta = 8;
+    const int per_cta = 8;           // 1..16 rows per CTA measured the same (PCIe-bound)
     const int64_t grid = (rows + per_cta - 1) / per_cta;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (aux_bytes) {
+        // fork: the aux DMA on the engine's side stream, concurrent with the row stores
+        if (!eng->side) {
+            e = cudaStreamCreateWithFlags(&eng->side, cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&eng->ev_ready, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&eng->ev_aux, cudaEventDisableTiming);
+            if (e != cudaSuccess) return cuda_fail(e, "dg_to_host: side stream");
+        }
+        e = cudaEventRecord(eng->ev_ready, st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(eng->side, eng->ev_ready, 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(host_aux, aux, aux_bytes, cudaMemcpyDeviceToHost, eng->side);
+        if (e == cudaSuccess) e = cudaEventRecord(eng->ev_aux, eng->side);
+        if (e != cudaSuccess) return cuda_fail(e, "dg_to_host: aux copy");
+    }
     if (grid > 0)
-        obs_to_host_kernel<<<unsigned(grid), 32 * per_cta, 0, static_cast<cudaStream_t>(stream)>>>(
+        obs_to_host_kernel<<<unsigned(grid), 32 * per_cta, 0, st>>>(
             obs, prefix, static_cast<float*>(dptr), prev_len, rows, d.obs_dim, d.ego_dim, 5 * d.k_road,
             7 * d.k_vehicles, bytes);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "dg_to_host");
     if (aux_bytes) {
-        e = cudaMemcpyAsync(host_aux, aux, aux_bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream));
-        if (e != cudaSuccess) return cuda_fail(e, "dg_to_host: aux copy");
+        e = cudaStreamWaitEvent(st, eng->ev_aux, 0);     // join: the stream's sync covers both
+        if (e != cudaSuccess) return cuda_fail(e, "dg_to_host: join");
     }
     return DG_OK;
 }

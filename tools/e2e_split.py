@@ -17,7 +17,10 @@ from paper_2605_08528_b200.policies import LaneFollower  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 dev = torch.device("cuda:0")
-eng = Engine(**C.build_inputs(C.RootConfig()).as_kwargs(), device=dev)
+import os  # noqa: E402
+mode = os.environ.get("DG_E2E_MODE")
+eng = Engine(**C.build_inputs(C.RootConfig()).as_kwargs(), device=dev,
+             launch_mode=None if mode is None else int(mode))
 pol = LaneFollower(obs_config=eng.obs_config)
 obs = eng.observe()
 for _ in range(5):
@@ -37,4 +40,4 @@ wall = time.perf_counter() - t_all
 print(json.dumps({"workload": "256x16 default pool, LaneFollower + autoreset, numpy API", "steps": steps,
                   "ms_per_step": 1e3 * wall / steps, "policy_ms": 1e3 * t_pol / steps,
                   "engine_step_ms": 1e3 * t_step / steps,
-                  "casps": eng.W * eng.M * steps / wall}))
+                  "casps": eng.W * eng.M * steps / wall, "launch_shape": eng.launch_shape()}))
