@@ -3057,10 +3057,20 @@ int dg_step_host(dg_engine* eng, const DgStepIO* io, const double* host_actions,
         return fail(DG_ENONFINITE, "dg_step_host: non-finite action");
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t e = cudaMemcpyAsync(const_cast<void*>(io->actions), pinned_actions, size_t(n) * sizeof(double),
-                                    cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "dg_step_host: action copy");
-    int rc = dg_step(eng, io, stream);
+    // the kernel reads the staged actions in place over PCIe (pinned host memory is
+    // device-mapped under unified addressing): no copy launch ahead of the step; a
+    // buffer without a device mapping goes through an H2D copy into io->actions
+    DgStepIO sio = *io;
+    void* mapped = nullptr;
+    if (cudaHostGetDevicePointer(&mapped, pinned_actions, 0) == cudaSuccess && mapped) {
+        sio.actions = mapped;
+    } else {
+        (void)cudaGetLastError();
+        cudaError_t e = cudaMemcpyAsync(const_cast<void*>(io->actions), pinned_actions,
+                                        size_t(n) * sizeof(double), cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "dg_step_host: action copy");
+    }
+    int rc = dg_step(eng, &sio, stream);
     if (rc != DG_OK || !host_obs) return rc;
     const int launches = eng->launches;
     rc = dg_to_host(eng, io->obs, io->prefix_out, host_obs, prev_len, aux, host_aux, aux_bytes, bytes, stream);
