@@ -13,7 +13,7 @@ step just wrote and emits the next tick's actions) -- one kernel per tick.
           rollout ring larger than L2 (no cache reuse between steps)
   e2e     the same metric through the reference-facing numpy API
           (Engine.step with host arrays: H2D actions, D2H obs/rewards/dones/
-          events/info every step, host numpy LaneFollower)
+          events/info every step, host LaneFollower: dg_lane_follower_rows)
 
 N>1 (torchrun): 4096x16 worlds sharded by contiguous world range (BASELINE
 configs[3]), no per-step communication; episode statistics all-gathered once
@@ -672,7 +672,7 @@ def e2e_numpy(eng, steps):
             "gpu_launches": eng.launches - launches0,
             "steps": steps, "ticks": ticks, "wall_s": wall,
             "ms_per_step": 1e3 * wall / steps, "host_slabs": eng._mapped_pool.slabs,
-            "api": "Engine.step(numpy actions) -> numpy StepOutput, autoreset, host numpy LaneFollower; "
+            "api": "Engine.step(numpy actions) -> numpy StepOutput, autoreset, host LaneFollower (dg_lane_follower_rows, the numpy expression bit for bit); "
                    "alive agents counted before each step (metrics.py:168-170)"}
 
 
