@@ -270,16 +270,73 @@ class StepOutput:
         if self._info is None:
             s = self._info_src
             as_bool = (lambda a: a.astype(bool)) if self._host else (lambda a: a.bool())
-            self._info = {
-                "alive": as_bool(s["alive"]),
-                "alive_pre": as_bool(s["alive_pre"]),
-                "state": {k: s["snapshot"][..., i, :, :] for i, k in enumerate(STATE_FIELDS)},
-                "reason": s["reason"],
-                "reward_terms": {k: s["terms"][..., i, :, :] for i, k in enumerate(TERM_NAMES)},
-                "ttc_min": s["ttc_min"],
-                "step": s["step"],
-            }
+            self._info = _LazyInfo({
+                "alive": lambda: as_bool(s["alive"]),
+                "alive_pre": lambda: as_bool(s["alive_pre"]),
+                "state": lambda: {k: s["snapshot"][..., i, :, :] for i, k in enumerate(STATE_FIELDS)},
+                "reason": lambda: s["reason"],
+                "reward_terms": lambda: {k: s["terms"][..., i, :, :] for i, k in enumerate(TERM_NAMES)},
+                "ttc_min": lambda: s["ttc_min"],
+                "step": lambda: s["step"],
+            })
         return self._info
+
+
+class _LazyInfo(dict):
+    """The step's info dict (engine.py:70-76 keys), each entry built on first
+    access -- a loop that reads one entry per step (measure_engine's
+    alive_pre, metrics.py:168-170) does not pay for the views of the others.
+    Any whole-dict use (iteration, len, equality, copies) builds them all."""
+
+    def __init__(self, makers: dict):
+        super().__init__()
+        self._makers = makers
+
+    def __missing__(self, key):
+        make = self._makers.get(key)
+        if make is None:
+            raise KeyError(key)
+        v = make()
+        dict.__setitem__(self, key, v)
+        return v
+
+    def _fill(self):
+        for k in self._makers:
+            if not dict.__contains__(self, k):
+                self[k]
+        return self
+
+    def get(self, key, default=None):
+        return self[key] if key in self._makers or dict.__contains__(self, key) else default
+
+    def __contains__(self, key):
+        return key in self._makers or dict.__contains__(self, key)
+
+    def __iter__(self):
+        return dict.__iter__(self._fill())
+
+    def __len__(self):
+        return dict.__len__(self._fill())
+
+    def keys(self):
+        return dict.keys(self._fill())
+
+    def values(self):
+        return dict.values(self._fill())
+
+    def items(self):
+        return dict.items(self._fill())
+
+    def copy(self):
+        return dict(self._fill().items())
+
+    def __eq__(self, other):
+        return dict.__eq__(self._fill(), other)
+
+    __hash__ = None
+
+    def __repr__(self):
+        return dict.__repr__(self._fill())
 
 
 @dataclass(eq=False)
