@@ -573,7 +573,10 @@ class Engine:
         if lay is None:
             lay = self._host_lay = [(name, o, n, torch.empty((), dtype=dt).numpy().dtype, shape)
                                     for name, (o, n, dt, shape) in self._aux_layout()[0].items()]
-        return {name: aux[o:o + n].view(dt).reshape(shape) for name, o, n, dt, shape in lay}
+        # each field's view is made on first access (a step reads rewards / dones /
+        # events; info entries only when asked for)
+        return _LazyInfo({name: (lambda o=o, n=n, dt=dt, shape=shape: aux[o:o + n].view(dt).reshape(shape))
+                          for name, o, n, dt, shape in lay})
 
     def _views(self, aux: torch.Tensor, slots: int | None = None) -> dict:
         lay, _ = self._aux_layout(slots)
@@ -1122,7 +1125,7 @@ class Engine:
         t2 = time.perf_counter()
         obs = hb[:self.W * self.M * self.obs_config.obs_dim * 4].view(np.float32).reshape(bufs.obs.shape)
         hv = self._host_views(hb[self._host_obs_bytes:])
-        src = dict(hv)
+        src = hv
         src["step"] = self._step_count
         self.phase_seconds["action"] += t1 - t0
         self._phase_host = hb[self._phase_off:self._phase_off + 40].view(np.int64).copy()   # no view: the slab recycles
