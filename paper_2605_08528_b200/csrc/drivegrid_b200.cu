@@ -3078,6 +3078,9 @@ int dg_step_host(dg_engine* eng, const DgStepIO* io, const double* host_actions,
     return rc;
 }
 
+#ifndef DG_LF_PREFETCH
+#define DG_LF_PREFETCH 16      // rows ahead: the slab rows arrive from the device, not in cache
+#endif
 // Host LaneFollower (policies.py:21-43) over float32 observation rows [rows][D]:
 // float64 arithmetic as the numpy expression -- np.clip(gain * sin, -1, 1) as
 // minimum(maximum(x, -1), 1), the goal-behind override, the distance-dependent
@@ -3087,7 +3090,7 @@ int dg_lane_follower_rows(const float* obs, int64_t rows, int32_t obs_dim, doubl
     if (!obs || !out || rows < 0 || obs_dim < 5) return fail(DG_EINVAL, "dg_lane_follower_rows: bad argument");
     const double half = throttle * 0.5;
     for (int64_t r = 0; r < rows; ++r) {
-        if (r + 16 < rows) __builtin_prefetch(obs + (r + 16) * obs_dim + 2);
+        if (r + DG_LF_PREFETCH < rows) __builtin_prefetch(obs + (r + DG_LF_PREFETCH) * obs_dim + 2);
         const float* g = obs + r * obs_dim + 2;
         const double sn = double(g[0]), cs = double(g[1]), dist = double(g[2]) * bbox_half;
         double steer = steer_gain * sn;

@@ -11,13 +11,19 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch  # noqa: E402
 
+import os  # noqa: E402
+
+from paper_2605_08528_b200 import _native as N  # noqa: E402
+
+if os.environ.get("DG_LIB_PATH"):          # a variant build
+    N.LIB_PATH = Path(os.environ["DG_LIB_PATH"])
+    N.load_library(build_if_missing=False)
 from paper_2605_08528_b200 import config as C  # noqa: E402
 from paper_2605_08528_b200.engine import Engine  # noqa: E402
 from paper_2605_08528_b200.policies import LaneFollower  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 dev = torch.device("cuda:0")
-import os  # noqa: E402
 mode = os.environ.get("DG_E2E_MODE")
 eng = Engine(**C.build_inputs(C.RootConfig()).as_kwargs(), device=dev,
              launch_mode=None if mode is None else int(mode))
