@@ -31,7 +31,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
+#include <unistd.h>
 #include <new>
 
 #include "dg_fastmath.cuh"
@@ -3085,12 +3090,11 @@ int dg_step_host(dg_engine* eng, const DgStepIO* io, const double* host_actions,
 // float64 arithmetic as the numpy expression -- np.clip(gain * sin, -1, 1) as
 // minimum(maximum(x, -1), 1), the goal-behind override, the distance-dependent
 // throttle -- NaN and -0.0 included; one pass, each row's ego features read once.
-int dg_lane_follower_rows(const float* obs, int64_t rows, int32_t obs_dim, double steer_gain, double throttle,
-                          double bbox_half, double* out) {
-    if (!obs || !out || rows < 0 || obs_dim < 5) return fail(DG_EINVAL, "dg_lane_follower_rows: bad argument");
+static void lf_rows(const float* obs, int64_t lo, int64_t hi, int32_t obs_dim, double steer_gain, double throttle,
+                    double bbox_half, double* out) {
     const double half = throttle * 0.5;
-    for (int64_t r = 0; r < rows; ++r) {
-        if (r + DG_LF_PREFETCH < rows) __builtin_prefetch(obs + (r + DG_LF_PREFETCH) * obs_dim + 2);
+    for (int64_t r = lo; r < hi; ++r) {
+        if (r + DG_LF_PREFETCH < hi) __builtin_prefetch(obs + (r + DG_LF_PREFETCH) * obs_dim + 2);
         const float* g = obs + r * obs_dim + 2;
         const double sn = double(g[0]), cs = double(g[1]), dist = double(g[2]) * bbox_half;
         double steer = steer_gain * sn;
@@ -3101,6 +3105,82 @@ int dg_lane_follower_rows(const float* obs, int64_t rows, int32_t obs_dim, doubl
         out[3 * r + 1] = steer;
         out[3 * r + 2] = 0.0;
     }
+}
+
+static inline void cpu_relax() {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+}
+
+// Helper threads for the host LaneFollower: a batch's rows are cache misses on a
+// slab the device just wrote, so one core is bound by its outstanding misses;
+// kLfWorkers threads take equal row ranges beside the caller.  They spin ~1 ms
+// after a batch (a loop calls the policy every few hundred us), then sleep.
+struct LfPool {
+    static constexpr int kLfWorkers = 3;
+    std::atomic<unsigned> gen{0};
+    std::atomic<int> done{0};
+    std::mutex mu;
+    std::condition_variable cv;
+    const float* obs = nullptr;
+    int64_t rows = 0;
+    int32_t obs_dim = 0;
+    double gain = 0, thr = 0, bh = 0;
+    double* out = nullptr;
+
+    void work(int id) {
+        unsigned seen = 0;
+        for (;;) {
+            const auto t0 = std::chrono::steady_clock::now();
+            unsigned g;
+            while ((g = gen.load(std::memory_order_acquire)) == seen) {
+                if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(1)) {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return gen.load(std::memory_order_acquire) != seen; });
+                } else {
+                    cpu_relax();
+                }
+            }
+            seen = g;
+            const int parts = kLfWorkers + 1;
+            lf_rows(obs, rows * (id + 1) / parts, rows * (id + 2) / parts, obs_dim, gain, thr, bh, out);
+            done.fetch_add(1, std::memory_order_acq_rel);
+        }
+    }
+};
+
+int dg_lane_follower_rows(const float* obs, int64_t rows, int32_t obs_dim, double steer_gain, double throttle,
+                          double bbox_half, double* out) {
+    if (!obs || !out || rows < 0 || obs_dim < 5) return fail(DG_EINVAL, "dg_lane_follower_rows: bad argument");
+    static std::mutex call_mu;
+    static LfPool* pool = nullptr;
+    static pid_t pool_pid = 0;
+    std::unique_lock<std::mutex> lk(call_mu, std::try_to_lock);
+    if (rows < 2048 || !lk.owns_lock()) {            // small batches / a concurrent caller: this thread only
+        lf_rows(obs, 0, rows, obs_dim, steer_gain, throttle, bbox_half, out);
+        return DG_OK;
+    }
+    if (!pool || pool_pid != getpid()) {             // (a forked child has no helper threads: a new pool)
+        pool = new LfPool;
+        pool_pid = getpid();
+        for (int i = 0; i < LfPool::kLfWorkers; ++i) std::thread(&LfPool::work, pool, i).detach();
+    }
+    pool->obs = obs;
+    pool->rows = rows;
+    pool->obs_dim = obs_dim;
+    pool->gain = steer_gain;
+    pool->thr = throttle;
+    pool->bh = bbox_half;
+    pool->out = out;
+    pool->done.store(0, std::memory_order_relaxed);
+    {
+        std::lock_guard<std::mutex> g(pool->mu);
+        pool->gen.fetch_add(1, std::memory_order_acq_rel);
+    }
+    pool->cv.notify_all();
+    lf_rows(obs, 0, rows / (LfPool::kLfWorkers + 1), obs_dim, steer_gain, throttle, bbox_half, out);
+    while (pool->done.load(std::memory_order_acquire) < LfPool::kLfWorkers) cpu_relax();
     return DG_OK;
 }
 

@@ -108,6 +108,14 @@ def test_native_lane_follower_rows_match_the_numpy_policy():
             a, b = lf(o), lf.numpy(o)
             assert a.shape == b.shape
             assert np.array_equal(a.view(np.int64), b.view(np.int64))
+    # a bench-sized batch (4,096 rows: the helper threads split it)
+    big = np.zeros((256, 16, 64), np.float32)
+    big[..., :11] = (rng.standard_normal((256, 16, 11)) * 3).astype(np.float32)
+    big[7, 3, 2:5] = np.nan
+    big[200, 9, 3] = -0.0
+    lf = LaneFollower(obs_config=ObsConfig())
+    for _ in range(3):
+        assert np.array_equal(lf(big).view(np.int64), lf.numpy(big).view(np.int64))
     # non-contiguous / float64 observations take the numpy expression
     lf = LaneFollower(obs_config=ObsConfig())
     assert np.array_equal(lf(obs[:, ::2]).view(np.int64), lf.numpy(obs[:, ::2]).view(np.int64))
